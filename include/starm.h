@@ -1,0 +1,177 @@
+/*
+ * libstarm -- C ABI of the B200 (sm_100a) t-SVDM hot path.
+ *
+ * The reference (arxiv 2605.16058 package `starm`, /root/reference/pkg) is
+ * pure Python over numpy/scipy; it has no FFI of its own.  These entry
+ * points sit UNDER the reference's Python operators and replace the
+ * numpy/LAPACK calls each one names.  The Python package
+ * paper_2605_16058_b200 binds them with ctypes.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated otherwise; the caller
+ *    allocates every buffer (outputs and workspace) and owns it.  Nothing
+ *    here allocates or frees caller memory.
+ *  - Tensors are column-major (Fortran) float64 exactly like the
+ *    reference's DenseTensor (tensor.py:76-98): frontal slice i of an
+ *    (m, p, N) tensor is the contiguous m x p column-major block at element
+ *    offset i*m*p.
+ *  - `stream` is a cudaStream_t passed as void*; every call is
+ *    stream-ordered and asynchronous unless documented otherwise.
+ *  - Return value: STARM_OK or an error code; the message is available
+ *    from starm_last_error().  Per-slice failures (non-finite data,
+ *    non-convergence) are reported through a device int32 status pair so
+ *    the host can raise the reference's exceptions naming the slice
+ *    (slicesvd.py:49-50,58-61).
+ */
+#ifndef STARM_H_
+#define STARM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STARM_ABI_VERSION 1
+
+enum starm_status {
+  STARM_OK = 0,
+  STARM_INVALID_ARG = 1,      /* -> ValueError                              */
+  STARM_NONFINITE_SLICE = 2,  /* -> ValueError("slice {i} contains ...")    */
+  STARM_NOCONVERGE = 3,       /* -> np.linalg.LinAlgError                   */
+  STARM_CUDA = 4,             /* -> RuntimeError                            */
+  STARM_UNSUPPORTED = 5       /* -> ValueError (shape outside kernel range) */
+};
+
+/* SVD jobs for starm_svd_f64 */
+enum starm_svd_job {
+  STARM_SVD_VALUES = 0,     /* slicesvd.py:139-177 svd_values_only            */
+  STARM_SVD_FULL = 1,       /* slicesvd.py:115-136 svd_all_slices             */
+  STARM_SVD_TRUNCATED = 2   /* slicesvd.py:259-292 svd_truncated_slices       */
+};
+
+int starm_abi_version(void);
+
+/* Copies the calling thread's last error message into buf (NUL-terminated,
+ * truncated to len); returns the full message length. */
+size_t starm_last_error(char* buf, size_t len);
+
+/* ---------------------------------------------------------------- K1 TTM
+ * Replaces ttm.py:113-135 (`_dispatch`, np.matmul -> OpenBLAS DGEMM).
+ * View of the column-major buffer: `batch` row-major blocks
+ * src[b] (inner x rows), dst[b] (out_cols x rows); computes
+ *     dst[b] = mat @ src[b]            for b in [0, batch)
+ * with `mat` ROW-MAJOR out_cols x inner (mat[j*inner + l]).  This is the
+ * mode-k product of ttm.py:87-104 for rows = prod(dims[:k]),
+ * inner = dims[k], batch = prod(dims[k+1:]) (TTMPlan, ttm.py:59-69).
+ * FP64 DMMA tiles, cp.async shared-memory staging. */
+int starm_ttm_f64(const double* src, const double* mat, double* dst, int64_t rows,
+                  int64_t inner, int64_t batch, int64_t out_cols, void* stream);
+
+/* ----------------------------------------------------- K11 facewise GEMM
+ * Replaces _facewise_matmul (tsvdm.py:205-216): for each slice i,
+ *   C_i (m x l) = A_i (m x p) * B_i (p x l), all column-major, slice
+ *   strides m*p, p*l, m*l. */
+int starm_facewise_gemm_f64(const double* a, const double* b, double* c, int64_t m,
+                            int64_t p, int64_t l, int64_t nslices, void* stream);
+
+/* ------------------------------------------------------ K3-K6 slice SVD
+ * Replaces _slice_svd/LAPACK dgesvd over slices (slicesvd.py:42-62 and the
+ * three drivers named by `job`).  One CTA per slice runs a blocked
+ * one-sided Jacobi SVD (Gram tiles on FP64 DMMA) in a global workspace.
+ *
+ *  ahat       (m, p, nslices) column-major input, never modified.
+ *  slice_ids  optional device int64 list of slices to factor (count
+ *             entries); NULL means all slices 0..nslices-1 (count ignored).
+ *  s          (r, nslices) column-major singular values, descending per
+ *             slice, r = min(m, p).  Required for VALUES/FULL, optional
+ *             (may be NULL) for TRUNCATED.
+ *  u, v       FULL: (m, r, nslices) and (p, r, nslices) column-major,
+ *             slice i reconstructs as u_i diag(s_i) v_i^T (SliceSVDSet).
+ *  ranks, u_off, g_off, u_data, g_data
+ *             TRUNCATED: packed VariableRankFactors (slicesvd.py:180-256):
+ *             u_data[u_off[i] ...] = U_i[:, :k] (m x k col-major),
+ *             g_data[g_off[i] ...] = diag(s[:k]) V_i[:, :k]^T (k x p col-major),
+ *             k = ranks[i]; offsets from starm_pack_offsets.
+ *  status     device int32[2]: status[0] = lowest slice index with a
+ *             non-finite entry, status[1] = lowest slice that did not
+ *             converge; both INT32_MAX when clean.  Reset by this call.
+ *  ws         device workspace of starm_svd_workspace_bytes() bytes.
+ * All-zero slices yield s = 0, U = eye(m, r), V = eye(p, r) (slicesvd.py:51-54). */
+size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t count, int job);
+/* Tuning / diagnostics (process-wide; a value < 0 leaves a knob unchanged):
+ * inner Jacobi sweeps per pair step (default 1), sweep cap (60), QR
+ * preconditioning (1 = when L >= 1.25 n, 0 = never, 2 = whenever it fits),
+ * kernel counters on/off.  starm_svd_stats copies 16 counters (slices,
+ * sweeps, pairs, rotated pairs, cycles in gram / eig / apply / qr /
+ * finalize / load) to host memory, synchronising the device. */
+int starm_svd_tune(int max_inner, int max_sweeps, int qr_mode, int stats);
+int starm_svd_stats(unsigned long long* host16, int reset);
+int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
+                  const int64_t* slice_ids, int64_t count, int job, double* s, double* u,
+                  double* v, const int64_t* ranks, const int64_t* u_off, const int64_t* g_off,
+                  double* u_data, double* g_data, int32_t* status, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* -------------------------------------------------------- K7 threshold
+ * Replaces compute_threshold (tsvdm.py:85-115) with identical semantics:
+ * squares, ascending sort, SEQUENTIAL running sums (np.cumsum), j =
+ * searchsorted(w, eps^2*total, 'left'), tau = v[j-1], strict keep
+ * sq > tau, discarded = numpy pairwise sum of the dropped squares in
+ * C order of the (r, N) matrix, tie-retain rule, ranks per slice.
+ *  s          (r, nslices) column-major, finite, >= 0, each column
+ *             descending (as produced by starm_svd_f64).
+ *  v_out,w_out optional (may be NULL) r*nslices sorted squares / sums.
+ *  ranks_out  int64[nslices].
+ *  scal_out   double[3] = {tau, discarded, total};  j_out int64[1].
+ * Output scalars are device-resident; the call is asynchronous. */
+size_t starm_threshold_workspace_bytes(int64_t r, int64_t nslices);
+int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, double epsilon,
+                        double* v_out, double* w_out, int64_t* ranks_out, double* scal_out,
+                        int64_t* j_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------- K8 offsets
+ * slicesvd.py:208-211: u_off[0]=g_off[0]=0, u_off[i+1] = u_off[i] +
+ * ranks[i]*m, g_off likewise with p.  Arrays hold nslices+1 int64. */
+int starm_pack_offsets(const int64_t* ranks, int64_t nslices, int64_t m, int64_t p,
+                       int64_t* u_off, int64_t* g_off, void* stream);
+
+/* ------------------------------------------- K9 facewise reconstruction
+ * tsvdm.py:346-355: chat_i = U_i G_i for ranks[i] > 0, zero otherwise.
+ * chat is (m, p, nslices) column-major and fully overwritten. */
+int starm_unpack_facewise_f64(const double* u_data, const double* g_data, const int64_t* ranks,
+                              const int64_t* u_off, const int64_t* g_off, int64_t m, int64_t p,
+                              int64_t nslices, double* chat, void* stream);
+
+/* ---------------------------------------------------- K10 error sums
+ * out2[0] = sum (a - b)^2, out2[1] = sum a^2 over `count` elements, with a
+ * fixed (deterministic) reduction tree.  Used for the relative
+ * reconstruction error of tests/helpers.py:44-47 and cli.py:185-197. */
+size_t starm_error_sums_workspace_bytes(int64_t count);
+int starm_error_sums_f64(const double* a, const double* b, int64_t count, double* out2,
+                         void* ws, size_t ws_bytes, void* stream);
+
+
+/* ------------------------------------------------- K8b pack from full
+ * _pack_from_full (tsvdm.py:324-339): from full factors (s (r,N), u
+ * (m,r,N), v (p,r,N)) write u_data block i = u_i[:, :k] and g_data block
+ * i = diag(s_i[:k]) v_i[:, :k]^T, k = ranks[i].  With ranks == r it also
+ * forms the operands of the lossless full_tsvdm reconstruction
+ * (tsvdm.py:190-202). */
+int starm_pack_from_full_f64(const double* s, const double* u, const double* v, int64_t m,
+                             int64_t p, int64_t nslices, const int64_t* ranks,
+                             const int64_t* u_off, const int64_t* g_off, double* u_data,
+                             double* g_data, void* stream);
+
+/* ------------------------------------------------ fixed-rank energies
+ * tsvdm.py:260-262: out2[0] = sum_{j >= rank} s[j,i]^2 (discarded),
+ * out2[1] = sum s^2 (total), deterministic single-CTA reduction. */
+int starm_tail_energy_f64(const double* s, int64_t r, int64_t nslices, int64_t rank,
+                          double* out2, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STARM_H_ */

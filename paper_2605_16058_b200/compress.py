@@ -1,0 +1,453 @@
+"""t-SVDM compression entry points on the B200 (reference tsvdm.py).
+
+Pipeline of ``tsvdm_tolerance`` for a tensor A (m x p x N slices):
+  K1 forward TTM (DMMA)  ->  K3-K6 values-only Jacobi over every slice
+  ->  K7 device threshold (exact compute_threshold semantics)
+  ->  one 40-byte D2H (ranks total, j, tau, energies)
+  ->  K3-K6 truncated Jacobi on the slices with rank > 0, writing the
+      packed factors directly (the pack is fused into the SVD epilogue).
+Everything stays in HBM; host inputs are uploaded once and outputs are
+copied back once.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from contextlib import contextmanager
+from dataclasses import dataclass
+from math import prod
+
+import numpy as np
+
+from . import _native as nat
+from .mode_product import BATCHED, VARIANTS, forward_device, inverse_device
+from .slice_svd import (SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
+                        VariableRankFactors, pack_offsets_device, svd_full_device,
+                        svd_truncated_device, svd_values_device)
+from .tensors import DenseTensor, DeviceTensor, as_device
+from .transform_set import CUSTOM, DATA_DRIVEN, TransformSet
+
+__all__ = [
+    "TRUNCATE", "COMPUTE_EFFICIENT", "MEMORY_EFFICIENT", "TOLERANCE_STRATEGIES",
+    "METHOD_FIXED_RANK", "METHOD_TOLERANCE", "StageClock", "ThresholdResult",
+    "compute_threshold", "TSVDMResult", "CompressedTensor", "starm_product", "full_tsvdm",
+    "tsvdm_fixed_rank", "tsvdm_tolerance", "reconstruct", "compression_ratio",
+    "threshold_device", "relative_error_device",
+]
+
+TRUNCATE = "truncate"
+COMPUTE_EFFICIENT = "compute-efficient"
+MEMORY_EFFICIENT = "memory-efficient"
+TOLERANCE_STRATEGIES = (TRUNCATE, COMPUTE_EFFICIENT, MEMORY_EFFICIENT)
+METHOD_FIXED_RANK = "tsvdm1"
+METHOD_TOLERANCE = "tsvdm2"
+
+
+class StageClock:
+    """Per-stage seconds (tsvdm.py:43-61).  On the device path each stage is
+    bracketed by CUDA events on the current stream, resolved lazily when
+    ``seconds`` is read, so timing adds no synchronisation."""
+
+    def __init__(self):
+        self._host = {}
+        self._events = {}
+
+    @contextmanager
+    def stage(self, name):
+        import torch
+        if torch.cuda.is_available():
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            try:
+                yield
+            finally:
+                b.record()
+                self._events.setdefault(name, []).append((a, b))
+        else:
+            t0 = time.perf_counter()
+            try:
+                yield
+            finally:
+                self._host[name] = self._host.get(name, 0.0) + time.perf_counter() - t0
+
+    def mark(self, name):
+        self._host.setdefault(name, 0.0)
+
+    @property
+    def seconds(self):
+        out = dict(self._host)
+        for name, pairs in self._events.items():
+            tot = 0.0
+            for a, b in pairs:
+                b.synchronize()
+                tot += a.elapsed_time(b) / 1e3
+            out[name] = out.get(name, 0.0) + tot
+        return out
+
+
+@dataclass
+class ThresholdResult:
+    """compute_threshold outcome (tsvdm.py:64-82)."""
+
+    v: object
+    w: object
+    j: int
+    tau: float
+    ranks: object
+    discarded_energy: float
+    total_energy: float
+
+
+def threshold_device(s_flat, r, n, epsilon, want_vw=False):
+    """K7 on a device (r, N) column-major value matrix.  Returns device
+    tensors (ranks, scal=[tau, discarded, total], j, v, w) -- asynchronous."""
+    import torch
+    dev = s_flat.device
+    lib = nat.load()
+    nbytes = lib.starm_threshold_workspace_bytes(r, n)
+    ws = nat.workspace(nbytes, dev)
+    ranks = torch.empty(n, dtype=torch.int64, device=dev)
+    scal = torch.empty(3, dtype=torch.float64, device=dev)
+    j = torch.empty(1, dtype=torch.int64, device=dev)
+    v = torch.empty(r * n, dtype=torch.float64, device=dev) if want_vw else None
+    w = torch.empty(r * n, dtype=torch.float64, device=dev) if want_vw else None
+    nat.call("starm_threshold_f64", s_flat.data_ptr(), r, n, float(epsilon), nat.ptr(v),
+             nat.ptr(w), ranks.data_ptr(), scal.data_ptr(), j.data_ptr(), ws.data_ptr(), nbytes,
+             nat.stream_ptr(dev))
+    return ranks, scal, j, v, w
+
+
+def compute_threshold(s, epsilon) -> ThresholdResult:
+    """Global energy threshold (tsvdm.py:85-115), run by the K7 kernels."""
+    import torch
+    epsilon = float(epsilon)
+    if not 0.0 < epsilon < 1.0:
+        raise ValueError(f"tolerance must lie in (0, 1), got {epsilon}")
+    on_device = isinstance(s, torch.Tensor)
+    if on_device:
+        if s.dim() != 2:
+            raise ValueError(f"expected an (r, N) value matrix, got {s.dim()} modes")
+        if not bool(torch.isfinite(s).all()):
+            raise ValueError("singular values must be finite")
+        if s.numel() and bool((s < 0).any()):
+            raise ValueError("singular values must be non-negative")
+        r, n = s.shape
+        flat = s.T.contiguous().reshape(-1).to(torch.float64)
+    else:
+        s = np.asarray(s, dtype=np.float64)
+        if s.ndim != 2:
+            raise ValueError(f"expected an (r, N) value matrix, got {s.ndim} modes")
+        if not np.isfinite(s).all():
+            raise ValueError("singular values must be finite")
+        if s.size and s.min() < 0:
+            raise ValueError("singular values must be non-negative")
+        r, n = s.shape
+        if s.size == 0:
+            return ThresholdResult(np.zeros(0), np.zeros(0), 0, 0.0,
+                                   np.zeros(n, dtype=np.int64), 0.0, 0.0)
+        dev = nat.require_cuda()
+        flat = torch.from_numpy(np.asfortranarray(s).reshape(-1, order="F").copy()).to(dev)
+    ranks, scal, j, v, w = threshold_device(flat, r, n, epsilon, want_vw=True)
+    sc = scal.cpu().numpy()
+    jj = int(j.cpu().numpy()[0])
+    if on_device:
+        return ThresholdResult(v, w, jj, float(sc[0]), ranks, float(sc[1]), float(sc[2]))
+    return ThresholdResult(v.cpu().numpy(), w.cpu().numpy(), jj, float(sc[0]),
+                           ranks.cpu().numpy(), float(sc[1]), float(sc[2]))
+
+
+@dataclass
+class TSVDMResult:
+    """Untruncated factorisation (tsvdm.py:118-130)."""
+
+    factors: SliceSVDSet
+    transforms: TransformSet
+    dims: tuple
+
+    def reconstruct(self, threads=1, ttm_variant=BATCHED):
+        import torch
+        f = self.factors
+        host = isinstance(f.u, DenseTensor)
+        dev = nat.require_cuda()
+        m, p = self.dims[0], self.dims[1]
+        n = prod(self.dims[2:])
+        r = min(m, p)
+        if host:
+            s = torch.from_numpy(np.asfortranarray(f.s).reshape(-1, order="F").copy()).to(dev)
+            u = as_device(f.u, dev).data
+            v = as_device(f.v, dev).data
+        else:
+            s, u, v = f.s.T.contiguous().reshape(-1), f.u.data, f.v.data
+            dev = u.device
+        ranks = torch.full((n,), r, dtype=torch.int64, device=dev)
+        u_off, g_off = pack_offsets_device(ranks, m, p)
+        g = torch.empty(r * p * n, dtype=torch.float64, device=dev)
+        st = nat.stream_ptr(dev)
+        u_copy = torch.empty_like(u)  # pack writes U too; slice i's U block is already packed
+        nat.call("starm_pack_from_full_f64", s.data_ptr(), u.data_ptr(), v.data_ptr(), m, p, n,
+                 ranks.data_ptr(), u_off.data_ptr(), g_off.data_ptr(), u_copy.data_ptr(),
+                 g.data_ptr(), st)
+        chat = DeviceTensor.empty(self.dims, dev)
+        nat.call("starm_unpack_facewise_f64", u.data_ptr(), g.data_ptr(), ranks.data_ptr(),
+                 u_off.data_ptr(), g_off.data_ptr(), m, p, n, chat.data.data_ptr(), st)
+        out = inverse_device(chat, self.transforms)
+        return out.to_host() if host else out
+
+
+@dataclass
+class CompressedTensor:
+    """Packed variable-rank factors + transforms + shape (tsvdm.py:132-182).
+    ``factors`` is a VariableRankFactors (host) or DeviceFactors (HBM)."""
+
+    dims: tuple
+    transforms: TransformSet
+    factors: object
+    method: str
+    param: float
+    discarded_energy: float | None = None
+    total_energy: float | None = None
+
+    def __post_init__(self):
+        self.dims = tuple(int(n) for n in self.dims)
+        if len(self.dims) < 3:
+            raise ValueError("compressed tensors have at least three modes")
+        if self.method not in (METHOD_FIXED_RANK, METHOD_TOLERANCE):
+            raise ValueError(f"unknown method {self.method!r}")
+        self.transforms.check_dims(self.dims)
+        f = self.factors
+        if (f.slice_rows, f.slice_cols) != (self.dims[0], self.dims[1]):
+            raise ValueError(f"factor slices are {f.slice_rows}x{f.slice_cols}, "
+                             f"tensor slices are {self.dims[0]}x{self.dims[1]}")
+        if f.num_slices != prod(self.dims[2:]):
+            raise ValueError(f"{f.num_slices} factor slices for {prod(self.dims[2:])} tensor slices")
+        if self.method == METHOD_FIXED_RANK and isinstance(f, VariableRankFactors):
+            r = int(self.param)
+            if f.ranks.size and not (f.ranks == r).all():
+                raise ValueError("fixed-rank artifacts must have one uniform rank")
+
+    @property
+    def ranks(self) -> np.ndarray:
+        return self.factors.ranks
+
+    def relative_error(self):
+        if self.discarded_energy is None or self.total_energy is None:
+            return None
+        if self.total_energy == 0.0:
+            return 0.0
+        return math.sqrt(self.discarded_energy / self.total_energy)
+
+    def to_host(self) -> "CompressedTensor":
+        return CompressedTensor(self.dims, self.transforms, self.factors.to_host(), self.method,
+                                self.param, self.discarded_energy, self.total_energy)
+
+
+def _check_decomposable(t):
+    if len(t.dims) < 3:
+        raise ValueError("decompositions apply to tensors with at least three modes")
+
+
+def _check_threads(threads):
+    if int(threads) < 1:
+        raise ValueError(f"thread count must be positive, got {threads}")
+
+
+def _check_common(threads, svd_strategy, ttm_variant):
+    _check_threads(threads)
+    if svd_strategy not in STRATEGIES:
+        raise ValueError(f"unknown slice SVD strategy {svd_strategy!r}")
+    if ttm_variant not in VARIANTS:
+        raise ValueError(f"unknown ttm variant {ttm_variant!r}")
+
+
+def starm_product(a, b, ts: TransformSet, ttm_variant=BATCHED, threads=1):
+    """A *_M B (tsvdm.py:219-233): forward TTMs, facewise DMMA GEMM, inverse TTMs."""
+    _check_decomposable(a)
+    _check_threads(threads)
+    if ttm_variant not in VARIANTS:
+        raise ValueError(f"unknown ttm variant {ttm_variant!r}")
+    if len(a.dims) != len(b.dims) or tuple(a.dims[2:]) != tuple(b.dims[2:]):
+        raise ValueError(f"trailing dims differ: {a.dims} vs {b.dims}")
+    if a.dims[1] != b.dims[0]:
+        raise ValueError(f"slice shapes {a.dims[:2]} and {b.dims[:2]} do not chain")
+    ts.check_dims(a.dims)
+    host = isinstance(a, DenseTensor)
+    dev = nat.require_cuda() if host else a.device
+    ahat = forward_device(as_device(a, dev), ts)
+    bhat = forward_device(as_device(b, dev), ts)
+    m, p, cols = a.dims[0], a.dims[1], b.dims[1]
+    n = prod(a.dims[2:])
+    out_dims = (m, cols) + tuple(a.dims[2:])
+    chat = DeviceTensor.empty(out_dims, dev)
+    nat.call("starm_facewise_gemm_f64", ahat.data.data_ptr(), bhat.data.data_ptr(),
+             chat.data.data_ptr(), m, p, cols, n, nat.stream_ptr(dev))
+    out = inverse_device(chat, ts)
+    return out.to_host() if host else out
+
+
+def full_tsvdm(a, ts: TransformSet, threads=1, svd_strategy=SLICES_PARALLEL,
+               ttm_variant=BATCHED) -> TSVDMResult:
+    """Every transform-domain slice factored (tsvdm.py:236-243)."""
+    from .slice_svd import svd_all_slices
+    _check_decomposable(a)
+    _check_common(threads, svd_strategy, ttm_variant)
+    ts.check_dims(a.dims)
+    host = isinstance(a, DenseTensor)
+    dev = nat.require_cuda() if host else a.device
+    ahat = forward_device(as_device(a, dev), ts)
+    factors = svd_all_slices(ahat.to_host() if host else ahat)
+    return TSVDMResult(factors, ts, tuple(a.dims))
+
+
+def _finish(a, ts, factors, method, param, discarded, total, host):
+    if host:
+        factors = factors.to_host()
+    return CompressedTensor(tuple(a.dims), ts, factors, method, param, discarded, total)
+
+
+def tsvdm_fixed_rank(a, ts: TransformSet, rank, threads=1, svd_strategy=SLICES_PARALLEL,
+                     ttm_variant=BATCHED) -> CompressedTensor:
+    """Uniform rank per slice (tsvdm.py:246-265)."""
+    import torch
+    _check_decomposable(a)
+    ts.check_dims(a.dims)
+    m, p = a.dims[0], a.dims[1]
+    rank = int(rank)
+    if not 1 <= rank <= min(m, p):
+        raise ValueError(f"rank must lie in [1, {min(m, p)}], got {rank}")
+    _check_common(threads, svd_strategy, ttm_variant)
+    host = isinstance(a, DenseTensor)
+    dev = nat.require_cuda() if host else a.device
+    n = prod(a.dims[2:])
+    r = min(m, p)
+    ahat = forward_device(as_device(a, dev), ts)
+    ahat3 = DeviceTensor(ahat.data, (m, p, n))
+    ranks = torch.full((n,), rank, dtype=torch.int64, device=dev)
+    factors, s = svd_truncated_device(ahat3, ranks, rank * n, keep_values=True)
+    factors._host_ranks = np.full(n, rank, dtype=np.int64)
+    en = torch.empty(2, dtype=torch.float64, device=dev)
+    nat.call("starm_tail_energy_f64", s.data_ptr(), r, n, rank, en.data_ptr(), nat.stream_ptr(dev))
+    d, t = en.cpu().numpy()
+    return _finish(a, ts, factors, METHOD_FIXED_RANK, float(rank), float(d), float(t), host)
+
+
+def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, threads=1,
+                    svd_strategy=SLICES_PARALLEL, ttm_variant=BATCHED, clock=None):
+    """Global-threshold ranks (tsvdm.py:268-321).  All three strategies give
+    identical ranks and factors; on the device ``memory-efficient`` and
+    ``compute-efficient`` are the same two-pass schedule (the transform-domain
+    tensor already stays resident in HBM), ``truncate`` factors every slice
+    fully and packs from the full factors."""
+    import torch
+    _check_decomposable(a)
+    ts.check_dims(a.dims)
+    epsilon = float(epsilon)
+    if not 0.0 < epsilon < 1.0:
+        raise ValueError(f"tolerance must lie in (0, 1), got {epsilon}")
+    if strategy not in TOLERANCE_STRATEGIES:
+        raise ValueError(f"unknown tolerance strategy {strategy!r}")
+    _check_common(threads, svd_strategy, ttm_variant)
+    clock = clock if clock is not None else StageClock()
+    host = isinstance(a, DenseTensor)
+    dev = nat.require_cuda() if host else a.device
+    m, p = a.dims[0], a.dims[1]
+    n = prod(a.dims[2:])
+    r = min(m, p)
+    ahat = forward_device(as_device(a, dev), ts)
+    ahat3 = DeviceTensor(ahat.data, (m, p, n))
+    if strategy == TRUNCATE:
+        with clock.stage("stage1-svd"):
+            s, u, v = svd_full_device(ahat3)
+        with clock.stage("threshold"):
+            ranks, scal, j, _, _ = threshold_device(s, r, n, epsilon)
+            summary = _summary(ranks, scal)
+        clock.mark("stage2-svd")
+        with clock.stage("pack"):
+            total_rank = summary[3]
+            u_off, g_off = pack_offsets_device(ranks, m, p)
+            u_data = torch.empty(max(total_rank * m, 1), dtype=torch.float64, device=dev)
+            g_data = torch.empty(max(total_rank * p, 1), dtype=torch.float64, device=dev)
+            nat.call("starm_pack_from_full_f64", s.data_ptr(), u.data_ptr(), v.data_ptr(), m, p, n,
+                     ranks.data_ptr(), u_off.data_ptr(), g_off.data_ptr(), u_data.data_ptr(),
+                     g_data.data_ptr(), nat.stream_ptr(dev))
+            factors = DeviceFactors(m, p, ranks, u_off, g_off, u_data[: total_rank * m],
+                                    g_data[: total_rank * p], total_rank)
+    else:
+        with clock.stage("stage1-svd"):
+            s = svd_values_device(ahat3)
+        with clock.stage("threshold"):
+            ranks, scal, j, _, _ = threshold_device(s, r, n, epsilon)
+            summary = _summary(ranks, scal)
+        with clock.stage("stage2-svd"):
+            factors, _ = svd_truncated_device(ahat3, ranks, summary[3])
+        clock.mark("pack")
+    tau, discarded, total, _ = summary
+    return _finish(a, ts, factors, METHOD_TOLERANCE, epsilon, discarded, total, host)
+
+
+def _summary(ranks, scal):
+    """One small D2H: (tau, discarded, total, sum of ranks)."""
+    import torch
+    packed = torch.cat([scal, ranks.sum().reshape(1).to(torch.float64)])
+    h = packed.cpu().numpy()
+    return float(h[0]), float(h[1]), float(h[2]), int(h[3])
+
+
+def _device_factors(c: CompressedTensor, dev):
+    import torch
+    f = c.factors
+    if isinstance(f, DeviceFactors):
+        return f
+    ranks = torch.from_numpy(np.ascontiguousarray(f.ranks)).to(dev)
+    u_off, g_off = pack_offsets_device(ranks, f.slice_rows, f.slice_cols)
+    u = torch.from_numpy(f.u_data).to(dev) if f.u_data.size else torch.empty(1, dtype=torch.float64, device=dev)
+    g = torch.from_numpy(f.g_data).to(dev) if f.g_data.size else torch.empty(1, dtype=torch.float64, device=dev)
+    return DeviceFactors(f.slice_rows, f.slice_cols, ranks, u_off, g_off, u, g, f.total_rank)
+
+
+def reconstruct_device(c: CompressedTensor, dev=None) -> DeviceTensor:
+    f = c.factors
+    if dev is None:
+        dev = f.u_data.device if isinstance(f, DeviceFactors) else nat.require_cuda()
+    df = _device_factors(c, dev)
+    m, p = c.dims[0], c.dims[1]
+    n = prod(c.dims[2:])
+    chat = DeviceTensor.empty(c.dims, dev)
+    nat.call("starm_unpack_facewise_f64", df.u_data.data_ptr(), df.g_data.data_ptr(),
+             df.ranks_dev.data_ptr(), df.u_off.data_ptr(), df.g_off.data_ptr(), m, p, n,
+             chat.data.data_ptr(), nat.stream_ptr(dev))
+    return inverse_device(chat, c.transforms)
+
+
+def reconstruct(c: CompressedTensor, threads=1, ttm_variant=BATCHED):
+    """Dense tensor from packed factors (tsvdm.py:342-357)."""
+    _check_threads(threads)
+    if ttm_variant not in VARIANTS:
+        raise ValueError(f"unknown ttm variant {ttm_variant!r}")
+    out = reconstruct_device(c)
+    return out if isinstance(c.factors, DeviceFactors) else out.to_host()
+
+
+def relative_error_device(a: DeviceTensor, b: DeviceTensor) -> float:
+    """||a - b|| / ||a|| with the K10 deterministic reduction."""
+    import torch
+    dev = a.device
+    lib = nat.load()
+    nbytes = lib.starm_error_sums_workspace_bytes(a.size)
+    ws = nat.workspace(nbytes, dev)
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    nat.call("starm_error_sums_f64", a.data.data_ptr(), b.data.data_ptr(), a.size, out.data_ptr(),
+             ws.data_ptr(), nbytes, nat.stream_ptr(dev))
+    d2, a2 = out.cpu().numpy()
+    return math.sqrt(d2 / a2) if a2 > 0 else 0.0
+
+
+def compression_ratio(c: CompressedTensor) -> float:
+    """Original entries / stored entries (tsvdm.py:360-372)."""
+    m, p = c.dims[0], c.dims[1]
+    stored = c.factors.total_rank * (m + p)
+    stored += sum(t.size ** 2 for t in c.transforms if t.kind in (DATA_DRIVEN, CUSTOM))
+    if stored == 0:
+        return math.inf
+    return prod(c.dims) / stored

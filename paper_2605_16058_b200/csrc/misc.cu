@@ -1,0 +1,298 @@
+// K8 packed offsets, K9 facewise reconstruction, K10 error sums, and the
+// C-ABI error plumbing.
+#include <string.h>
+
+#include <string>
+
+#include "common.cuh"
+
+namespace starm {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+namespace {
+
+// ---------------------------------------------------------------- offsets
+// slicesvd.py:208-211 -- exclusive scans of ranks*m and ranks*p, one CTA.
+__global__ void __launch_bounds__(1024) offsets_kernel(const int64_t* ranks, int64_t N, int64_t m,
+                                                       int64_t p, int64_t* u_off, int64_t* g_off) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t chunk = (N + 1023) / 1024;
+  const int64_t lo = t * chunk;
+  const int64_t hi = lo + chunk < N ? lo + chunk : N;
+  int64_t local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += ranks[i];
+  part[t] = local;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int64_t x = part[i];
+      part[i] = acc;
+      acc += x;
+    }
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  if (t == 0) {
+    u_off[0] = 0;
+    g_off[0] = 0;
+  }
+  for (int64_t i = lo; i < hi; ++i) {
+    acc += ranks[i];
+    u_off[i + 1] = acc * m;
+    g_off[i + 1] = acc * p;
+  }
+}
+
+// ------------------------------------------------- facewise U_i G_i tiles
+// chat_i (m x p) = U_i (m x k) * G_i (k x p), k = ranks[i] (0 -> zeros).
+constexpr int RT = 64, KC = 16;
+
+__global__ void __launch_bounds__(256) unpack_kernel(const double* u_data, const double* g_data,
+                                                     const int64_t* ranks, const int64_t* u_off,
+                                                     const int64_t* g_off, int64_t m, int64_t p,
+                                                     int64_t tiles_m, int64_t tiles_p,
+                                                     double* chat) {
+  __shared__ double us[KC][RT];
+  __shared__ double gs[KC][RT + 1];
+  const int64_t per_slice = tiles_m * tiles_p;
+  const int64_t slice = blockIdx.x / per_slice;
+  const int64_t tile = blockIdx.x % per_slice;
+  const int64_t m0 = (tile % tiles_m) * RT, p0 = (tile / tiles_m) * RT;
+  const int64_t k = ranks[slice];
+  const double* U = u_data + u_off[slice];
+  const double* G = g_data + g_off[slice];
+  double* C = chat + slice * m * p;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t k0 = 0; k0 < k; k0 += KC) {
+    for (int e = threadIdx.x; e < KC * RT; e += 256) {
+      const int kk = e / RT, rr = e % RT;
+      const int64_t row = m0 + rr, kx = k0 + kk;
+      us[kk][rr] = (row < m && kx < k) ? U[row + kx * m] : 0.0;
+      const int cc = e / KC, k2 = e % KC;
+      const int64_t col = p0 + cc, ky = k0 + k2;
+      gs[k2][cc] = (col < p && ky < k) ? G[ky + col * k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = us[kk][tx * 4 + q];
+        b[q] = gs[kk][ty * 4 + q];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const int64_t col = p0 + ty * 4 + y;
+    if (col >= p) continue;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int64_t row = m0 + tx * 4 + x;
+      if (row < m) C[row + col * m] = acc[x][y];
+    }
+  }
+}
+
+// ------------------------------------------------------------- error sums
+constexpr int ES_THREADS = 256, ES_BLOCKS = 148 * 4;
+
+__global__ void __launch_bounds__(ES_THREADS) err_partial_kernel(const double* a, const double* b,
+                                                                 int64_t count, double* part) {
+  __shared__ double red[2][ES_THREADS / 32];
+  double d2 = 0.0, a2 = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(ES_THREADS) + threadIdx.x; i < count;
+       i += int64_t(ES_BLOCKS) * ES_THREADS) {
+    const double x = a[i], y = b[i];
+    const double d = x - y;
+    d2 = fma(d, d, d2);
+    a2 = fma(x, x, a2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[0][warp] = d2;
+    red[1][warp] = a2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < ES_THREADS / 32; ++w) {
+      s0 += red[0][w];
+      s1 += red[1][w];
+    }
+    part[2 * blockIdx.x] = s0;
+    part[2 * blockIdx.x + 1] = s1;
+  }
+}
+
+__global__ void err_final_kernel(const double* part, double* out2) {
+  if (threadIdx.x != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int b = 0; b < ES_BLOCKS; ++b) {
+    s0 += part[2 * b];
+    s1 += part[2 * b + 1];
+  }
+  out2[0] = s0;
+  out2[1] = s1;
+}
+
+
+// ------------------------------------------------------- pack from full
+__global__ void pack_full_kernel(const double* s, const double* u, const double* v, int64_t m,
+                                 int64_t p, int64_t r, const int64_t* ranks, const int64_t* u_off,
+                                 const int64_t* g_off, double* u_data, double* g_data) {
+  const int64_t i = blockIdx.x;
+  const int64_t k = ranks[i];
+  if (k == 0) return;
+  const double* ui = u + i * m * r;
+  const double* vi = v + i * p * r;
+  const double* si = s + i * r;
+  double* ud = u_data + u_off[i];
+  double* gd = g_data + g_off[i];
+  for (int64_t e = threadIdx.x; e < m * k; e += blockDim.x) ud[e] = ui[e];
+  for (int64_t e = threadIdx.x; e < k * p; e += blockDim.x) {
+    const int64_t j = e % k, c = e / k;
+    gd[e] = si[j] * vi[c + j * p];
+  }
+}
+
+__global__ void __launch_bounds__(256) tail_energy_kernel(const double* s, int64_t r, int64_t N,
+                                                          int64_t rank, double* out2) {
+  __shared__ double red[2][256];
+  double tail = 0.0, tot = 0.0;
+  for (int64_t e = threadIdx.x; e < r * N; e += 256) {
+    const double x = s[e];
+    const double sq = x * x;
+    tot += sq;
+    if (e % r >= rank) tail += sq;
+  }
+  red[0][threadIdx.x] = tail;
+  red[1][threadIdx.x] = tot;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + o];
+      red[1][threadIdx.x] += red[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = red[0][0];
+    out2[1] = red[1][0];
+  }
+}
+
+}  // namespace
+}  // namespace starm
+
+using namespace starm;
+
+extern "C" int starm_pack_from_full_f64(const double* s, const double* u, const double* v,
+                                        int64_t m, int64_t p, int64_t nslices,
+                                        const int64_t* ranks, const int64_t* u_off,
+                                        const int64_t* g_off, double* u_data, double* g_data,
+                                        void* stream) {
+  STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "pack_from_full: bad extents");
+  STARM_CHECK_ARG(s && u && v && ranks && u_off && g_off && u_data && g_data,
+                  "pack_from_full: null pointer");
+  STARM_CHECK_ARG(nslices < (int64_t(1) << 31), "pack_from_full: too many slices");
+  const int64_t r = m < p ? m : p;
+  pack_full_kernel<<<unsigned(nslices), 256, 0, as_stream(stream)>>>(s, u, v, m, p, r, ranks, u_off,
+                                                                     g_off, u_data, g_data);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" int starm_tail_energy_f64(const double* s, int64_t r, int64_t nslices, int64_t rank,
+                                     double* out2, void* stream) {
+  STARM_CHECK_ARG(r >= 1 && nslices >= 1 && rank >= 0, "tail_energy: bad extents");
+  STARM_CHECK_ARG(s && out2, "tail_energy: null pointer");
+  tail_energy_kernel<<<1, 256, 0, as_stream(stream)>>>(s, r, nslices, rank, out2);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" int starm_abi_version(void) { return STARM_ABI_VERSION; }
+
+extern "C" size_t starm_last_error(char* buf, size_t len) {
+  const std::string& e = g_last_error;
+  if (buf && len) {
+    const size_t n = e.size() < len - 1 ? e.size() : len - 1;
+    memcpy(buf, e.data(), n);
+    buf[n] = 0;
+  }
+  return e.size();
+}
+
+extern "C" int starm_pack_offsets(const int64_t* ranks, int64_t nslices, int64_t m, int64_t p,
+                                  int64_t* u_off, int64_t* g_off, void* stream) {
+  STARM_CHECK_ARG(nslices >= 0 && m >= 1 && p >= 1, "pack_offsets: bad extents");
+  STARM_CHECK_ARG(u_off && g_off && (ranks || nslices == 0), "pack_offsets: null pointer");
+  offsets_kernel<<<1, 1024, 0, as_stream(stream)>>>(ranks, nslices, m, p, u_off, g_off);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" int starm_unpack_facewise_f64(const double* u_data, const double* g_data,
+                                         const int64_t* ranks, const int64_t* u_off,
+                                         const int64_t* g_off, int64_t m, int64_t p,
+                                         int64_t nslices, double* chat, void* stream) {
+  STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "unpack: bad extents");
+  STARM_CHECK_ARG(ranks && u_off && g_off && chat, "unpack: null pointer");
+  const int64_t tm = ceil_div(m, RT), tp = ceil_div(p, RT);
+  const int64_t blocks = tm * tp * nslices;
+  STARM_CHECK_ARG(blocks < (int64_t(1) << 31), "unpack: grid too large");
+  unpack_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(u_data, g_data, ranks, u_off,
+                                                                 g_off, m, p, tm, tp, chat);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" size_t starm_error_sums_workspace_bytes(int64_t count) {
+  (void)count;
+  return size_t(2) * ES_BLOCKS * sizeof(double);
+}
+
+extern "C" int starm_error_sums_f64(const double* a, const double* b, int64_t count, double* out2,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(count >= 0, "error sums: bad count");
+  STARM_CHECK_ARG(a && b && out2 && ws, "error sums: null pointer");
+  STARM_CHECK_ARG(ws_bytes >= starm_error_sums_workspace_bytes(count), "error sums: workspace too small");
+  double* part = reinterpret_cast<double*>(ws);
+  cudaStream_t st = as_stream(stream);
+  err_partial_kernel<<<ES_BLOCKS, ES_THREADS, 0, st>>>(a, b, count, part);
+  STARM_LAUNCH_CHECK();
+  err_final_kernel<<<1, 32, 0, st>>>(part, out2);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}

@@ -1,0 +1,1157 @@
+// K3-K6: batched slice SVD -- QR-preconditioned blocked one-sided (Hestenes)
+// Jacobi, FP64.
+//
+// Replaces the per-slice LAPACK dgesvd loop of the reference
+// (slicesvd.py:42-62 `_slice_svd`, driven by svd_all_slices :115-136,
+// _values_pass :139-168 and svd_truncated_slices :259-292).
+//
+// Per slice (m x p, column-major) let X be the L x n working matrix
+// (L = max(m,p), n = min(m,p)):  X = A if m >= p, X = A^T otherwise.
+//
+//  1. (tall X, L >= 1.25 n) Householder QR  X = Q R  in a first kernel:
+//     16-column panels factored in shared memory, compact-WY trailing
+//     updates C -= V (T^T (V^T C)) on FP64 DMMA tiles.  The Jacobi target is
+//     then the n x n R (half the work per sweep for c2's 720 x 361 slices).
+//     Otherwise the target is X itself.
+//  2. Blocked one-sided Jacobi on the target T (columns in blocks of 16,
+//     one "pair step" = 32 columns):  Gram G = T_P^T T_P on DMMA (streamed
+//     64-row chunks, cp.async double buffering), skip if converged, one
+//     inner sweep of round-robin cyclic Jacobi on G in shared memory (16
+//     disjoint rotations per round) -> rotation W, T_P <- T_P W (and
+//     V_P <- V_P W when vectors are wanted), again on DMMA.
+//  3. sigma = column norms of T V (descending bitonic sort).  T V = U_T S so
+//     X V = Q U_T S: right singular vectors of X are V, left ones are the
+//     normalised columns of X V -- taken directly from T V (no QR) or
+//     recomputed as X * V_sel from the untouched input slice (QR path), then
+//     re-orthonormalised (CGS2) where sigma_j < 1e-4 sigma_max.
+// Because every rotation is applied to the data and every Gram is recomputed
+// from it, sigma are column norms of X V with V orthogonal to working
+// precision: backward error O(u ||A||) like dgesvd; the Gram only chooses
+// rotations.
+//
+// Scheduling: persistent grids (SMs x resident CTAs) pull slices from atomic
+// counters; workspace is per resident CTA (plus one n x n R per slice on the
+// QR path).
+#include <float.h>
+#include <limits.h>
+
+#include "common.cuh"
+
+namespace starm {
+namespace {
+
+constexpr int TPB = 256;
+constexpr int GW = 32;        // columns per pair step
+constexpr int BW = 16;        // columns per block / QR panel width
+constexpr int RCH = 64;       // rows per streamed chunk
+constexpr int XS = RCH + 4;   // chunk column stride (doubles)
+constexpr int GS = 33;        // Gram row stride
+constexpr int WS = 36;        // rotation column stride
+constexpr int MAX_NS = 4096;  // largest supported min(m, p) (sort buffer)
+constexpr int QR_MAX_LP = 1344;
+constexpr int ZS = 20;        // Z (16 x 32) column stride
+
+enum { ST_SLICES = 0, ST_SWEEPS, ST_PAIRS, ST_ROTATED, ST_CYC_GRAM, ST_CYC_EIG, ST_CYC_APPLY,
+       ST_CYC_QR, ST_CYC_FINAL, ST_CYC_LOAD, ST_COUNT };
+
+__device__ unsigned long long g_stats[16];
+
+struct SvdParams {
+  const double* A;
+  int64_t m, p, N;
+  const int64_t* ids;
+  int64_t count;
+  int job;
+  double* s;
+  double* u;
+  double* v;
+  const int64_t* ranks;
+  const int64_t* u_off;
+  const int64_t* g_off;
+  double* u_data;
+  double* g_data;
+  int32_t* status;
+  unsigned long long* counter;  // [0] qr kernel, [1] jacobi kernel
+  double* xslots;               // per-CTA X (LP x NP)
+  double* wslots;               // per-CTA V (RP x NP), vector jobs
+  double* rbuf;                 // per-slice R (RP x NP), QR path
+  int32_t* flags;               // per-slice load flags, QR path
+  int64_t L, n, LP, NP, RP;
+  int transposed, use_qr, stats;
+  double tol;
+  int max_sweeps, max_inner;
+};
+
+struct __align__(16) JacobiSmem {
+  double xs[2][GW * XS];
+  double g[2][GW * GS];
+  double w[2][GW * WS];
+  double cd[GW];
+  double co[GW];
+  double nd[GW];
+  int partner[GW];
+  int flag[4];
+};
+
+// Finalize scratch lives after JacobiSmem (sized by NS = next_pow2(n)), so
+// the sort keys survive while the Jacobi staging buffers are reused.
+struct FinalView {
+  double* key;
+  int* idx;
+  double* dots;
+  double* red;
+};
+
+__device__ __forceinline__ FinalView final_view(unsigned char* base, int ns) {
+  FinalView f;
+  f.key = reinterpret_cast<double*>(base + sizeof(JacobiSmem));
+  f.dots = f.key + ns;
+  f.red = f.dots + TPB;
+  f.idx = reinterpret_cast<int*>(f.red + TPB / 32);
+  return f;
+}
+
+size_t jacobi_smem_bytes(int ns) {
+  return sizeof(JacobiSmem) + size_t(ns) * (sizeof(double) + sizeof(int)) +
+         (TPB + TPB / 32) * sizeof(double);
+}
+
+struct __align__(16) QrSmemFixed {
+  double cbuf[2][GW * XS];
+  double t[BW * 17];
+  double sg[2][BW * 17];
+  double y[BW * GS];
+  double z[GW * ZS];
+  double red[TPB / 32][BW];
+  double sums[BW];
+  double wv[BW];
+  double tau[BW];
+  double scal[4];
+};
+
+__device__ __forceinline__ void stat_add(const SvdParams& P, int k, unsigned long long v) {
+  if (P.stats && threadIdx.x == 0) atomicAdd(&g_stats[k], v);
+}
+
+__device__ __forceinline__ int64_t gcol(int k, int I, int J) {
+  return k < BW ? int64_t(I) * BW + k : int64_t(J) * BW + (k - BW);
+}
+
+// Stage rows [r0, r0+RCH) of the 32 pair columns (blocks I, J) of M into buf.
+__device__ __forceinline__ void stage_pair(double* buf, const double* M, int64_t ld, int64_t r0,
+                                           int I, int J) {
+#pragma unroll
+  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
+    const int c = threadIdx.x + q * TPB;
+    const int col = c >> 5;
+    const int r2 = (c & 31) * 2;
+    cp_async16(buf + col * XS + r2, M + r0 + r2 + gcol(col, I, J) * ld);
+  }
+  cp_async_commit();
+}
+
+// Stage rows [r0, r0+RCH) of 32 contiguous columns col0.. (zero past ncols).
+__device__ __forceinline__ void stage_cols(double* buf, const double* M, int64_t ld, int64_t r0,
+                                           int64_t col0, int64_t ncols) {
+#pragma unroll
+  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
+    const int c = threadIdx.x + q * TPB;
+    const int col = c >> 5;
+    const int r2 = (c & 31) * 2;
+    const bool in = col0 + col < ncols;
+    cp_async16(buf + col * XS + r2, in ? M + r0 + r2 + (col0 + col) * ld : M, in ? 16 : 0);
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void store_cols(double* M, int64_t ld, int64_t r0, int64_t col0,
+                                           int64_t ncols, const double* buf) {
+#pragma unroll
+  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
+    const int c = threadIdx.x + q * TPB;
+    const int col = c >> 5;
+    const int r2 = (c & 31) * 2;
+    if (col0 + col < ncols)
+      *reinterpret_cast<double2*>(M + r0 + r2 + (col0 + col) * ld) =
+          *reinterpret_cast<const double2*>(buf + col * XS + r2);
+  }
+}
+
+// ======================================================================
+//                               Jacobi core
+// ======================================================================
+
+// G = T_P^T T_P over `rows` rows (multiple of RCH).  Result in g (row-major, GS).
+__device__ void gram_pair(JacobiSmem& sm, const double* T, int64_t ld, int64_t rows, int I, int J,
+                          double* g) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+  const int64_t nch = rows / RCH;
+  stage_pair(sm.xs[0], T, ld, 0, I, J);
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage_pair(sm.xs[(ch + 1) & 1], T, ld, (ch + 1) * RCH, I, J);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* xs = sm.xs[ch & 1];
+    const double* xa = xs + (ti * 8 + gq) * XS + tq;
+    const double* xb = xs + (tj0 * 8 + gq) * XS + tq;
+#pragma unroll
+    for (int k4 = 0; k4 < RCH / 4; ++k4) {
+      const double a = xa[k4 * 4];
+      dmma884(a00, a01, a, xb[k4 * 4]);
+      dmma884(a10, a11, a, xb[8 * XS + k4 * 4]);
+    }
+    __syncthreads();
+  }
+  const int row = ti * 8 + gq;
+  g[row * GS + tj0 * 8 + 2 * tq] = a00;
+  g[row * GS + tj0 * 8 + 2 * tq + 1] = a01;
+  g[row * GS + (tj0 + 1) * 8 + 2 * tq] = a10;
+  g[row * GS + (tj0 + 1) * 8 + 2 * tq + 1] = a11;
+  __syncthreads();
+}
+
+// M_P <- M_P * W over `rows` rows (W column-major, stride WS).
+__device__ void apply_pair(JacobiSmem& sm, double* M, int64_t ld, int64_t rows, int I, int J,
+                           const double* w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t nch = rows / RCH;
+  stage_pair(sm.xs[0], M, ld, 0, I, J);
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage_pair(sm.xs[(ch + 1) & 1], M, ld, (ch + 1) * RCH, I, J);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double* xs = sm.xs[ch & 1];
+    double acc[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+    const double* xa = xs + tq * XS + warp * 8 + gq;
+    const double* wb = w + gq * WS + tq;
+#pragma unroll
+    for (int k4 = 0; k4 < GW / 4; ++k4) {
+      const double a = xa[k4 * 4 * XS];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dmma884(acc[c][0], acc[c][1], a, wb[c * 8 * WS + k4 * 4]);
+    }
+    // Each warp reads and writes only its own 8 rows: in-place is safe.
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      xs[(c * 8 + 2 * tq) * XS + warp * 8 + gq] = acc[c][0];
+      xs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] = acc[c][1];
+    }
+    __syncthreads();
+    const int64_t r0 = ch * RCH;
+#pragma unroll
+    for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
+      const int c = threadIdx.x + q * TPB;
+      const int col = c >> 5;
+      const int r2 = (c & 31) * 2;
+      *reinterpret_cast<double2*>(M + r0 + r2 + gcol(col, I, J) * ld) =
+          *reinterpret_cast<const double2*>(xs + col * XS + r2);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int rr_pos(int i, int round) {
+  return i == 0 ? 0 : ((i - 1 + round) % (GW - 1)) + 1;
+}
+
+// Rotation W of the 32x32 Gram in sm.g[0] (cyclic round-robin Jacobi,
+// `max_inner` sweeps).  Returns the sm.w buffer index holding W.
+__device__ int eig_pair(JacobiSmem& sm, double tol, int max_inner) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < GW * GW; e += TPB) {
+    const int j = e >> 5, r = e & 31;
+    sm.w[0][j * WS + r] = (j == r) ? 1.0 : 0.0;
+  }
+  int gb = 0, wb = 0;
+  for (int sweep = 0; sweep < max_inner; ++sweep) {
+    if (tid == 0) sm.flag[1] = 0;
+    __syncthreads();
+    for (int round = 0; round < GW - 1; ++round) {
+      const double* G = sm.g[gb];
+      if (tid < GW / 2) {
+        const int p = rr_pos(tid, round), q = rr_pos(GW - 1 - tid, round);
+        const double a = G[p * GS + p], d = G[q * GS + q], b = G[p * GS + q];
+        double c = 1.0, s = 0.0, npp = a, nqq = d;
+        if (a > 0.0 && d > 0.0 && fabs(b) > tol * sqrt(a * d)) {
+          const double zeta = (d - a) / (2.0 * b);
+          double t;
+          if (fabs(zeta) > 1e150) {
+            t = 0.5 / zeta;
+          } else {
+            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          }
+          c = rsqrt(1.0 + t * t);
+          s = t * c;
+          npp = a - t * b;
+          nqq = d + t * b;
+          sm.flag[1] = 1;
+        }
+        sm.cd[p] = c;
+        sm.cd[q] = c;
+        sm.co[p] = -s;
+        sm.co[q] = s;
+        sm.nd[p] = npp;
+        sm.nd[q] = nqq;
+        sm.partner[p] = q;
+        sm.partner[q] = p;
+      }
+      __syncthreads();
+      double* Gn = sm.g[gb ^ 1];
+      const double* W = sm.w[wb];
+      double* Wn = sm.w[wb ^ 1];
+      const int i = tid >> 3, j0 = tid & 7;
+      const double di = sm.cd[i], oi = sm.co[i];
+      const int pi = sm.partner[i];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j0 + 8 * jj;
+        const int pj = sm.partner[j];
+        const double dj = sm.cd[j], oj = sm.co[j];
+        double val;
+        if (j == i) {
+          val = sm.nd[i];
+        } else if (j == pi) {
+          val = 0.0;
+        } else {
+          val = di * (dj * G[i * GS + j] + oj * G[i * GS + pj]) +
+                oi * (dj * G[pi * GS + j] + oj * G[pi * GS + pj]);
+        }
+        Gn[i * GS + j] = val;
+        Wn[j * WS + i] = dj * W[j * WS + i] + oj * W[pj * WS + i];
+      }
+      __syncthreads();
+      gb ^= 1;
+      wb ^= 1;
+    }
+    const int any = sm.flag[1];
+    __syncthreads();
+    if (!any) break;
+  }
+  return wb;
+}
+
+__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < TPB / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+// Orthonormalise column cols[j] of Q (ld, length len) against cols[0..j-1]
+// (Gram-Schmidt twice, 8 columns per block pass); a vanished column is
+// replaced by the next canonical basis vector orthogonalised likewise.
+__device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, const int* cols, int j) {
+  int64_t basis = 0;
+  double* qj = Q + int64_t(cols ? cols[j] : j) * ld;
+  for (int attempt = 0; attempt < 4 + j; ++attempt) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i0 = 0; i0 < j; i0 += TPB / 32) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int i = i0 + warp;
+        double d = 0.0;
+        if (i < j) {
+          const double* qi = Q + int64_t(cols ? cols[i] : i) * ld;
+          for (int64_t r = lane; r < len; r += 32) d += qi[r] * qj[r];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0) fs.dots[warp] = d;
+        __syncthreads();
+        const int cnt = min(TPB / 32, j - i0);
+        for (int64_t r = threadIdx.x; r < len; r += TPB) {
+          double x = qj[r];
+          for (int q = 0; q < cnt; ++q) x -= fs.dots[q] * Q[r + int64_t(cols ? cols[i0 + q] : i0 + q) * ld];
+          qj[r] = x;
+        }
+        __syncthreads();
+      }
+    }
+    double nrm2 = 0.0;
+    for (int64_t r = threadIdx.x; r < len; r += TPB) nrm2 += qj[r] * qj[r];
+    nrm2 = block_sum(nrm2, fs.red);
+    const double nrm = sqrt(nrm2);
+    if (nrm > 0.5) {
+      const double inv = 1.0 / nrm;
+      for (int64_t r = threadIdx.x; r < len; r += TPB) qj[r] *= inv;
+      __syncthreads();
+      return;
+    }
+    for (int64_t r = threadIdx.x; r < len; r += TPB) qj[r] = (r == basis) ? 1.0 : 0.0;
+    ++basis;
+    __syncthreads();
+  }
+}
+
+// Copy slice into X (LP x NP, ld LP), transposing when m < p; zero padding.
+// Returns flag: 0 ok, 1 all-zero, 2 non-finite.
+__device__ int load_slice(const SvdParams& P, const double* A, double* X, double* tile) {
+  const int tid = threadIdx.x;
+  const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP;
+  int bad = 0, nonzero = 0;
+  if (!P.transposed) {
+    for (int64_t c = 0; c < NP; ++c) {
+      for (int64_t r = tid; r < LP; r += TPB) {
+        double x = 0.0;
+        if (r < L && c < n) {
+          x = A[r + c * P.m];
+          bad |= !isfinite(x);
+          nonzero |= (x != 0.0);
+        }
+        X[r + c * LP] = x;
+      }
+    }
+  } else {
+    for (int64_t c0 = 0; c0 < NP; c0 += 32) {
+      for (int64_t r0 = 0; r0 < LP; r0 += 32) {
+        for (int e = tid; e < 1024; e += TPB) {
+          const int cc = e & 31, rr = e >> 5;
+          const int64_t c = c0 + cc, r = r0 + rr;
+          double x = 0.0;
+          if (r < L && c < n) {
+            x = A[c + r * P.m];
+            bad |= !isfinite(x);
+            nonzero |= (x != 0.0);
+          }
+          tile[rr * 33 + cc] = x;
+        }
+        __syncthreads();
+        for (int e = tid; e < 1024; e += TPB) {
+          const int rr = e & 31, cc = e >> 5;
+          const int64_t c = c0 + cc, r = r0 + rr;
+          if (c < NP) X[r + c * LP] = tile[rr * 33 + cc];
+        }
+        __syncthreads();
+      }
+    }
+  }
+  bad = __syncthreads_or(bad);
+  nonzero = __syncthreads_or(nonzero);
+  return bad ? 2 : (nonzero ? 0 : 1);
+}
+
+// ======================================================================
+//                      Householder QR kernel (tall X)
+// ======================================================================
+
+__device__ __forceinline__ double& PAN(double* pan, int64_t prs, int c, int64_t r) {
+  return pan[c * prs + r];
+}
+
+// Unblocked Householder on panel columns [0,16) of pan (rows k0.., ld prs).
+// Leaves R (upper) in rows <= k0+j and v below; tau in q.tau.
+__device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t LP) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int j = 0; j < BW; ++j) {
+    const int64_t pr = k0 + j;
+    double acc[BW];
+#pragma unroll
+    for (int c = 0; c < BW; ++c) acc[c] = 0.0;
+    for (int64_t r = pr + 1 + tid; r < LP; r += TPB) {
+      const double x = PAN(pan, prs, j, r);
+      acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+      for (int c = 1; c < BW; ++c)
+        if (c > j) acc[c] = fma(x, PAN(pan, prs, c, r), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < BW; ++c) {
+      double v = acc[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) q.red[warp][c] = v;
+    }
+    __syncthreads();
+    if (tid < BW) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < TPB / 32; ++w) s += q.red[w][tid];
+      q.sums[tid] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double alpha = PAN(pan, prs, j, pr);
+      const double xn2 = q.sums[0];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      q.tau[j] = tau;
+      q.scal[0] = scal;
+      q.scal[1] = beta;
+      for (int c = j + 1; c < BW; ++c) q.wv[c] = PAN(pan, prs, c, pr) + scal * q.sums[c];
+    }
+    __syncthreads();
+    const double tau = q.tau[j], scal = q.scal[0], beta = q.scal[1];
+    if (tau != 0.0) {
+      for (int64_t r = pr + tid; r < LP; r += TPB) {
+        const double x = PAN(pan, prs, j, r);
+        const double vr = (r == pr) ? 1.0 : x * scal;
+        for (int c = j + 1; c < BW; ++c) PAN(pan, prs, c, r) -= tau * vr * q.wv[c];
+        PAN(pan, prs, j, r) = (r == pr) ? beta : vr;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// S = V^T V (16x16) on DMMA; V = explicit panel (zeros above, 1 on pivots).
+__device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64_t kc, int64_t LP) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int tile = warp & 3, half = warp >> 2;
+  const int ti = tile >> 1, tj = tile & 1;
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t r0 = kc + half * 4; r0 < LP; r0 += 8) {
+    const double a = pan[(ti * 8 + gq) * prs + r0 + tq];
+    const double b = pan[(tj * 8 + gq) * prs + r0 + tq];
+    dmma884(d0, d1, a, b);
+  }
+  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq] = d0;
+  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq + 1] = d1;
+  __syncthreads();
+  // T (forward, columnwise; LAPACK dlarft): T_jj = tau_j,
+  // T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] S[l][j]   (thread i owns row i)
+  const int i = threadIdx.x;
+  if (i < BW) {
+    for (int j = 0; j < BW; ++j) q.t[i * 17 + j] = 0.0;
+    q.t[i * 17 + i] = q.tau[i];
+    for (int j = i + 1; j < BW; ++j) {
+      double acc = 0.0;
+      for (int l = i; l < j; ++l) acc += q.t[i * 17 + l] * (q.sg[0][l * 17 + j] + q.sg[1][l * 17 + j]);
+      q.t[i * 17 + j] = -q.tau[j] * acc;
+    }
+  }
+  __syncthreads();
+}
+
+// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld LP, NP columns), rows kc..LP.
+__device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, double* X,
+                                int64_t LP, int64_t NP, int64_t kc, int64_t c0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t nch = (LP - kc) / RCH;
+  // ---- Y = V^T C (16 x 32): warp -> tile (ti = warp>>2, tj = warp&3)
+  {
+    const int ti = warp >> 2, tj = warp & 3;
+    double y0 = 0.0, y1 = 0.0;
+    stage_cols(q.cbuf[0], X, LP, kc, c0, NP);
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        stage_cols(q.cbuf[(ch + 1) & 1], X, LP, kc + (ch + 1) * RCH, c0, NP);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* cs = q.cbuf[ch & 1];
+      const int64_t r0 = kc + ch * RCH;
+      const double* va = pan + (ti * 8 + gq) * prs + r0 + tq;
+      const double* cb = cs + (tj * 8 + gq) * XS + tq;
+#pragma unroll
+      for (int k4 = 0; k4 < RCH / 4; ++k4) dmma884(y0, y1, va[k4 * 4], cb[k4 * 4]);
+      __syncthreads();
+    }
+    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq] = y0;
+    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq + 1] = y1;
+  }
+  __syncthreads();
+  // ---- Z = T^T Y (16 x 32), stored column-major (stride ZS) for B fragments
+  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
+    const int i = e & 15, c = e >> 4;
+    double acc = 0.0;
+    for (int l = 0; l <= i; ++l) acc += q.t[l * 17 + i] * q.y[l * GS + c];
+    q.z[c * ZS + i] = acc;
+  }
+  __syncthreads();
+  // ---- C -= V Z, streamed again
+  stage_cols(q.cbuf[0], X, LP, kc, c0, NP);
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage_cols(q.cbuf[(ch + 1) & 1], X, LP, kc + (ch + 1) * RCH, c0, NP);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double* cs = q.cbuf[ch & 1];
+    const int64_t r0 = kc + ch * RCH;
+    double acc[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < BW / 4; ++k4) {
+      const double a = pan[(k4 * 4 + tq) * prs + r0 + warp * 8 + gq];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        dmma884(acc[c][0], acc[c][1], a, q.z[(c * 8 + gq) * ZS + k4 * 4 + tq]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cs[(c * 8 + 2 * tq) * XS + warp * 8 + gq] -= acc[c][0];
+      cs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] -= acc[c][1];
+    }
+    __syncthreads();
+    store_cols(X, LP, r0, c0, NP, cs);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(TPB) svd_qr_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
+  const int64_t prs = P.LP + 4;
+  double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
+  __shared__ int64_t cur;
+  const int tid = threadIdx.x;
+  const int64_t LP = P.LP, NP = P.NP, RP = P.RP;
+  double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
+
+  for (;;) {
+    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[0], 1ull));
+    __syncthreads();
+    const int64_t it = cur;
+    __syncthreads();
+    if (it >= P.count) break;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    long long t0 = clock64();
+    const int flag = load_slice(P, P.A + slice * P.m * P.p, X, q.cbuf[0]);
+    if (tid == 0) P.flags[it] = flag;
+    if (flag) continue;
+    long long t1 = clock64();
+    for (int64_t k0 = 0; k0 < NP; k0 += BW) {
+      const int64_t kc = (k0 / RCH) * RCH;
+      // panel -> shared memory (all LP rows of the 16 columns)
+      for (int64_t e = tid; e < BW * LP; e += TPB) {
+        const int c = int(e / LP);
+        const int64_t r = e % LP;
+        pan[c * prs + r] = X[r + (k0 + c) * LP];
+      }
+      __syncthreads();
+      panel_factor(q, pan, prs, k0, LP);
+      // R part back to global (rows k0..k0+c of panel column c), then make V explicit
+      for (int64_t e = tid; e < BW * BW; e += TPB) {
+        const int c = int(e / BW), r = int(e % BW);
+        if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+      }
+      __syncthreads();
+      for (int64_t e = tid; e < BW * LP; e += TPB) {
+        const int c = int(e / LP);
+        const int64_t r = e % LP;
+        if (r < k0 + c) pan[c * prs + r] = 0.0;
+        else if (r == k0 + c) pan[c * prs + r] = 1.0;
+      }
+      __syncthreads();
+      if (k0 + BW < NP) {
+        panel_gram(q, pan, prs, kc, LP);
+        for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW) trailing_update(q, pan, prs, X, LP, NP, kc, c0);
+      }
+      __syncthreads();
+    }
+    // R -> per-slice buffer (RP x NP), zero below the diagonal and in padding rows
+    double* R = P.rbuf + it * RP * NP;
+    for (int64_t c = 0; c < NP; ++c)
+      for (int64_t r = tid; r < RP; r += TPB) R[r + c * RP] = (r <= c && r < NP) ? X[r + c * LP] : 0.0;
+    __syncthreads();
+    long long t2 = clock64();
+    stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
+    stat_add(P, ST_CYC_QR, (unsigned long long)(t2 - t1));
+  }
+}
+
+// ======================================================================
+//                     Jacobi + finalize kernel
+// ======================================================================
+
+// Qside (L x k, ld LP, columns 0..k-1) = X * V[:, idx[0..k)] from the
+// untouched slice (X = A or A^T), on DMMA.  Uses sm.xs / sm.w as staging.
+__device__ void gemm_xv(const SvdParams& P, JacobiSmem& sm, const double* A, const double* V,
+                        const int* idx, int64_t k, double* Q) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP, RP = P.RP;
+  for (int64_t kb = 0; kb < k; kb += GW) {
+    for (int64_t r0 = 0; r0 < LP; r0 += RCH) {
+      double acc[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+      for (int64_t kk = 0; kk < NP; kk += GW) {
+        double* xs = sm.xs[0];
+        double* wt = sm.w[0];
+        // X tile: rows r0..r0+63, cols kk..kk+31 -> xs[col*XS + row]
+        for (int e = tid; e < GW * RCH; e += TPB) {
+          int col, row;
+          if (P.transposed) { col = e & 31; row = e >> 5; }   // consecutive col -> contiguous A
+          else { row = e & 63; col = e >> 6; }                // consecutive row -> contiguous A
+          const int64_t r = r0 + row, c = kk + col;
+          double x = 0.0;
+          if (r < L && c < n) x = P.transposed ? A[c + r * P.m] : A[r + c * P.m];
+          xs[col * XS + row] = x;
+        }
+        // W tile: W[kk+i][idx[kb+j]] -> wt[j*WS + i]
+        for (int e = tid; e < GW * GW; e += TPB) {
+          const int i = e & 31, j = e >> 5;
+          const int64_t jj = kb + j;
+          wt[j * WS + i] = (jj < k) ? V[(kk + i) + int64_t(idx[jj]) * RP] : 0.0;
+        }
+        __syncthreads();
+        const double* xa = xs + tq * XS + warp * 8 + gq;
+        const double* wb = wt + gq * WS + tq;
+#pragma unroll
+        for (int k4 = 0; k4 < GW / 4; ++k4) {
+          const double a = xa[k4 * 4 * XS];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dmma884(acc[c][0], acc[c][1], a, wb[c * 8 * WS + k4 * 4]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = kb + c * 8 + 2 * tq + e;
+          const int64_t row = r0 + warp * 8 + gq;
+          if (col < k && row < L) Q[row + col * LP] = acc[c][e];
+        }
+    }
+  }
+  __syncthreads();
+}
+
+template <bool WANTV>
+__global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  JacobiSmem& sm = *reinterpret_cast<JacobiSmem*>(smem_raw);
+  int NS = 1;
+  while (NS < P.n) NS <<= 1;
+  FinalView fs = final_view(smem_raw, NS);
+  __shared__ int64_t cur;
+  const int tid = threadIdx.x;
+  const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP, RP = P.RP;
+  double* Xslot = P.xslots + int64_t(blockIdx.x) * LP * NP;
+  double* V = WANTV ? P.wslots + int64_t(blockIdx.x) * RP * NP : nullptr;
+  const int nb = int(NP / BW);
+
+  for (;;) {
+    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[1], 1ull));
+    __syncthreads();
+    const int64_t it = cur;
+    __syncthreads();
+    if (it >= P.count) break;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const double* A = P.A + slice * P.m * P.p;
+    long long t0 = clock64();
+
+    double* T;
+    int64_t ldt, rows;
+    int flag;
+    if (P.use_qr) {
+      flag = P.flags[it];
+      T = P.rbuf + it * RP * NP;
+      ldt = RP;
+      rows = RP;
+    } else {
+      flag = load_slice(P, A, Xslot, sm.xs[0]);
+      T = Xslot;
+      ldt = LP;
+      rows = LP;
+    }
+    if (flag == 2) {
+      if (tid == 0) atomicMin(&P.status[0], int32_t(slice));
+      __syncthreads();
+      continue;
+    }
+    const int64_t r = n;
+    if (flag == 1) {
+      // slicesvd.py:51-54: identity bases, zero values.
+      if (P.s)
+        for (int64_t j = tid; j < r; j += TPB) P.s[j + slice * r] = 0.0;
+      if (P.job == STARM_SVD_FULL) {
+        double* U = P.u + slice * P.m * r;
+        double* Vo = P.v + slice * P.p * r;
+        for (int64_t e = tid; e < P.m * r; e += TPB) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
+        for (int64_t e = tid; e < P.p * r; e += TPB) Vo[e] = ((e % P.p) == (e / P.p)) ? 1.0 : 0.0;
+      } else if (P.job == STARM_SVD_TRUNCATED) {
+        const int64_t k = P.ranks[slice];
+        double* U = P.u_data + P.u_off[slice];
+        double* G = P.g_data + P.g_off[slice];
+        for (int64_t e = tid; e < P.m * k; e += TPB) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
+        for (int64_t e = tid; e < k * P.p; e += TPB) G[e] = 0.0;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (WANTV) {
+      for (int64_t c = 0; c < NP; ++c)
+        for (int64_t rr = tid; rr < RP; rr += TPB) V[rr + c * RP] = (rr == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    unsigned long long cg = 0, ce = 0, ca = 0, npairs = 0, nrot = 0;
+
+    // ---- Jacobi sweeps over block pairs
+    int converged = 0, sweeps = 0;
+    for (int sweep = 0; sweep < P.max_sweeps && !converged; ++sweep) {
+      int rotated = 0;
+      ++sweeps;
+      for (int I = 0; I < nb - 1; ++I) {
+        for (int J = I + 1; J < nb; ++J) {
+          long long a0 = clock64();
+          gram_pair(sm, T, ldt, rows, I, J, sm.g[0]);
+          int need = 0;
+          const double* G = sm.g[0];
+          for (int e = tid; e < GW * GW; e += TPB) {
+            const int i = e >> 5, j = e & 31;
+            if (i < j) {
+              const double a = G[i * GS + i], d = G[j * GS + j];
+              if (a > 0.0 && d > 0.0 && fabs(G[i * GS + j]) > P.tol * sqrt(a * d)) need = 1;
+            }
+          }
+          need = __syncthreads_or(need);
+          long long a1 = clock64();
+          cg += a1 - a0;
+          ++npairs;
+          if (!need) continue;
+          rotated = 1;
+          ++nrot;
+          const int wb = eig_pair(sm, P.tol, P.max_inner);
+          long long a2 = clock64();
+          apply_pair(sm, T, ldt, rows, I, J, sm.w[wb]);
+          if (WANTV) apply_pair(sm, V, RP, RP, I, J, sm.w[wb]);
+          long long a3 = clock64();
+          ce += a2 - a1;
+          ca += a3 - a2;
+        }
+      }
+      converged = !rotated;
+    }
+    if (!converged && tid == 0) atomicMin(&P.status[1], int32_t(slice));
+    __syncthreads();
+    long long t2 = clock64();
+
+    // ---- finalize: column norms of T (= sigma), descending sort
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int64_t c = warp; c < NS; c += TPB / 32) {
+        double acc = 0.0;
+        if (c < n)
+          for (int64_t rr = lane; rr < rows; rr += 32) {
+            const double x = T[rr + c * ldt];
+            acc += x * x;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          fs.key[c] = (c < n) ? sqrt(acc) : -1.0;
+          fs.idx[c] = (c < n) ? int(c) : INT_MAX;
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= NS; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < NS; i += TPB) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const double ka = fs.key[i], kb = fs.key[ixj];
+            const int ia = fs.idx[i], ib = fs.idx[ixj];
+            const bool up = (i & k) == 0;
+            const bool sw = up ? before(kb, ib, ka, ia) : before(ka, ia, kb, ib);
+            if (sw) {
+              fs.key[i] = kb;
+              fs.key[ixj] = ka;
+              fs.idx[i] = ib;
+              fs.idx[ixj] = ia;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (P.s)
+      for (int64_t j = tid; j < r; j += TPB) P.s[j + slice * r] = fs.key[j];
+
+    if (WANTV && P.job != STARM_SVD_VALUES) {
+      __syncthreads();
+      const double smax = fs.key[0];
+      const int64_t kout = (P.job == STARM_SVD_FULL) ? r : P.ranks[slice];
+      // Q side = normalised columns of X V (length L).  QR path: X * V_sel
+      // recomputed from the untouched input into the free X slot (sorted
+      // order); direct path: the target's own columns (permuted order).
+      double* Qb;
+      int64_t ldq;
+      const int* qc;
+      if (P.use_qr) {
+        gemm_xv(P, sm, A, V, fs.idx, kout, Xslot);
+        Qb = Xslot;
+        ldq = LP;
+        qc = nullptr;
+      } else {
+        Qb = T;
+        ldq = ldt;
+        qc = fs.idx;
+      }
+      for (int64_t j = 0; j < kout; ++j) {
+        const double sj = fs.key[j];
+        const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+        double* col = Qb + int64_t(qc ? qc[j] : j) * ldq;
+        for (int64_t rr = tid; rr < L; rr += TPB) col[rr] *= inv;
+      }
+      __syncthreads();
+      for (int64_t j = 0; j < kout; ++j)
+        if (!(fs.key[j] > 1e-4 * smax)) cgs2_fix(fs, Qb, ldq, L, qc, int(j));
+      __syncthreads();
+      if (P.job == STARM_SVD_FULL) {
+        double* Uo = P.u + slice * P.m * r;
+        double* Vo = P.v + slice * P.p * r;
+        double* Qd = P.transposed ? Vo : Uo;  // ld L
+        double* Wd = P.transposed ? Uo : Vo;  // ld n
+        for (int64_t j = 0; j < kout; ++j) {
+          const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
+          for (int64_t rr = tid; rr < L; rr += TPB) Qd[rr + j * L] = qcol[rr];
+          const double* vcol = V + int64_t(fs.idx[j]) * RP;
+          for (int64_t rr = tid; rr < n; rr += TPB) Wd[rr + j * n] = vcol[rr];
+        }
+      } else {
+        double* Uk = P.u_data + P.u_off[slice];
+        double* G = P.g_data + P.g_off[slice];
+        if (!P.transposed) {
+          for (int64_t j = 0; j < kout; ++j) {
+            const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
+            for (int64_t rr = tid; rr < L; rr += TPB) Uk[rr + j * L] = qcol[rr];
+          }
+          for (int64_t e = tid; e < kout * n; e += TPB) {
+            const int64_t j = e % kout, col = e / kout;
+            G[e] = fs.key[j] * V[col + int64_t(fs.idx[j]) * RP];
+          }
+        } else {
+          for (int64_t j = 0; j < kout; ++j) {
+            const double* vcol = V + int64_t(fs.idx[j]) * RP;
+            for (int64_t rr = tid; rr < n; rr += TPB) Uk[rr + j * n] = vcol[rr];
+          }
+          for (int64_t e = tid; e < kout * L; e += TPB) {
+            const int64_t j = e % kout, col = e / kout;
+            G[e] = fs.key[j] * Qb[col + int64_t(qc ? qc[j] : j) * ldq];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    long long t3 = clock64();
+    stat_add(P, ST_SLICES, 1);
+    stat_add(P, ST_SWEEPS, sweeps);
+    stat_add(P, ST_PAIRS, npairs);
+    stat_add(P, ST_ROTATED, nrot);
+    stat_add(P, ST_CYC_GRAM, cg);
+    stat_add(P, ST_CYC_EIG, ce);
+    stat_add(P, ST_CYC_APPLY, ca);
+    stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
+    stat_add(P, ST_CYC_FINAL, (unsigned long long)(t3 - t2));
+  }
+}
+
+__global__ void reset_status_kernel(int32_t* status, unsigned long long* counters) {
+  if (threadIdx.x < 2) status[threadIdx.x] = INT32_MAX;
+  if (threadIdx.x < 4) counters[threadIdx.x] = 0ull;
+}
+
+// ---------------------------------------------------------------- host side
+
+struct Plan {
+  int64_t L, n, LP, NP, RP;
+  bool transposed, use_qr, wantv;
+  int ns;
+  size_t jsmem, qsmem;
+  int slots_j, slots_q;
+  size_t off_x, off_w, off_r, off_f, total;
+};
+
+int g_tune_inner = 1;
+int g_tune_sweeps = 60;
+int g_tune_qr = 1;  // 1 = shape rule, 0 = never, 2 = always when it fits
+int g_stats_on = 0;
+
+int occupancy(const void* fn, size_t smem, int* per_sm) {
+  STARM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  STARM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, TPB, smem));
+  if (*per_sm < 1) *per_sm = 1;
+  return STARM_OK;
+}
+
+int make_plan(int64_t m, int64_t p, int64_t count, int job, Plan* pl) {
+  Plan g{};
+  g.L = m > p ? m : p;
+  g.n = m < p ? m : p;
+  g.transposed = m < p;
+  g.wantv = job != STARM_SVD_VALUES;
+  g.LP = round_up(g.L, RCH);
+  g.NP = round_up(g.n, BW);
+  if (g.NP < GW) g.NP = GW;
+  g.RP = round_up(g.NP, RCH);
+  bool tall = 4 * g.L >= 5 * g.n;
+  g.use_qr = (g_tune_qr == 2 || (g_tune_qr == 1 && tall)) && g.LP <= QR_MAX_LP;
+  g.ns = 1;
+  while (g.ns < g.n) g.ns <<= 1;
+  g.jsmem = jacobi_smem_bytes(g.ns);
+  g.qsmem = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 4) * sizeof(double);
+  int dev = 0, sms = 0, per = 0;
+  STARM_CUDA_TRY(cudaGetDevice(&dev));
+  STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int rc = g.wantv ? occupancy((const void*)svd_jacobi_kernel<true>, g.jsmem, &per)
+                   : occupancy((const void*)svd_jacobi_kernel<false>, g.jsmem, &per);
+  if (rc) return rc;
+  g.slots_j = int(count < int64_t(sms) * per ? count : int64_t(sms) * per);
+  if (g.slots_j < 1) g.slots_j = 1;
+  g.slots_q = 0;
+  if (g.use_qr) {
+    rc = occupancy((const void*)svd_qr_kernel, g.qsmem, &per);
+    if (rc) return rc;
+    g.slots_q = int(count < int64_t(sms) * per ? count : int64_t(sms) * per);
+    if (g.slots_q < 1) g.slots_q = 1;
+  }
+  const int64_t xslots = g.slots_j > g.slots_q ? g.slots_j : g.slots_q;
+  size_t off = 256;
+  g.off_x = off;
+  off += size_t(xslots) * g.LP * g.NP * sizeof(double);
+  g.off_w = off;
+  if (g.wantv) off += size_t(g.slots_j) * g.RP * g.NP * sizeof(double);
+  g.off_r = off;
+  if (g.use_qr) off += size_t(count) * g.RP * g.NP * sizeof(double);
+  g.off_f = off;
+  if (g.use_qr) off += round_up(count * 4, 256);
+  g.total = off;
+  *pl = g;
+  return STARM_OK;
+}
+
+}  // namespace
+}  // namespace starm
+
+using namespace starm;
+
+extern "C" size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t count, int job) {
+  if (m < 1 || p < 1 || count < 1) return 0;
+  Plan pl;
+  if (make_plan(m, p, count, job, &pl) != STARM_OK) return 0;
+  return pl.total;
+}
+
+extern "C" int starm_svd_tune(int max_inner, int max_sweeps, int qr_mode, int stats) {
+  if (max_inner > 0) g_tune_inner = max_inner;
+  if (max_sweeps > 0) g_tune_sweeps = max_sweeps;
+  if (qr_mode >= 0) g_tune_qr = qr_mode;
+  if (stats >= 0) g_stats_on = stats;
+  return STARM_OK;
+}
+
+extern "C" int starm_svd_stats(unsigned long long* host16, int reset) {
+  STARM_CUDA_TRY(cudaDeviceSynchronize());
+  STARM_CUDA_TRY(cudaMemcpyFromSymbol(host16, g_stats, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    STARM_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
+  }
+  return STARM_OK;
+}
+
+extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
+                             const int64_t* slice_ids, int64_t count, int job, double* s,
+                             double* u, double* v, const int64_t* ranks, const int64_t* u_off,
+                             const int64_t* g_off, double* u_data, double* g_data,
+                             int32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "svd: extents must be positive");
+  STARM_CHECK_ARG(job == STARM_SVD_VALUES || job == STARM_SVD_FULL || job == STARM_SVD_TRUNCATED,
+                  "svd: unknown job %d", job);
+  const int64_t r = m < p ? m : p;
+  if (r > MAX_NS) {
+    set_error("svd: min(m, p) = %lld exceeds the supported %d", (long long)r, MAX_NS);
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG(ahat && status && ws, "svd: null pointer");
+  STARM_CHECK_ARG(job != STARM_SVD_VALUES || s, "svd: values job needs s");
+  STARM_CHECK_ARG(job != STARM_SVD_FULL || (s && u && v), "svd: full job needs s, u, v");
+  STARM_CHECK_ARG(job != STARM_SVD_TRUNCATED || (ranks && u_off && g_off && u_data && g_data),
+                  "svd: truncated job needs ranks, offsets and packed buffers");
+  if (!slice_ids) count = nslices;
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(ws);
+  reset_status_kernel<<<1, 32, 0, st>>>(status, counters);
+  STARM_LAUNCH_CHECK();
+  if (count <= 0) return STARM_OK;
+  Plan pl;
+  int rc = make_plan(m, p, count, job, &pl);
+  if (rc != STARM_OK) return rc;
+  STARM_CHECK_ARG(ws_bytes >= pl.total, "svd: workspace too small (%zu < %zu)", ws_bytes, pl.total);
+  char* base = reinterpret_cast<char*>(ws);
+
+  SvdParams P{};
+  P.A = ahat;
+  P.m = m;
+  P.p = p;
+  P.N = nslices;
+  P.ids = slice_ids;
+  P.count = count;
+  P.job = job;
+  P.s = s;
+  P.u = u;
+  P.v = v;
+  P.ranks = ranks;
+  P.u_off = u_off;
+  P.g_off = g_off;
+  P.u_data = u_data;
+  P.g_data = g_data;
+  P.status = status;
+  P.counter = counters;
+  P.xslots = reinterpret_cast<double*>(base + pl.off_x);
+  P.wslots = reinterpret_cast<double*>(base + pl.off_w);
+  P.rbuf = reinterpret_cast<double*>(base + pl.off_r);
+  P.flags = reinterpret_cast<int32_t*>(base + pl.off_f);
+  P.L = pl.L;
+  P.n = pl.n;
+  P.LP = pl.LP;
+  P.NP = pl.NP;
+  P.RP = pl.RP;
+  P.transposed = pl.transposed;
+  P.use_qr = pl.use_qr;
+  P.stats = g_stats_on;
+  // Convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).
+  P.tol = double(pl.L > 32 ? pl.L : 32) * DBL_EPSILON;
+  P.max_sweeps = g_tune_sweeps;
+  P.max_inner = g_tune_inner;
+  if (pl.use_qr) {
+    svd_qr_kernel<<<pl.slots_q, TPB, pl.qsmem, st>>>(P);
+    STARM_LAUNCH_CHECK();
+  }
+  if (pl.wantv)
+    svd_jacobi_kernel<true><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
+  else
+    svd_jacobi_kernel<false><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}

@@ -1,0 +1,332 @@
+// K7: tolerance-driven rank selection on the device, bit-for-bit the
+// semantics of compute_threshold (tsvdm.py:85-115):
+//
+//   sq = s*s; v = sort(sq) ascending; w = cumsum(v) (sequential fp64);
+//   total = w[-1]; budget = eps*eps*total; j = searchsorted(w, budget, 'left');
+//   tau = v[j-1] (0 if j == 0); keep = sq > tau;
+//   discarded = sum(sq[~keep])   <- numpy pairwise add-reduce over the C-order
+//                                   (row-major) masked copy of the (r, N) matrix
+//   if discarded >= budget and tau > 0: keep = sq >= tau; discarded = sum(sq[~keep])
+//   ranks = keep.sum(axis=0)
+//
+// Pipeline (one stream, no host round trip):
+//   square_keys -> radix sort (64-bit keys: non-negative doubles order like
+//   their bit patterns) -> sequential running sums + lower_bound -> masks for
+//   both candidate rules in C order -> exclusive scans -> order-preserving
+//   compaction -> numpy-pairwise sums of both candidates (one CTA, the
+//   pairwise tree cut at depth 8 into 256 per-thread subtrees and recombined
+//   in the same shape) -> tie rule -> per-slice ranks.
+// All products use __dmul_rn so no FMA contraction changes a rounding.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace starm {
+namespace {
+
+constexpr int PW_THREADS = 256;
+constexpr int PW_DEPTH = 8;  // 2^8 == PW_THREADS
+
+struct ThState {
+  double budget;
+  double tau;
+  double total;
+  double disc[2];  // candidate discarded sums: [0] strict rule, [1] tie-retain rule
+  int64_t j;
+  int64_t cnt[2];
+  int mode;        // -1: all-zero total, 0: keep sq > tau, 1: keep sq >= tau
+};
+
+__global__ void square_keys_kernel(const double* s, int64_t count, unsigned long long* keys) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double x = s[i];
+    keys[i] = __double_as_longlong(__dmul_rn(x, x));
+  }
+}
+
+// Sequential running sums (np.cumsum) and the lower_bound search.
+__global__ void cumsum_search_kernel(const unsigned long long* vbits, int64_t count, double eps,
+                                     double* w, double* v_out, ThState* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* v = reinterpret_cast<const double*>(vbits);
+  double acc = 0.0;
+  for (int64_t k = 0; k < count; ++k) {
+    const double x = v[k];
+    acc = (k == 0) ? x : __dadd_rn(acc, x);
+    w[k] = acc;
+    if (v_out) v_out[k] = x;
+  }
+  const double total = count ? acc : 0.0;
+  st->total = total;
+  if (total == 0.0) {
+    st->mode = -1;
+    st->j = 0;
+    st->tau = 0.0;
+    st->budget = 0.0;
+    return;
+  }
+  const double budget = __dmul_rn(__dmul_rn(eps, eps), total);
+  // searchsorted(w, budget, side='left'): first k with w[k] >= budget.
+  int64_t lo = 0, hi = count;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (w[mid] < budget)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  st->budget = budget;
+  st->j = lo;
+  st->tau = lo > 0 ? v[lo - 1] : 0.0;
+  st->mode = 0;
+}
+
+// Masks in C (row-major) order of the (r, N) matrix: c = row*N + slice.
+__global__ void mask_kernel(const double* s, int64_t r, int64_t N, const ThState* st, int* fa,
+                            int* fb) {
+  const int64_t count = r * N;
+  const double tau = st->tau;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < count;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = c / N, slice = c % N;
+    const double x = s[row + slice * r];
+    const double sq = __dmul_rn(x, x);
+    fa[c] = !(sq > tau);   // dropped under keep = sq > tau
+    fb[c] = !(sq >= tau);  // dropped under keep = sq >= tau
+  }
+}
+
+__global__ void scatter_kernel(const double* s, int64_t r, int64_t N, const int* fa, const int* fb,
+                               const int* pa, const int* pb, double* da, double* db) {
+  const int64_t count = r * N;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < count;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = c / N, slice = c % N;
+    const double x = s[row + slice * r];
+    const double sq = __dmul_rn(x, x);
+    if (fa[c]) da[pa[c]] = sq;
+    if (fb[c]) db[pb[c]] = sq;
+  }
+}
+
+// numpy DOUBLE_pairwise_sum (loops_utils.h.src), recursive.
+__device__ double pw_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  if (n <= 128) {
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+    int64_t i = 8;
+    const int64_t stop = n - (n % 8);
+    for (; i < stop; i += 8) {
+      r0 = __dadd_rn(r0, a[i + 0]);
+      r1 = __dadd_rn(r1, a[i + 1]);
+      r2 = __dadd_rn(r2, a[i + 2]);
+      r3 = __dadd_rn(r3, a[i + 3]);
+      r4 = __dadd_rn(r4, a[i + 4]);
+      r5 = __dadd_rn(r5, a[i + 5]);
+      r6 = __dadd_rn(r6, a[i + 6]);
+      r7 = __dadd_rn(r7, a[i + 7]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                           __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pw_sum(a, n2), pw_sum(a + n2, n - n2));
+}
+
+__device__ __forceinline__ int64_t pw_split(int64_t n) {
+  int64_t n2 = n / 2;
+  return n2 - n2 % 8;
+}
+
+// Recombine per-thread subtree sums in the same tree shape.
+__device__ double pw_combine(const double* part, int64_t n, int depth, int path) {
+  if (depth == PW_DEPTH) return part[path];
+  if (n <= 128) return part[path << (PW_DEPTH - depth)];
+  const int64_t n2 = pw_split(n);
+  return __dadd_rn(pw_combine(part, n2, depth + 1, path * 2),
+                   pw_combine(part, n - n2, depth + 1, path * 2 + 1));
+}
+
+__device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
+  const int t = threadIdx.x;
+  int64_t lo = 0, len = n;
+  bool owner = true;
+  int depth = 0;
+  for (; depth < PW_DEPTH; ++depth) {
+    if (len <= 128) {
+      // Leaf above the cut: only the all-zero-suffix descendant computes it.
+      const int rest = t & ((1 << (PW_DEPTH - depth)) - 1);
+      owner = (rest == 0);
+      break;
+    }
+    const int64_t n2 = pw_split(len);
+    if ((t >> (PW_DEPTH - 1 - depth)) & 1) {
+      lo += n2;
+      len -= n2;
+    } else {
+      len = n2;
+    }
+  }
+  part[t] = owner ? pw_sum(a + lo, len) : 0.0;
+  __syncthreads();
+  double res = 0.0;
+  if (t == 0) res = (n == 0) ? 0.0 : __dadd_rn(0.0, pw_combine(part, n, 0, 0));
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(PW_THREADS) pairwise_kernel(const int* fa, const int* fb,
+                                                               const int* pa, const int* pb,
+                                                               const double* da, const double* db,
+                                                               int64_t count, ThState* st) {
+  __shared__ double part[PW_THREADS];
+  if (st->mode < 0) return;
+  const int64_t na = count ? int64_t(pa[count - 1]) + fa[count - 1] : 0;
+  const int64_t nb = count ? int64_t(pb[count - 1]) + fb[count - 1] : 0;
+  const double sa = pw_sum_parallel(da, na, part);
+  const double sb = pw_sum_parallel(db, nb, part);
+  if (threadIdx.x == 0) {
+    st->disc[0] = sa;
+    st->disc[1] = sb;
+    st->cnt[0] = na;
+    st->cnt[1] = nb;
+    st->mode = (sa >= st->budget && st->tau > 0.0) ? 1 : 0;
+  }
+}
+
+__global__ void ranks_kernel(const double* s, int64_t r, int64_t N, const ThState* st,
+                             int64_t* ranks, double* scal, int64_t* j_out) {
+  const int mode = st->mode;
+  const double tau = st->tau;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t k = 0;
+    if (mode >= 0) {
+      for (int64_t row = 0; row < r; ++row) {
+        const double x = s[row + i * r];
+        const double sq = __dmul_rn(x, x);
+        k += (mode == 0) ? (sq > tau) : (sq >= tau);
+      }
+    }
+    ranks[i] = k;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (mode < 0) {
+      scal[0] = 0.0;
+      scal[1] = 0.0;
+      scal[2] = 0.0;
+      *j_out = 0;
+    } else {
+      scal[0] = tau;
+      scal[1] = st->disc[mode];
+      scal[2] = st->total;
+      *j_out = st->j;
+    }
+  }
+}
+
+struct ThLayout {
+  size_t keys, sorted, w, fa, fb, pa, pb, da, db, state, cub, total;
+  size_t cub_bytes;
+};
+
+ThLayout layout(int64_t count) {
+  ThLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  L.keys = take(count * 8);
+  L.sorted = take(count * 8);
+  L.w = take(count * 8);
+  L.fa = take(count * 4);
+  L.fb = take(count * 4);
+  L.pa = take(count * 4);
+  L.pb = take(count * 4);
+  L.da = take(count * 8);
+  L.db = take(count * 8);
+  L.state = take(sizeof(ThState));
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                 (unsigned long long*)nullptr, int(count));
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int*)nullptr, (int*)nullptr,
+                                int(count));
+  L.cub_bytes = sort_bytes > scan_bytes ? sort_bytes : scan_bytes;
+  L.cub = take(L.cub_bytes);
+  L.total = off;
+  return L;
+}
+
+int grid_for(int64_t count) {
+  int64_t g = (count + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+}  // namespace
+}  // namespace starm
+
+using namespace starm;
+
+extern "C" size_t starm_threshold_workspace_bytes(int64_t r, int64_t nslices) {
+  if (r < 1 || nslices < 1) return 0;
+  return layout(r * nslices).total;
+}
+
+extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, double epsilon,
+                                   double* v_out, double* w_out, int64_t* ranks_out,
+                                   double* scal_out, int64_t* j_out, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  STARM_CHECK_ARG(r >= 1 && nslices >= 1, "threshold: extents must be positive");
+  STARM_CHECK_ARG(epsilon > 0.0 && epsilon < 1.0, "tolerance must lie in (0, 1), got %g", epsilon);
+  const int64_t count = r * nslices;
+  STARM_CHECK_ARG(count < (int64_t(1) << 31), "threshold: too many values (%lld)", (long long)count);
+  STARM_CHECK_ARG(s && ranks_out && scal_out && j_out && ws, "threshold: null pointer");
+  const ThLayout L = layout(count);
+  STARM_CHECK_ARG(ws_bytes >= L.total, "threshold: workspace too small (%zu < %zu)", ws_bytes, L.total);
+  char* base = reinterpret_cast<char*>(ws);
+  auto* keys = reinterpret_cast<unsigned long long*>(base + L.keys);
+  auto* sorted = reinterpret_cast<unsigned long long*>(base + L.sorted);
+  double* w = w_out ? w_out : reinterpret_cast<double*>(base + L.w);
+  int* fa = reinterpret_cast<int*>(base + L.fa);
+  int* fb = reinterpret_cast<int*>(base + L.fb);
+  int* pa = reinterpret_cast<int*>(base + L.pa);
+  int* pb = reinterpret_cast<int*>(base + L.pb);
+  double* da = reinterpret_cast<double*>(base + L.da);
+  double* db = reinterpret_cast<double*>(base + L.db);
+  ThState* stt = reinterpret_cast<ThState*>(base + L.state);
+  void* cubtmp = base + L.cub;
+  size_t cub_bytes = L.cub_bytes;
+  cudaStream_t st = as_stream(stream);
+  const int grid = grid_for(count);
+
+  square_keys_kernel<<<grid, 256, 0, st>>>(s, count, keys);
+  STARM_LAUNCH_CHECK();
+  STARM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(cubtmp, cub_bytes, keys, sorted, int(count), 0, 64, st));
+  cumsum_search_kernel<<<1, 32, 0, st>>>(sorted, count, epsilon, w, v_out, stt);
+  STARM_LAUNCH_CHECK();
+  mask_kernel<<<grid, 256, 0, st>>>(s, r, nslices, stt, fa, fb);
+  STARM_LAUNCH_CHECK();
+  cub_bytes = L.cub_bytes;
+  STARM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cubtmp, cub_bytes, fa, pa, int(count), st));
+  cub_bytes = L.cub_bytes;
+  STARM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cubtmp, cub_bytes, fb, pb, int(count), st));
+  scatter_kernel<<<grid, 256, 0, st>>>(s, r, nslices, fa, fb, pa, pb, da, db);
+  STARM_LAUNCH_CHECK();
+  pairwise_kernel<<<1, PW_THREADS, 0, st>>>(fa, fb, pa, pb, da, db, count, stt);
+  STARM_LAUNCH_CHECK();
+  ranks_kernel<<<grid_for(nslices), 256, 0, st>>>(s, r, nslices, stt, ranks_out, scal_out, j_out);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}

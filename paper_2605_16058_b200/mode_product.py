@@ -1,0 +1,182 @@
+"""Mode-k tensor-times-matrix on the B200 (reference ttm.py).
+
+Every variant of the reference (``batched`` / ``loop`` / ``parfor``,
+ttm.py:113-135) is one launch of the FP64 DMMA GEMM kernel here: the
+column-major buffer is ``batch`` row-major (inner x rows) blocks and the
+kernel computes dst[b] = M @ src[b] for all b in a single grid.  The
+variant and thread arguments are validated exactly like the reference and
+then have no further effect.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import prod
+
+import numpy as np
+
+from . import _native as nat
+from .tensors import DenseTensor, DeviceTensor, as_device
+from .transform_set import Transform, TransformSet
+
+__all__ = ["BATCHED", "LOOP", "PARFOR", "VARIANTS", "TTMPlan", "ttm", "ttm_inverse",
+           "to_transform_domain", "from_transform_domain", "ttm_device"]
+
+BATCHED = "batched"
+LOOP = "loop"
+PARFOR = "parfor"
+VARIANTS = (BATCHED, LOOP, PARFOR)
+
+
+@dataclass(frozen=True)
+class TTMPlan:
+    """Geometry of one mode-k contraction (ttm.py:34-73)."""
+
+    mode: int
+    rows: int
+    inner: int
+    batch: int
+    out_cols: int
+    variant: str = BATCHED
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown ttm variant {self.variant!r}")
+
+    @classmethod
+    def for_dims(cls, dims, mode, out_cols, variant=BATCHED):
+        dims = tuple(dims)
+        mode = int(mode)
+        if mode < 2:
+            raise ValueError("the first two modes are never contracted")
+        if mode >= len(dims):
+            raise ValueError(f"mode {mode} out of range for {len(dims)} modes")
+        return cls(mode, prod(dims[:mode]), dims[mode], prod(dims[mode + 1:]), int(out_cols), variant)
+
+    @property
+    def is_last_mode(self) -> bool:
+        return self.batch == 1
+
+
+def _threads(threads) -> int:
+    threads = int(threads)
+    if threads < 1:
+        raise ValueError(f"thread count must be positive, got {threads}")
+    return threads
+
+
+def _matrix_operand(m, device, transpose=False):
+    """Row-major device copy of M (or M^T) and its (out_cols, inner) shape."""
+    import torch
+    if isinstance(m, Transform):
+        op = m.device_operand(device, transpose)
+        return op, op.shape[0], op.shape[1]
+    if isinstance(m, torch.Tensor):
+        mat = m.to(device=device, dtype=torch.float64)
+        if mat.dim() != 2:
+            raise ValueError(f"expected a matrix, got {mat.dim()} modes")
+        mat = (mat.T if transpose else mat).contiguous()
+        return mat, mat.shape[0], mat.shape[1]
+    mat = np.asarray(m, dtype=np.float64)
+    if mat.ndim != 2:
+        raise ValueError(f"expected a matrix, got {mat.ndim} modes")
+    if transpose:
+        mat = mat.T
+    op = torch.from_numpy(np.ascontiguousarray(mat)).to(device)
+    return op, mat.shape[0], mat.shape[1]
+
+
+def ttm_device(x: DeviceTensor, mode: int, op, out_cols: int, inner: int) -> DeviceTensor:
+    """One K1 launch: result.unfold(mode) = op @ x.unfold(mode)."""
+    plan = TTMPlan.for_dims(x.dims, mode, out_cols)
+    if inner != plan.inner:
+        raise ValueError(f"matrix has {inner} columns, mode {plan.mode} extent is {plan.inner}")
+    out_dims = x.dims[:mode] + (out_cols,) + x.dims[mode + 1:]
+    out = DeviceTensor.empty(out_dims, x.device)
+    nat.call("starm_ttm_f64", x.data.data_ptr(), op.data_ptr(), out.data.data_ptr(), plan.rows,
+             plan.inner, plan.batch, out_cols, nat.stream_ptr(x.device))
+    return out
+
+
+def _shape(m):
+    if isinstance(m, Transform):
+        return m.matrix.shape
+    if hasattr(m, "shape") and not isinstance(m, np.ndarray):
+        return tuple(m.shape)
+    return np.shape(m)
+
+
+def _run(t, fn):
+    """Host in -> host out; device in -> device out."""
+    if isinstance(t, DeviceTensor):
+        return fn(t)
+    if not isinstance(t, DenseTensor):
+        raise TypeError(f"expected DenseTensor or DeviceTensor, got {type(t).__name__}")
+    dev = nat.require_cuda()
+    return fn(as_device(t, dev)).to_host()
+
+
+def ttm(t, mode, m, variant=BATCHED, threads=1):
+    """Contract mode ``mode`` (>= 2) with ``m`` of shape (J, n_mode)."""
+    _threads(threads)
+    TTMPlan.for_dims(t.dims, mode, 1, variant)  # validates mode and variant
+    shape = _shape(m)
+    if len(shape) != 2:
+        raise ValueError(f"expected a matrix, got {len(shape)} modes")
+    if shape[1] != t.dims[mode]:
+        raise ValueError(f"matrix has {shape[1]} columns, mode {mode} extent is {t.dims[mode]}")
+
+    def go(x):
+        op, j, n = _matrix_operand(m, x.device)
+        return ttm_device(x, mode, op, j, n)
+
+    return _run(t, go)
+
+
+def ttm_inverse(t, mode, m, variant=BATCHED, threads=1):
+    """Contract with m^T (ttm.py:107-110)."""
+    _threads(threads)
+    TTMPlan.for_dims(t.dims, mode, 1, variant)
+    shape = _shape(m)
+    if len(shape) != 2 or shape[0] != t.dims[mode]:
+        raise ValueError(f"matrix of shape {shape} cannot undo mode {mode} of extent {t.dims[mode]}")
+
+    def go(x):
+        op, j, n = _matrix_operand(m, x.device, transpose=True)
+        return ttm_device(x, mode, op, j, n)
+
+    return _run(t, go)
+
+
+def forward_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
+    out = x
+    for k, tr in enumerate(ts, start=2):
+        op, j, n = _matrix_operand(tr, x.device)
+        out = ttm_device(out, k, op, j, n)
+    return out
+
+
+def inverse_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
+    out = x
+    for k in range(len(ts) + 1, 1, -1):
+        op, j, n = _matrix_operand(ts[k - 2], x.device, transpose=True)
+        out = ttm_device(out, k, op, j, n)
+    return out
+
+
+def to_transform_domain(t, ts: TransformSet, variant=BATCHED, threads=1):
+    """Ascending modes (ttm.py:138-144)."""
+    _threads(threads)
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown ttm variant {variant!r}")
+    ts.check_dims(t.dims)
+    return _run(t, lambda x: forward_device(x, ts))
+
+
+def from_transform_domain(t, ts: TransformSet, variant=BATCHED, threads=1):
+    """Descending modes with the transposes (ttm.py:147-153)."""
+    _threads(threads)
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown ttm variant {variant!r}")
+    ts.check_dims(t.dims)
+    return _run(t, lambda x: inverse_device(x, ts))

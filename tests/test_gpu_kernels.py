@@ -1,0 +1,259 @@
+"""GPU parity of each kernel family against the CPU oracle (oracle/).
+
+Run on a B200: ``pytest -m gpu``.  Every call goes through the public API
+into libstarm.so; the oracle is only the checker.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2605_16058_b200 as sb
+from helpers import projector_distance, random_array, random_orthonormal, rel_error, sigma_close
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(5, 3, 4), (3, 5, 2, 3), (7, 7, 6), (1, 4, 3), (4, 1, 2), (33, 17, 5), (17, 33, 4),
+          (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3)]
+
+
+# ------------------------------------------------------------------ TTM (K1)
+
+@pytest.mark.parametrize("dims", [(3, 4, 5), (2, 3, 4, 2), (2, 2, 3, 2, 2), (3, 1, 4, 2),
+                                  (16, 16, 64), (33, 5, 130), (7, 9, 257)])
+def test_ttm_matches_oracle(dims):
+    rng = np.random.default_rng(sum(dims))
+    a = random_array(dims, sum(dims))
+    t = sb.DenseTensor(a)
+    for mode in range(2, len(dims)):
+        for out_rows in (dims[mode], max(1, dims[mode] - 1), dims[mode] + 2):
+            mat = rng.standard_normal((out_rows, dims[mode]))
+            got = sb.ttm(t, mode, mat)
+            ref = oracle.ttm(a, mode, mat)
+            assert got.dims == ref.shape
+            assert rel_error(ref, got.array) <= 1e-13
+
+
+def test_ttm_large_dct_round_trip():
+    dims = (37, 41, 96)
+    a = random_array(dims, 3)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(dims, "dct")
+    ahat = sb.to_transform_domain(t, ts)
+    ref = oracle.to_transform_domain(a, [oracle.dct_matrix(96)])
+    assert rel_error(ref, ahat.array) <= 1e-13
+    back = sb.from_transform_domain(ahat, ts)
+    assert rel_error(a, back.array) <= 1e-12
+    assert abs(ahat.frobenius_norm() - t.frobenius_norm()) <= 1e-12 * t.frobenius_norm()
+
+
+# ------------------------------------------------------------- slice SVD (K3-K6)
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_svd_values_match_lapack(dims):
+    a = random_array(dims, 7 + sum(dims))
+    s = sb.svd_values_only(sb.DenseTensor(a))
+    ref = oracle.svd_values_only(a)
+    assert s.shape == ref.shape
+    for i in range(ref.shape[1]):
+        ok, excess = sigma_close(s[:, i], ref[:, i])
+        assert ok, (dims, i, excess)
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_svd_full_factors(dims):
+    a = random_array(dims, 11 + sum(dims))
+    t = sb.DenseTensor(a)
+    out = sb.svd_all_slices(t)
+    m, p = dims[0], dims[1]
+    r = min(m, p)
+    n = t.num_slices
+    assert out.u.dims == (m, r, n) and out.v.dims == (p, r, n) and out.s.shape == (r, n)
+    values = sb.svd_values_only(t)
+    assert np.array_equal(values, out.s)  # same rotation sequence -> bitwise
+    for i in range(n):
+        u = out.u.frontal_slice(i)
+        v = out.v.frontal_slice(i)
+        assert np.linalg.norm(u.T @ u - np.eye(r)) <= 1e-10 * math.sqrt(r)
+        assert np.linalg.norm(v.T @ v - np.eye(r)) <= 1e-10 * math.sqrt(r)
+        sl = t.frontal_slice(i)
+        assert np.linalg.norm(out.reconstruct_slice(i) - sl) <= 1e-12 * np.linalg.norm(sl)
+        assert (np.diff(out.s[:, i]) <= 0).all()
+
+
+def test_zero_and_rank_deficient_slices():
+    arr = np.zeros((4, 3, 2), order="F")
+    arr[:, :, 1] = np.arange(12.0).reshape(4, 3)
+    out = sb.svd_all_slices(sb.DenseTensor(arr, copy=False))
+    assert np.array_equal(out.s[:, 0], np.zeros(3))
+    assert np.array_equal(out.u.frontal_slice(0), np.eye(4, 3))
+    assert np.array_equal(out.v.frontal_slice(0), np.eye(3, 3))
+    u = out.u.frontal_slice(1)
+    assert np.linalg.norm(u.T @ u - np.eye(3)) <= 1e-10 * math.sqrt(3)
+    ref = oracle.svd_values_only(arr)
+    ok, _ = sigma_close(out.s[:, 1], ref[:, 1])
+    assert ok
+
+
+def test_non_finite_slice_named():
+    arr = np.zeros((3, 3, 5), order="F")
+    arr[1, 1, 3] = np.nan
+    arr[0, 0, 4] = np.inf
+    t = sb.DenseTensor(arr, copy=False)
+    with pytest.raises(ValueError, match="slice 3"):
+        sb.svd_all_slices(t)
+    with pytest.raises(ValueError, match="slice 3"):
+        sb.svd_values_only(t)
+
+
+def test_truncated_match_leading_triplets_bitwise():
+    for dims in [(6, 5, 8), (5, 9, 8), (40, 70, 8)]:
+        a = random_array(dims, 10)
+        t = sb.DenseTensor(a)
+        full = sb.svd_all_slices(t)
+        r = min(dims[0], dims[1])
+        ranks = np.array([0, 1, 2, 3, 4, r, 2, 1])
+        f = sb.svd_truncated_slices(t, ranks)
+        assert f.total_rank == int(ranks.sum())
+        for i, k in enumerate(ranks):
+            assert np.array_equal(f.u_block(i), full.u.frontal_slice(i)[:, :k])
+            g = full.s[:k, i, None] * full.v.frontal_slice(i)[:, :k].T
+            assert np.array_equal(f.g_block(i), g)
+
+
+def test_graded_spectrum_values():
+    # c5-like slice spectrum 0.8^j with Haar factors: analytic golden.
+    rng = np.random.default_rng(5)
+    m, p, n = 512, 64, 6
+    arr = np.empty((m, p, n), order="F")
+    sig = 0.8 ** np.arange(p)
+    for i in range(n):
+        u = np.linalg.qr(rng.standard_normal((m, p)))[0]
+        v = np.linalg.qr(rng.standard_normal((p, p)))[0]
+        arr[:, :, i] = (u * sig) @ v.T
+    s = sb.svd_values_only(sb.DenseTensor(arr))
+    ref = oracle.svd_values_only(arr)
+    for i in range(n):
+        ok, excess = sigma_close(s[:, i], ref[:, i])
+        assert ok, excess
+        assert np.max(np.abs(s[:, i] - sig) / sig) <= 1e-9
+
+
+# ------------------------------------------------------------- threshold (K7)
+
+def _threshold_equal(s, eps):
+    got = sb.compute_threshold(s, eps)
+    ref = oracle.compute_threshold(s, eps)
+    assert np.array_equal(got.v, ref["v"])
+    assert np.array_equal(got.w, ref["w"])
+    assert got.j == ref["j"]
+    assert got.tau == ref["tau"]
+    assert np.array_equal(got.ranks, ref["ranks"])
+    assert got.discarded_energy == ref["discarded_energy"]
+    assert got.total_energy == ref["total_energy"]
+
+
+def test_threshold_fixtures_bitwise():
+    _threshold_equal(np.array([[3.0], [2.0], [1.0]]), 0.32)
+    _threshold_equal(np.array([[2.0, 1.0], [1.0, 1.0]]), math.sqrt(2.5 / 7.0))
+    _threshold_equal(np.array([[2.0], [1.0], [1.0]]), math.sqrt(2.5 / 6.0))
+    _threshold_equal(np.array([[3.0], [1.0]]), 0.01)
+    _threshold_equal(np.array([[3.0, 0.0], [1.0, 0.0]]), 0.01)
+    th = sb.compute_threshold(np.zeros((3, 4)), 0.3)
+    assert th.total_energy == 0.0 and th.tau == 0.0 and not th.ranks.any()
+
+
+def test_threshold_random_bitwise():
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        r, n = int(rng.integers(1, 40)), int(rng.integers(1, 300))
+        s = -np.sort(-np.abs(rng.standard_normal((r, n))) * 10 ** rng.uniform(-3, 3, (1, n)), axis=0)
+        for eps in (0.05, 0.2, 0.5, 0.9, 1e-3):
+            _threshold_equal(np.asfortranarray(s), eps)
+
+
+def test_threshold_ties_large():
+    # many exact duplicates at the cutoff, > 128 dropped values (pairwise tree)
+    rng = np.random.default_rng(3)
+    vals = rng.choice(np.array([0.5, 1.0, 1.5, 2.0, 3.0]), size=(64, 500))
+    s = -np.sort(-vals, axis=0)
+    for eps in (0.1, 0.3, 0.5, 0.7):
+        _threshold_equal(np.asfortranarray(s), eps)
+
+
+# --------------------------------------------------------- end-to-end paths
+
+def _kinds(dims, seed):
+    return [sb.validate_transform(random_orthonormal(n, seed + k)) for k, n in enumerate(dims[2:])]
+
+
+@pytest.mark.parametrize("dims", [(6, 5, 4, 2), (9, 13, 7), (20, 12, 16)])
+def test_fixed_rank_matches_oracle(dims):
+    a = random_array(dims, 4)
+    t = sb.DenseTensor(a)
+    for kinds in ("dct", "identity", "custom"):
+        entries = _kinds(dims, 3) if kinds == "custom" else kinds
+        ts = sb.TransformSet.build(dims, entries)
+        mats = [tr.matrix for tr in ts]
+        for rank in (1, 2, min(dims[0], dims[1])):
+            c = sb.tsvdm_fixed_rank(t, ts, rank)
+            ref = oracle.tsvdm_fixed_rank(a, mats, rank)
+            assert np.array_equal(c.ranks, ref["ranks"])
+            tot = ref["total_energy"]
+            assert abs(c.total_energy - tot) <= 1e-12 * tot
+            assert abs(c.discarded_energy - ref["discarded_energy"]) <= 1e-10 * tot
+            rec = sb.reconstruct(c)
+            rec_ref = oracle.reconstruct_packed(dims, mats, ref["ranks"], ref["u_data"], ref["g_data"])
+            assert rel_error(rec_ref, rec.array) <= 1e-8
+            err_sq = float(np.linalg.norm(rec.data - t.data) ** 2)
+            assert abs(err_sq - ref["discarded_energy"]) <= 1e-10 * tot
+
+
+@pytest.mark.parametrize("dims", [(5, 6, 4, 3), (12, 9, 10), (30, 50, 24)])
+def test_tolerance_matches_oracle(dims):
+    a = random_array(dims, 9)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(dims, "dct")
+    mats = [tr.matrix for tr in ts]
+    for eps in (0.4, 0.15, 0.05):
+        ref = oracle.tsvdm_tolerance(a, mats, eps)
+        recs = {}
+        for strategy in (sb.TRUNCATE, sb.COMPUTE_EFFICIENT, sb.MEMORY_EFFICIENT):
+            c = sb.tsvdm_tolerance(t, ts, eps, strategy=strategy)
+            assert np.array_equal(c.ranks, ref["ranks"]), strategy
+            recs[strategy] = sb.reconstruct(c)
+            err = rel_error(a, recs[strategy].array)
+            assert err < eps
+            assert abs(c.relative_error() - err) <= 1e-8
+        for strategy in recs:
+            assert rel_error(recs[sb.TRUNCATE].array, recs[strategy].array) <= 1e-10
+
+
+def test_tolerance_zero_tensor():
+    t = sb.DenseTensor.zeros((4, 4, 3))
+    ts = sb.TransformSet.build(t.dims, "identity")
+    c = sb.tsvdm_tolerance(t, ts, 0.3)
+    assert (c.ranks == 0).all()
+    assert c.relative_error() == 0.0
+    assert np.array_equal(sb.reconstruct(c).data, np.zeros(48))
+
+
+def test_starm_product_matches_oracle():
+    a = random_array((4, 3, 5, 2), 1)
+    b = random_array((3, 6, 5, 2), 2)
+    for kinds in ("identity", "dct"):
+        ts = sb.TransformSet.build((4, 6, 5, 2), kinds)
+        got = sb.starm_product(sb.DenseTensor(a), sb.DenseTensor(b), ts)
+        ref = oracle.starm_product(a, b, [tr.matrix for tr in ts])
+        assert rel_error(ref, got.array) <= 1e-12
+
+
+def test_full_tsvdm_lossless():
+    for dims in [(4, 5, 3), (3, 3, 2, 4), (5, 2, 3, 2, 2), (40, 30, 6)]:
+        a = random_array(dims, 2)
+        t = sb.DenseTensor(a)
+        ts = sb.TransformSet.build(dims, "dct")
+        res = sb.full_tsvdm(t, ts)
+        assert rel_error(a, res.reconstruct().array) <= 1e-11
