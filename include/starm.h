@@ -53,6 +53,10 @@ enum starm_svd_job {
 
 int starm_abi_version(void);
 
+/* Number of kernel launches issued by the library since the last call
+ * (CUB device-wide primitives count as one each); resets the counter. */
+long long starm_launch_count_reset(void);
+
 /* Copies the calling thread's last error message into buf (NUL-terminated,
  * truncated to len); returns the full message length. */
 size_t starm_last_error(char* buf, size_t len);

@@ -20,6 +20,7 @@ from math import prod
 
 import numpy as np
 from scipy.linalg import get_lapack_funcs
+from threadpoolctl import threadpool_limits
 
 __all__ = [
     "dct_matrix", "orthonormality_residual", "ttm", "to_transform_domain",
@@ -58,7 +59,7 @@ def orthonormality_residual(m) -> float:
 
 # ----------------------------------------------------------------------- TTM
 
-def ttm(arr: np.ndarray, mode: int, mat: np.ndarray) -> np.ndarray:
+def ttm(arr: np.ndarray, mode: int, mat: np.ndarray, threads: int = 1) -> np.ndarray:
     """Mode-``mode`` product, ttm.py:87-104 with the batched dispatch of
     ttm.py:113-122: the column-major buffer viewed C-order as
     (batch, inner, rows) and ``dst[b] = mat @ src[b]``."""
@@ -71,7 +72,9 @@ def ttm(arr: np.ndarray, mode: int, mat: np.ndarray) -> np.ndarray:
     flat = arr.reshape(-1, order="F")
     src = flat.reshape(batch, inner, rows)
     out = np.empty(batch * mat.shape[0] * rows)
-    np.matmul(mat, src, out=out.reshape(batch, mat.shape[0], rows))
+    # reference default threads=1 (ttm.py:87,121): same BLAS blocking -> same bits
+    with threadpool_limits(limits=threads, user_api="blas"):
+        np.matmul(mat, src, out=out.reshape(batch, mat.shape[0], rows))
     out_dims = dims[:mode] + (mat.shape[0],) + dims[mode + 1:]
     return out.reshape(out_dims, order="F")
 

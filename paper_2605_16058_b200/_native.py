@@ -54,6 +54,7 @@ SIGNATURES = {
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p]),
     "starm_tail_energy_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "starm_launch_count_reset": (ctypes.c_longlong, []),
     "starm_svd_tune": (c_int, [c_int, c_int, c_int, c_int]),
     "starm_svd_stats": (c_int, [c_void_p, c_int]),
 }

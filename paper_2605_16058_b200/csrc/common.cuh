@@ -15,6 +15,10 @@ namespace starm {
 // Thread-local last error message, read back by starm_last_error().
 void set_error(const char* fmt, ...);
 
+// Process-wide count of kernel launches issued by this library (bench claim
+// `gpu_launches`); CUB device-wide calls count as one launch each.
+void count_launch(int n = 1);
+
 #define STARM_CHECK_ARG(cond, ...)                                   \
   do {                                                               \
     if (!(cond)) {                                                   \
@@ -33,7 +37,11 @@ void set_error(const char* fmt, ...);
     }                                                                \
   } while (0)
 
-#define STARM_LAUNCH_CHECK() STARM_CUDA_TRY(cudaGetLastError())
+#define STARM_LAUNCH_CHECK()                                         \
+  do {                                                               \
+    ::starm::count_launch(1);                                        \
+    STARM_CUDA_TRY(cudaGetLastError());                              \
+  } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -2,6 +2,7 @@
 // C-ABI error plumbing.
 #include <string.h>
 
+#include <atomic>
 #include <string>
 
 #include "common.cuh"
@@ -10,7 +11,10 @@ namespace starm {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
 }
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -243,6 +247,8 @@ extern "C" int starm_tail_energy_f64(const double* s, int64_t r, int64_t nslices
 }
 
 extern "C" int starm_abi_version(void) { return STARM_ABI_VERSION; }
+
+extern "C" long long starm_launch_count_reset(void) { return g_launches.exchange(0); }
 
 extern "C" size_t starm_last_error(char* buf, size_t len) {
   const std::string& e = g_last_error;

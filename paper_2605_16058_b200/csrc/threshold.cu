@@ -314,6 +314,7 @@ extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, 
   square_keys_kernel<<<grid, 256, 0, st>>>(s, count, keys);
   STARM_LAUNCH_CHECK();
   STARM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(cubtmp, cub_bytes, keys, sorted, int(count), 0, 64, st));
+  count_launch(3);  // the three CUB device-wide calls of this function
   cumsum_search_kernel<<<1, 32, 0, st>>>(sorted, count, epsilon, w, v_out, stt);
   STARM_LAUNCH_CHECK();
   mask_kernel<<<grid, 256, 0, st>>>(s, r, nslices, stt, fa, fb);
