@@ -101,16 +101,18 @@ int starm_facewise_gemm_f64(const double* a, const double* b, double* c, int64_t
  *  status     device int32[2]: status[0] = lowest slice index with a
  *             non-finite entry, status[1] = lowest slice that did not
  *             converge; both INT32_MAX when clean.  Reset by this call.
- *  ws         device workspace of starm_svd_workspace_bytes() bytes.
+ *  ws         device workspace of starm_svd_workspace_bytes(m, p, nslices,
+ *             count, job) bytes (count = number of slices factored).
  * All-zero slices yield s = 0, U = eye(m, r), V = eye(p, r) (slicesvd.py:51-54). */
-size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t count, int job);
+size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t nslices, int64_t count, int job);
 /* Tuning / diagnostics (process-wide; a value < 0 leaves a knob unchanged):
- * inner Jacobi sweeps per pair step (default 1), sweep cap (60), QR
- * preconditioning (1 = when L >= 1.25 n, 0 = never, 2 = whenever it fits),
+ * inner Jacobi sweeps per pair step (default 1), sweep cap (60), values
+ * path (1 = QR + band reduction + bulge chasing + bisection whenever a
+ * 16-column panel of the slice fits in shared memory, 0 = Jacobi only),
  * kernel counters on/off.  starm_svd_stats copies 16 counters (slices,
  * sweeps, pairs, rotated pairs, cycles in gram / eig / apply / qr /
- * finalize / load) to host memory, synchronising the device. */
-int starm_svd_tune(int max_inner, int max_sweeps, int qr_mode, int stats);
+ * finalize / load / band / bulge) to host memory, synchronising the device. */
+int starm_svd_tune(int max_inner, int max_sweeps, int mode, int stats);
 int starm_svd_stats(unsigned long long* host16, int reset);
 int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
                   const int64_t* slice_ids, int64_t count, int job, double* s, double* u,

@@ -36,7 +36,7 @@ SIGNATURES = {
                               c_void_p]),
     "starm_facewise_gemm_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                                         c_int64, c_void_p]),
-    "starm_svd_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int]),
+    "starm_svd_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int]),
     "starm_svd_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
@@ -60,7 +60,7 @@ SIGNATURES = {
 }
 
 SVD_STAT_NAMES = ("slices", "sweeps", "pairs", "rotated", "cyc_gram", "cyc_eig", "cyc_apply",
-                  "cyc_qr", "cyc_final", "cyc_load")
+                  "cyc_qr", "cyc_final", "cyc_load", "cyc_band", "cyc_bulge")
 
 
 def svd_stats(reset=True) -> dict:

@@ -52,7 +52,7 @@ constexpr int QR_MAX_LP = 1344;
 constexpr int ZS = 20;        // Z (16 x 32) column stride
 
 enum { ST_SLICES = 0, ST_SWEEPS, ST_PAIRS, ST_ROTATED, ST_CYC_GRAM, ST_CYC_EIG, ST_CYC_APPLY,
-       ST_CYC_QR, ST_CYC_FINAL, ST_CYC_LOAD, ST_COUNT };
+       ST_CYC_QR, ST_CYC_FINAL, ST_CYC_LOAD, ST_CYC_BAND, ST_CYC_BULGE, ST_COUNT };
 
 __device__ unsigned long long g_stats[16];
 
@@ -74,10 +74,12 @@ struct SvdParams {
   unsigned long long* counter;  // [0] qr kernel, [1] jacobi kernel
   double* xslots;               // per-CTA X (LP x NP)
   double* wslots;               // per-CTA V (RP x NP), vector jobs
-  double* rbuf;                 // per-slice R (RP x NP), QR path
-  int32_t* flags;               // per-slice load flags, QR path
+  double* rbuf;                 // per-slice R (RP x NP), QR path with vectors
+  int32_t* flags;               // per-slice load flags (reduce kernel)
+  double* bandbuf;              // per-slice 17 diagonals (17 x NP)
+  double* debuf;                // per-slice bidiagonal d, e (2 x NP)
   int64_t L, n, LP, NP, RP;
-  int transposed, use_qr, stats;
+  int transposed, use_qr, bidiag, stats;
   double tol;
   int max_sweeps, max_inner;
 };
@@ -122,6 +124,8 @@ struct __align__(16) QrSmemFixed {
   double sg[2][BW * 17];
   double y[BW * GS];
   double z[GW * ZS];
+  double yr[RCH * 17];
+  double zr[BW * XS];
   double red[TPB / 32][BW];
   double sums[BW];
   double wv[BW];
@@ -551,20 +555,20 @@ __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64
   __syncthreads();
 }
 
-// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld LP, NP columns), rows kc..LP.
+// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns), rows kc..nrows.
 __device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, double* X,
-                                int64_t LP, int64_t NP, int64_t kc, int64_t c0) {
+                                int64_t ld, int64_t nrows, int64_t NP, int64_t kc, int64_t c0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const int64_t nch = (LP - kc) / RCH;
+  const int64_t nch = (nrows - kc) / RCH;
   // ---- Y = V^T C (16 x 32): warp -> tile (ti = warp>>2, tj = warp&3)
   {
     const int ti = warp >> 2, tj = warp & 3;
     double y0 = 0.0, y1 = 0.0;
-    stage_cols(q.cbuf[0], X, LP, kc, c0, NP);
+    stage_cols(q.cbuf[0], X, ld, kc, c0, NP);
     for (int64_t ch = 0; ch < nch; ++ch) {
       if (ch + 1 < nch) {
-        stage_cols(q.cbuf[(ch + 1) & 1], X, LP, kc + (ch + 1) * RCH, c0, NP);
+        stage_cols(q.cbuf[(ch + 1) & 1], X, ld, kc + (ch + 1) * RCH, c0, NP);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -591,10 +595,10 @@ __device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, 
   }
   __syncthreads();
   // ---- C -= V Z, streamed again
-  stage_cols(q.cbuf[0], X, LP, kc, c0, NP);
+  stage_cols(q.cbuf[0], X, ld, kc, c0, NP);
   for (int64_t ch = 0; ch < nch; ++ch) {
     if (ch + 1 < nch) {
-      stage_cols(q.cbuf[(ch + 1) & 1], X, LP, kc + (ch + 1) * RCH, c0, NP);
+      stage_cols(q.cbuf[(ch + 1) & 1], X, ld, kc + (ch + 1) * RCH, c0, NP);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -618,19 +622,131 @@ __device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, 
       cs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] -= acc[c][1];
     }
     __syncthreads();
-    store_cols(X, LP, r0, c0, NP, cs);
+    store_cols(X, ld, r0, c0, NP, cs);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(TPB) svd_qr_kernel(SvdParams P) {
+// Store rows >= rmin of a staged 64 x 32 chunk (rmin even).
+__device__ __forceinline__ void store_cols_from(double* M, int64_t ld, int64_t r0, int64_t col0,
+                                                int64_t ncols, const double* buf, int64_t rmin) {
+#pragma unroll
+  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
+    const int c = threadIdx.x + q * TPB;
+    const int col = c >> 5;
+    const int r2 = (c & 31) * 2;
+    if (col0 + col < ncols && r0 + r2 >= rmin)
+      *reinterpret_cast<double2*>(M + r0 + r2 + (col0 + col) * ld) =
+          *reinterpret_cast<const double2*>(buf + col * XS + r2);
+  }
+}
+
+// LQ half-step update of the band reduction:  C <- C (I - V T V^T) for
+// columns [j0, NP) and rows [rmin, nrows) of A (ld), chunks starting at rc.
+// V[j][c] = pan2[c * prs + j] (explicit, zero outside [j0 + c, NP)).
+__device__ void right_update(QrSmemFixed& q, const double* pan2, int64_t prs, double* A,
+                             int64_t ld, int64_t nrows, int64_t NP, int64_t rc, int64_t rmin,
+                             int64_t j0) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  for (int64_t r0 = rc; r0 < nrows; r0 += RCH) {
+    // ---- Y = C V (64 x 16): warp -> row tile `warp`, column tiles 0..1
+    double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    int buf = 0;
+    stage_cols(q.cbuf[0], A, ld, r0, j0, NP);
+    for (int64_t jb = j0; jb < NP; jb += GW) {
+      if (jb + GW < NP) {
+        stage_cols(q.cbuf[buf ^ 1], A, ld, r0, jb + GW, NP);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* cs = q.cbuf[buf];
+#pragma unroll
+      for (int k4 = 0; k4 < GW / 4; ++k4) {
+        const double a = cs[(k4 * 4 + tq) * XS + warp * 8 + gq];
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct)
+          dmma884(y[ct][0], y[ct][1], a, pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int ct = 0; ct < 2; ++ct) {
+      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq] = y[ct][0];
+      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq + 1] = y[ct][1];
+    }
+    __syncthreads();
+    // ---- Z = Y T (64 x 16), column-major (stride XS) for A fragments
+    for (int e = tid; e < RCH * BW; e += TPB) {
+      const int r = e & 63, c = e >> 6;
+      double acc = 0.0;
+      for (int l = 0; l <= c; ++l) acc += q.yr[r * 17 + l] * q.t[l * 17 + c];
+      q.zr[c * XS + r] = acc;
+    }
+    __syncthreads();
+    // ---- C -= Z V^T, column block by column block
+    buf = 0;
+    stage_cols(q.cbuf[0], A, ld, r0, j0, NP);
+    for (int64_t jb = j0; jb < NP; jb += GW) {
+      if (jb + GW < NP) {
+        stage_cols(q.cbuf[buf ^ 1], A, ld, r0, jb + GW, NP);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      double* cs = q.cbuf[buf];
+      double acc[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < BW / 4; ++k4) {
+        const double a = q.zr[(k4 * 4 + tq) * XS + warp * 8 + gq];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          dmma884(acc[c][0], acc[c][1], a, pan2[(k4 * 4 + tq) * prs + jb + c * 8 + gq]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cs[(c * 8 + 2 * tq) * XS + warp * 8 + gq] -= acc[c][0];
+        cs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] -= acc[c][1];
+      }
+      __syncthreads();
+      store_cols_from(A, ld, r0, jb, NP, cs, rmin);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+}
+
+// Panel -> explicit V (zeros above the pivot, 1 on it) for rows [0, prs).
+__device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0, int64_t nrows) {
+  for (int64_t e = threadIdx.x; e < BW * prs; e += TPB) {
+    const int c = int(e / prs);
+    const int64_t r = e % prs;
+    if (r < k0 + c || r >= nrows) pan[e] = 0.0;
+    else if (r == k0 + c) pan[e] = 1.0;
+  }
+  __syncthreads();
+}
+
+// Load / factorisation kernel (one CTA per slice, persistent):
+//   X (L x n) -> [Householder QR if L > n] -> n x n matrix A (upper
+//   triangular R or X itself) -> [vector jobs on the QR path: R -> rbuf]
+//   -> band reduction  A = Q1 B P1^T  with B upper band (bandwidth 16) by
+//   alternating 16-column QR and 16-row LQ panels (compact-WY updates on
+//   DMMA) -> the 17 diagonals of B to bandbuf.
+__global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
-  const int64_t prs = P.LP + 4;
+  const int64_t LP = P.LP, NP = P.NP, RP = P.RP, n = P.n;
+  const int64_t prs = LP + 36;
   double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
-  const int64_t LP = P.LP, NP = P.NP, RP = P.RP;
   double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
 
   for (;;) {
@@ -642,46 +758,275 @@ __global__ void __launch_bounds__(TPB) svd_qr_kernel(SvdParams P) {
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
     const int flag = load_slice(P, P.A + slice * P.m * P.p, X, q.cbuf[0]);
-    if (tid == 0) P.flags[it] = flag;
+    if (tid == 0) {
+      P.flags[it] = flag;
+      if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
+    }
     if (flag) continue;
     long long t1 = clock64();
-    for (int64_t k0 = 0; k0 < NP; k0 += BW) {
-      const int64_t kc = (k0 / RCH) * RCH;
-      // panel -> shared memory (all LP rows of the 16 columns)
-      for (int64_t e = tid; e < BW * LP; e += TPB) {
-        const int c = int(e / LP);
-        const int64_t r = e % LP;
-        pan[c * prs + r] = X[r + (k0 + c) * LP];
+    // ---------------- QR of the tall X (rows LP)
+    if (P.L > P.n) {
+      for (int64_t k0 = 0; k0 < NP; k0 += BW) {
+        const int64_t kc = (k0 / RCH) * RCH;
+        for (int64_t e = tid; e < BW * prs; e += TPB) {
+          const int c = int(e / prs);
+          const int64_t r = e % prs;
+          pan[e] = r < LP ? X[r + (k0 + c) * LP] : 0.0;
+        }
+        __syncthreads();
+        panel_factor(q, pan, prs, k0, LP);
+        for (int e = tid; e < BW * BW; e += TPB) {
+          const int c = e / BW, r = e % BW;
+          if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+        }
+        __syncthreads();
+        if (k0 + BW < NP) {
+          explicit_v(pan, prs, k0, LP);
+          panel_gram(q, pan, prs, kc, LP);
+          for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
+            trailing_update(q, pan, prs, X, LP, LP, NP, kc, c0);
+        }
+        __syncthreads();
+      }
+      // keep only R (upper triangle of the leading NP x NP block)
+      for (int64_t c = 0; c < NP; ++c)
+        for (int64_t r = tid; r < LP; r += TPB)
+          if (r > c) X[r + c * LP] = 0.0;
+      __syncthreads();
+      if (P.rbuf) {
+        double* R = P.rbuf + it * RP * NP;
+        for (int64_t c = 0; c < NP; ++c)
+          for (int64_t r = tid; r < RP; r += TPB) R[r + c * RP] = X[r + c * LP];
+        __syncthreads();
+      }
+    }
+    long long t2 = clock64();
+    // ---------------- band reduction of the leading NP x NP block (rows RP)
+    for (int64_t k = 0; k < NP; k += BW) {
+      const int64_t kc = (k / RCH) * RCH;
+      for (int64_t e = tid; e < BW * prs; e += TPB) {
+        const int c = int(e / prs);
+        const int64_t r = e % prs;
+        pan[e] = r < RP ? X[r + (k + c) * LP] : 0.0;
       }
       __syncthreads();
-      panel_factor(q, pan, prs, k0, LP);
-      // R part back to global (rows k0..k0+c of panel column c), then make V explicit
-      for (int64_t e = tid; e < BW * BW; e += TPB) {
-        const int c = int(e / BW), r = int(e % BW);
-        if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+      panel_factor(q, pan, prs, k, RP);
+      for (int e = tid; e < BW * BW; e += TPB) {
+        const int c = e / BW, r = e % BW;
+        if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
       }
       __syncthreads();
-      for (int64_t e = tid; e < BW * LP; e += TPB) {
-        const int c = int(e / LP);
-        const int64_t r = e % LP;
-        if (r < k0 + c) pan[c * prs + r] = 0.0;
-        else if (r == k0 + c) pan[c * prs + r] = 1.0;
+      if (k + BW >= NP) break;
+      explicit_v(pan, prs, k, RP);
+      panel_gram(q, pan, prs, kc, RP);
+      for (int64_t c0 = k + BW; c0 < NP; c0 += GW) trailing_update(q, pan, prs, X, LP, RP, NP, kc, c0);
+      __syncthreads();
+      // LQ half-step on rows [k, k+16), columns [k+16, NP)
+      const int64_t j0 = k + BW;
+      for (int64_t e = tid; e < BW * prs; e += TPB) {
+        const int c = int(e / prs);
+        const int64_t j = e % prs;
+        pan[e] = (j >= j0 && j < NP) ? X[(k + c) + j * LP] : 0.0;
       }
       __syncthreads();
-      if (k0 + BW < NP) {
-        panel_gram(q, pan, prs, kc, LP);
-        for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW) trailing_update(q, pan, prs, X, LP, NP, kc, c0);
+      panel_factor(q, pan, prs, j0, NP);
+      for (int e = tid; e < BW * BW; e += TPB) {
+        const int c = e / BW, r = e % BW;  // R2[r][c] -> A[k+c][j0+r]
+        if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
+      }
+      __syncthreads();
+      if (j0 + BW < NP || true) {
+        explicit_v(pan, prs, j0, NP);
+        panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
+        right_update(q, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
       }
       __syncthreads();
     }
-    // R -> per-slice buffer (RP x NP), zero below the diagonal and in padding rows
-    double* R = P.rbuf + it * RP * NP;
-    for (int64_t c = 0; c < NP; ++c)
-      for (int64_t r = tid; r < RP; r += TPB) R[r + c * RP] = (r <= c && r < NP) ? X[r + c * LP] : 0.0;
+    // ---------------- the 17 diagonals of the band
+    double* band = P.bandbuf + it * (BW + 1) * NP;
+    for (int64_t e = tid; e < (BW + 1) * NP; e += TPB) {
+      const int64_t d = e / NP, i = e % NP;
+      band[e] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
+    }
     __syncthreads();
-    long long t2 = clock64();
+    long long t3 = clock64();
     stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
     stat_add(P, ST_CYC_QR, (unsigned long long)(t2 - t1));
+    stat_add(P, ST_CYC_BAND, (unsigned long long)(t3 - t2));
+  }
+}
+
+// ----------------------------------------------------------------------
+// Band (bandwidth 16) -> upper bidiagonal by Givens bulge chasing, one
+// warp per slice with the band (+ one fill diagonal on each side) in
+// shared memory.  Row i's extra entries are annihilated outermost first
+// with a column rotation; the fill below the diagonal is chased down by
+// alternating row / column rotations in steps of 16.
+// ----------------------------------------------------------------------
+constexpr int BWS = BW + 3;  // band row stride: offsets -1 .. BW+1
+
+__device__ __forceinline__ double& BEL(double* W, int i, int j) {
+  return W[i * BWS + (j - i + 1)];
+}
+
+// Rotation [c s; -s c] with c x + s y = r, -s x + c y = 0.  Division-free:
+// one rsqrt of x^2 + y^2 (scaled only when that would over/underflow).
+__device__ __forceinline__ void givens(double x, double y, double& c, double& s) {
+  if (y == 0.0) {
+    c = 1.0;
+    s = 0.0;
+    return;
+  }
+  double r2 = fma(x, x, y * y);
+  if (!(r2 > 1e-290 && r2 < 1e290)) {
+    const double ax = fabs(x), ay = fabs(y);
+    const double inv = 1.0 / (ax > ay ? ax : ay);
+    x *= inv;
+    y *= inv;
+    r2 = fma(x, x, y * y);
+  }
+  const double rinv = rsqrt(r2);
+  c = x * rinv;
+  s = y * rinv;
+}
+
+__global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* W = reinterpret_cast<double*>(smem_raw);
+  const int lane = threadIdx.x;
+  const int64_t n = P.n, NP = P.NP;
+  for (;;) {
+    int64_t it = 0;
+    if (lane == 0) it = int64_t(atomicAdd(&P.counter[2], 1ull));
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= P.count) break;
+    if (P.flags[it]) continue;
+    long long t0 = clock64();
+    const double* band = P.bandbuf + it * (BW + 1) * NP;
+    for (int64_t e = lane; e < n * BWS; e += 32) {
+      const int64_t i = e / BWS, k = e % BWS;
+      const int64_t d = k - 1;
+      W[e] = (d >= 0 && d <= BW && i + d < n) ? band[d * NP + i] : 0.0;
+    }
+    __syncwarp();
+    const int nn = int(n);
+    for (int i = 0; i + 2 < nn; ++i) {
+      const int jtop = (i + BW < nn - 1) ? i + BW : nn - 1;
+      for (int j = jtop; j >= i + 2; --j) {
+        double c, s;
+        givens(BEL(W, i, j - 1), BEL(W, i, j), c, s);
+        __syncwarp();
+        if (s == 0.0) continue;
+        {  // columns (j-1, j), rows i .. j; lane 0 owns the annihilated entry
+          const int r = i + lane;
+          if (r <= j) {
+            const double a = BEL(W, r, j - 1), b = BEL(W, r, j);
+            BEL(W, r, j - 1) = c * a + s * b;
+            BEL(W, r, j) = lane ? -s * a + c * b : 0.0;
+          }
+        }
+        __syncwarp();
+        int rr = j;
+        while (true) {
+          // row rotation (rr-1, rr) annihilating the fill at (rr, rr-1)
+          givens(BEL(W, rr - 1, rr - 1), BEL(W, rr, rr - 1), c, s);
+          __syncwarp();
+          if (s != 0.0) {
+            const int cend = (rr + BW < nn - 1) ? rr + BW : nn - 1;
+            const int col = rr - 1 + lane;
+            if (col <= cend) {
+              const double a = BEL(W, rr - 1, col), b = BEL(W, rr, col);
+              BEL(W, rr - 1, col) = c * a + s * b;
+              BEL(W, rr, col) = lane ? -s * a + c * b : 0.0;
+            }
+            __syncwarp();
+          }
+          const int cc = rr + BW;
+          if (cc >= nn) break;
+          // column rotation (cc-1, cc) annihilating the fill at (rr-1, cc)
+          givens(BEL(W, rr - 1, cc - 1), BEL(W, rr - 1, cc), c, s);
+          __syncwarp();
+          if (s == 0.0) break;
+          const int r2 = rr - 1 + lane;
+          if (r2 <= cc) {
+            const double a = BEL(W, r2, cc - 1), b = BEL(W, r2, cc);
+            BEL(W, r2, cc - 1) = c * a + s * b;
+            BEL(W, r2, cc) = lane ? -s * a + c * b : 0.0;
+          }
+          __syncwarp();
+          rr = cc;
+        }
+      }
+    }
+    double* de = P.debuf + it * 2 * NP;
+    for (int64_t i = lane; i < NP; i += 32) {
+      de[i] = i < n ? BEL(W, i, i) : 0.0;
+      de[NP + i] = i + 1 < n ? BEL(W, i, i + 1) : 0.0;
+    }
+    __syncwarp();
+    long long t1 = clock64();
+    if (lane == 0 && P.stats) atomicAdd(&g_stats[ST_CYC_BULGE], (unsigned long long)(t1 - t0));
+  }
+}
+
+// ----------------------------------------------------------------------
+// Singular values of the upper bidiagonal (d, e) by bisection on the
+// Golub-Kahan tridiagonal T_GK (zero diagonal, off-diagonals d0,e0,d1,...),
+// whose eigenvalues are +-sigma: #sigma < x = (#negative Sturm pivots of
+// T_GK - x I) - n.  One thread per (slice, sigma_j), sigma_j the j-th
+// largest; interval shrunk to 2u * max(sigma_j, 1e-3 * bound).
+// ----------------------------------------------------------------------
+__device__ __forceinline__ int64_t count_below(const double* d, const double* e, int64_t n, double x,
+                                               double pivmin) {
+  int64_t neg = 0;
+  double q = -x;
+  neg += (q < 0.0);
+  for (int64_t k = 0; k < 2 * n - 1; ++k) {
+    const double a = (k & 1) ? e[k >> 1] : d[k >> 1];
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - (a * a) / q;
+    neg += (q < 0.0);
+  }
+  return neg - n;
+}
+
+__global__ void svd_bisect_kernel(SvdParams P) {
+  const int64_t n = P.n, NP = P.NP;
+  const int64_t total = P.count * n;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t it = g / n, j = g % n;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int flag = P.flags[it];
+    if (flag == 2) continue;
+    double sigma = 0.0;
+    if (flag == 0) {
+      const double* d = P.debuf + it * 2 * NP;
+      const double* e = d + NP;
+      double bound = 0.0, amax = 0.0;
+      for (int64_t k = 0; k < n; ++k) {
+        const double dk = fabs(d[k]), ek = (k + 1 < n) ? fabs(e[k]) : 0.0;
+        const double ekm = k > 0 ? fabs(e[k - 1]) : 0.0;
+        bound = fmax(bound, fmax(dk + ek, dk + ekm));
+        amax = fmax(amax, fmax(dk, ek));
+      }
+      if (bound > 0.0) {
+        const double pivmin = fmax(DBL_MIN, amax * amax * 1e-300);
+        const int64_t target = n - 1 - j;  // want count_below(x) <= target
+        double lo = 0.0, hi = bound * (1.0 + 4.0 * DBL_EPSILON) + DBL_MIN;
+        for (int iter = 0; iter < 120; ++iter) {
+          const double mid = 0.5 * (lo + hi);
+          if (!(mid > lo && mid < hi)) break;
+          if (hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, 1e-3 * bound)) break;
+          if (count_below(d, e, n, mid, pivmin) <= target)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        sigma = 0.5 * (lo + hi);
+      }
+    }
+    P.s[j + slice * n] = sigma;
   }
 }
 
@@ -894,8 +1239,12 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
         __syncthreads();
       }
     }
-    if (P.s)
+    // Reported sigma: the bidiagonal/bisection values when that path ran
+    // (so values-only, full and truncated jobs agree bitwise), else the
+    // Jacobi column norms.
+    if (P.s && !P.bidiag)
       for (int64_t j = tid; j < r; j += TPB) P.s[j + slice * r] = fs.key[j];
+    __syncthreads();
 
     if (WANTV && P.job != STARM_SVD_VALUES) {
       __syncthreads();
@@ -948,7 +1297,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
           }
           for (int64_t e = tid; e < kout * n; e += TPB) {
             const int64_t j = e % kout, col = e / kout;
-            G[e] = fs.key[j] * V[col + int64_t(fs.idx[j]) * RP];
+            G[e] = P.s[j + slice * r] * V[col + int64_t(fs.idx[j]) * RP];
           }
         } else {
           for (int64_t j = 0; j < kout; ++j) {
@@ -957,7 +1306,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
           }
           for (int64_t e = tid; e < kout * L; e += TPB) {
             const int64_t j = e % kout, col = e / kout;
-            G[e] = fs.key[j] * Qb[col + int64_t(qc ? qc[j] : j) * ldq];
+            G[e] = P.s[j + slice * r] * Qb[col + int64_t(qc ? qc[j] : j) * ldq];
           }
         }
       }
@@ -985,26 +1334,26 @@ __global__ void reset_status_kernel(int32_t* status, unsigned long long* counter
 
 struct Plan {
   int64_t L, n, LP, NP, RP;
-  bool transposed, use_qr, wantv;
+  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s;
   int ns;
-  size_t jsmem, qsmem;
-  int slots_j, slots_q;
-  size_t off_x, off_w, off_r, off_f, total;
+  size_t jsmem, rsmem, bsmem;
+  int slots_j, slots_r, slots_b, bisect_blocks;
+  size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, total;
 };
 
 int g_tune_inner = 1;
 int g_tune_sweeps = 60;
-int g_tune_qr = 1;  // 1 = shape rule, 0 = never, 2 = always when it fits
+int g_tune_mode = 1;  // 1 = bidiagonal values path when the panel fits, 0 = Jacobi only
 int g_stats_on = 0;
 
-int occupancy(const void* fn, size_t smem, int* per_sm) {
+int occupancy(const void* fn, int threads, size_t smem, int* per_sm) {
   STARM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  STARM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, TPB, smem));
+  STARM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, threads, smem));
   if (*per_sm < 1) *per_sm = 1;
   return STARM_OK;
 }
 
-int make_plan(int64_t m, int64_t p, int64_t count, int job, Plan* pl) {
+int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, bool have_s, Plan* pl) {
   Plan g{};
   g.L = m > p ? m : p;
   g.n = m < p ? m : p;
@@ -1014,37 +1363,51 @@ int make_plan(int64_t m, int64_t p, int64_t count, int job, Plan* pl) {
   g.NP = round_up(g.n, BW);
   if (g.NP < GW) g.NP = GW;
   g.RP = round_up(g.NP, RCH);
-  bool tall = 4 * g.L >= 5 * g.n;
-  g.use_qr = (g_tune_qr == 2 || (g_tune_qr == 1 && tall)) && g.LP <= QR_MAX_LP;
+  g.bidiag = g_tune_mode == 1 && g.LP <= QR_MAX_LP;
+  g.use_qr = g.bidiag && g.L > g.n;
+  g.run_jacobi = g.wantv || !g.bidiag;
+  g.internal_s = g.wantv && !have_s;
   g.ns = 1;
   while (g.ns < g.n) g.ns <<= 1;
   g.jsmem = jacobi_smem_bytes(g.ns);
-  g.qsmem = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 4) * sizeof(double);
+  g.rsmem = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
+  g.bsmem = size_t(g.NP) * BWS * sizeof(double);
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
   STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int rc = g.wantv ? occupancy((const void*)svd_jacobi_kernel<true>, g.jsmem, &per)
-                   : occupancy((const void*)svd_jacobi_kernel<false>, g.jsmem, &per);
-  if (rc) return rc;
-  g.slots_j = int(count < int64_t(sms) * per ? count : int64_t(sms) * per);
-  if (g.slots_j < 1) g.slots_j = 1;
-  g.slots_q = 0;
-  if (g.use_qr) {
-    rc = occupancy((const void*)svd_qr_kernel, g.qsmem, &per);
+  auto clampc = [&](int64_t v) { return int(v < 1 ? 1 : (v > count ? count : v)); };
+  int rc;
+  if (g.run_jacobi) {
+    rc = g.wantv ? occupancy((const void*)svd_jacobi_kernel<true>, TPB, g.jsmem, &per)
+                 : occupancy((const void*)svd_jacobi_kernel<false>, TPB, g.jsmem, &per);
     if (rc) return rc;
-    g.slots_q = int(count < int64_t(sms) * per ? count : int64_t(sms) * per);
-    if (g.slots_q < 1) g.slots_q = 1;
+    g.slots_j = clampc(int64_t(sms) * per);
   }
-  const int64_t xslots = g.slots_j > g.slots_q ? g.slots_j : g.slots_q;
+  if (g.bidiag) {
+    rc = occupancy((const void*)svd_reduce_kernel, TPB, g.rsmem, &per);
+    if (rc) return rc;
+    g.slots_r = clampc(int64_t(sms) * per);
+    rc = occupancy((const void*)svd_bulge_kernel, 32, g.bsmem, &per);
+    if (rc) return rc;
+    g.slots_b = clampc(int64_t(sms) * per);
+    int64_t bb = (count * g.n + 127) / 128;
+    g.bisect_blocks = int(bb < int64_t(sms) * 16 ? bb : int64_t(sms) * 16);
+    if (g.bisect_blocks < 1) g.bisect_blocks = 1;
+  }
+  const int64_t xslots = g.slots_j > g.slots_r ? g.slots_j : g.slots_r;
   size_t off = 256;
-  g.off_x = off;
-  off += size_t(xslots) * g.LP * g.NP * sizeof(double);
-  g.off_w = off;
-  if (g.wantv) off += size_t(g.slots_j) * g.RP * g.NP * sizeof(double);
-  g.off_r = off;
-  if (g.use_qr) off += size_t(count) * g.RP * g.NP * sizeof(double);
-  g.off_f = off;
-  if (g.use_qr) off += round_up(count * 4, 256);
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  g.off_x = take(size_t(xslots) * g.LP * g.NP * sizeof(double));
+  g.off_w = take(g.wantv ? size_t(g.slots_j) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_r = take((g.use_qr && g.wantv) ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_f = take(size_t(count) * 4);
+  g.off_band = take(g.bidiag ? size_t(count) * (BW + 1) * g.NP * sizeof(double) : 0);
+  g.off_de = take(g.bidiag ? size_t(count) * 2 * g.NP * sizeof(double) : 0);
+  g.off_s = take(g.internal_s ? size_t(nslices) * g.n * sizeof(double) : 0);
   g.total = off;
   *pl = g;
   return STARM_OK;
@@ -1055,17 +1418,19 @@ int make_plan(int64_t m, int64_t p, int64_t count, int job, Plan* pl) {
 
 using namespace starm;
 
-extern "C" size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t count, int job) {
-  if (m < 1 || p < 1 || count < 1) return 0;
+extern "C" size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t nslices, int64_t count,
+                                            int job) {
+  if (m < 1 || p < 1 || nslices < 1) return 0;
+  if (count < 1 || count > nslices) count = nslices;
   Plan pl;
-  if (make_plan(m, p, count, job, &pl) != STARM_OK) return 0;
+  if (make_plan(m, p, count, nslices, job, false, &pl) != STARM_OK) return 0;
   return pl.total;
 }
 
-extern "C" int starm_svd_tune(int max_inner, int max_sweeps, int qr_mode, int stats) {
+extern "C" int starm_svd_tune(int max_inner, int max_sweeps, int mode, int stats) {
   if (max_inner > 0) g_tune_inner = max_inner;
   if (max_sweeps > 0) g_tune_sweeps = max_sweeps;
-  if (qr_mode >= 0) g_tune_qr = qr_mode;
+  if (mode >= 0) g_tune_mode = mode;
   if (stats >= 0) g_stats_on = stats;
   return STARM_OK;
 }
@@ -1105,7 +1470,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   STARM_LAUNCH_CHECK();
   if (count <= 0) return STARM_OK;
   Plan pl;
-  int rc = make_plan(m, p, count, job, &pl);
+  int rc = make_plan(m, p, count, nslices, job, s != nullptr, &pl);
   if (rc != STARM_OK) return rc;
   STARM_CHECK_ARG(ws_bytes >= pl.total, "svd: workspace too small (%zu < %zu)", ws_bytes, pl.total);
   char* base = reinterpret_cast<char*>(ws);
@@ -1118,7 +1483,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.ids = slice_ids;
   P.count = count;
   P.job = job;
-  P.s = s;
+  P.s = pl.internal_s ? reinterpret_cast<double*>(base + pl.off_s) : s;
   P.u = u;
   P.v = v;
   P.ranks = ranks;
@@ -1130,8 +1495,10 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.counter = counters;
   P.xslots = reinterpret_cast<double*>(base + pl.off_x);
   P.wslots = reinterpret_cast<double*>(base + pl.off_w);
-  P.rbuf = reinterpret_cast<double*>(base + pl.off_r);
+  P.rbuf = (pl.use_qr && pl.wantv) ? reinterpret_cast<double*>(base + pl.off_r) : nullptr;
   P.flags = reinterpret_cast<int32_t*>(base + pl.off_f);
+  P.bandbuf = reinterpret_cast<double*>(base + pl.off_band);
+  P.debuf = reinterpret_cast<double*>(base + pl.off_de);
   P.L = pl.L;
   P.n = pl.n;
   P.LP = pl.LP;
@@ -1139,19 +1506,26 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.RP = pl.RP;
   P.transposed = pl.transposed;
   P.use_qr = pl.use_qr;
+  P.bidiag = pl.bidiag;
   P.stats = g_stats_on;
-  // Convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).
+  // Jacobi convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).
   P.tol = double(pl.L > 32 ? pl.L : 32) * DBL_EPSILON;
   P.max_sweeps = g_tune_sweeps;
   P.max_inner = g_tune_inner;
-  if (pl.use_qr) {
-    svd_qr_kernel<<<pl.slots_q, TPB, pl.qsmem, st>>>(P);
+  if (pl.bidiag) {
+    svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
+    STARM_LAUNCH_CHECK();
+    svd_bulge_kernel<<<pl.slots_b, 32, pl.bsmem, st>>>(P);
+    STARM_LAUNCH_CHECK();
+    svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
     STARM_LAUNCH_CHECK();
   }
-  if (pl.wantv)
-    svd_jacobi_kernel<true><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
-  else
-    svd_jacobi_kernel<false><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
-  STARM_LAUNCH_CHECK();
+  if (pl.run_jacobi) {
+    if (pl.wantv)
+      svd_jacobi_kernel<true><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
+    else
+      svd_jacobi_kernel<false><<<pl.slots_j, TPB, pl.jsmem, st>>>(P);
+    STARM_LAUNCH_CHECK();
+  }
   return STARM_OK;
 }

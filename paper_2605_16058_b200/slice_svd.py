@@ -170,7 +170,7 @@ def _svd_launch(x: DeviceTensor, job, ids=None, s=None, u=None, v=None, ranks=No
         return
     status = torch.empty(2, dtype=torch.int32, device=dev)
     lib = nat.load()
-    nbytes = lib.starm_svd_workspace_bytes(m, p, count, job)
+    nbytes = lib.starm_svd_workspace_bytes(m, p, n, count, job)
     ws = nat.workspace(nbytes, dev)
     nat.call("starm_svd_f64", x.data.data_ptr(), m, p, n, nat.ptr(ids), count, job, nat.ptr(s),
              nat.ptr(u), nat.ptr(v), nat.ptr(ranks), nat.ptr(u_off), nat.ptr(g_off),
