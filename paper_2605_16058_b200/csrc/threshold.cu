@@ -46,17 +46,47 @@ __global__ void square_keys_kernel(const double* s, int64_t count, unsigned long
 }
 
 // Sequential running sums (np.cumsum) and the lower_bound search.
-__global__ void cumsum_search_kernel(const unsigned long long* vbits, int64_t count, double eps,
-                                     double* w, double* v_out, ThState* st) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One warp: tiles of 1024 sorted values are staged in shared memory by all
+// lanes (coalesced), lane 0 runs the strictly sequential fp64 chain, and the
+// running sums go back out coalesced.  The chain itself is the only serial
+// part (one dependent DADD per value).
+constexpr int CS_TILE = 1024;
+
+__global__ void __launch_bounds__(32) cumsum_search_kernel(const unsigned long long* vbits,
+                                                           int64_t count, double eps, double* w,
+                                                           double* v_out, ThState* st) {
+  __shared__ double tile[CS_TILE];
+  __shared__ double wt[CS_TILE];
+  const int lane = threadIdx.x;
   const double* v = reinterpret_cast<const double*>(vbits);
   double acc = 0.0;
-  for (int64_t k = 0; k < count; ++k) {
-    const double x = v[k];
-    acc = (k == 0) ? x : __dadd_rn(acc, x);
-    w[k] = acc;
-    if (v_out) v_out[k] = x;
+  for (int64_t base = 0; base < count; base += CS_TILE) {
+    const int len = int(count - base < CS_TILE ? count - base : CS_TILE);
+    for (int k = lane; k < len; k += 32) {
+      const double x = v[base + k];
+      tile[k] = x;
+      if (v_out) v_out[base + k] = x;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int k = 0;
+      if (base == 0) {
+        acc = tile[0];
+        wt[0] = acc;
+        k = 1;
+      }
+#pragma unroll 8
+      for (; k < len; ++k) {
+        acc = __dadd_rn(acc, tile[k]);
+        wt[k] = acc;
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < len; k += 32) w[base + k] = wt[k];
+    __syncwarp();
   }
+  acc = __shfl_sync(0xffffffffu, acc, 0);
+  if (lane != 0) return;
   const double total = count ? acc : 0.0;
   st->total = total;
   if (total == 0.0) {
