@@ -78,6 +78,15 @@ struct SvdParams {
   int32_t* flags;               // per-slice load flags (reduce kernel)
   double* bandbuf;              // per-slice 17 diagonals (17 x NP)
   double* debuf;                // per-slice bidiagonal d, e (2 x NP)
+  // bidiagonal vector path (vector jobs): logs of the right-side transforms
+  double* rvlog;                // per slice, per LQ panel: V (16 x NP) then T (16 x 16)
+  double* rotcs;                // per slice: rotcap (c, s) of the bulge column rotations
+  int32_t* rotcol;              // per slice: rotcap column indices (second column)
+  int64_t* rotcnt;              // per slice: rotations logged
+  int64_t rotcap;
+  double* vsel;                 // per slice: right singular vectors (RP x NP)
+  double* iiscr;                // inverse-iteration scratch
+  int btw;                      // back-transform vectors per pass
   int64_t L, n, LP, NP, RP;
   int transposed, use_qr, bidiag, stats;
   double tol;
@@ -838,6 +847,11 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       if (j0 + BW < NP || true) {
         explicit_v(pan, prs, j0, NP);
         panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
+        if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
+          double* dst = P.rvlog + (it * (NP / BW) + k / BW) * (BW * NP + BW * BW);
+          for (int64_t e = tid; e < BW * NP; e += TPB) dst[e] = pan[(e / NP) * prs + (e % NP)];
+          for (int e = tid; e < BW * BW; e += TPB) dst[BW * NP + e] = q.t[(e / BW) * 17 + (e % BW)];
+        }
         right_update(q, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
       }
       __syncthreads();
@@ -910,6 +924,11 @@ __global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
     }
     __syncwarp();
     const int nn = int(n);
+    // vector jobs: log every column rotation (c, s, second column) so the
+    // right singular vectors can be back-transformed (svd_backtransform_kernel)
+    int64_t nlog = 0;
+    double* lcs = P.rotcs ? P.rotcs + it * P.rotcap * 2 : nullptr;
+    int32_t* lcol = P.rotcol ? P.rotcol + it * P.rotcap : nullptr;
     for (int i = 0; i + 2 < nn; ++i) {
       const int jtop = (i + BW < nn - 1) ? i + BW : nn - 1;
       for (int j = jtop; j >= i + 2; --j) {
@@ -917,6 +936,12 @@ __global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
         givens(BEL(W, i, j - 1), BEL(W, i, j), c, s);
         __syncwarp();
         if (s == 0.0) continue;
+        if (lcs && lane == 0 && nlog < P.rotcap) {
+          lcs[2 * nlog] = c;
+          lcs[2 * nlog + 1] = s;
+          lcol[nlog] = j;
+        }
+        ++nlog;
         {  // columns (j-1, j), rows i .. j; lane 0 owns the annihilated entry
           const int r = i + lane;
           if (r <= j) {
@@ -947,6 +972,12 @@ __global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
           givens(BEL(W, rr - 1, cc - 1), BEL(W, rr - 1, cc), c, s);
           __syncwarp();
           if (s == 0.0) break;
+          if (lcs && lane == 0 && nlog < P.rotcap) {
+            lcs[2 * nlog] = c;
+            lcs[2 * nlog + 1] = s;
+            lcol[nlog] = cc;
+          }
+          ++nlog;
           const int r2 = rr - 1 + lane;
           if (r2 <= cc) {
             const double a = BEL(W, r2, cc - 1), b = BEL(W, r2, cc);
@@ -958,6 +989,7 @@ __global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
         }
       }
     }
+    if (lcs && lane == 0) P.rotcnt[it] = nlog < P.rotcap ? nlog : P.rotcap;
     double* de = P.debuf + it * 2 * NP;
     for (int64_t i = lane; i < NP; i += 32) {
       de[i] = i < n ? BEL(W, i, i) : 0.0;
@@ -1089,6 +1121,349 @@ __device__ void gemm_xv(const SvdParams& P, JacobiSmem& sm, const double* A, con
   __syncthreads();
 }
 
+
+// slicesvd.py:51-54: an all-zero slice has zero values and identity bases.
+__device__ void emit_zero_slice(const SvdParams& P, int64_t slice) {
+  const int tid = threadIdx.x;
+  const int64_t r = P.n;
+  if (P.s)
+    for (int64_t j = tid; j < r; j += blockDim.x) P.s[j + slice * r] = 0.0;
+  if (P.job == STARM_SVD_FULL) {
+    double* U = P.u + slice * P.m * r;
+    double* Vo = P.v + slice * P.p * r;
+    for (int64_t e = tid; e < P.m * r; e += blockDim.x) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
+    for (int64_t e = tid; e < P.p * r; e += blockDim.x) Vo[e] = ((e % P.p) == (e / P.p)) ? 1.0 : 0.0;
+  } else if (P.job == STARM_SVD_TRUNCATED) {
+    const int64_t k = P.ranks[slice];
+    double* U = P.u_data + P.u_off[slice];
+    double* G = P.g_data + P.g_off[slice];
+    for (int64_t e = tid; e < P.m * k; e += blockDim.x) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
+    for (int64_t e = tid; e < k * P.p; e += blockDim.x) G[e] = 0.0;
+  }
+  __syncthreads();
+}
+
+// Write the requested factors of one slice given the right singular vectors
+// of the working matrix X (columns vidx[j] of V, ld RP, j in descending sigma
+// order) and sigma in P.s.  The other side is X V normalised: recomputed
+// from the input slice (qgemm) or taken from the Jacobi target T (= X V).
+// Columns whose sigma is below 1e-4 sigma_max are re-orthonormalised (CGS2).
+__device__ void emit_vectors(const SvdParams& P, JacobiSmem& sm, FinalView& fs, int64_t slice,
+                             const double* A, const double* V, const int* vidx, double* Xslot,
+                             bool qgemm, double* T, int64_t ldt) {
+  const int tid = threadIdx.x;
+  const int64_t L = P.L, n = P.n, LP = P.LP, RP = P.RP, r = n;
+  const double* sg = P.s + slice * r;
+  const double smax = sg[0];
+  const int64_t kout = (P.job == STARM_SVD_FULL) ? r : P.ranks[slice];
+  double* Qb;
+  int64_t ldq;
+  const int* qc;
+  if (qgemm) {
+    gemm_xv(P, sm, A, V, vidx, kout, Xslot);
+    Qb = Xslot;
+    ldq = LP;
+    qc = nullptr;
+  } else {
+    Qb = T;
+    ldq = ldt;
+    qc = vidx;
+  }
+  // normalise by the actual column norms (deterministic warp-per-column sums)
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int64_t j = warp; j < kout; j += TPB / 32) {
+      double* col = Qb + int64_t(qc ? qc[j] : j) * ldq;
+      double acc = 0.0;
+      for (int64_t rr = lane; rr < L; rr += 32) acc += col[rr] * col[rr];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const double nrm = sqrt(acc);
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      for (int64_t rr = lane; rr < L; rr += 32) col[rr] *= inv;
+    }
+  }
+  __syncthreads();
+  for (int64_t j = 0; j < kout; ++j)
+    if (!(sg[j] > 1e-4 * smax)) cgs2_fix(fs, Qb, ldq, L, qc, int(j));
+  __syncthreads();
+  if (P.job == STARM_SVD_FULL) {
+    double* Uo = P.u + slice * P.m * r;
+    double* Vo = P.v + slice * P.p * r;
+    double* Qd = P.transposed ? Vo : Uo;  // ld L
+    double* Wd = P.transposed ? Uo : Vo;  // ld n
+    for (int64_t j = 0; j < kout; ++j) {
+      const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
+      for (int64_t rr = tid; rr < L; rr += TPB) Qd[rr + j * L] = qcol[rr];
+      const double* vcol = V + int64_t(vidx[j]) * RP;
+      for (int64_t rr = tid; rr < n; rr += TPB) Wd[rr + j * n] = vcol[rr];
+    }
+  } else {
+    double* Uk = P.u_data + P.u_off[slice];
+    double* G = P.g_data + P.g_off[slice];
+    if (!P.transposed) {
+      for (int64_t j = 0; j < kout; ++j) {
+        const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
+        for (int64_t rr = tid; rr < L; rr += TPB) Uk[rr + j * L] = qcol[rr];
+      }
+      for (int64_t e = tid; e < kout * n; e += TPB) {
+        const int64_t j = e % kout, col = e / kout;
+        G[e] = sg[j] * V[col + int64_t(vidx[j]) * RP];
+      }
+    } else {
+      for (int64_t j = 0; j < kout; ++j) {
+        const double* vcol = V + int64_t(vidx[j]) * RP;
+        for (int64_t rr = tid; rr < n; rr += TPB) Uk[rr + j * n] = vcol[rr];
+      }
+      for (int64_t e = tid; e < kout * L; e += TPB) {
+        const int64_t j = e % kout, col = e / kout;
+        G[e] = sg[j] * Qb[col + int64_t(qc ? qc[j] : j) * ldq];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ======================================================================
+//        Vectors on the bidiagonal path (no Jacobi): inverse iteration
+//        on T_GK + back-transformation through the logged right-side
+//        transformations (bulge column rotations, band LQ reflectors).
+// ======================================================================
+
+__device__ __forceinline__ int64_t kout_of(const SvdParams& P, int64_t slice) {
+  return (P.job == STARM_SVD_FULL) ? P.n : P.ranks[slice];
+}
+
+// Right singular vectors of the bidiagonal (d, e) for sigma_j, j < k, by
+// inverse iteration on T_GK - sigma_j I (tridiagonal LU with partial
+// pivoting, LAPACK dgttrf/dgttrs), 3 solves from a fixed start vector.  The
+// even entries of the T_GK eigenvector are v (B v = sigma u).  One thread per
+// (slice, j); per-thread scratch of 5 x 2n doubles.
+__global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
+  const int64_t n = P.n, NP = P.NP, RP = P.RP, N2 = 2 * P.n;
+  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  double* scr = P.iiscr + gtid * 5 * 2 * NP;
+  double* dd = scr;
+  double* du = dd + 2 * NP;
+  double* du2 = du + 2 * NP;
+  double* dl = du2 + 2 * NP;  // multipliers
+  double* z = dl + 2 * NP;    // 1.0 where rows i, i+1 were interchanged
+  for (int64_t g = gtid; g < total_work; g += nthreads) {
+    const int64_t it = g / n, j = g % n;
+    if (P.flags[it]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    if (j >= kout_of(P, slice)) continue;
+    const double* bd = P.debuf + it * 2 * NP;
+    const double* be = bd + NP;
+    const double lam = P.s[j + slice * n];
+    double tnorm = 0.0;
+    for (int64_t k = 0; k < n; ++k) tnorm = fmax(tnorm, fabs(bd[k]) + (k + 1 < n ? fabs(be[k]) : 0.0));
+    const double pert = fmax(tnorm * DBL_EPSILON, DBL_MIN);
+    // factor T - lam I (diagonal -lam, off-diagonals a_k = d0, e0, d1, ...)
+    for (int64_t i = 0; i < N2; ++i) {
+      dd[i] = -lam;
+      du[i] = (i + 1 < N2) ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0;
+      du2[i] = 0.0;
+    }
+    for (int64_t i = 0; i + 1 < N2; ++i) {
+      // original sub-diagonal (T is symmetric); du[i] may already hold fill
+      const double sub = (i & 1) ? be[i >> 1] : bd[i >> 1];
+      if (fabs(dd[i]) >= fabs(sub)) {
+        if (dd[i] == 0.0) dd[i] = pert;
+        const double fact = sub / dd[i];
+        dl[i] = fact;
+        dd[i + 1] -= fact * du[i];
+        z[i] = 0.0;
+      } else {
+        const double fact = dd[i] / sub;
+        dd[i] = sub;
+        dl[i] = fact;
+        const double temp = du[i];
+        du[i] = dd[i + 1];
+        dd[i + 1] = temp - fact * dd[i + 1];
+        if (i + 2 < N2) {
+          du2[i] = du[i + 1];
+          du[i + 1] = -fact * du[i + 1];
+        }
+        z[i] = 1.0;
+      }
+    }
+    if (dd[N2 - 1] == 0.0) dd[N2 - 1] = pert;
+    double* vout = P.vsel + it * RP * NP + j * RP;
+    double* x = P.iiscr + nthreads * 5 * 2 * NP + gtid * 2 * NP;  // the iterate
+    for (int64_t i = 0; i < N2; ++i)
+      x[i] = 1.0 + 0.25 * double(((i + 1) * 7919 + (j + 1) * 104729) % 97) / 97.0;
+    for (int iter = 0; iter < 3; ++iter) {
+      // forward: apply L and the row interchanges
+      for (int64_t i = 0; i + 1 < N2; ++i) {
+        if (z[i] != 0.0) {
+          const double t = x[i];
+          x[i] = x[i + 1];
+          x[i + 1] = t - dl[i] * x[i + 1];
+        } else {
+          x[i + 1] -= dl[i] * x[i];
+        }
+      }
+      // backward: U has diagonal dd, super du, second super du2
+      x[N2 - 1] /= dd[N2 - 1];
+      if (N2 > 1) x[N2 - 2] = (x[N2 - 2] - du[N2 - 2] * x[N2 - 1]) / dd[N2 - 2];
+      for (int64_t i = N2 - 3; i >= 0; --i)
+        x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
+      double nrm = 0.0;
+      for (int64_t i = 0; i < N2; ++i) nrm = fmax(nrm, fabs(x[i]));
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+      for (int64_t i = 0; i < N2; ++i) x[i] *= inv;
+    }
+    // v = even entries, unit 2-norm
+    double nv = 0.0;
+    for (int64_t i = 0; i < n; ++i) nv += x[2 * i] * x[2 * i];
+    const double inv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;
+    for (int64_t i = 0; i < RP; ++i) vout[i] = (i < n) ? x[2 * i] * inv : 0.0;
+  }
+}
+
+// One warp per slice: (1) Gram-Schmidt twice of the k bidiagonal vectors in
+// order (a vanished vector is replaced by a canonical basis vector), then
+// (2) back-transformation v <- P1 P2 v: the logged bulge-chasing column
+// rotations in reverse order, then the band-reduction LQ reflectors
+// (I - V T V^T) from the last panel to the first.  Vectors are processed 32
+// at a time, one per lane, staged in shared memory.
+__global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* vm = reinterpret_cast<double*>(smem_raw);  // [P.btw][ls]
+  const int lane = threadIdx.x;
+  const int64_t n = P.n, NP = P.NP, RP = P.RP;
+  const int64_t npan = NP / BW;
+  const int64_t ls = n | 1;  // odd lane stride: conflict-free column access
+  for (;;) {
+    int64_t it = 0;
+    if (lane == 0) it = int64_t(atomicAdd(&P.counter[3], 1ull));
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= P.count) break;
+    if (P.flags[it]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int64_t k = kout_of(P, slice);
+    double* Vb = P.vsel + it * RP * NP;
+    // ---- (1) orthonormalise the bidiagonal vectors (CGS2 with fallback)
+    for (int64_t j = 0; j < k; ++j) {
+      double* vj = Vb + j * RP;
+      int64_t basis = 0;
+      for (int attempt = 0; attempt < 4 + j; ++attempt) {
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int64_t i = 0; i < j; ++i) {
+            const double* vi = Vb + i * RP;
+            double d = 0.0;
+            for (int64_t q = lane; q < n; q += 32) d += vi[q] * vj[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            for (int64_t q = lane; q < n; q += 32) vj[q] -= d * vi[q];
+            __syncwarp();
+          }
+        }
+        double nr = 0.0;
+        for (int64_t q = lane; q < n; q += 32) nr += vj[q] * vj[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
+        nr = sqrt(nr);
+        if (nr > 0.5) {
+          const double inv = 1.0 / nr;
+          for (int64_t q = lane; q < n; q += 32) vj[q] *= inv;
+          __syncwarp();
+          break;
+        }
+        for (int64_t q = lane; q < n; q += 32) vj[q] = (q == basis) ? 1.0 : 0.0;
+        ++basis;
+        __syncwarp();
+      }
+    }
+    // ---- (2) back-transformation, 32 vectors per pass
+    const int64_t nrot = P.rotcnt[it];
+    const double* rcs = P.rotcs + it * P.rotcap * 2;
+    const int32_t* rcol = P.rotcol + it * P.rotcap;
+    const double* rv = P.rvlog + it * npan * (BW * NP + BW * BW);
+    for (int64_t j0 = 0; j0 < k; j0 += P.btw) {
+      const int64_t j = j0 + lane;
+      const bool act = lane < P.btw && j < k;
+      double* mine = vm + lane * ls;
+      if (act)
+        for (int64_t q = 0; q < n; ++q) mine[q] = Vb[j * RP + q];
+      __syncwarp();
+      if (act) {
+        for (int64_t t = nrot - 1; t >= 0; --t) {
+          const double c = rcs[2 * t], s = rcs[2 * t + 1];
+          const int col = rcol[t];
+          const double a = mine[col - 1], b = mine[col];
+          mine[col - 1] = c * a - s * b;
+          mine[col] = s * a + c * b;
+        }
+        for (int64_t pk = npan - 2; pk >= 0; --pk) {
+          const double* Vp = rv + pk * (BW * NP + BW * BW);  // V[c][jj], jj < NP
+          const double* Tp = Vp + BW * NP;                     // T[a][b]
+          const int64_t jlo = pk * BW + BW;                    // V rows start at the LQ pivots
+          double y[BW];
+#pragma unroll
+          for (int c = 0; c < BW; ++c) y[c] = 0.0;
+          for (int64_t q = jlo; q < n; ++q) {
+            const double x = mine[q];
+#pragma unroll
+            for (int c = 0; c < BW; ++c) y[c] = fma(Vp[c * NP + q], x, y[c]);
+          }
+          double zz[BW];
+#pragma unroll
+          for (int a = 0; a < BW; ++a) {
+            double acc = 0.0;
+#pragma unroll
+            for (int b = 0; b < BW; ++b) acc = fma(Tp[a * BW + b], y[b], acc);
+            zz[a] = acc;
+          }
+          for (int64_t q = jlo; q < n; ++q) {
+            double acc = mine[q];
+#pragma unroll
+            for (int c = 0; c < BW; ++c) acc = fma(-Vp[c * NP + q], zz[c], acc);
+            mine[q] = acc;
+          }
+        }
+        for (int64_t q = 0; q < RP; ++q) Vb[j * RP + q] = q < n ? mine[q] : 0.0;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Output kernel of the bidiagonal vector path: sigma are in P.s (bisection),
+// right singular vectors of X in vsel (sorted order); emit U / V / packed
+// factors through the shared emit_vectors (other side = X V / ||X V||).
+__global__ void __launch_bounds__(TPB) svd_vecout_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  JacobiSmem& sm = *reinterpret_cast<JacobiSmem*>(smem_raw);
+  int NS = 1;
+  while (NS < P.n) NS <<= 1;
+  FinalView fs = final_view(smem_raw, NS);
+  __shared__ int64_t cur;
+  const int tid = threadIdx.x;
+  const int64_t LP = P.LP, NP = P.NP, RP = P.RP;
+  double* Xslot = P.xslots + int64_t(blockIdx.x) * LP * NP;
+  for (;;) {
+    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[1], 1ull));
+    __syncthreads();
+    const int64_t it = cur;
+    __syncthreads();
+    if (it >= P.count) break;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int flag = P.flags[it];
+    if (flag == 2) continue;
+    if (flag == 1) {
+      emit_zero_slice(P, slice);
+      continue;
+    }
+    for (int j = tid; j < NS; j += TPB) fs.idx[j] = j;
+    __syncthreads();
+    emit_vectors(P, sm, fs, slice, P.A + slice * P.m * P.p, P.vsel + it * RP * NP, fs.idx, Xslot,
+                 true, nullptr, 0);
+  }
+}
+
 template <bool WANTV>
 __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1134,22 +1509,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
     }
     const int64_t r = n;
     if (flag == 1) {
-      // slicesvd.py:51-54: identity bases, zero values.
-      if (P.s)
-        for (int64_t j = tid; j < r; j += TPB) P.s[j + slice * r] = 0.0;
-      if (P.job == STARM_SVD_FULL) {
-        double* U = P.u + slice * P.m * r;
-        double* Vo = P.v + slice * P.p * r;
-        for (int64_t e = tid; e < P.m * r; e += TPB) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
-        for (int64_t e = tid; e < P.p * r; e += TPB) Vo[e] = ((e % P.p) == (e / P.p)) ? 1.0 : 0.0;
-      } else if (P.job == STARM_SVD_TRUNCATED) {
-        const int64_t k = P.ranks[slice];
-        double* U = P.u_data + P.u_off[slice];
-        double* G = P.g_data + P.g_off[slice];
-        for (int64_t e = tid; e < P.m * k; e += TPB) U[e] = ((e % P.m) == (e / P.m)) ? 1.0 : 0.0;
-        for (int64_t e = tid; e < k * P.p; e += TPB) G[e] = 0.0;
-      }
-      __syncthreads();
+      emit_zero_slice(P, slice);
       continue;
     }
     if (WANTV) {
@@ -1248,68 +1608,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
 
     if (WANTV && P.job != STARM_SVD_VALUES) {
       __syncthreads();
-      const double smax = fs.key[0];
-      const int64_t kout = (P.job == STARM_SVD_FULL) ? r : P.ranks[slice];
-      // Q side = normalised columns of X V (length L).  QR path: X * V_sel
-      // recomputed from the untouched input into the free X slot (sorted
-      // order); direct path: the target's own columns (permuted order).
-      double* Qb;
-      int64_t ldq;
-      const int* qc;
-      if (P.use_qr) {
-        gemm_xv(P, sm, A, V, fs.idx, kout, Xslot);
-        Qb = Xslot;
-        ldq = LP;
-        qc = nullptr;
-      } else {
-        Qb = T;
-        ldq = ldt;
-        qc = fs.idx;
-      }
-      for (int64_t j = 0; j < kout; ++j) {
-        const double sj = fs.key[j];
-        const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
-        double* col = Qb + int64_t(qc ? qc[j] : j) * ldq;
-        for (int64_t rr = tid; rr < L; rr += TPB) col[rr] *= inv;
-      }
-      __syncthreads();
-      for (int64_t j = 0; j < kout; ++j)
-        if (!(fs.key[j] > 1e-4 * smax)) cgs2_fix(fs, Qb, ldq, L, qc, int(j));
-      __syncthreads();
-      if (P.job == STARM_SVD_FULL) {
-        double* Uo = P.u + slice * P.m * r;
-        double* Vo = P.v + slice * P.p * r;
-        double* Qd = P.transposed ? Vo : Uo;  // ld L
-        double* Wd = P.transposed ? Uo : Vo;  // ld n
-        for (int64_t j = 0; j < kout; ++j) {
-          const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
-          for (int64_t rr = tid; rr < L; rr += TPB) Qd[rr + j * L] = qcol[rr];
-          const double* vcol = V + int64_t(fs.idx[j]) * RP;
-          for (int64_t rr = tid; rr < n; rr += TPB) Wd[rr + j * n] = vcol[rr];
-        }
-      } else {
-        double* Uk = P.u_data + P.u_off[slice];
-        double* G = P.g_data + P.g_off[slice];
-        if (!P.transposed) {
-          for (int64_t j = 0; j < kout; ++j) {
-            const double* qcol = Qb + int64_t(qc ? qc[j] : j) * ldq;
-            for (int64_t rr = tid; rr < L; rr += TPB) Uk[rr + j * L] = qcol[rr];
-          }
-          for (int64_t e = tid; e < kout * n; e += TPB) {
-            const int64_t j = e % kout, col = e / kout;
-            G[e] = P.s[j + slice * r] * V[col + int64_t(fs.idx[j]) * RP];
-          }
-        } else {
-          for (int64_t j = 0; j < kout; ++j) {
-            const double* vcol = V + int64_t(fs.idx[j]) * RP;
-            for (int64_t rr = tid; rr < n; rr += TPB) Uk[rr + j * n] = vcol[rr];
-          }
-          for (int64_t e = tid; e < kout * L; e += TPB) {
-            const int64_t j = e % kout, col = e / kout;
-            G[e] = P.s[j + slice * r] * Qb[col + int64_t(qc ? qc[j] : j) * ldq];
-          }
-        }
-      }
+      emit_vectors(P, sm, fs, slice, A, V, fs.idx, Xslot, P.use_qr, T, ldt);
     }
     __syncthreads();
     long long t3 = clock64();
@@ -1334,11 +1633,14 @@ __global__ void reset_status_kernel(int32_t* status, unsigned long long* counter
 
 struct Plan {
   int64_t L, n, LP, NP, RP;
-  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s;
+  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, bdvec;
   int ns;
   size_t jsmem, rsmem, bsmem;
-  int slots_j, slots_r, slots_b, bisect_blocks;
-  size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, total;
+  int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw;
+  int64_t rotcap;
+  size_t vsmem, tsmem;
+  size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
+      off_vsel, off_ii, total;
 };
 
 int g_tune_inner = 1;
@@ -1364,8 +1666,9 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   if (g.NP < GW) g.NP = GW;
   g.RP = round_up(g.NP, RCH);
   g.bidiag = g_tune_mode == 1 && g.LP <= QR_MAX_LP;
-  g.use_qr = g.bidiag && g.L > g.n;
-  g.run_jacobi = g.wantv || !g.bidiag;
+  g.use_qr = false;  // Jacobi (non-bidiagonal mode) works on X directly
+  g.run_jacobi = !g.bidiag;
+  g.bdvec = g.bidiag && g.wantv;
   g.internal_s = g.wantv && !have_s;
   g.ns = 1;
   while (g.ns < g.n) g.ns <<= 1;
@@ -1382,6 +1685,23 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
                  : occupancy((const void*)svd_jacobi_kernel<false>, TPB, g.jsmem, &per);
     if (rc) return rc;
     g.slots_j = clampc(int64_t(sms) * per);
+  }
+  if (g.bdvec) {
+    rc = occupancy((const void*)svd_vecout_kernel, TPB, g.jsmem, &per);
+    if (rc) return rc;
+    g.slots_v = clampc(int64_t(sms) * per);
+    g.slots_j = g.slots_v;  // vecout uses the X slots
+    const int64_t ls = g.n | 1;
+    int64_t tw = int64_t(200 * 1024) / (ls * 8);
+    g.btw = int(tw > 32 ? 32 : (tw < 1 ? 1 : tw));
+    g.tsmem = size_t(g.btw) * ls * sizeof(double);
+    rc = occupancy((const void*)svd_backtransform_kernel, 32, g.tsmem, &per);
+    if (rc) return rc;
+    g.slots_t = clampc(int64_t(sms) * per);
+    const int64_t work = count * g.n;
+    g.ii_threads = int(work < int64_t(sms) * 128 ? work : int64_t(sms) * 128);
+    if (g.ii_threads < 1) g.ii_threads = 1;
+    g.rotcap = g.n * g.n + g.n * BW + 64;
   }
   if (g.bidiag) {
     rc = occupancy((const void*)svd_reduce_kernel, TPB, g.rsmem, &per);
@@ -1408,6 +1728,13 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.off_band = take(g.bidiag ? size_t(count) * (BW + 1) * g.NP * sizeof(double) : 0);
   g.off_de = take(g.bidiag ? size_t(count) * 2 * g.NP * sizeof(double) : 0);
   g.off_s = take(g.internal_s ? size_t(nslices) * g.n * sizeof(double) : 0);
+  const size_t npan = size_t(g.NP / BW);
+  g.off_rv = take(g.bdvec ? size_t(count) * npan * (BW * g.NP + BW * BW) * sizeof(double) : 0);
+  g.off_rcs = take(g.bdvec ? size_t(count) * g.rotcap * 2 * sizeof(double) : 0);
+  g.off_rcol = take(g.bdvec ? size_t(count) * g.rotcap * sizeof(int32_t) : 0);
+  g.off_rcnt = take(g.bdvec ? size_t(count) * sizeof(int64_t) : 0);
+  g.off_vsel = take(g.bdvec ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_ii = take(g.bdvec ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
   g.total = off;
   *pl = g;
   return STARM_OK;
@@ -1512,12 +1839,30 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.tol = double(pl.L > 32 ? pl.L : 32) * DBL_EPSILON;
   P.max_sweeps = g_tune_sweeps;
   P.max_inner = g_tune_inner;
+  if (pl.bdvec) {
+    P.rvlog = reinterpret_cast<double*>(base + pl.off_rv);
+    P.rotcs = reinterpret_cast<double*>(base + pl.off_rcs);
+    P.rotcol = reinterpret_cast<int32_t*>(base + pl.off_rcol);
+    P.rotcnt = reinterpret_cast<int64_t*>(base + pl.off_rcnt);
+    P.rotcap = pl.rotcap;
+    P.vsel = reinterpret_cast<double*>(base + pl.off_vsel);
+    P.iiscr = reinterpret_cast<double*>(base + pl.off_ii);
+    P.btw = pl.btw;
+  }
   if (pl.bidiag) {
     svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     svd_bulge_kernel<<<pl.slots_b, 32, pl.bsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
+    STARM_LAUNCH_CHECK();
+  }
+  if (pl.bdvec) {
+    svd_bdvec_kernel<<<(pl.ii_threads + 127) / 128, 128, 0, st>>>(P, count * pl.n);
+    STARM_LAUNCH_CHECK();
+    svd_backtransform_kernel<<<pl.slots_t, 32, pl.tsmem, st>>>(P);
+    STARM_LAUNCH_CHECK();
+    svd_vecout_kernel<<<pl.slots_v, TPB, pl.jsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
   }
   if (pl.run_jacobi) {
