@@ -904,100 +904,189 @@ __device__ __forceinline__ void givens(double x, double y, double& c, double& s)
   s = y * rinv;
 }
 
-__global__ void __launch_bounds__(32) svd_bulge_kernel(SvdParams P) {
+// Chase schedule.  Chases are ordered by row i (ascending) then j
+// (descending, j = min(i+BW, n-1) .. i+2); one empty slot follows every row
+// so the next row's first chase (which starts to the right of the previous
+// chase) begins 2*lag steps later.  Slot e returns its (i, j) or false for
+// an empty slot.
+__device__ __forceinline__ bool chase_slot(int64_t e, int n, int& i, int& j) {
+  const int nfull = n - BW > 0 ? n - BW : 0;  // rows with i + BW <= n - 1
+  const int64_t ef = int64_t(nfull) * BW;
+  if (e < ef) {
+    i = int(e / BW);
+    const int q = int(e % BW);
+    if (q == BW - 1) return false;
+    j = i + BW - q;
+    return true;
+  }
+  int64_t r = e - ef;
+  for (int ii = nfull; ii + 2 <= n - 1; ++ii) {
+    const int cnt = n - 2 - ii;
+    if (r < cnt) {
+      i = ii;
+      j = n - 1 - int(r);
+      return true;
+    }
+    r -= cnt;
+    if (r == 0) return false;  // the empty slot after row ii
+    r -= 1;
+  }
+  return false;
+}
+
+__host__ __device__ __forceinline__ int64_t chase_slots(int64_t n) {
+  const int64_t nfull = n - BW > 0 ? n - BW : 0;
+  int64_t e = nfull * BW;
+  for (int64_t ii = nfull; ii + 2 <= n - 1; ++ii) e += (n - 2 - ii) + 1;
+  return e;
+}
+
+__host__ __device__ __forceinline__ int chase_maxlen(int64_t n) {
+  return n >= 3 ? int(2 + 2 * ((n - 3) / BW)) : 1;
+}
+
+__host__ __device__ __forceinline__ int chase_logmax(int64_t n) {
+  return n >= 3 ? int(2 + (n - 3) / BW) : 1;
+}
+
+constexpr int BULGE_WARPS = 16;
+
+// Band (bandwidth 16) -> upper bidiagonal by Givens bulge chasing, one CTA
+// per slice with the band (+ one fill diagonal on each side) in shared
+// memory.  Row i's extra entries are annihilated outermost first by a column
+// rotation whose fill below the diagonal is chased down by alternating row /
+// column rotations in steps of 16.  Chases run as a wavefront: slot e starts
+// at time lag*e on warp e % 16, one rotation per warp per time step, a CTA
+// barrier between steps.  Footprints of chases >= 2 steps apart on the same
+// row (and >= 6 steps apart across a row boundary) are disjoint, so every
+// entry sees the same sequence of updates as in the sequential algorithm and
+// the chases commute.  Vector jobs log each chase's column rotations.
+__global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* W = reinterpret_cast<double*>(smem_raw);
-  const int lane = threadIdx.x;
+  __shared__ int64_t cur;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = P.n, NP = P.NP;
+  const int nn = int(n);
+  const int64_t nslot = chase_slots(n);
+  const int maxlen = chase_maxlen(n);
+  const int lmax = chase_logmax(n);
+  int lag = (maxlen + 1 + BULGE_WARPS - 1) / BULGE_WARPS;
+  if (lag < 3) lag = 3;
   for (;;) {
-    int64_t it = 0;
-    if (lane == 0) it = int64_t(atomicAdd(&P.counter[2], 1ull));
-    it = __shfl_sync(0xffffffffu, it, 0);
+    if (threadIdx.x == 0) cur = int64_t(atomicAdd(&P.counter[2], 1ull));
+    __syncthreads();
+    const int64_t it = cur;
+    __syncthreads();
     if (it >= P.count) break;
     if (P.flags[it]) continue;
     long long t0 = clock64();
     const double* band = P.bandbuf + it * (BW + 1) * NP;
-    for (int64_t e = lane; e < n * BWS; e += 32) {
+    for (int64_t e = threadIdx.x; e < n * BWS; e += blockDim.x) {
       const int64_t i = e / BWS, k = e % BWS;
       const int64_t d = k - 1;
       W[e] = (d >= 0 && d <= BW && i + d < n) ? band[d * NP + i] : 0.0;
     }
-    __syncwarp();
-    const int nn = int(n);
-    // vector jobs: log every column rotation (c, s, second column) so the
-    // right singular vectors can be back-transformed (svd_backtransform_kernel)
-    int64_t nlog = 0;
+    __syncthreads();
     double* lcs = P.rotcs ? P.rotcs + it * P.rotcap * 2 : nullptr;
     int32_t* lcol = P.rotcol ? P.rotcol + it * P.rotcap : nullptr;
-    for (int i = 0; i + 2 < nn; ++i) {
-      const int jtop = (i + BW < nn - 1) ? i + BW : nn - 1;
-      for (int j = jtop; j >= i + 2; --j) {
-        double c, s;
-        givens(BEL(W, i, j - 1), BEL(W, i, j), c, s);
-        __syncwarp();
-        if (s == 0.0) continue;
-        if (lcs && lane == 0 && nlog < P.rotcap) {
-          lcs[2 * nlog] = c;
-          lcs[2 * nlog + 1] = s;
-          lcol[nlog] = j;
-        }
-        ++nlog;
-        {  // columns (j-1, j), rows i .. j; lane 0 owns the annihilated entry
-          const int r = i + lane;
-          if (r <= j) {
-            const double a = BEL(W, r, j - 1), b = BEL(W, r, j);
-            BEL(W, r, j - 1) = c * a + s * b;
-            BEL(W, r, j) = lane ? -s * a + c * b : 0.0;
+    int32_t* lcnt = P.rotcs ? reinterpret_cast<int32_t*>(P.rotcnt) + it * nslot : nullptr;
+    // per-warp chase state
+    int64_t e = warp;
+    int ci = 0, cj = 0, rr = 0, phase = -1, nlog = 0;  // phase -1: not started
+    const int64_t tend = int64_t(lag) * (nslot + BULGE_WARPS) + maxlen + 2;
+    for (int64_t t = 0; t < tend; ++t) {
+      if (e < nslot && t >= lag * e) {
+        if (phase < 0) {
+          if (!chase_slot(e, nn, ci, cj)) {  // empty slot: nothing to do
+            if (lcnt && lane == 0) lcnt[e] = 0;
+            e += BULGE_WARPS;
+            goto barrier;
           }
+          phase = 0;
+          nlog = 0;
         }
-        __syncwarp();
-        int rr = j;
-        while (true) {
-          // row rotation (rr-1, rr) annihilating the fill at (rr, rr-1)
-          givens(BEL(W, rr - 1, rr - 1), BEL(W, rr, rr - 1), c, s);
-          __syncwarp();
-          if (s != 0.0) {
-            const int cend = (rr + BW < nn - 1) ? rr + BW : nn - 1;
-            const int col = rr - 1 + lane;
-            if (col <= cend) {
-              const double a = BEL(W, rr - 1, col), b = BEL(W, rr, col);
-              BEL(W, rr - 1, col) = c * a + s * b;
-              BEL(W, rr, col) = lane ? -s * a + c * b : 0.0;
-            }
+        {
+          double c, s;
+          bool done = false;
+          if (phase == 0) {  // column rotation (cj-1, cj) on rows ci .. cj
+            givens(BEL(W, ci, cj - 1), BEL(W, ci, cj), c, s);
             __syncwarp();
+            if (s == 0.0) {
+              done = true;
+            } else {
+              const int r = ci + lane;
+              if (r <= cj) {
+                const double a = BEL(W, r, cj - 1), b = BEL(W, r, cj);
+                BEL(W, r, cj - 1) = c * a + s * b;
+                BEL(W, r, cj) = lane ? -s * a + c * b : 0.0;
+              }
+              if (lcs && lane == 0) {
+                const int64_t q = e * lmax + nlog;
+                lcs[2 * q] = c;
+                lcs[2 * q + 1] = s;
+                lcol[q] = cj;
+              }
+              ++nlog;
+              rr = cj;
+              phase = 1;
+            }
+          } else if (phase == 1) {  // row rotation (rr-1, rr) annihilating the fill at (rr, rr-1)
+            givens(BEL(W, rr - 1, rr - 1), BEL(W, rr, rr - 1), c, s);
+            __syncwarp();
+            if (s != 0.0) {
+              const int cend = (rr + BW < nn - 1) ? rr + BW : nn - 1;
+              const int col = rr - 1 + lane;
+              if (col <= cend) {
+                const double a = BEL(W, rr - 1, col), b = BEL(W, rr, col);
+                BEL(W, rr - 1, col) = c * a + s * b;
+                BEL(W, rr, col) = lane ? -s * a + c * b : 0.0;
+              }
+            }
+            if (rr + BW >= nn) done = true;
+            else phase = 2;
+          } else {  // column rotation (cc-1, cc) annihilating the fill at (rr-1, cc)
+            const int cc = rr + BW;
+            givens(BEL(W, rr - 1, cc - 1), BEL(W, rr - 1, cc), c, s);
+            __syncwarp();
+            if (s == 0.0) {
+              done = true;
+            } else {
+              const int r2 = rr - 1 + lane;
+              if (r2 <= cc) {
+                const double a = BEL(W, r2, cc - 1), b = BEL(W, r2, cc);
+                BEL(W, r2, cc - 1) = c * a + s * b;
+                BEL(W, r2, cc) = lane ? -s * a + c * b : 0.0;
+              }
+              if (lcs && lane == 0) {
+                const int64_t q = e * lmax + nlog;
+                lcs[2 * q] = c;
+                lcs[2 * q + 1] = s;
+                lcol[q] = cc;
+              }
+              ++nlog;
+              rr = cc;
+              phase = 1;
+            }
           }
-          const int cc = rr + BW;
-          if (cc >= nn) break;
-          // column rotation (cc-1, cc) annihilating the fill at (rr-1, cc)
-          givens(BEL(W, rr - 1, cc - 1), BEL(W, rr - 1, cc), c, s);
-          __syncwarp();
-          if (s == 0.0) break;
-          if (lcs && lane == 0 && nlog < P.rotcap) {
-            lcs[2 * nlog] = c;
-            lcs[2 * nlog + 1] = s;
-            lcol[nlog] = cc;
+          if (done) {
+            if (lcnt && lane == 0) lcnt[e] = nlog;
+            e += BULGE_WARPS;
+            phase = -1;
           }
-          ++nlog;
-          const int r2 = rr - 1 + lane;
-          if (r2 <= cc) {
-            const double a = BEL(W, r2, cc - 1), b = BEL(W, r2, cc);
-            BEL(W, r2, cc - 1) = c * a + s * b;
-            BEL(W, r2, cc) = lane ? -s * a + c * b : 0.0;
-          }
-          __syncwarp();
-          rr = cc;
         }
       }
+    barrier:
+      __syncthreads();
     }
-    if (lcs && lane == 0) P.rotcnt[it] = nlog < P.rotcap ? nlog : P.rotcap;
     double* de = P.debuf + it * 2 * NP;
-    for (int64_t i = lane; i < NP; i += 32) {
+    for (int64_t i = threadIdx.x; i < NP; i += blockDim.x) {
       de[i] = i < n ? BEL(W, i, i) : 0.0;
       de[NP + i] = i + 1 < n ? BEL(W, i, i + 1) : 0.0;
     }
-    __syncwarp();
+    __syncthreads();
     long long t1 = clock64();
-    if (lane == 0 && P.stats) atomicAdd(&g_stats[ST_CYC_BULGE], (unsigned long long)(t1 - t0));
+    if (threadIdx.x == 0 && P.stats) atomicAdd(&g_stats[ST_CYC_BULGE], (unsigned long long)(t1 - t0));
   }
 }
 
@@ -1378,7 +1467,9 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
       }
     }
     // ---- (2) back-transformation, 32 vectors per pass
-    const int64_t nrot = P.rotcnt[it];
+    const int64_t nslot = chase_slots(n);
+    const int lmax = chase_logmax(n);
+    const int32_t* rcnt = reinterpret_cast<const int32_t*>(P.rotcnt) + it * nslot;
     const double* rcs = P.rotcs + it * P.rotcap * 2;
     const int32_t* rcol = P.rotcol + it * P.rotcap;
     const double* rv = P.rvlog + it * npan * (BW * NP + BW * BW);
@@ -1390,12 +1481,16 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
         for (int64_t q = 0; q < n; ++q) mine[q] = Vb[j * RP + q];
       __syncwarp();
       if (act) {
-        for (int64_t t = nrot - 1; t >= 0; --t) {
-          const double c = rcs[2 * t], s = rcs[2 * t + 1];
-          const int col = rcol[t];
-          const double a = mine[col - 1], b = mine[col];
-          mine[col - 1] = c * a - s * b;
-          mine[col] = s * a + c * b;
+        // chases in reverse order, each chase's column rotations in reverse
+        for (int64_t e = nslot - 1; e >= 0; --e) {
+          for (int q = rcnt[e] - 1; q >= 0; --q) {
+            const int64_t t = e * lmax + q;
+            const double c = rcs[2 * t], s = rcs[2 * t + 1];
+            const int col = rcol[t];
+            const double a = mine[col - 1], b = mine[col];
+            mine[col - 1] = c * a - s * b;
+            mine[col] = s * a + c * b;
+          }
         }
         for (int64_t pk = npan - 2; pk >= 0; --pk) {
           const double* Vp = rv + pk * (BW * NP + BW * BW);  // V[c][jj], jj < NP
@@ -1700,14 +1795,14 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.slots_t = clampc(int64_t(sms) * per);
     const int64_t work = count * g.n;
     g.ii_threads = int(work < int64_t(sms) * 128 ? work : int64_t(sms) * 128);
-    if (g.ii_threads < 1) g.ii_threads = 1;
-    g.rotcap = g.n * g.n + g.n * BW + 64;
+    g.ii_threads = int(round_up(g.ii_threads < 1 ? 1 : g.ii_threads, 128));  // whole blocks
+    g.rotcap = chase_slots(g.n) * chase_logmax(g.n);
   }
   if (g.bidiag) {
     rc = occupancy((const void*)svd_reduce_kernel, TPB, g.rsmem, &per);
     if (rc) return rc;
     g.slots_r = clampc(int64_t(sms) * per);
-    rc = occupancy((const void*)svd_bulge_kernel, 32, g.bsmem, &per);
+    rc = occupancy((const void*)svd_bulge_kernel, BULGE_WARPS * 32, g.bsmem, &per);
     if (rc) return rc;
     g.slots_b = clampc(int64_t(sms) * per);
     int64_t bb = (count * g.n + 127) / 128;
@@ -1732,7 +1827,7 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.off_rv = take(g.bdvec ? size_t(count) * npan * (BW * g.NP + BW * BW) * sizeof(double) : 0);
   g.off_rcs = take(g.bdvec ? size_t(count) * g.rotcap * 2 * sizeof(double) : 0);
   g.off_rcol = take(g.bdvec ? size_t(count) * g.rotcap * sizeof(int32_t) : 0);
-  g.off_rcnt = take(g.bdvec ? size_t(count) * sizeof(int64_t) : 0);
+  g.off_rcnt = take(g.bdvec ? size_t(count) * chase_slots(g.n) * sizeof(int32_t) : 0);
   g.off_vsel = take(g.bdvec ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
   g.off_ii = take(g.bdvec ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
   g.total = off;
@@ -1852,7 +1947,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   if (pl.bidiag) {
     svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
-    svd_bulge_kernel<<<pl.slots_b, 32, pl.bsmem, st>>>(P);
+    svd_bulge_kernel<<<pl.slots_b, BULGE_WARPS * 32, pl.bsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
     STARM_LAUNCH_CHECK();

@@ -16,7 +16,8 @@ from helpers import projector_distance, random_array, random_orthonormal, rel_er
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(5, 3, 4), (3, 5, 2, 3), (7, 7, 6), (1, 4, 3), (4, 1, 2), (33, 17, 5), (17, 33, 4),
-          (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3)]
+          (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3),
+          (300, 257, 2), (257, 300, 2), (361, 720, 1)]
 
 
 # ------------------------------------------------------------------ TTM (K1)
