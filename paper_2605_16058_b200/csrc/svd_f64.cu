@@ -87,6 +87,7 @@ struct SvdParams {
   double* vsel;                 // per slice: right singular vectors (RP x NP)
   double* iiscr;                // inverse-iteration scratch
   int btw;                      // back-transform vectors per pass
+  int qr_stages;                // cp.async ring depth of the reduce kernel
   int64_t L, n, LP, NP, RP;
   int transposed, use_qr, bidiag, stats;
   double tol;
@@ -128,7 +129,6 @@ size_t jacobi_smem_bytes(int ns) {
 }
 
 struct __align__(16) QrSmemFixed {
-  double cbuf[2][GW * XS];
   double t[BW * 17];
   double sg[2][BW * 17];
   double y[BW * GS];
@@ -475,10 +475,53 @@ __device__ __forceinline__ double& PAN(double* pan, int64_t prs, int c, int64_t 
   return pan[c * prs + r];
 }
 
-// Unblocked Householder on panel columns [0,16) of pan (rows k0.., ld prs).
-// Leaves R (upper) in rows <= k0+j and v below; tau in q.tau.
+// Sum 16 per-thread partials over the CTA: butterfly inside each warp (16
+// shuffles leave lanes 2v, 2v+1 holding warp-sum v), then 8 warp partials.
+__device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[TPB / 32][BW],
+                                         double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v8[8], v4[4], v2[2], v1;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double keep = h16 ? acc[8 + i] : acc[i];
+    const double give = h16 ? acc[i] : acc[8 + i];
+    v8[i] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double keep = h8 ? v8[4 + i] : v8[i];
+    const double give = h8 ? v8[i] : v8[4 + i];
+    v4[i] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double keep = h4 ? v4[2 + i] : v4[i];
+    const double give = h4 ? v4[i] : v4[2 + i];
+    v2[i] = keep + __shfl_xor_sync(0xffffffffu, give, 4);
+  }
+  {
+    const double keep = h2 ? v2[1] : v2[0];
+    const double give = h2 ? v2[0] : v2[1];
+    v1 = keep + __shfl_xor_sync(0xffffffffu, give, 2);
+  }
+  v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+  if (!(lane & 1)) red[warp][(lane >> 1) & 15] = v1;
+  __syncthreads();
+  if (threadIdx.x < BW) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < TPB / 32; ++w) s += red[w][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Unblocked Householder on panel columns [0,16) of pan (rows k0.., ld prs):
+// LAPACK dlarfg/dlarf per column.  Leaves R (upper) in rows <= k0+j and v
+// below; tau in q.tau.
 __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t LP) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   for (int j = 0; j < BW; ++j) {
     const int64_t pr = k0 + j;
     double acc[BW];
@@ -491,21 +534,7 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
       for (int c = 1; c < BW; ++c)
         if (c > j) acc[c] = fma(x, PAN(pan, prs, c, r), acc[c]);
     }
-#pragma unroll
-    for (int c = 0; c < BW; ++c) {
-      double v = acc[c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) q.red[warp][c] = v;
-    }
-    __syncthreads();
-    if (tid < BW) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < TPB / 32; ++w) s += q.red[w][tid];
-      q.sums[tid] = s;
-    }
-    __syncthreads();
+    reduce16(acc, q.red, q.sums);
     if (tid == 0) {
       const double alpha = PAN(pan, prs, j, pr);
       const double xn2 = q.sums[0];
@@ -526,7 +555,10 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
       for (int64_t r = pr + tid; r < LP; r += TPB) {
         const double x = PAN(pan, prs, j, r);
         const double vr = (r == pr) ? 1.0 : x * scal;
-        for (int c = j + 1; c < BW; ++c) PAN(pan, prs, c, r) -= tau * vr * q.wv[c];
+        const double tv = tau * vr;
+#pragma unroll
+        for (int c = 1; c < BW; ++c)
+          if (c > j) PAN(pan, prs, c, r) -= tv * q.wv[c];
         PAN(pan, prs, j, r) = (r == pr) ? beta : vr;
       }
     }
@@ -564,33 +596,53 @@ __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64
   __syncthreads();
 }
 
-// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns), rows kc..nrows.
-__device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, double* X,
-                                int64_t ld, int64_t nrows, int64_t NP, int64_t kc, int64_t c0) {
+// cp.async multi-stage ring of 64 x 32 chunks (nst stages, runtime 2..4).
+__device__ __forceinline__ void cp_wait_dyn(int pending) {
+  switch (pending) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    default: cp_async_wait<3>(); break;
+  }
+}
+
+struct Ring {
+  double* base;
+  int nst;
+  __device__ __forceinline__ double* buf(int64_t i) const { return base + (i % nst) * (GW * XS); }
+};
+
+// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
+// rows kc..nrows (multiple of RCH); V = explicit panel in shared memory.
+__device__ void trailing_update(QrSmemFixed& q, const Ring& ring, const double* pan, int64_t prs,
+                                double* X, int64_t ld, int64_t nrows, int64_t NP, int64_t kc,
+                                int64_t c0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int64_t nch = (nrows - kc) / RCH;
+  const int nst = ring.nst;
   // ---- Y = V^T C (16 x 32): warp -> tile (ti = warp>>2, tj = warp&3)
   {
     const int ti = warp >> 2, tj = warp & 3;
     double y0 = 0.0, y1 = 0.0;
-    stage_cols(q.cbuf[0], X, ld, kc, c0, NP);
+    for (int s = 0; s < nst - 1; ++s) {
+      if (s < nch) stage_cols(ring.buf(s), X, ld, kc + s * RCH, c0, NP);
+      else cp_async_commit();
+    }
     for (int64_t ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) {
-        stage_cols(q.cbuf[(ch + 1) & 1], X, ld, kc + (ch + 1) * RCH, c0, NP);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      cp_wait_dyn(nst - 2);
       __syncthreads();
-      const double* cs = q.cbuf[ch & 1];
+      const int64_t nx = ch + nst - 1;
+      if (nx < nch) stage_cols(ring.buf(nx), X, ld, kc + nx * RCH, c0, NP);
+      else cp_async_commit();
+      const double* cs = ring.buf(ch);
       const int64_t r0 = kc + ch * RCH;
       const double* va = pan + (ti * 8 + gq) * prs + r0 + tq;
       const double* cb = cs + (tj * 8 + gq) * XS + tq;
 #pragma unroll
       for (int k4 = 0; k4 < RCH / 4; ++k4) dmma884(y0, y1, va[k4 * 4], cb[k4 * 4]);
-      __syncthreads();
     }
+    cp_async_wait<0>();
     q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq] = y0;
     q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq + 1] = y1;
   }
@@ -604,16 +656,17 @@ __device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, 
   }
   __syncthreads();
   // ---- C -= V Z, streamed again
-  stage_cols(q.cbuf[0], X, ld, kc, c0, NP);
+  for (int s = 0; s < nst - 1; ++s) {
+    if (s < nch) stage_cols(ring.buf(s), X, ld, kc + s * RCH, c0, NP);
+    else cp_async_commit();
+  }
   for (int64_t ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) {
-      stage_cols(q.cbuf[(ch + 1) & 1], X, ld, kc + (ch + 1) * RCH, c0, NP);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_wait_dyn(nst - 2);
     __syncthreads();
-    double* cs = q.cbuf[ch & 1];
+    const int64_t nx = ch + nst - 1;
+    if (nx < nch) stage_cols(ring.buf(nx), X, ld, kc + nx * RCH, c0, NP);
+    else cp_async_commit();
+    double* cs = ring.buf(ch);
     const int64_t r0 = kc + ch * RCH;
     double acc[4][2];
 #pragma unroll
@@ -632,8 +685,9 @@ __device__ void trailing_update(QrSmemFixed& q, const double* pan, int64_t prs, 
     }
     __syncthreads();
     store_cols(X, ld, r0, c0, NP, cs);
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
 // Store rows >= rmin of a staged 64 x 32 chunk (rmin even).
@@ -653,25 +707,28 @@ __device__ __forceinline__ void store_cols_from(double* M, int64_t ld, int64_t r
 // LQ half-step update of the band reduction:  C <- C (I - V T V^T) for
 // columns [j0, NP) and rows [rmin, nrows) of A (ld), chunks starting at rc.
 // V[j][c] = pan2[c * prs + j] (explicit, zero outside [j0 + c, NP)).
-__device__ void right_update(QrSmemFixed& q, const double* pan2, int64_t prs, double* A,
-                             int64_t ld, int64_t nrows, int64_t NP, int64_t rc, int64_t rmin,
-                             int64_t j0) {
+__device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan2, int64_t prs,
+                             double* A, int64_t ld, int64_t nrows, int64_t NP, int64_t rc,
+                             int64_t rmin, int64_t j0) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
+  const int nst = ring.nst;
+  const int64_t nblk = (NP - j0 + GW - 1) / GW;
   for (int64_t r0 = rc; r0 < nrows; r0 += RCH) {
     // ---- Y = C V (64 x 16): warp -> row tile `warp`, column tiles 0..1
     double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    int buf = 0;
-    stage_cols(q.cbuf[0], A, ld, r0, j0, NP);
-    for (int64_t jb = j0; jb < NP; jb += GW) {
-      if (jb + GW < NP) {
-        stage_cols(q.cbuf[buf ^ 1], A, ld, r0, jb + GW, NP);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+    for (int s = 0; s < nst - 1; ++s) {
+      if (s < nblk) stage_cols(ring.buf(s), A, ld, r0, j0 + s * GW, NP);
+      else cp_async_commit();
+    }
+    for (int64_t b = 0; b < nblk; ++b) {
+      cp_wait_dyn(nst - 2);
       __syncthreads();
-      const double* cs = q.cbuf[buf];
+      const int64_t nx = b + nst - 1;
+      if (nx < nblk) stage_cols(ring.buf(nx), A, ld, r0, j0 + nx * GW, NP);
+      else cp_async_commit();
+      const double* cs = ring.buf(b);
+      const int64_t jb = j0 + b * GW;
 #pragma unroll
       for (int k4 = 0; k4 < GW / 4; ++k4) {
         const double a = cs[(k4 * 4 + tq) * XS + warp * 8 + gq];
@@ -679,9 +736,8 @@ __device__ void right_update(QrSmemFixed& q, const double* pan2, int64_t prs, do
         for (int ct = 0; ct < 2; ++ct)
           dmma884(y[ct][0], y[ct][1], a, pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
       }
-      __syncthreads();
-      buf ^= 1;
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int ct = 0; ct < 2; ++ct) {
       q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq] = y[ct][0];
@@ -697,17 +753,18 @@ __device__ void right_update(QrSmemFixed& q, const double* pan2, int64_t prs, do
     }
     __syncthreads();
     // ---- C -= Z V^T, column block by column block
-    buf = 0;
-    stage_cols(q.cbuf[0], A, ld, r0, j0, NP);
-    for (int64_t jb = j0; jb < NP; jb += GW) {
-      if (jb + GW < NP) {
-        stage_cols(q.cbuf[buf ^ 1], A, ld, r0, jb + GW, NP);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+    for (int s = 0; s < nst - 1; ++s) {
+      if (s < nblk) stage_cols(ring.buf(s), A, ld, r0, j0 + s * GW, NP);
+      else cp_async_commit();
+    }
+    for (int64_t b = 0; b < nblk; ++b) {
+      cp_wait_dyn(nst - 2);
       __syncthreads();
-      double* cs = q.cbuf[buf];
+      const int64_t nx = b + nst - 1;
+      if (nx < nblk) stage_cols(ring.buf(nx), A, ld, r0, j0 + nx * GW, NP);
+      else cp_async_commit();
+      double* cs = ring.buf(b);
+      const int64_t jb = j0 + b * GW;
       double acc[4][2];
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
@@ -725,35 +782,37 @@ __device__ void right_update(QrSmemFixed& q, const double* pan2, int64_t prs, do
       }
       __syncthreads();
       store_cols_from(A, ld, r0, jb, NP, cs, rmin);
-      __syncthreads();
-      buf ^= 1;
     }
+    cp_async_wait<0>();
+    __syncthreads();
   }
 }
 
 // Panel -> explicit V (zeros above the pivot, 1 on it) for rows [0, prs).
 __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0, int64_t nrows) {
-  for (int64_t e = threadIdx.x; e < BW * prs; e += TPB) {
-    const int c = int(e / prs);
-    const int64_t r = e % prs;
-    if (r < k0 + c || r >= nrows) pan[e] = 0.0;
-    else if (r == k0 + c) pan[e] = 1.0;
+  for (int c = 0; c < BW; ++c) {
+    double* col = pan + c * prs;
+    for (int64_t r = threadIdx.x; r < prs; r += TPB) {
+      if (r < k0 + c || r >= nrows) col[r] = 0.0;
+      else if (r == k0 + c) col[r] = 1.0;
+    }
   }
   __syncthreads();
 }
 
 // Load / factorisation kernel (one CTA per slice, persistent):
 //   X (L x n) -> [Householder QR if L > n] -> n x n matrix A (upper
-//   triangular R or X itself) -> [vector jobs on the QR path: R -> rbuf]
-//   -> band reduction  A = Q1 B P1^T  with B upper band (bandwidth 16) by
-//   alternating 16-column QR and 16-row LQ panels (compact-WY updates on
-//   DMMA) -> the 17 diagonals of B to bandbuf.
+//   triangular R or X itself) -> band reduction  A = Q1 B P1^T  with B
+//   upper band (bandwidth 16) by alternating 16-column QR and 16-row LQ
+//   panels (compact-WY updates on DMMA, nst-stage cp.async ring) -> the 17
+//   diagonals of B to bandbuf.  Vector jobs also log P1's panels (V, T).
 __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
   const int64_t LP = P.LP, NP = P.NP, RP = P.RP, n = P.n;
   const int64_t prs = LP + 36;
   double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
+  const Ring ring{pan + BW * prs, P.qr_stages};
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
   double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
@@ -766,7 +825,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     if (it >= P.count) break;
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
-    const int flag = load_slice(P, P.A + slice * P.m * P.p, X, q.cbuf[0]);
+    const int flag = load_slice(P, P.A + slice * P.m * P.p, X, ring.buf(0));
     if (tid == 0) {
       P.flags[it] = flag;
       if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
@@ -777,15 +836,12 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     if (P.L > P.n) {
       for (int64_t k0 = 0; k0 < NP; k0 += BW) {
         const int64_t kc = (k0 / RCH) * RCH;
-        for (int64_t e = tid; e < BW * prs; e += TPB) {
-          const int c = int(e / prs);
-          const int64_t r = e % prs;
-          pan[e] = r < LP ? X[r + (k0 + c) * LP] : 0.0;
-        }
+        for (int c = 0; c < BW; ++c)
+          for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < LP ? X[r + (k0 + c) * LP] : 0.0;
         __syncthreads();
         panel_factor(q, pan, prs, k0, LP);
-        for (int e = tid; e < BW * BW; e += TPB) {
-          const int c = e / BW, r = e % BW;
+        if (tid < BW * BW) {
+          const int c = tid / BW, r = tid % BW;
           if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
         }
         __syncthreads();
@@ -793,75 +849,62 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
           explicit_v(pan, prs, k0, LP);
           panel_gram(q, pan, prs, kc, LP);
           for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
-            trailing_update(q, pan, prs, X, LP, LP, NP, kc, c0);
+            trailing_update(q, ring, pan, prs, X, LP, LP, NP, kc, c0);
         }
         __syncthreads();
       }
       // keep only R (upper triangle of the leading NP x NP block)
       for (int64_t c = 0; c < NP; ++c)
-        for (int64_t r = tid; r < LP; r += TPB)
-          if (r > c) X[r + c * LP] = 0.0;
+        for (int64_t r = c + 1 + tid; r < LP; r += TPB) X[r + c * LP] = 0.0;
       __syncthreads();
-      if (P.rbuf) {
-        double* R = P.rbuf + it * RP * NP;
-        for (int64_t c = 0; c < NP; ++c)
-          for (int64_t r = tid; r < RP; r += TPB) R[r + c * RP] = X[r + c * LP];
-        __syncthreads();
-      }
     }
     long long t2 = clock64();
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
       const int64_t kc = (k / RCH) * RCH;
-      for (int64_t e = tid; e < BW * prs; e += TPB) {
-        const int c = int(e / prs);
-        const int64_t r = e % prs;
-        pan[e] = r < RP ? X[r + (k + c) * LP] : 0.0;
-      }
+      for (int c = 0; c < BW; ++c)
+        for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < RP ? X[r + (k + c) * LP] : 0.0;
       __syncthreads();
       panel_factor(q, pan, prs, k, RP);
-      for (int e = tid; e < BW * BW; e += TPB) {
-        const int c = e / BW, r = e % BW;
+      if (tid < BW * BW) {
+        const int c = tid / BW, r = tid % BW;
         if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
       }
       __syncthreads();
       if (k + BW >= NP) break;
       explicit_v(pan, prs, k, RP);
       panel_gram(q, pan, prs, kc, RP);
-      for (int64_t c0 = k + BW; c0 < NP; c0 += GW) trailing_update(q, pan, prs, X, LP, RP, NP, kc, c0);
-      __syncthreads();
+      for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
+        trailing_update(q, ring, pan, prs, X, LP, RP, NP, kc, c0);
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
-      for (int64_t e = tid; e < BW * prs; e += TPB) {
-        const int c = int(e / prs);
-        const int64_t j = e % prs;
-        pan[e] = (j >= j0 && j < NP) ? X[(k + c) + j * LP] : 0.0;
+      for (int64_t j = tid; j < prs; j += TPB) {
+        const bool in = (j >= j0 && j < NP);
+#pragma unroll
+        for (int c = 0; c < BW; ++c) pan[c * prs + j] = in ? X[(k + c) + j * LP] : 0.0;
       }
       __syncthreads();
       panel_factor(q, pan, prs, j0, NP);
-      for (int e = tid; e < BW * BW; e += TPB) {
-        const int c = e / BW, r = e % BW;  // R2[r][c] -> A[k+c][j0+r]
+      if (tid < BW * BW) {
+        const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
         if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
       }
       __syncthreads();
-      if (j0 + BW < NP || true) {
-        explicit_v(pan, prs, j0, NP);
-        panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
-        if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
-          double* dst = P.rvlog + (it * (NP / BW) + k / BW) * (BW * NP + BW * BW);
-          for (int64_t e = tid; e < BW * NP; e += TPB) dst[e] = pan[(e / NP) * prs + (e % NP)];
-          for (int e = tid; e < BW * BW; e += TPB) dst[BW * NP + e] = q.t[(e / BW) * 17 + (e % BW)];
-        }
-        right_update(q, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+      explicit_v(pan, prs, j0, NP);
+      panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
+      if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
+        double* dst = P.rvlog + (it * (NP / BW) + k / BW) * (BW * NP + BW * BW);
+        for (int c = 0; c < BW; ++c)
+          for (int64_t jj = tid; jj < NP; jj += TPB) dst[c * NP + jj] = pan[c * prs + jj];
+        if (tid < BW * BW) dst[BW * NP + tid] = q.t[(tid / BW) * 17 + (tid % BW)];
       }
+      right_update(q, ring, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
       __syncthreads();
     }
     // ---------------- the 17 diagonals of the band
     double* band = P.bandbuf + it * (BW + 1) * NP;
-    for (int64_t e = tid; e < (BW + 1) * NP; e += TPB) {
-      const int64_t d = e / NP, i = e % NP;
-      band[e] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
-    }
+    for (int d = 0; d <= BW; ++d)
+      for (int64_t i = tid; i < NP; i += TPB) band[d * NP + i] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
     __syncthreads();
     long long t3 = clock64();
     stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
@@ -870,13 +913,6 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
   }
 }
 
-// ----------------------------------------------------------------------
-// Band (bandwidth 16) -> upper bidiagonal by Givens bulge chasing, one
-// warp per slice with the band (+ one fill diagonal on each side) in
-// shared memory.  Row i's extra entries are annihilated outermost first
-// with a column rotation; the fill below the diagonal is chased down by
-// alternating row / column rotations in steps of 16.
-// ----------------------------------------------------------------------
 constexpr int BWS = BW + 3;  // band row stride: offsets -1 .. BW+1
 
 __device__ __forceinline__ double& BEL(double* W, int i, int j) {
@@ -1731,7 +1767,7 @@ struct Plan {
   bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, bdvec;
   int ns;
   size_t jsmem, rsmem, bsmem;
-  int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw;
+  int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages;
   int64_t rotcap;
   size_t vsmem, tsmem;
   size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
@@ -1768,7 +1804,17 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.ns = 1;
   while (g.ns < g.n) g.ns <<= 1;
   g.jsmem = jacobi_smem_bytes(g.ns);
-  g.rsmem = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
+  {
+    const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
+    const size_t ring = size_t(GW) * XS * sizeof(double);
+    g.qr_stages = 4;
+    while (g.qr_stages > 2 && fixed + g.qr_stages * ring > size_t(227 * 1024)) --g.qr_stages;
+    g.rsmem = fixed + g.qr_stages * ring;
+    if (g.rsmem > size_t(227 * 1024)) g.bidiag = false;  // panel does not fit: Jacobi path
+    g.use_qr = false;
+    g.run_jacobi = !g.bidiag;
+    g.bdvec = g.bidiag && g.wantv;
+  }
   g.bsmem = size_t(g.NP) * BWS * sizeof(double);
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
@@ -1920,6 +1966,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.rbuf = (pl.use_qr && pl.wantv) ? reinterpret_cast<double*>(base + pl.off_r) : nullptr;
   P.flags = reinterpret_cast<int32_t*>(base + pl.off_f);
   P.bandbuf = reinterpret_cast<double*>(base + pl.off_band);
+  P.qr_stages = pl.qr_stages;
   P.debuf = reinterpret_cast<double*>(base + pl.off_de);
   P.L = pl.L;
   P.n = pl.n;
