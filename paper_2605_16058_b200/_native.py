@@ -60,7 +60,8 @@ SIGNATURES = {
 }
 
 SVD_STAT_NAMES = ("slices", "sweeps", "pairs", "rotated", "cyc_gram", "cyc_eig", "cyc_apply",
-                  "cyc_qr", "cyc_final", "cyc_load", "cyc_band", "cyc_bulge")
+                  "cyc_qr", "cyc_final", "cyc_load", "cyc_band", "cyc_bulge", "cyc_pfact",
+                  "cyc_trail", "cyc_right", "cyc_pmisc")
 
 
 def svd_stats(reset=True) -> dict:

@@ -52,7 +52,8 @@ constexpr int QR_MAX_LP = 1344;
 constexpr int ZS = 20;        // Z (16 x 32) column stride
 
 enum { ST_SLICES = 0, ST_SWEEPS, ST_PAIRS, ST_ROTATED, ST_CYC_GRAM, ST_CYC_EIG, ST_CYC_APPLY,
-       ST_CYC_QR, ST_CYC_FINAL, ST_CYC_LOAD, ST_CYC_BAND, ST_CYC_BULGE, ST_COUNT };
+       ST_CYC_QR, ST_CYC_FINAL, ST_CYC_LOAD, ST_CYC_BAND, ST_CYC_BULGE, ST_CYC_PFACT, ST_CYC_TRAIL,
+       ST_CYC_RIGHT, ST_CYC_PMISC, ST_COUNT };
 
 __device__ unsigned long long g_stats[16];
 
@@ -139,7 +140,9 @@ struct __align__(16) QrSmemFixed {
   double sums[BW];
   double wv[BW];
   double tau[BW];
-  double scal[4];
+  double scal[2 + BW];
+  double prow[2][BW];
+  double psum[2][BW];
 };
 
 __device__ __forceinline__ void stat_add(const SvdParams& P, int k, unsigned long long v) {
@@ -200,7 +203,7 @@ __device__ void gram_pair(JacobiSmem& sm, const double* T, int64_t ld, int64_t r
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int ti = warp >> 1, tj0 = (warp & 1) * 2;
-  double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+  double a00[2] = {0, 0}, a01[2] = {0, 0}, a10[2] = {0, 0}, a11[2] = {0, 0};
   const int64_t nch = rows / RCH;
   stage_pair(sm.xs[0], T, ld, 0, I, J);
   for (int64_t ch = 0; ch < nch; ++ch) {
@@ -217,16 +220,16 @@ __device__ void gram_pair(JacobiSmem& sm, const double* T, int64_t ld, int64_t r
 #pragma unroll
     for (int k4 = 0; k4 < RCH / 4; ++k4) {
       const double a = xa[k4 * 4];
-      dmma884(a00, a01, a, xb[k4 * 4]);
-      dmma884(a10, a11, a, xb[8 * XS + k4 * 4]);
+      dmma884(a00[k4 & 1], a01[k4 & 1], a, xb[k4 * 4]);
+      dmma884(a10[k4 & 1], a11[k4 & 1], a, xb[8 * XS + k4 * 4]);
     }
     __syncthreads();
   }
   const int row = ti * 8 + gq;
-  g[row * GS + tj0 * 8 + 2 * tq] = a00;
-  g[row * GS + tj0 * 8 + 2 * tq + 1] = a01;
-  g[row * GS + (tj0 + 1) * 8 + 2 * tq] = a10;
-  g[row * GS + (tj0 + 1) * 8 + 2 * tq + 1] = a11;
+  g[row * GS + tj0 * 8 + 2 * tq] = a00[0] + a00[1];
+  g[row * GS + tj0 * 8 + 2 * tq + 1] = a01[0] + a01[1];
+  g[row * GS + (tj0 + 1) * 8 + 2 * tq] = a10[0] + a10[1];
+  g[row * GS + (tj0 + 1) * 8 + 2 * tq + 1] = a11[0] + a11[1];
   __syncthreads();
 }
 
@@ -566,20 +569,105 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
   }
 }
 
+// Register-resident variant: thread t owns rows t + i*TPB (i < RPT) of all
+// 16 panel columns, so the BLAS2 column steps touch no shared memory; only
+// the 16 reductions per column and the pivot row go through it.
+template <int RPT>
+__device__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
+                                 int64_t nrows) {
+  const int tid = threadIdx.x;
+  double a[RPT][BW];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int64_t r = tid + i * TPB;
+#pragma unroll
+    for (int c = 0; c < BW; ++c) a[i][c] = (r < nrows) ? pan[c * prs + r] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < BW; ++j) {
+    const int64_t pr = k0 + j;
+    const int par = j & 1;  // double-buffered pivot row / sums: 2 barriers per column
+    double acc[BW];
+#pragma unroll
+    for (int c = 0; c < BW; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = tid + i * TPB;
+      if (r == pr) {
+#pragma unroll
+        for (int c = 0; c < BW; ++c) q.prow[par][c] = a[i][c];
+      }
+      if (r > pr) {
+        const double x = a[i][j];
+        acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+        for (int c = j + 1; c < BW; ++c) acc[c] = fma(x, a[i][c], acc[c]);
+      }
+    }
+    reduce16(acc, q.red, q.psum[par]);
+    // every thread derives the reflector (dlarfg) redundantly
+    const double alpha = q.prow[par][j];
+    const double xn2 = q.psum[par][0];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) q.tau[j] = tau;
+    if (tau != 0.0) {
+      double tw[BW];
+#pragma unroll
+      for (int c = j + 1; c < BW; ++c) tw[c] = tau * fma(scal, q.psum[par][c], q.prow[par][c]);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t r = tid + i * TPB;
+        if (r >= pr) {
+          const double vr = (r == pr) ? 1.0 : a[i][j] * scal;
+#pragma unroll
+          for (int c = j + 1; c < BW; ++c) a[i][c] = fma(-vr, tw[c], a[i][c]);
+          a[i][j] = (r == pr) ? beta : vr;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int64_t r = tid + i * TPB;
+    if (r < nrows) {
+#pragma unroll
+      for (int c = 0; c < BW; ++c) pan[c * prs + r] = a[i][c];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows) {
+  const int64_t rpt = (nrows + TPB - 1) / TPB;
+  switch (rpt) {
+    case 1: panel_factor_reg<1>(q, pan, prs, k0, nrows); break;
+    case 2: panel_factor_reg<2>(q, pan, prs, k0, nrows); break;
+    case 3: panel_factor_reg<3>(q, pan, prs, k0, nrows); break;
+    case 4: panel_factor_reg<4>(q, pan, prs, k0, nrows); break;
+    default: panel_factor(q, pan, prs, k0, nrows); break;
+  }
+}
+
 // S = V^T V (16x16) on DMMA; V = explicit panel (zeros above, 1 on pivots).
 __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64_t kc, int64_t LP) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int tile = warp & 3, half = warp >> 2;
   const int ti = tile >> 1, tj = tile & 1;
-  double d0 = 0.0, d1 = 0.0;
-  for (int64_t r0 = kc + half * 4; r0 < LP; r0 += 8) {
+  double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+  int u = 0;
+  for (int64_t r0 = kc + half * 4; r0 < LP; r0 += 8, u = (u + 1) & 3) {
     const double a = pan[(ti * 8 + gq) * prs + r0 + tq];
     const double b = pan[(tj * 8 + gq) * prs + r0 + tq];
-    dmma884(d0, d1, a, b);
+    dmma884(d0[u], d1[u], a, b);
   }
-  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq] = d0;
-  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq + 1] = d1;
+  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq] = (d0[0] + d0[1]) + (d0[2] + d0[3]);
+  q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq + 1] = (d1[0] + d1[1]) + (d1[2] + d1[3]);
   __syncthreads();
   // T (forward, columnwise; LAPACK dlarft): T_jj = tau_j,
   // T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] S[l][j]   (thread i owns row i)
@@ -624,7 +712,8 @@ __device__ void trailing_update(QrSmemFixed& q, const Ring& ring, const double* 
   // ---- Y = V^T C (16 x 32): warp -> tile (ti = warp>>2, tj = warp&3)
   {
     const int ti = warp >> 2, tj = warp & 3;
-    double y0 = 0.0, y1 = 0.0;
+    // four independent accumulator pairs break the DMMA dependency chain
+    double ya[4] = {0.0, 0.0, 0.0, 0.0}, yb[4] = {0.0, 0.0, 0.0, 0.0};
     for (int s = 0; s < nst - 1; ++s) {
       if (s < nch) stage_cols(ring.buf(s), X, ld, kc + s * RCH, c0, NP);
       else cp_async_commit();
@@ -640,11 +729,11 @@ __device__ void trailing_update(QrSmemFixed& q, const Ring& ring, const double* 
       const double* va = pan + (ti * 8 + gq) * prs + r0 + tq;
       const double* cb = cs + (tj * 8 + gq) * XS + tq;
 #pragma unroll
-      for (int k4 = 0; k4 < RCH / 4; ++k4) dmma884(y0, y1, va[k4 * 4], cb[k4 * 4]);
+      for (int k4 = 0; k4 < RCH / 4; ++k4) dmma884(ya[k4 & 3], yb[k4 & 3], va[k4 * 4], cb[k4 * 4]);
     }
     cp_async_wait<0>();
-    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq] = y0;
-    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq + 1] = y1;
+    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq] = (ya[0] + ya[1]) + (ya[2] + ya[3]);
+    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq + 1] = (yb[0] + yb[1]) + (yb[2] + yb[3]);
   }
   __syncthreads();
   // ---- Z = T^T Y (16 x 32), stored column-major (stride ZS) for B fragments
@@ -716,7 +805,7 @@ __device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan
   const int64_t nblk = (NP - j0 + GW - 1) / GW;
   for (int64_t r0 = rc; r0 < nrows; r0 += RCH) {
     // ---- Y = C V (64 x 16): warp -> row tile `warp`, column tiles 0..1
-    double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double y[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [ct][k4&1][e]
     for (int s = 0; s < nst - 1; ++s) {
       if (s < nblk) stage_cols(ring.buf(s), A, ld, r0, j0 + s * GW, NP);
       else cp_async_commit();
@@ -734,14 +823,15 @@ __device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan
         const double a = cs[(k4 * 4 + tq) * XS + warp * 8 + gq];
 #pragma unroll
         for (int ct = 0; ct < 2; ++ct)
-          dmma884(y[ct][0], y[ct][1], a, pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
+          dmma884(y[ct][k4 & 1][0], y[ct][k4 & 1][1], a,
+                  pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
       }
     }
     cp_async_wait<0>();
 #pragma unroll
     for (int ct = 0; ct < 2; ++ct) {
-      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq] = y[ct][0];
-      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq + 1] = y[ct][1];
+      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq] = y[ct][0][0] + y[ct][1][0];
+      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq + 1] = y[ct][0][1] + y[ct][1][1];
     }
     __syncthreads();
     // ---- Z = Y T (64 x 16), column-major (stride XS) for A fragments
@@ -788,6 +878,269 @@ __device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan
   }
 }
 
+// ---------------------------------------------------------------------
+// Warp-private streaming trailing updates (no CTA barrier per chunk).
+// Each warp owns a private region of WREG doubles (a 2-stage cp.async ring
+// plus scratch) after the panel in shared memory.
+// ---------------------------------------------------------------------
+constexpr int WREG = 1280;  // doubles per warp
+constexpr int CS16 = 20;    // column stride of a staged 16-row chunk
+
+// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
+// rows [kc, nrows) in 16-row chunks dealt round-robin to the warps.
+__device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs,
+                                  double* X, int64_t ld, int64_t nrows, int64_t NP, int64_t kc,
+                                  int64_t c0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  double* wr = wbase + warp * WREG;  // [2][32 * CS16]
+  const int64_t nck = (nrows - kc) / 16;
+  auto stage = [&](int64_t ck, int b) {
+    const int64_t r0 = kc + ck * 16;
+    double* dst = wr + b * (GW * CS16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int qq = lane + 32 * i;
+      const int col = qq >> 3, r2 = (qq & 7) * 2;
+      const bool in = c0 + col < NP;
+      cp_async16(dst + col * CS16 + r2, in ? X + r0 + r2 + (c0 + col) * ld : X, in ? 16 : 0);
+    }
+    cp_async_commit();
+  };
+  // ---- Y = V^T C  (16 x 32): every warp accumulates all 8 tiles over its chunks
+  double y[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) y[a][b][0] = y[a][b][1] = 0.0;
+  int64_t ck = warp;
+  if (ck < nck) stage(ck, 0);
+  for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
+    const int64_t nx = ck + TPB / 32;
+    if (nx < nck) {
+      stage(nx, (it + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const double* cs = wr + (it & 1) * (GW * CS16);
+    const int64_t r0 = kc + ck * 16;
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) av[a] = pan[(a * 8 + gq) * prs + r0 + k4 * 4 + tq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = cs[(b * 8 + gq) * CS16 + k4 * 4 + tq];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(y[a][b][0], y[a][b][1], av[a], bv[b]);
+    }
+    __syncwarp();
+  }
+  // ---- deterministic cross-warp sum (fixed warp order) into q.y
+  {
+    double* part = wr;  // 16 x 32 row-major partial of this warp
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        part[(a * 8 + gq) * GW + b * 8 + 2 * tq] = y[a][b][0];
+        part[(a * 8 + gq) * GW + b * 8 + 2 * tq + 1] = y[a][b][1];
+      }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < TPB / 32; ++w) sacc += wbase[w * WREG + e];
+    q.y[(e / GW) * GS + (e % GW)] = sacc;
+  }
+  __syncthreads();
+  // ---- Z = T^T Y (16 x 32), column-major (stride ZS) for B fragments
+  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
+    const int i = e & 15, c = e >> 4;
+    double sacc = 0.0;
+    for (int l = 0; l <= i; ++l) sacc += q.t[l * 17 + i] * q.y[l * GS + c];
+    q.z[c * ZS + i] = sacc;
+  }
+  __syncthreads();
+  // ---- C -= V Z per chunk, warp-private
+  ck = warp;
+  if (ck < nck) stage(ck, 0);
+  for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
+    const int64_t nx = ck + TPB / 32;
+    if (nx < nck) {
+      stage(nx, (it + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    double* cs = wr + (it & 1) * (GW * CS16);
+    const int64_t r0 = kc + ck * 16;
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < BW / 4; ++k4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) av[a] = pan[(k4 * 4 + tq) * prs + r0 + a * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = q.z[(b * 8 + gq) * ZS + k4 * 4 + tq];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        cs[(b * 8 + 2 * tq) * CS16 + a * 8 + gq] -= acc[a][b][0];
+        cs[(b * 8 + 2 * tq + 1) * CS16 + a * 8 + gq] -= acc[a][b][1];
+      }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int qq = lane + 32 * i;
+      const int col = qq >> 3, r2 = (qq & 7) * 2;
+      if (c0 + col < NP)
+        *reinterpret_cast<double2*>(X + r0 + r2 + (c0 + col) * ld) =
+            *reinterpret_cast<const double2*>(cs + col * CS16 + r2);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// LQ half-step update, warp-private:  C <- C (I - V T V^T) for columns
+// [j0, NP) and rows [rmin, nrows) of A (ld).  Each warp owns 8-row tiles
+// (rows rc + 8*t, t = warp, warp+8, ...) end to end: Y = C V, Z = Y T and
+// C -= Z V^T never leave the warp.  V[j][c] = pan2[c * prs + j].
+constexpr int CS8 = 12;  // column stride of a staged 8-row tile
+
+__device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2, int64_t prs,
+                               double* A, int64_t ld, int64_t nrows, int64_t NP, int64_t rc,
+                               int64_t rmin, int64_t j0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  double* wr = wbase + warp * WREG;          // ring [2][32 * CS8]
+  double* zs = wr + 2 * GW * CS8;            // Y / Z scratch [16 * CS8]
+  const double* Tm = q.t;
+  const int64_t nblk = (NP - j0 + GW - 1) / GW;
+  const int64_t ntile = (nrows - rc) / 8;
+  auto stage = [&](int64_t r0, int64_t b, int slot) {
+    const int64_t jb = j0 + b * GW;
+    double* dst = wr + slot * (GW * CS8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int qq = lane + 32 * i;
+      const int col = qq >> 2, r2 = (qq & 3) * 2;
+      const bool in = jb + col < NP;
+      cp_async16(dst + col * CS8 + r2, in ? A + r0 + r2 + (jb + col) * ld : A, in ? 16 : 0);
+    }
+    cp_async_commit();
+  };
+  for (int64_t tile = warp; tile < ntile; tile += TPB / 32) {
+    const int64_t r0 = rc + tile * 8;
+    if (r0 + 8 <= rmin) continue;  // rows above the panel are final
+    // ---- Y = C V (8 x 16)
+    double y[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [ct][k4&1][e]
+    stage(r0, 0, 0);
+    for (int64_t b = 0; b < nblk; ++b) {
+      if (b + 1 < nblk) {
+        stage(r0, b + 1, int((b + 1) & 1));
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const double* cs = wr + (b & 1) * (GW * CS8);
+      const int64_t jb = j0 + b * GW;
+#pragma unroll
+      for (int k4 = 0; k4 < GW / 4; ++k4) {
+        const double a = cs[(k4 * 4 + tq) * CS8 + gq];
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct)
+          dmma884(y[ct][k4 & 1][0], y[ct][k4 & 1][1], a,
+                  pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
+      }
+      __syncwarp();
+    }
+    // ---- Z = Y T (8 x 16): Y -> zs (row-major 8 x 16), Z -> zs as A fragments
+#pragma unroll
+    for (int ct = 0; ct < 2; ++ct) {
+      zs[gq * 16 + ct * 8 + 2 * tq] = y[ct][0][0] + y[ct][1][0];
+      zs[gq * 16 + ct * 8 + 2 * tq + 1] = y[ct][0][1] + y[ct][1][1];
+    }
+    __syncwarp();
+    double zv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = lane + 32 * u;  // 128 outputs
+      const int r = e & 7, c = e >> 3;
+      double sacc = 0.0;
+      for (int l = 0; l <= c; ++l) sacc += zs[r * 16 + l] * Tm[l * 17 + c];
+      zv[u] = sacc;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = lane + 32 * u;
+      const int r = e & 7, c = e >> 3;
+      zs[c * CS8 + r] = zv[u];
+    }
+    __syncwarp();
+    // ---- C -= Z V^T, block by block
+    stage(r0, 0, 0);
+    for (int64_t b = 0; b < nblk; ++b) {
+      if (b + 1 < nblk) {
+        stage(r0, b + 1, int((b + 1) & 1));
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      double* cs = wr + (b & 1) * (GW * CS8);
+      const int64_t jb = j0 + b * GW;
+      double acc[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < BW / 4; ++k4) {
+        const double a = zs[(k4 * 4 + tq) * CS8 + gq];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          dmma884(acc[c][0], acc[c][1], a, pan2[(k4 * 4 + tq) * prs + jb + c * 8 + gq]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cs[(c * 8 + 2 * tq) * CS8 + gq] -= acc[c][0];
+        cs[(c * 8 + 2 * tq + 1) * CS8 + gq] -= acc[c][1];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int qq = lane + 32 * i;
+        const int col = qq >> 2, r2 = (qq & 3) * 2;
+        if (jb + col < NP)
+          *reinterpret_cast<double2*>(A + r0 + r2 + (jb + col) * ld) =
+              *reinterpret_cast<const double2*>(cs + col * CS8 + r2);
+      }
+      __syncwarp();
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
 // Panel -> explicit V (zeros above the pivot, 1 on it) for rows [0, prs).
 __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0, int64_t nrows) {
   for (int c = 0; c < BW; ++c) {
@@ -813,6 +1166,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
   const int64_t prs = LP + 36;
   double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
   const Ring ring{pan + BW * prs, P.qr_stages};
+  double* wbase = pan + BW * prs;  // per-warp regions (aliases the ring, used exclusively)
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
   double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
@@ -832,6 +1186,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     }
     if (flag) continue;
     long long t1 = clock64();
+    long long pf = 0, tr = 0, ru = 0;
     // ---------------- QR of the tall X (rows LP)
     if (P.L > P.n) {
       for (int64_t k0 = 0; k0 < NP; k0 += BW) {
@@ -839,7 +1194,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
         for (int c = 0; c < BW; ++c)
           for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < LP ? X[r + (k0 + c) * LP] : 0.0;
         __syncthreads();
-        panel_factor(q, pan, prs, k0, LP);
+        { long long _a = clock64(); panel_factor_any(q, pan, prs, k0, LP); pf += clock64() - _a; }
         if (tid < BW * BW) {
           const int c = tid / BW, r = tid % BW;
           if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
@@ -848,8 +1203,10 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
         if (k0 + BW < NP) {
           explicit_v(pan, prs, k0, LP);
           panel_gram(q, pan, prs, kc, LP);
+          long long _a = clock64();
           for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
-            trailing_update(q, ring, pan, prs, X, LP, LP, NP, kc, c0);
+            trailing_update_w(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
+          tr += clock64() - _a;
         }
         __syncthreads();
       }
@@ -865,7 +1222,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       for (int c = 0; c < BW; ++c)
         for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < RP ? X[r + (k + c) * LP] : 0.0;
       __syncthreads();
-      panel_factor(q, pan, prs, k, RP);
+      { long long _a = clock64(); panel_factor_any(q, pan, prs, k, RP); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;
         if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
@@ -874,8 +1231,12 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       if (k + BW >= NP) break;
       explicit_v(pan, prs, k, RP);
       panel_gram(q, pan, prs, kc, RP);
-      for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
-        trailing_update(q, ring, pan, prs, X, LP, RP, NP, kc, c0);
+      {
+        long long _a = clock64();
+        for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
+          trailing_update_w(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
+        tr += clock64() - _a;
+      }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
       for (int64_t j = tid; j < prs; j += TPB) {
@@ -884,7 +1245,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
         for (int c = 0; c < BW; ++c) pan[c * prs + j] = in ? X[(k + c) + j * LP] : 0.0;
       }
       __syncthreads();
-      panel_factor(q, pan, prs, j0, NP);
+      { long long _a = clock64(); panel_factor_any(q, pan, prs, j0, NP); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
         if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
@@ -898,7 +1259,11 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
           for (int64_t jj = tid; jj < NP; jj += TPB) dst[c * NP + jj] = pan[c * prs + jj];
         if (tid < BW * BW) dst[BW * NP + tid] = q.t[(tid / BW) * 17 + (tid % BW)];
       }
-      right_update(q, ring, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+      {
+        long long _a = clock64();
+        right_update_w(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        ru += clock64() - _a;
+      }
       __syncthreads();
     }
     // ---------------- the 17 diagonals of the band
@@ -910,6 +1275,9 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
     stat_add(P, ST_CYC_QR, (unsigned long long)(t2 - t1));
     stat_add(P, ST_CYC_BAND, (unsigned long long)(t3 - t2));
+    stat_add(P, ST_CYC_PFACT, (unsigned long long)pf);
+    stat_add(P, ST_CYC_TRAIL, (unsigned long long)tr);
+    stat_add(P, ST_CYC_RIGHT, (unsigned long long)ru);
   }
 }
 
@@ -1133,16 +1501,34 @@ __global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P
 // T_GK - x I) - n.  One thread per (slice, sigma_j), sigma_j the j-th
 // largest; interval shrunk to 2u * max(sigma_j, 1e-3 * bound).
 // ----------------------------------------------------------------------
-__device__ __forceinline__ int64_t count_below(const double* d, const double* e, int64_t n, double x,
-                                               double pivmin) {
-  int64_t neg = 0;
+// 1/q from the MUFU approximation plus two Newton steps (relative error
+// ~1e-15): a Sturm pivot computed this way is the exact pivot of T_GK with
+// off-diagonals perturbed by a few ulps, which is all the count needs.
+__device__ __forceinline__ double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ int count_below(const double* d, const double* e, int n, double x,
+                                           double pivmin) {
+  int neg = 0;
   double q = -x;
   neg += (q < 0.0);
-  for (int64_t k = 0; k < 2 * n - 1; ++k) {
-    const double a = (k & 1) ? e[k >> 1] : d[k >> 1];
+  for (int k = 0; k < n; ++k) {
+    const double dk = d[k];
     if (fabs(q) < pivmin) q = -pivmin;
-    q = -x - (a * a) / q;
+    q = fma(-dk * dk, rcp_nr(q), -x);
     neg += (q < 0.0);
+    if (k + 1 < n) {
+      const double ek = e[k];
+      if (fabs(q) < pivmin) q = -pivmin;
+      q = fma(-ek * ek, rcp_nr(q), -x);
+      neg += (q < 0.0);
+    }
   }
   return neg - n;
 }
@@ -1175,7 +1561,7 @@ __global__ void svd_bisect_kernel(SvdParams P) {
           const double mid = 0.5 * (lo + hi);
           if (!(mid > lo && mid < hi)) break;
           if (hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, 1e-3 * bound)) break;
-          if (count_below(d, e, n, mid, pivmin) <= target)
+          if (count_below(d, e, int(n), mid, pivmin) <= target)
             lo = mid;
           else
             hi = mid;
@@ -1518,9 +1904,34 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
       __syncwarp();
       if (act) {
         // chases in reverse order, each chase's column rotations in reverse
+        // (a chase's rotations act on distinct column pairs, 16 apart, so
+        //  four at a time are loaded, rotated and stored without hazards)
         for (int64_t e = nslot - 1; e >= 0; --e) {
-          for (int q = rcnt[e] - 1; q >= 0; --q) {
-            const int64_t t = e * lmax + q;
+          int q = rcnt[e] - 1;
+          const int64_t tb = e * lmax;
+          for (; q >= 3; q -= 4) {
+            double c[4], s[4], a[4], b[4];
+            int col[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int64_t t = tb + q - u;
+              c[u] = rcs[2 * t];
+              s[u] = rcs[2 * t + 1];
+              col[u] = rcol[t];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              a[u] = mine[col[u] - 1];
+              b[u] = mine[col[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              mine[col[u] - 1] = c[u] * a[u] - s[u] * b[u];
+              mine[col[u]] = s[u] * a[u] + c[u] * b[u];
+            }
+          }
+          for (; q >= 0; --q) {
+            const int64_t t = tb + q;
             const double c = rcs[2 * t], s = rcs[2 * t + 1];
             const int col = rcol[t];
             const double a = mine[col - 1], b = mine[col];
@@ -1807,9 +2218,11 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   {
     const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
     const size_t ring = size_t(GW) * XS * sizeof(double);
-    g.qr_stages = 4;
-    while (g.qr_stages > 2 && fixed + g.qr_stages * ring > size_t(227 * 1024)) --g.qr_stages;
-    g.rsmem = fixed + g.qr_stages * ring;
+    g.qr_stages = 2;
+    size_t extra = size_t(g.qr_stages) * ring;
+    const size_t wreg = size_t(TPB / 32) * WREG * sizeof(double);
+    if (wreg > extra) extra = wreg;
+    g.rsmem = fixed + extra;
     if (g.rsmem > size_t(227 * 1024)) g.bidiag = false;  // panel does not fit: Jacobi path
     g.use_qr = false;
     g.run_jacobi = !g.bidiag;

@@ -46,47 +46,100 @@ __global__ void square_keys_kernel(const double* s, int64_t count, unsigned long
 }
 
 // Sequential running sums (np.cumsum) and the lower_bound search.
-// One warp: tiles of 1024 sorted values are staged in shared memory by all
-// lanes (coalesced), lane 0 runs the strictly sequential fp64 chain, and the
-// running sums go back out coalesced.  The chain itself is the only serial
-// part (one dependent DADD per value).
+// Two warps: warp 1 streams tiles of 1024 sorted values into shared memory
+// (and the running sums of the previous tile back out) while lane 0 of warp 0
+// runs the strictly sequential fp64 chain on the current tile; loads of the
+// next 8 values are issued ahead of the 8 dependent adds so the chain runs
+// at DADD latency.  The chain is the only serial part of the threshold.
 constexpr int CS_TILE = 1024;
 
-__global__ void __launch_bounds__(32) cumsum_search_kernel(const unsigned long long* vbits,
+__global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long long* vbits,
                                                            int64_t count, double eps, double* w,
                                                            double* v_out, ThState* st) {
-  __shared__ double tile[CS_TILE];
-  __shared__ double wt[CS_TILE];
-  const int lane = threadIdx.x;
+  __shared__ double tile[2][CS_TILE];
+  __shared__ double wt[2][CS_TILE];
+  __shared__ double acc_sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* v = reinterpret_cast<const double*>(vbits);
-  double acc = 0.0;
-  for (int64_t base = 0; base < count; base += CS_TILE) {
-    const int len = int(count - base < CS_TILE ? count - base : CS_TILE);
+  const int64_t ntiles = (count + CS_TILE - 1) / CS_TILE;
+  auto tlen = [&](int64_t t) { return int(count - t * CS_TILE < CS_TILE ? count - t * CS_TILE : CS_TILE); };
+  if (warp == 1 && ntiles > 0) {
+    const int len = tlen(0);
     for (int k = lane; k < len; k += 32) {
-      const double x = v[base + k];
-      tile[k] = x;
-      if (v_out) v_out[base + k] = x;
+      const double x = v[k];
+      tile[0][k] = x;
+      if (v_out) v_out[k] = x;
     }
-    __syncwarp();
-    if (lane == 0) {
-      int k = 0;
-      if (base == 0) {
-        acc = tile[0];
-        wt[0] = acc;
-        k = 1;
-      }
-#pragma unroll 8
-      for (; k < len; ++k) {
-        acc = __dadd_rn(acc, tile[k]);
-        wt[k] = acc;
-      }
-    }
-    __syncwarp();
-    for (int k = lane; k < len; k += 32) w[base + k] = wt[k];
-    __syncwarp();
   }
-  acc = __shfl_sync(0xffffffffu, acc, 0);
-  if (lane != 0) return;
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int b = int(t & 1);
+    if (warp == 0) {
+      if (lane == 0) {
+        const double* tl = tile[b];
+        double* wl = wt[b];
+        const int len = tlen(t);
+        int k = 0;
+        if (t == 0) {
+          acc = tl[0];
+          wl[0] = acc;
+          k = 1;
+        }
+        double nx[8];
+        if (k + 8 <= len) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) nx[q] = tl[k + q];
+        }
+        for (; k + 8 <= len; k += 8) {
+          double cur[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cur[q] = nx[q];
+          if (k + 16 <= len) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) nx[q] = tl[k + 8 + q];
+          }
+          double w8[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            acc = __dadd_rn(acc, cur[q]);
+            w8[q] = acc;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wl[k + q] = w8[q];
+        }
+        for (; k < len; ++k) {
+          acc = __dadd_rn(acc, tl[k]);
+          wl[k] = acc;
+        }
+      }
+    } else {
+      if (t + 1 < ntiles) {  // prefetch the next tile
+        const int len = tlen(t + 1);
+        const int64_t base = (t + 1) * CS_TILE;
+        for (int k = lane; k < len; k += 32) {
+          const double x = v[base + k];
+          tile[b ^ 1][k] = x;
+          if (v_out) v_out[base + k] = x;
+        }
+      }
+      if (t > 0) {  // running sums of the previous tile out
+        const int len = tlen(t - 1);
+        const int64_t base = (t - 1) * CS_TILE;
+        for (int k = lane; k < len; k += 32) w[base + k] = wt[b ^ 1][k];
+      }
+    }
+    __syncthreads();
+  }
+  if (warp == 1 && ntiles > 0) {
+    const int64_t t = ntiles - 1;
+    const int len = tlen(t);
+    for (int k = lane; k < len; k += 32) w[t * CS_TILE + k] = wt[t & 1][k];
+  }
+  if (threadIdx.x == 0) acc_sh = acc;
+  __syncthreads();
+  acc = acc_sh;
+  if (threadIdx.x != 0) return;
   const double total = count ? acc : 0.0;
   st->total = total;
   if (total == 0.0) {
@@ -345,7 +398,7 @@ extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, 
   STARM_LAUNCH_CHECK();
   STARM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(cubtmp, cub_bytes, keys, sorted, int(count), 0, 64, st));
   count_launch(3);  // the three CUB device-wide calls of this function
-  cumsum_search_kernel<<<1, 32, 0, st>>>(sorted, count, epsilon, w, v_out, stt);
+  cumsum_search_kernel<<<1, 64, 0, st>>>(sorted, count, epsilon, w, v_out, stt);
   STARM_LAUNCH_CHECK();
   mask_kernel<<<grid, 256, 0, st>>>(s, r, nslices, stt, fa, fb);
   STARM_LAUNCH_CHECK();
