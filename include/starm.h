@@ -48,7 +48,15 @@ enum starm_status {
 enum starm_svd_job {
   STARM_SVD_VALUES = 0,     /* slicesvd.py:139-177 svd_values_only            */
   STARM_SVD_FULL = 1,       /* slicesvd.py:115-136 svd_all_slices             */
-  STARM_SVD_TRUNCATED = 2   /* slicesvd.py:259-292 svd_truncated_slices       */
+  STARM_SVD_TRUNCATED = 2,  /* slicesvd.py:259-292 svd_truncated_slices       */
+  /* Two-pass form of tsvdm_tolerance (tsvdm.py:268-321): VALUES_STATE is a
+   * values pass over every slice that also keeps each slice's factorisation
+   * (bidiagonal, logged right-side transformations) in `ws`; a following
+   * TRUNCATED_STATE call with the SAME ws, shapes and s computes the packed
+   * factors of `slice_ids` from that state without refactoring (the device
+   * analogue of the reference's compute-efficient strategy). */
+  STARM_SVD_VALUES_STATE = 3,
+  STARM_SVD_TRUNCATED_STATE = 4
 };
 
 int starm_abi_version(void);

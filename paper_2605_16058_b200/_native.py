@@ -27,6 +27,8 @@ UNSUPPORTED = 5
 SVD_VALUES = 0
 SVD_FULL = 1
 SVD_TRUNCATED = 2
+SVD_VALUES_STATE = 3
+SVD_TRUNCATED_STATE = 4
 
 # name -> (restype, argtypes); mirrors include/starm.h one-to-one.
 SIGNATURES = {

@@ -374,16 +374,32 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
             factors = DeviceFactors(m, p, ranks, u_off, g_off, u_data[: total_rank * m],
                                     g_data[: total_rank * p], total_rank)
     else:
+        # Keep every slice's factorisation in HBM between the passes when it
+        # fits comfortably (always for compute-efficient); otherwise refactor
+        # the rank>0 slices (memory-efficient in the reference's sense).
+        keep = strategy == COMPUTE_EFFICIENT or _state_fits(ahat3)
         with clock.stage("stage1-svd"):
-            s = svd_values_device(ahat3)
+            if keep:
+                s, state = svd_values_device(ahat3, keep_state=True)
+            else:
+                s, state = svd_values_device(ahat3), None
         with clock.stage("threshold"):
             ranks, scal, j, _, _ = threshold_device(s, r, n, epsilon)
             summary = _summary(ranks, scal)
         with clock.stage("stage2-svd"):
-            factors, _ = svd_truncated_device(ahat3, ranks, summary[3])
+            factors, _ = svd_truncated_device(ahat3, ranks, summary[3], state=state)
+        del state
         clock.mark("pack")
     tau, discarded, total, _ = summary
     return _finish(a, ts, factors, METHOD_TOLERANCE, epsilon, discarded, total, host)
+
+
+def _state_fits(x) -> bool:
+    """True when the per-slice SVD state needs < 1/4 of the free HBM."""
+    import torch
+    from .slice_svd import state_bytes
+    free, _ = torch.cuda.mem_get_info(x.device)
+    return state_bytes(x) < free // 4
 
 
 def _summary(ranks, scal):

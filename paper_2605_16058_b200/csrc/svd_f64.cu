@@ -88,6 +88,7 @@ struct SvdParams {
   double* vsel;                 // per slice: right singular vectors (RP x NP)
   double* iiscr;                // inverse-iteration scratch
   int btw;                      // back-transform vectors per pass
+  int by_slice;                 // state arrays indexed by slice (state-keeping jobs)
   int qr_stages;                // cp.async ring depth of the reduce kernel
   int64_t L, n, LP, NP, RP;
   int transposed, use_qr, bidiag, stats;
@@ -144,6 +145,12 @@ struct __align__(16) QrSmemFixed {
   double prow[2][BW];
   double psum[2][BW];
 };
+
+// Index of a slice's factorisation state: its list position, or (for the
+// state-keeping jobs) the slice number itself so a later call can find it.
+__device__ __forceinline__ int64_t state_index(const SvdParams& P, int64_t it) {
+  return P.by_slice ? (P.ids ? P.ids[it] : it) : it;
+}
 
 __device__ __forceinline__ void stat_add(const SvdParams& P, int k, unsigned long long v) {
   if (P.stats && threadIdx.x == 0) atomicAdd(&g_stats[k], v);
@@ -1177,11 +1184,12 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     const int64_t it = cur;
     __syncthreads();
     if (it >= P.count) break;
+    const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
     const int flag = load_slice(P, P.A + slice * P.m * P.p, X, ring.buf(0));
     if (tid == 0) {
-      P.flags[it] = flag;
+      P.flags[si] = flag;
       if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
     }
     if (flag) continue;
@@ -1254,7 +1262,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       explicit_v(pan, prs, j0, NP);
       panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
       if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
-        double* dst = P.rvlog + (it * (NP / BW) + k / BW) * (BW * NP + BW * BW);
+        double* dst = P.rvlog + (si * (NP / BW) + k / BW) * (BW * NP + BW * BW);
         for (int c = 0; c < BW; ++c)
           for (int64_t jj = tid; jj < NP; jj += TPB) dst[c * NP + jj] = pan[c * prs + jj];
         if (tid < BW * BW) dst[BW * NP + tid] = q.t[(tid / BW) * 17 + (tid % BW)];
@@ -1267,7 +1275,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       __syncthreads();
     }
     // ---------------- the 17 diagonals of the band
-    double* band = P.bandbuf + it * (BW + 1) * NP;
+    double* band = P.bandbuf + si * (BW + 1) * NP;
     for (int d = 0; d <= BW; ++d)
       for (int64_t i = tid; i < NP; i += TPB) band[d * NP + i] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
     __syncthreads();
@@ -1383,18 +1391,19 @@ __global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P
     const int64_t it = cur;
     __syncthreads();
     if (it >= P.count) break;
-    if (P.flags[it]) continue;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
     long long t0 = clock64();
-    const double* band = P.bandbuf + it * (BW + 1) * NP;
+    const double* band = P.bandbuf + si * (BW + 1) * NP;
     for (int64_t e = threadIdx.x; e < n * BWS; e += blockDim.x) {
       const int64_t i = e / BWS, k = e % BWS;
       const int64_t d = k - 1;
       W[e] = (d >= 0 && d <= BW && i + d < n) ? band[d * NP + i] : 0.0;
     }
     __syncthreads();
-    double* lcs = P.rotcs ? P.rotcs + it * P.rotcap * 2 : nullptr;
-    int32_t* lcol = P.rotcol ? P.rotcol + it * P.rotcap : nullptr;
-    int32_t* lcnt = P.rotcs ? reinterpret_cast<int32_t*>(P.rotcnt) + it * nslot : nullptr;
+    double* lcs = P.rotcs ? P.rotcs + si * P.rotcap * 2 : nullptr;
+    int32_t* lcol = P.rotcol ? P.rotcol + si * P.rotcap : nullptr;
+    int32_t* lcnt = P.rotcs ? reinterpret_cast<int32_t*>(P.rotcnt) + si * nslot : nullptr;
     // per-warp chase state
     int64_t e = warp;
     int ci = 0, cj = 0, rr = 0, phase = -1, nlog = 0;  // phase -1: not started
@@ -1483,7 +1492,7 @@ __global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P
     barrier:
       __syncthreads();
     }
-    double* de = P.debuf + it * 2 * NP;
+    double* de = P.debuf + si * 2 * NP;
     for (int64_t i = threadIdx.x; i < NP; i += blockDim.x) {
       de[i] = i < n ? BEL(W, i, i) : 0.0;
       de[NP + i] = i + 1 < n ? BEL(W, i, i + 1) : 0.0;
@@ -1539,12 +1548,13 @@ __global__ void svd_bisect_kernel(SvdParams P) {
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
        g += int64_t(gridDim.x) * blockDim.x) {
     const int64_t it = g / n, j = g % n;
+    const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
-    const int flag = P.flags[it];
+    const int flag = P.flags[si];
     if (flag == 2) continue;
     double sigma = 0.0;
     if (flag == 0) {
-      const double* d = P.debuf + it * 2 * NP;
+      const double* d = P.debuf + si * 2 * NP;
       const double* e = d + NP;
       double bound = 0.0, amax = 0.0;
       for (int64_t k = 0; k < n; ++k) {
@@ -1762,10 +1772,11 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   double* z = dl + 2 * NP;    // 1.0 where rows i, i+1 were interchanged
   for (int64_t g = gtid; g < total_work; g += nthreads) {
     const int64_t it = g / n, j = g % n;
-    if (P.flags[it]) continue;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
     if (j >= kout_of(P, slice)) continue;
-    const double* bd = P.debuf + it * 2 * NP;
+    const double* bd = P.debuf + si * 2 * NP;
     const double* be = bd + NP;
     const double lam = P.s[j + slice * n];
     double tnorm = 0.0;
@@ -1801,7 +1812,7 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
       }
     }
     if (dd[N2 - 1] == 0.0) dd[N2 - 1] = pert;
-    double* vout = P.vsel + it * RP * NP + j * RP;
+    double* vout = P.vsel + si * RP * NP + j * RP;
     double* x = P.iiscr + nthreads * 5 * 2 * NP + gtid * 2 * NP;  // the iterate
     for (int64_t i = 0; i < N2; ++i)
       x[i] = 1.0 + 0.25 * double(((i + 1) * 7919 + (j + 1) * 104729) % 97) / 97.0;
@@ -1852,10 +1863,11 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
     if (lane == 0) it = int64_t(atomicAdd(&P.counter[3], 1ull));
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= P.count) break;
-    if (P.flags[it]) continue;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
     const int64_t k = kout_of(P, slice);
-    double* Vb = P.vsel + it * RP * NP;
+    double* Vb = P.vsel + si * RP * NP;
     // ---- (1) orthonormalise the bidiagonal vectors (CGS2 with fallback)
     for (int64_t j = 0; j < k; ++j) {
       double* vj = Vb + j * RP;
@@ -1891,10 +1903,10 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
     // ---- (2) back-transformation, 32 vectors per pass
     const int64_t nslot = chase_slots(n);
     const int lmax = chase_logmax(n);
-    const int32_t* rcnt = reinterpret_cast<const int32_t*>(P.rotcnt) + it * nslot;
-    const double* rcs = P.rotcs + it * P.rotcap * 2;
-    const int32_t* rcol = P.rotcol + it * P.rotcap;
-    const double* rv = P.rvlog + it * npan * (BW * NP + BW * BW);
+    const int32_t* rcnt = reinterpret_cast<const int32_t*>(P.rotcnt) + si * nslot;
+    const double* rcs = P.rotcs + si * P.rotcap * 2;
+    const int32_t* rcol = P.rotcol + si * P.rotcap;
+    const double* rv = P.rvlog + si * npan * (BW * NP + BW * BW);
     for (int64_t j0 = 0; j0 < k; j0 += P.btw) {
       const int64_t j = j0 + lane;
       const bool act = lane < P.btw && j < k;
@@ -1992,8 +2004,9 @@ __global__ void __launch_bounds__(TPB) svd_vecout_kernel(SvdParams P) {
     const int64_t it = cur;
     __syncthreads();
     if (it >= P.count) break;
+    const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
-    const int flag = P.flags[it];
+    const int flag = P.flags[si];
     if (flag == 2) continue;
     if (flag == 1) {
       emit_zero_slice(P, slice);
@@ -2001,7 +2014,7 @@ __global__ void __launch_bounds__(TPB) svd_vecout_kernel(SvdParams P) {
     }
     for (int j = tid; j < NS; j += TPB) fs.idx[j] = j;
     __syncthreads();
-    emit_vectors(P, sm, fs, slice, P.A + slice * P.m * P.p, P.vsel + it * RP * NP, fs.idx, Xslot,
+    emit_vectors(P, sm, fs, slice, P.A + slice * P.m * P.p, P.vsel + si * RP * NP, fs.idx, Xslot,
                  true, nullptr, 0);
   }
 }
@@ -2026,6 +2039,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
     const int64_t it = cur;
     __syncthreads();
     if (it >= P.count) break;
+    const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     const double* A = P.A + slice * P.m * P.p;
     long long t0 = clock64();
@@ -2034,7 +2048,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
     int64_t ldt, rows;
     int flag;
     if (P.use_qr) {
-      flag = P.flags[it];
+      flag = P.flags[si];
       T = P.rbuf + it * RP * NP;
       ldt = RP;
       rows = RP;
@@ -2175,11 +2189,16 @@ __global__ void reset_status_kernel(int32_t* status, unsigned long long* counter
 
 struct Plan {
   int64_t L, n, LP, NP, RP;
-  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, bdvec;
+  int job;                  // effective job after the fallback mapping
+  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s;
+  bool logs;                // right-side transformation logs (vector machinery buffers)
+  bool run_front;           // reduce / bulge / bisect
+  bool run_vec;             // inverse iteration / back-transform / output
+  bool by_slice;            // state kept per slice across calls
   int ns;
   size_t jsmem, rsmem, bsmem;
   int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages;
-  int64_t rotcap;
+  int64_t rotcap, count;
   size_t vsmem, tsmem;
   size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
       off_vsel, off_ii, total;
@@ -2202,19 +2221,14 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.L = m > p ? m : p;
   g.n = m < p ? m : p;
   g.transposed = m < p;
-  g.wantv = job != STARM_SVD_VALUES;
   g.LP = round_up(g.L, RCH);
   g.NP = round_up(g.n, BW);
   if (g.NP < GW) g.NP = GW;
   g.RP = round_up(g.NP, RCH);
-  g.bidiag = g_tune_mode == 1 && g.LP <= QR_MAX_LP;
-  g.use_qr = false;  // Jacobi (non-bidiagonal mode) works on X directly
-  g.run_jacobi = !g.bidiag;
-  g.bdvec = g.bidiag && g.wantv;
-  g.internal_s = g.wantv && !have_s;
   g.ns = 1;
   while (g.ns < g.n) g.ns <<= 1;
   g.jsmem = jacobi_smem_bytes(g.ns);
+  g.bidiag = g_tune_mode == 1 && g.LP <= QR_MAX_LP;
   {
     const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
     const size_t ring = size_t(GW) * XS * sizeof(double);
@@ -2224,10 +2238,24 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     if (wreg > extra) extra = wreg;
     g.rsmem = fixed + extra;
     if (g.rsmem > size_t(227 * 1024)) g.bidiag = false;  // panel does not fit: Jacobi path
-    g.use_qr = false;
-    g.run_jacobi = !g.bidiag;
-    g.bdvec = g.bidiag && g.wantv;
   }
+  // Without the bidiagonal path the state-keeping jobs degrade to the plain
+  // ones (the Jacobi kernel recomputes).
+  if (!g.bidiag && job == STARM_SVD_VALUES_STATE) job = STARM_SVD_VALUES;
+  if (!g.bidiag && job == STARM_SVD_TRUNCATED_STATE) job = STARM_SVD_TRUNCATED;
+  g.job = job;
+  g.by_slice = job == STARM_SVD_VALUES_STATE || job == STARM_SVD_TRUNCATED_STATE;
+  if (g.by_slice) count = nslices;  // state for every slice, indexed by slice
+  g.count = count;
+  g.wantv = job == STARM_SVD_FULL || job == STARM_SVD_TRUNCATED || job == STARM_SVD_TRUNCATED_STATE;
+  g.use_qr = false;  // the Jacobi fallback works on X directly
+  g.run_jacobi = !g.bidiag;
+  g.logs = g.bidiag && job != STARM_SVD_VALUES;
+  g.run_front = g.bidiag && job != STARM_SVD_TRUNCATED_STATE;
+  g.run_vec = g.bidiag && g.wantv;
+  // (the state-keeping truncated job always receives the values pass's s,
+  //  so its workspace has exactly the values-state layout)
+  g.internal_s = g.wantv && !have_s && !g.by_slice;
   g.bsmem = size_t(g.NP) * BWS * sizeof(double);
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
@@ -2240,7 +2268,7 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     if (rc) return rc;
     g.slots_j = clampc(int64_t(sms) * per);
   }
-  if (g.bdvec) {
+  if (g.logs) {
     rc = occupancy((const void*)svd_vecout_kernel, TPB, g.jsmem, &per);
     if (rc) return rc;
     g.slots_v = clampc(int64_t(sms) * per);
@@ -2276,19 +2304,19 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     return o;
   };
   g.off_x = take(size_t(xslots) * g.LP * g.NP * sizeof(double));
-  g.off_w = take(g.wantv ? size_t(g.slots_j) * g.RP * g.NP * sizeof(double) : 0);
-  g.off_r = take((g.use_qr && g.wantv) ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_w = take(g.wantv && g.run_jacobi ? size_t(g.slots_j) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_r = take(0);
   g.off_f = take(size_t(count) * 4);
   g.off_band = take(g.bidiag ? size_t(count) * (BW + 1) * g.NP * sizeof(double) : 0);
   g.off_de = take(g.bidiag ? size_t(count) * 2 * g.NP * sizeof(double) : 0);
   g.off_s = take(g.internal_s ? size_t(nslices) * g.n * sizeof(double) : 0);
   const size_t npan = size_t(g.NP / BW);
-  g.off_rv = take(g.bdvec ? size_t(count) * npan * (BW * g.NP + BW * BW) * sizeof(double) : 0);
-  g.off_rcs = take(g.bdvec ? size_t(count) * g.rotcap * 2 * sizeof(double) : 0);
-  g.off_rcol = take(g.bdvec ? size_t(count) * g.rotcap * sizeof(int32_t) : 0);
-  g.off_rcnt = take(g.bdvec ? size_t(count) * chase_slots(g.n) * sizeof(int32_t) : 0);
-  g.off_vsel = take(g.bdvec ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
-  g.off_ii = take(g.bdvec ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
+  g.off_rv = take(g.logs ? size_t(count) * npan * (BW * g.NP + BW * BW) * sizeof(double) : 0);
+  g.off_rcs = take(g.logs ? size_t(count) * g.rotcap * 2 * sizeof(double) : 0);
+  g.off_rcol = take(g.logs ? size_t(count) * g.rotcap * sizeof(int32_t) : 0);
+  g.off_rcnt = take(g.logs ? size_t(count) * chase_slots(g.n) * sizeof(int32_t) : 0);
+  g.off_vsel = take(g.logs ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
+  g.off_ii = take(g.logs ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
   g.total = off;
   *pl = g;
   return STARM_OK;
@@ -2332,7 +2360,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
                              const int64_t* g_off, double* u_data, double* g_data,
                              int32_t* status, void* ws, size_t ws_bytes, void* stream) {
   STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "svd: extents must be positive");
-  STARM_CHECK_ARG(job == STARM_SVD_VALUES || job == STARM_SVD_FULL || job == STARM_SVD_TRUNCATED,
+  STARM_CHECK_ARG(job >= STARM_SVD_VALUES && job <= STARM_SVD_TRUNCATED_STATE,
                   "svd: unknown job %d", job);
   const int64_t r = m < p ? m : p;
   if (r > MAX_NS) {
@@ -2340,10 +2368,16 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     return STARM_UNSUPPORTED;
   }
   STARM_CHECK_ARG(ahat && status && ws, "svd: null pointer");
-  STARM_CHECK_ARG(job != STARM_SVD_VALUES || s, "svd: values job needs s");
+  STARM_CHECK_ARG((job != STARM_SVD_VALUES && job != STARM_SVD_VALUES_STATE) || s,
+                  "svd: values jobs need s");
   STARM_CHECK_ARG(job != STARM_SVD_FULL || (s && u && v), "svd: full job needs s, u, v");
-  STARM_CHECK_ARG(job != STARM_SVD_TRUNCATED || (ranks && u_off && g_off && u_data && g_data),
-                  "svd: truncated job needs ranks, offsets and packed buffers");
+  STARM_CHECK_ARG((job != STARM_SVD_TRUNCATED && job != STARM_SVD_TRUNCATED_STATE) ||
+                      (ranks && u_off && g_off && u_data && g_data),
+                  "svd: truncated jobs need ranks, offsets and packed buffers");
+  STARM_CHECK_ARG(job != STARM_SVD_TRUNCATED_STATE || s,
+                  "svd: the state-keeping truncated job needs the values pass's s");
+  STARM_CHECK_ARG(job != STARM_SVD_VALUES_STATE || !slice_ids,
+                  "svd: the state-keeping values job factors every slice (slice_ids must be NULL)");
   if (!slice_ids) count = nslices;
   cudaStream_t st = as_stream(stream);
   unsigned long long* counters = reinterpret_cast<unsigned long long*>(ws);
@@ -2363,7 +2397,9 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.N = nslices;
   P.ids = slice_ids;
   P.count = count;
-  P.job = job;
+  P.job = pl.job == STARM_SVD_TRUNCATED_STATE ? STARM_SVD_TRUNCATED
+          : pl.job == STARM_SVD_VALUES_STATE  ? STARM_SVD_VALUES
+                                              : pl.job;
   P.s = pl.internal_s ? reinterpret_cast<double*>(base + pl.off_s) : s;
   P.u = u;
   P.v = v;
@@ -2376,7 +2412,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.counter = counters;
   P.xslots = reinterpret_cast<double*>(base + pl.off_x);
   P.wslots = reinterpret_cast<double*>(base + pl.off_w);
-  P.rbuf = (pl.use_qr && pl.wantv) ? reinterpret_cast<double*>(base + pl.off_r) : nullptr;
+  P.rbuf = nullptr;
   P.flags = reinterpret_cast<int32_t*>(base + pl.off_f);
   P.bandbuf = reinterpret_cast<double*>(base + pl.off_band);
   P.qr_stages = pl.qr_stages;
@@ -2389,12 +2425,13 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.transposed = pl.transposed;
   P.use_qr = pl.use_qr;
   P.bidiag = pl.bidiag;
+  P.by_slice = pl.by_slice;
   P.stats = g_stats_on;
   // Jacobi convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).
   P.tol = double(pl.L > 32 ? pl.L : 32) * DBL_EPSILON;
   P.max_sweeps = g_tune_sweeps;
   P.max_inner = g_tune_inner;
-  if (pl.bdvec) {
+  if (pl.logs) {
     P.rvlog = reinterpret_cast<double*>(base + pl.off_rv);
     P.rotcs = reinterpret_cast<double*>(base + pl.off_rcs);
     P.rotcol = reinterpret_cast<int32_t*>(base + pl.off_rcol);
@@ -2404,7 +2441,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     P.iiscr = reinterpret_cast<double*>(base + pl.off_ii);
     P.btw = pl.btw;
   }
-  if (pl.bidiag) {
+  if (pl.run_front) {
     svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     svd_bulge_kernel<<<pl.slots_b, BULGE_WARPS * 32, pl.bsmem, st>>>(P);
@@ -2412,8 +2449,8 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
     STARM_LAUNCH_CHECK();
   }
-  if (pl.bdvec) {
-    svd_bdvec_kernel<<<(pl.ii_threads + 127) / 128, 128, 0, st>>>(P, count * pl.n);
+  if (pl.run_vec) {
+    svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n);
     STARM_LAUNCH_CHECK();
     svd_backtransform_kernel<<<pl.slots_t, 32, pl.tsmem, st>>>(P);
     STARM_LAUNCH_CHECK();

@@ -158,32 +158,56 @@ def _raise_slice_status(status_host, what):
 
 
 def _svd_launch(x: DeviceTensor, job, ids=None, s=None, u=None, v=None, ranks=None, u_off=None,
-                g_off=None, u_data=None, g_data=None):
-    """One persistent-grid launch of starm_svd_f64 over ``ids`` (device int64,
-    or None for every slice).  The workspace is one X/V slot per resident
-    CTA, so it is bounded by the SM count, not by the slice count."""
+                g_off=None, u_data=None, g_data=None, ws=None):
+    """One call of starm_svd_f64 over ``ids`` (device int64, or None for every
+    slice).  Returns the workspace (which carries the per-slice state after a
+    VALUES_STATE job).  Work is scheduled on persistent grids; the scratch is
+    per resident CTA except for the per-slice factorisation state."""
     import torch
     m, p, r, n = _geometry(x)
     dev = x.device
     count = n if ids is None else int(ids.numel())
     if count == 0:
-        return
+        return ws
     status = torch.empty(2, dtype=torch.int32, device=dev)
     lib = nat.load()
     nbytes = lib.starm_svd_workspace_bytes(m, p, n, count, job)
-    ws = nat.workspace(nbytes, dev)
+    if ws is None:
+        ws = nat.workspace(nbytes, dev)
+    elif ws.numel() < nbytes:
+        raise RuntimeError(f"SVD state workspace too small ({ws.numel()} < {nbytes} bytes)")
     nat.call("starm_svd_f64", x.data.data_ptr(), m, p, n, nat.ptr(ids), count, job, nat.ptr(s),
              nat.ptr(u), nat.ptr(v), nat.ptr(ranks), nat.ptr(u_off), nat.ptr(g_off),
-             nat.ptr(u_data), nat.ptr(g_data), status.data_ptr(), ws.data_ptr(), nbytes,
+             nat.ptr(u_data), nat.ptr(g_data), status.data_ptr(), ws.data_ptr(), ws.numel(),
              nat.stream_ptr(dev))
-    _raise_slice_status(status.cpu().numpy(), "jacobi")
+    _raise_slice_status(status.cpu().numpy(), "slice SVD")
+    return ws
 
 
-def svd_values_device(x: DeviceTensor):
-    """(r, N) singular values as a column-major torch tensor (flat r*N)."""
+class SvdState:
+    """Factorisation state of every slice kept in HBM by a VALUES_STATE pass
+    (bidiagonals and logged right-side transformations); lets the truncated
+    pass skip refactoring (the device form of the compute-efficient strategy)."""
+
+    def __init__(self, ws, s):
+        self.ws = ws
+        self.s = s
+
+
+def state_bytes(x: DeviceTensor) -> int:
+    m, p, r, n = _geometry(x)
+    return int(nat.load().starm_svd_workspace_bytes(m, p, n, n, nat.SVD_VALUES_STATE))
+
+
+def svd_values_device(x: DeviceTensor, keep_state=False):
+    """(r, N) singular values as a column-major torch tensor (flat r*N); with
+    ``keep_state`` also returns the SvdState for svd_truncated_device."""
     import torch
     m, p, r, n = _geometry(x)
     s = torch.empty(r * n, dtype=torch.float64, device=x.device)
+    if keep_state:
+        ws = _svd_launch(x, nat.SVD_VALUES_STATE, s=s)
+        return s, SvdState(ws, s)
     _svd_launch(x, nat.SVD_VALUES, s=s)
     return s
 
@@ -208,10 +232,13 @@ def pack_offsets_device(ranks_dev, m, p):
     return u_off, g_off
 
 
-def svd_truncated_device(x: DeviceTensor, ranks_dev, total_rank, ids=None, keep_values=False):
+def svd_truncated_device(x: DeviceTensor, ranks_dev, total_rank, ids=None, keep_values=False,
+                         state=None):
     """Packed leading-rank factors.  ``ids`` lists the slices to factor
     (device int64); by default all slices with rank > 0, or every slice
-    when ``keep_values``.  Returns (DeviceFactors, s or None)."""
+    when ``keep_values``.  With ``state`` (from svd_values_device(...,
+    keep_state=True)) the slices are not refactored.  Returns
+    (DeviceFactors, s or None)."""
     import torch
     m, p, r, n = _geometry(x)
     dev = x.device
@@ -224,8 +251,12 @@ def svd_truncated_device(x: DeviceTensor, ranks_dev, total_rank, ids=None, keep_
     if keep_values:
         ids = None
     if ids is None or ids.numel() > 0:
-        _svd_launch(x, nat.SVD_TRUNCATED, ids=ids, s=s, ranks=ranks_dev, u_off=u_off, g_off=g_off,
-                    u_data=u_data, g_data=g_data)
+        if state is not None and not keep_values:
+            _svd_launch(x, nat.SVD_TRUNCATED_STATE, ids=ids, s=state.s, ranks=ranks_dev,
+                        u_off=u_off, g_off=g_off, u_data=u_data, g_data=g_data, ws=state.ws)
+        else:
+            _svd_launch(x, nat.SVD_TRUNCATED, ids=ids, s=s, ranks=ranks_dev, u_off=u_off,
+                        g_off=g_off, u_data=u_data, g_data=g_data)
     factors = DeviceFactors(m, p, ranks_dev, u_off, g_off, u_data[: total_rank * m],
                             g_data[: total_rank * p], total_rank)
     return factors, s
