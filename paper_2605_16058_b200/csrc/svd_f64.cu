@@ -1292,7 +1292,18 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
 constexpr int BWS = BW + 3;  // band row stride: offsets -1 .. BW+1
 
 __device__ __forceinline__ double& BEL(double* W, int i, int j) {
-  return W[i * BWS + (j - i + 1)];
+  return W[i * (BWS - 1) + j + 1];  // == W[i * BWS + (j - i + 1)]
+}
+
+// 1/sqrt(x) from the MUFU approximation and two Newton steps (full fp64
+// precision, no special-case paths: x is a positive normal here).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
 }
 
 // Rotation [c s; -s c] with c x + s y = r, -s x + c y = 0.  Division-free:
@@ -1311,7 +1322,7 @@ __device__ __forceinline__ void givens(double x, double y, double& c, double& s)
     y *= inv;
     r2 = fma(x, x, y * y);
   }
-  const double rinv = rsqrt(r2);
+  const double rinv = rsqrt_nr(r2);
   c = x * rinv;
   s = y * rinv;
 }
