@@ -92,6 +92,7 @@ struct SvdParams {
   int qr_stages;                // cp.async ring depth of the reduce kernel
   int64_t L, n, LP, NP, RP;
   int transposed, use_qr, bidiag, stats;
+  int wtwo;                     // reduce kernel: two-stage warp rings (else one stage)
   double tol;
   int max_sweeps, max_inner;
 };
@@ -391,7 +392,11 @@ __device__ double block_sum(double v, double* red) {
 __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, const int* cols, int j) {
   int64_t basis = 0;
   double* qj = Q + int64_t(cols ? cols[j] : j) * ld;
-  for (int attempt = 0; attempt < 4 + j; ++attempt) {
+  // The complement of the j previous columns has dimension len - j, so some
+  // canonical vector keeps a residual >= sqrt((len - j) / len): accept the
+  // first one above half of that bound.
+  const double cthr = 0.5 * sqrt(double(len - j) / double(len));
+  for (int64_t attempt = 0; attempt <= len; ++attempt) {
     for (int pass = 0; pass < 2; ++pass) {
       for (int i0 = 0; i0 < j; i0 += TPB / 32) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,10 +423,38 @@ __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, cons
     for (int64_t r = threadIdx.x; r < len; r += TPB) nrm2 += qj[r] * qj[r];
     nrm2 = block_sum(nrm2, fs.red);
     const double nrm = sqrt(nrm2);
-    if (nrm > 0.5) {
-      const double inv = 1.0 / nrm;
+    if (nrm > (attempt ? cthr : 0.5) || attempt == len) {
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
       for (int64_t r = threadIdx.x; r < len; r += TPB) qj[r] *= inv;
       __syncthreads();
+      if (attempt) {  // one more CGS2 pass after a canonical replacement
+        for (int i0 = 0; i0 < j; i0 += TPB / 32) {
+          const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+          const int i = i0 + warp;
+          double d = 0.0;
+          if (i < j) {
+            const double* qi = Q + int64_t(cols ? cols[i] : i) * ld;
+            for (int64_t r = lane; r < len; r += 32) d += qi[r] * qj[r];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (lane == 0) fs.dots[warp] = d;
+          __syncthreads();
+          const int cnt = min(TPB / 32, j - i0);
+          for (int64_t r = threadIdx.x; r < len; r += TPB) {
+            double x = qj[r];
+            for (int q = 0; q < cnt; ++q) x -= fs.dots[q] * Q[r + int64_t(cols ? cols[i0 + q] : i0 + q) * ld];
+            qj[r] = x;
+          }
+          __syncthreads();
+        }
+        double n2 = 0.0;
+        for (int64_t r = threadIdx.x; r < len; r += TPB) n2 += qj[r] * qj[r];
+        n2 = block_sum(n2, fs.red);
+        const double iv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;
+        for (int64_t r = threadIdx.x; r < len; r += TPB) qj[r] *= iv;
+        __syncthreads();
+      }
       return;
     }
     for (int64_t r = threadIdx.x; r < len; r += TPB) qj[r] = (r == basis) ? 1.0 : 0.0;
@@ -890,17 +923,20 @@ __device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan
 // Each warp owns a private region of WREG doubles (a 2-stage cp.async ring
 // plus scratch) after the panel in shared memory.
 // ---------------------------------------------------------------------
-constexpr int WREG = 1280;  // doubles per warp
+constexpr int WREG = 1280;  // doubles per warp (two-stage ring)
+constexpr int WREG1 = 640;  // single-stage variant for panels too tall for WREG
 constexpr int CS16 = 20;    // column stride of a staged 16-row chunk
 
 // C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
 // rows [kc, nrows) in 16-row chunks dealt round-robin to the warps.
+template <bool TWO>
 __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs,
                                   double* X, int64_t ld, int64_t nrows, int64_t NP, int64_t kc,
                                   int64_t c0) {
+  constexpr int WR = TWO ? WREG : WREG1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  double* wr = wbase + warp * WREG;  // [2][32 * CS16]
+  double* wr = wbase + warp * WR;  // [TWO ? 2 : 1][32 * CS16]
   const int64_t nck = (nrows - kc) / 16;
   auto stage = [&](int64_t ck, int b) {
     const int64_t r0 = kc + ck * 16;
@@ -924,14 +960,15 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   if (ck < nck) stage(ck, 0);
   for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
     const int64_t nx = ck + TPB / 32;
-    if (nx < nck) {
+    if (!TWO && it > 0) stage(ck, 0);
+    if (TWO && nx < nck) {
       stage(nx, (it + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
-    const double* cs = wr + (it & 1) * (GW * CS16);
+    const double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
     const int64_t r0 = kc + ck * 16;
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
@@ -962,7 +999,7 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   for (int e = threadIdx.x; e < BW * GW; e += TPB) {
     double sacc = 0.0;
 #pragma unroll
-    for (int w = 0; w < TPB / 32; ++w) sacc += wbase[w * WREG + e];
+    for (int w = 0; w < TPB / 32; ++w) sacc += wbase[w * WR + e];
     q.y[(e / GW) * GS + (e % GW)] = sacc;
   }
   __syncthreads();
@@ -979,14 +1016,15 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   if (ck < nck) stage(ck, 0);
   for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
     const int64_t nx = ck + TPB / 32;
-    if (nx < nck) {
+    if (!TWO && it > 0) stage(ck, 0);
+    if (TWO && nx < nck) {
       stage(nx, (it + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
-    double* cs = wr + (it & 1) * (GW * CS16);
+    double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
     const int64_t r0 = kc + ck * 16;
     double acc[2][4][2];
 #pragma unroll
@@ -1033,13 +1071,15 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
 // C -= Z V^T never leave the warp.  V[j][c] = pan2[c * prs + j].
 constexpr int CS8 = 12;  // column stride of a staged 8-row tile
 
+template <bool TWO>
 __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2, int64_t prs,
                                double* A, int64_t ld, int64_t nrows, int64_t NP, int64_t rc,
                                int64_t rmin, int64_t j0) {
+  constexpr int WR = TWO ? WREG : WREG1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  double* wr = wbase + warp * WREG;          // ring [2][32 * CS8]
-  double* zs = wr + 2 * GW * CS8;            // Y / Z scratch [16 * CS8]
+  double* wr = wbase + warp * WR;            // ring [TWO ? 2 : 1][32 * CS8]
+  double* zs = wr + (TWO ? 2 : 1) * GW * CS8;  // Y / Z scratch [16 * CS8]
   const double* Tm = q.t;
   const int64_t nblk = (NP - j0 + GW - 1) / GW;
   const int64_t ntile = (nrows - rc) / 8;
@@ -1062,14 +1102,15 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
     double y[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [ct][k4&1][e]
     stage(r0, 0, 0);
     for (int64_t b = 0; b < nblk; ++b) {
-      if (b + 1 < nblk) {
+      if (!TWO && b > 0) stage(r0, b, 0);
+      if (TWO && b + 1 < nblk) {
         stage(r0, b + 1, int((b + 1) & 1));
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      const double* cs = wr + (b & 1) * (GW * CS8);
+      const double* cs = wr + (TWO ? (b & 1) : 0) * (GW * CS8);
       const int64_t jb = j0 + b * GW;
 #pragma unroll
       for (int k4 = 0; k4 < GW / 4; ++k4) {
@@ -1108,14 +1149,15 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
     // ---- C -= Z V^T, block by block
     stage(r0, 0, 0);
     for (int64_t b = 0; b < nblk; ++b) {
-      if (b + 1 < nblk) {
+      if (!TWO && b > 0) stage(r0, b, 0);
+      if (TWO && b + 1 < nblk) {
         stage(r0, b + 1, int((b + 1) & 1));
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      double* cs = wr + (b & 1) * (GW * CS8);
+      double* cs = wr + (TWO ? (b & 1) : 0) * (GW * CS8);
       const int64_t jb = j0 + b * GW;
       double acc[4][2];
 #pragma unroll
@@ -1213,7 +1255,8 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
           panel_gram(q, pan, prs, kc, LP);
           long long _a = clock64();
           for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
-            trailing_update_w(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
+            P.wtwo ? trailing_update_w<true>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0)
+                   : trailing_update_w<false>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
           tr += clock64() - _a;
         }
         __syncthreads();
@@ -1242,7 +1285,8 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       {
         long long _a = clock64();
         for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
-          trailing_update_w(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
+          P.wtwo ? trailing_update_w<true>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0)
+                 : trailing_update_w<false>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
         tr += clock64() - _a;
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
@@ -1269,7 +1313,8 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       }
       {
         long long _a = clock64();
-        right_update_w(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        if (P.wtwo) right_update_w<true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        else right_update_w<false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         ru += clock64() - _a;
       }
       __syncthreads();
@@ -1769,8 +1814,88 @@ __device__ __forceinline__ int64_t kout_of(const SvdParams& P, int64_t slice) {
 // Right singular vectors of the bidiagonal (d, e) for sigma_j, j < k, by
 // inverse iteration on T_GK - sigma_j I (tridiagonal LU with partial
 // pivoting, LAPACK dgttrf/dgttrs), 3 solves from a fixed start vector.  The
-// even entries of the T_GK eigenvector are v (B v = sigma u).  One thread per
-// (slice, j); per-thread scratch of 5 x 2n doubles.
+// even entries of the T_GK eigenvector are v (B v = sigma u).
+// Close singular values (gap <= 1e-6 ||T||) form clusters that one thread
+// processes in order, as LAPACK dstein does: equal shifts are separated by
+// 10 eps ||T|| and every iterate is orthogonalised (MGS) against the cluster's
+// earlier eigenvectors z = [v; B v / sigma] (rebuilt from the stored v), so a
+// degenerate pair yields two orthogonal vectors of its eigenspace instead of
+// the same one twice.  Clusters are cut into chunks of II_CMAX vectors.
+// One thread per (slice, cluster head); per-thread scratch of 6 x 2n doubles.
+constexpr int II_CMAX = 32;
+
+__device__ void ii_factor(const double* bd, const double* be, int64_t N2, double lam, double pert,
+                          double* dd, double* du, double* du2, double* dl, double* z) {
+  for (int64_t i = 0; i < N2; ++i) {
+    dd[i] = -lam;
+    du[i] = (i + 1 < N2) ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0;
+    du2[i] = 0.0;
+  }
+  for (int64_t i = 0; i + 1 < N2; ++i) {
+    // original sub-diagonal (T is symmetric); du[i] may already hold fill
+    const double sub = (i & 1) ? be[i >> 1] : bd[i >> 1];
+    if (fabs(dd[i]) >= fabs(sub)) {
+      if (dd[i] == 0.0) dd[i] = pert;
+      const double fact = sub / dd[i];
+      dl[i] = fact;
+      dd[i + 1] -= fact * du[i];
+      z[i] = 0.0;
+    } else {
+      const double fact = dd[i] / sub;
+      dd[i] = sub;
+      dl[i] = fact;
+      const double temp = du[i];
+      du[i] = dd[i + 1];
+      dd[i + 1] = temp - fact * dd[i + 1];
+      if (i + 2 < N2) {
+        du2[i] = du[i + 1];
+        du[i + 1] = -fact * du[i + 1];
+      }
+      z[i] = 1.0;
+    }
+  }
+  if (dd[N2 - 1] == 0.0) dd[N2 - 1] = pert;
+}
+
+__device__ void ii_solve(int64_t N2, const double* dd, const double* du, const double* du2,
+                         const double* dl, const double* z, double* x) {
+  for (int64_t i = 0; i + 1 < N2; ++i) {  // apply L and the row interchanges
+    if (z[i] != 0.0) {
+      const double t = x[i];
+      x[i] = x[i + 1];
+      x[i + 1] = t - dl[i] * x[i + 1];
+    } else {
+      x[i + 1] -= dl[i] * x[i];
+    }
+  }
+  // U has diagonal dd, super du, second super du2
+  x[N2 - 1] /= dd[N2 - 1];
+  if (N2 > 1) x[N2 - 2] = (x[N2 - 2] - du[N2 - 2] * x[N2 - 1]) / dd[N2 - 2];
+  for (int64_t i = N2 - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
+}
+
+// x -= (x.z / z.z) z for the T_GK eigenvector z of a previous cluster member
+// (v = stored right vector, sig its shift; u = B v / sig, 0 when sig == 0).
+__device__ void ii_orth(const double* bd, const double* be, int64_t n, const double* v, double sig,
+                        double* x) {
+  const double rs = sig > 0.0 ? 1.0 / sig : 0.0;
+  double dot = 0.0, nz = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double zv = v[i];
+    const double zu = (bd[i] * v[i] + (i + 1 < n ? be[i] * v[i + 1] : 0.0)) * rs;
+    dot += x[2 * i] * zv + x[2 * i + 1] * zu;
+    nz += zv * zv + zu * zu;
+  }
+  if (nz <= 0.0) return;
+  const double c = dot / nz;
+  for (int64_t i = 0; i < n; ++i) {
+    const double zv = v[i];
+    const double zu = (bd[i] * v[i] + (i + 1 < n ? be[i] * v[i + 1] : 0.0)) * rs;
+    x[2 * i] -= c * zv;
+    x[2 * i + 1] -= c * zu;
+  }
+}
+
 __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   const int64_t n = P.n, NP = P.NP, RP = P.RP, N2 = 2 * P.n;
   const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
@@ -1781,78 +1906,51 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   double* du2 = du + 2 * NP;
   double* dl = du2 + 2 * NP;  // multipliers
   double* z = dl + 2 * NP;    // 1.0 where rows i, i+1 were interchanged
+  double* x = P.iiscr + nthreads * 5 * 2 * NP + gtid * 2 * NP;  // the iterate
   for (int64_t g = gtid; g < total_work; g += nthreads) {
     const int64_t it = g / n, j = g % n;
     const int64_t si = state_index(P, it);
     if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
-    if (j >= kout_of(P, slice)) continue;
+    const int64_t kout = kout_of(P, slice);
+    if (j >= kout) continue;
     const double* bd = P.debuf + si * 2 * NP;
     const double* be = bd + NP;
-    const double lam = P.s[j + slice * n];
+    const double* sv = P.s + slice * n;
     double tnorm = 0.0;
     for (int64_t k = 0; k < n; ++k) tnorm = fmax(tnorm, fabs(bd[k]) + (k + 1 < n ? fabs(be[k]) : 0.0));
     const double pert = fmax(tnorm * DBL_EPSILON, DBL_MIN);
-    // factor T - lam I (diagonal -lam, off-diagonals a_k = d0, e0, d1, ...)
-    for (int64_t i = 0; i < N2; ++i) {
-      dd[i] = -lam;
-      du[i] = (i + 1 < N2) ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0;
-      du2[i] = 0.0;
-    }
-    for (int64_t i = 0; i + 1 < N2; ++i) {
-      // original sub-diagonal (T is symmetric); du[i] may already hold fill
-      const double sub = (i & 1) ? be[i >> 1] : bd[i >> 1];
-      if (fabs(dd[i]) >= fabs(sub)) {
-        if (dd[i] == 0.0) dd[i] = pert;
-        const double fact = sub / dd[i];
-        dl[i] = fact;
-        dd[i + 1] -= fact * du[i];
-        z[i] = 0.0;
-      } else {
-        const double fact = dd[i] / sub;
-        dd[i] = sub;
-        dl[i] = fact;
-        const double temp = du[i];
-        du[i] = dd[i + 1];
-        dd[i + 1] = temp - fact * dd[i + 1];
-        if (i + 2 < N2) {
-          du2[i] = du[i + 1];
-          du[i + 1] = -fact * du[i + 1];
-        }
-        z[i] = 1.0;
+    const double ctol = 1e-6 * tnorm;
+    // cluster run containing j: [r0, ...); j heads a chunk iff (j - r0) % II_CMAX == 0
+    int64_t r0 = j;
+    while (r0 > 0 && sv[r0 - 1] - sv[r0] <= ctol) --r0;
+    if ((j - r0) % II_CMAX) continue;
+    int64_t jend = j + 1;
+    while (jend < kout && jend - j < II_CMAX && sv[jend - 1] - sv[jend] <= ctol) ++jend;
+    double lprev = 0.0;
+    for (int64_t jj = j; jj < jend; ++jj) {
+      double lam = sv[jj];
+      if (jj > j && lam > lprev - 10.0 * pert) lam = lprev - 10.0 * pert;  // separate equal shifts
+      lprev = lam;
+      ii_factor(bd, be, N2, lam, pert, dd, du, du2, dl, z);
+      for (int64_t i = 0; i < N2; ++i)
+        x[i] = 1.0 + 0.25 * double(((i + 1) * 7919 + (jj + 1) * 104729) % 97) / 97.0;
+      for (int iter = 0; iter < 3; ++iter) {
+        for (int64_t q = j; q < jj; ++q) ii_orth(bd, be, n, P.vsel + si * RP * NP + q * RP, sv[q], x);
+        ii_solve(N2, dd, du, du2, dl, z, x);
+        double nrm = 0.0;
+        for (int64_t i = 0; i < N2; ++i) nrm = fmax(nrm, fabs(x[i]));
+        const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+        for (int64_t i = 0; i < N2; ++i) x[i] *= inv;
       }
+      for (int64_t q = j; q < jj; ++q) ii_orth(bd, be, n, P.vsel + si * RP * NP + q * RP, sv[q], x);
+      // v = even entries, unit 2-norm
+      double nv = 0.0;
+      for (int64_t i = 0; i < n; ++i) nv += x[2 * i] * x[2 * i];
+      const double inv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;
+      double* vout = P.vsel + si * RP * NP + jj * RP;
+      for (int64_t i = 0; i < RP; ++i) vout[i] = (i < n) ? x[2 * i] * inv : 0.0;
     }
-    if (dd[N2 - 1] == 0.0) dd[N2 - 1] = pert;
-    double* vout = P.vsel + si * RP * NP + j * RP;
-    double* x = P.iiscr + nthreads * 5 * 2 * NP + gtid * 2 * NP;  // the iterate
-    for (int64_t i = 0; i < N2; ++i)
-      x[i] = 1.0 + 0.25 * double(((i + 1) * 7919 + (j + 1) * 104729) % 97) / 97.0;
-    for (int iter = 0; iter < 3; ++iter) {
-      // forward: apply L and the row interchanges
-      for (int64_t i = 0; i + 1 < N2; ++i) {
-        if (z[i] != 0.0) {
-          const double t = x[i];
-          x[i] = x[i + 1];
-          x[i + 1] = t - dl[i] * x[i + 1];
-        } else {
-          x[i + 1] -= dl[i] * x[i];
-        }
-      }
-      // backward: U has diagonal dd, super du, second super du2
-      x[N2 - 1] /= dd[N2 - 1];
-      if (N2 > 1) x[N2 - 2] = (x[N2 - 2] - du[N2 - 2] * x[N2 - 1]) / dd[N2 - 2];
-      for (int64_t i = N2 - 3; i >= 0; --i)
-        x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
-      double nrm = 0.0;
-      for (int64_t i = 0; i < N2; ++i) nrm = fmax(nrm, fabs(x[i]));
-      const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
-      for (int64_t i = 0; i < N2; ++i) x[i] *= inv;
-    }
-    // v = even entries, unit 2-norm
-    double nv = 0.0;
-    for (int64_t i = 0; i < n; ++i) nv += x[2 * i] * x[2 * i];
-    const double inv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;
-    for (int64_t i = 0; i < RP; ++i) vout[i] = (i < n) ? x[2 * i] * inv : 0.0;
   }
 }
 
@@ -1883,8 +1981,9 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
     for (int64_t j = 0; j < k; ++j) {
       double* vj = Vb + j * RP;
       int64_t basis = 0;
-      for (int attempt = 0; attempt < 4 + j; ++attempt) {
-        for (int pass = 0; pass < 2; ++pass) {
+      const double cthr = 0.5 * sqrt(double(n - j) / double(n));  // see cgs2_fix
+      for (int64_t attempt = 0; attempt <= n; ++attempt) {
+        for (int pass = 0; pass < (attempt ? 3 : 2); ++pass) {
           for (int64_t i = 0; i < j; ++i) {
             const double* vi = Vb + i * RP;
             double d = 0.0;
@@ -1900,8 +1999,8 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
         nr = sqrt(nr);
-        if (nr > 0.5) {
-          const double inv = 1.0 / nr;
+        if (nr > (attempt ? cthr : 0.5) || attempt == n) {
+          const double inv = nr > 0.0 ? 1.0 / nr : 0.0;
           for (int64_t q = lane; q < n; q += 32) vj[q] *= inv;
           __syncwarp();
           break;
@@ -2201,7 +2300,7 @@ __global__ void reset_status_kernel(int32_t* status, unsigned long long* counter
 struct Plan {
   int64_t L, n, LP, NP, RP;
   int job;                  // effective job after the fallback mapping
-  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s;
+  bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, wtwo;
   bool logs;                // right-side transformation logs (vector machinery buffers)
   bool run_front;           // reduce / bulge / bisect
   bool run_vec;             // inverse iteration / back-transform / output
@@ -2246,7 +2345,11 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.qr_stages = 2;
     size_t extra = size_t(g.qr_stages) * ring;
     const size_t wreg = size_t(TPB / 32) * WREG * sizeof(double);
-    if (wreg > extra) extra = wreg;
+    const size_t wreg1 = size_t(TPB / 32) * WREG1 * sizeof(double);
+    // two-stage warp rings when they fit next to the panel, else one stage
+    g.wtwo = fixed + (wreg > extra ? wreg : extra) <= size_t(227 * 1024);
+    const size_t w = g.wtwo ? wreg : wreg1;
+    if (w > extra) extra = w;
     g.rsmem = fixed + extra;
     if (g.rsmem > size_t(227 * 1024)) g.bidiag = false;  // panel does not fit: Jacobi path
   }
@@ -2436,6 +2539,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.transposed = pl.transposed;
   P.use_qr = pl.use_qr;
   P.bidiag = pl.bidiag;
+  P.wtwo = pl.wtwo;
   P.by_slice = pl.by_slice;
   P.stats = g_stats_on;
   // Jacobi convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).

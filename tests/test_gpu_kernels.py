@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [(5, 3, 4), (3, 5, 2, 3), (7, 7, 6), (1, 4, 3), (4, 1, 2), (33, 17, 5), (17, 33, 4),
           (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3),
-          (300, 257, 2), (257, 300, 2), (361, 720, 1)]
+          (300, 257, 2), (257, 300, 2), (361, 720, 1), (1024, 1024, 2), (900, 1100, 1)]
 
 
 # ------------------------------------------------------------------ TTM (K1)
@@ -122,6 +122,49 @@ def test_truncated_match_leading_triplets_bitwise():
             assert np.array_equal(f.u_block(i), full.u.frontal_slice(i)[:, :k])
             g = full.s[:k, i, None] * full.v.frontal_slice(i)[:, :k].T
             assert np.array_equal(f.g_block(i), g)
+
+
+def _degenerate_slices():
+    """Slices whose singular values repeat exactly: blockdiag(B, B) (the two
+    copies decouple in the bidiagonal), U diag(pairs) V^T, and rank-deficient
+    traveling-Fourier-mode slices as in config c3 (cos/sin pairs)."""
+    rng = np.random.default_rng(21)
+    out = []
+    for m, p in [(80, 60), (60, 80), (128, 128)]:
+        b = rng.standard_normal((m // 2, p // 2))
+        a = np.zeros((m, p))
+        a[: m // 2, : p // 2] = b
+        a[m // 2:, p // 2:] = b
+        out.append(a)
+        r = min(m, p)
+        sig = np.repeat(np.linspace(3.0, 0.5, (r + 1) // 2), 2)[:r]
+        u = np.linalg.qr(rng.standard_normal((m, r)))[0]
+        v = np.linalg.qr(rng.standard_normal((p, r)))[0]
+        out.append((u * sig) @ v.T)
+    from paper_2605_16058_b200.configs import config3
+    x, mm = config3(nx=128, ny=128, nt=16, modes=24, kmax=8)
+    xh = oracle.ttm(x, 2, mm)
+    out.extend(xh[:, :, i] for i in range(4))
+    return out
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_degenerate_spectrum_vectors(case):
+    a = _degenerate_slices()[case]
+    m, p = a.shape
+    r = min(m, p)
+    t = sb.DenseTensor(np.asfortranarray(a[:, :, None]))
+    full = sb.svd_all_slices(t)
+    u, v, s = full.u.frontal_slice(0), full.v.frontal_slice(0), full.s[:, 0]
+    assert np.linalg.norm(u.T @ u - np.eye(r)) <= 1e-10 * math.sqrt(r)
+    assert np.linalg.norm(v.T @ v - np.eye(r)) <= 1e-10 * math.sqrt(r)
+    assert np.linalg.norm(full.reconstruct_slice(0) - a) <= 1e-12 * np.linalg.norm(a)
+    ref = np.linalg.svd(a, compute_uv=False)
+    for k in (1, 2, 3, 5, 8, 13, r // 2 + 1):
+        f = sb.svd_truncated_slices(t, np.array([k]))
+        err2 = np.sum((a - f.u_block(0) @ f.g_block(0)) ** 2)
+        tail = np.sum(ref[k:] ** 2)
+        assert abs(err2 - tail) <= 1e-9 * np.sum(ref ** 2), (k, err2, tail)
 
 
 def test_graded_spectrum_values():
