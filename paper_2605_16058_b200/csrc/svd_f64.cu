@@ -81,10 +81,9 @@ struct SvdParams {
   double* debuf;                // per-slice bidiagonal d, e (2 x NP)
   // bidiagonal vector path (vector jobs): logs of the right-side transforms
   double* rvlog;                // per slice, per LQ panel: V (16 x NP) then T (16 x 16)
-  double* rotcs;                // per slice: rotcap (c, s) of the bulge column rotations
-  int32_t* rotcol;              // per slice: rotcap column indices (second column)
-  int64_t* rotcnt;              // per slice: rotations logged
-  int64_t rotcap;
+  double* hhlog;                // per slice: hhcap doubles, right reflectors of the bulge chase
+  int64_t hhcap;
+  double* hbbuf;                // bulge-chase windows in global memory (large n)
   double* vsel;                 // per slice: right singular vectors (RP x NP)
   double* iiscr;                // inverse-iteration scratch
   int btw;                      // back-transform vectors per pass
@@ -1334,14 +1333,44 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
   }
 }
 
-constexpr int BWS = BW + 3;  // band row stride: offsets -1 .. BW+1
+// ----------------------------------------------------------------------
+// Band (upper bandwidth BW) -> upper bidiagonal by Householder bulge
+// chasing.  Sweep i (for row i) runs tasks k = 0, 1, ...; task (i, k) has
+//   c0 = i + k*BW + 1,  c1 = min(c0 + BW - 1, n - 1),  L = c1 - c0 + 1:
+//   right: reflector H on columns [c0, c1] that annihilates row rho's
+//          entries (c0, c1] (rho = i for k = 0, else c0 - BW), applied to
+//          rows [rho, c1]  (creates fill below the diagonal);
+//   left:  reflector G on rows [c0, c1] that annihilates column c0 below
+//          the diagonal, applied to columns [c0, min(c0 + 2 BW - 1, n - 1)]
+//          (creates the bulge above the band that task k + 1 removes).
+// Every task stays inside rows [c0 - BW, c0 + BW - 1] x columns
+// [c0, c0 + 2 BW - 1], so tasks whose c0 differ by >= 2 BW are independent.
+// Sweep i starts at time step 3 i: tasks of one step have c0 differing by
+// >= 3 BW - 1, and every conflicting pair runs in the sequential
+// (sweep-major) order, so the result equals the sequential algorithm's bit
+// for bit.  One warp per task, a CTA barrier per time step, ~3n steps.
+// The working matrix is kept as a diagonal window per row (offsets
+// -(BW-1) .. 2 BW - 1, stride HB): in shared memory when it fits, else in a
+// per-CTA global (L2-resident) buffer.  Vector jobs log each right
+// reflector as 16 doubles (tau, v_1 .. v_{BW-1}).
+// ----------------------------------------------------------------------
+constexpr int HB = 3 * BW;    // window row stride (odd HB - 1: conflict-free columns)
+constexpr int HOFF = BW - 1;  // window index of the diagonal
+constexpr int HLOG = BW;      // doubles per logged reflector
 
-__device__ __forceinline__ double& BEL(double* W, int i, int j) {
-  return W[i * (BWS - 1) + j + 1];  // == W[i * BWS + (j - i + 1)]
+__host__ __device__ __forceinline__ int64_t hb_tasks(int64_t n, int64_t i) {  // tasks of sweep i
+  return (i >= 0 && i <= n - 3) ? (n - 3 - i) / BW + 1 : 0;
 }
+__host__ __device__ __forceinline__ int64_t hb_kmax(int64_t n) { return n >= 3 ? hb_tasks(n, 0) : 1; }
+__host__ __device__ __forceinline__ int64_t hb_steps(int64_t n) {
+  return n >= 3 ? 3 * (n - 3) + hb_tasks(n, n - 3) : 0;
+}
+__host__ __device__ __forceinline__ int hb_warps(int64_t n) {  // concurrent sweeps <= ceil(kmax / 3)
+  const int64_t w = (hb_kmax(n) + 2) / 3;
+  return int(w < 1 ? 1 : (w > 16 ? 16 : w));
+}
+__device__ __forceinline__ double& HEL(double* W, int r, int c) { return W[r * (HB - 1) + c + HOFF]; }
 
-// 1/sqrt(x) from the MUFU approximation and two Newton steps (full fp64
-// precision, no special-case paths: x is a positive normal here).
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -1351,96 +1380,116 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-// Rotation [c s; -s c] with c x + s y = r, -s x + c y = 0.  Division-free:
-// one rsqrt of x^2 + y^2 (scaled only when that would over/underflow).
-__device__ __forceinline__ void givens(double x, double y, double& c, double& s) {
-  if (y == 0.0) {
-    c = 1.0;
-    s = 0.0;
-    return;
-  }
-  double r2 = fma(x, x, y * y);
-  if (!(r2 > 1e-290 && r2 < 1e290)) {
-    const double ax = fabs(x), ay = fabs(y);
-    const double inv = 1.0 / (ax > ay ? ax : ay);
-    x *= inv;
-    y *= inv;
-    r2 = fma(x, x, y * y);
-  }
-  const double rinv = rsqrt_nr(r2);
-  c = x * rinv;
-  s = y * rinv;
+__device__ __forceinline__ double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
 }
 
-// Chase schedule.  Chases are ordered by row i (ascending) then j
-// (descending, j = min(i+BW, n-1) .. i+2); one empty slot follows every row
-// so the next row's first chase (which starts to the right of the previous
-// chase) begins 2*lag steps later.  Slot e returns its (i, j) or false for
-// an empty slot.
-__device__ __forceinline__ bool chase_slot(int64_t e, int n, int& i, int& j) {
-  const int nfull = n - BW > 0 ? n - BW : 0;  // rows with i + BW <= n - 1
-  const int64_t ef = int64_t(nfull) * BW;
-  if (e < ef) {
-    i = int(e / BW);
-    const int q = int(e % BW);
-    if (q == BW - 1) return false;
-    j = i + BW - q;
-    return true;
+// Warp-wide dlarfg: lanes 0..L-1 hold x (0 beyond); on return x holds v
+// (lane 0: 1, 0 beyond L), beta the new leading entry; returns tau (0: H = I).
+// sqrt and the two divisions go through MUFU rsqrt/rcp + Newton steps:
+// tau = 1 + |alpha| / norm, 1 / (alpha - beta) = sign(alpha) / (|alpha| + norm).
+__device__ __forceinline__ double warp_house(double& x, int lane, double& beta) {
+  double s2 = lane ? x * x : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  const double alpha = __shfl_sync(0xffffffffu, x, 0);
+  beta = alpha;
+  if (s2 == 0.0) return 0.0;
+  const double nrm2 = fma(alpha, alpha, s2);
+  double rn, nrm;
+  if (nrm2 > 1e-280 && nrm2 < 1e280) {
+    rn = rsqrt_nr(nrm2);
+    nrm = nrm2 * rn;
+  } else {
+    nrm = sqrt(nrm2);
+    rn = 1.0 / nrm;
   }
-  int64_t r = e - ef;
-  for (int ii = nfull; ii + 2 <= n - 1; ++ii) {
-    const int cnt = n - 2 - ii;
-    if (r < cnt) {
-      i = ii;
-      j = n - 1 - int(r);
-      return true;
+  const double aa = fabs(alpha);
+  beta = -copysign(nrm, alpha);
+  const double tau = fma(aa, rn, 1.0);
+  const double scal = copysign(rcp_nr(aa + nrm), alpha);
+  x = lane ? x * scal : 1.0;
+  return tau;
+}
+
+// One task of the chase (see above).  The window has BW zero rows of
+// padding below row n - 1, so the reflector loops run over all BW entries
+// with v_l = 0 beyond L and constant offsets from one base pointer.
+__device__ __forceinline__ void hb_task(double* W, int n, int i, int k, int lane, double* vs,
+                                        double* lg) {
+  const int c0 = i + k * BW + 1;
+  const int c1 = min(c0 + BW - 1, n - 1);
+  const int L = c1 - c0 + 1;
+  const int rho = k ? c0 - BW : i;
+  double beta;
+  // ---- right reflector from row rho, applied to rows (rho, c1]
+  double x = lane < L ? HEL(W, rho, c0 + lane) : 0.0;
+  const double tau = warp_house(x, lane, beta);
+  if (lg && lane < BW) lg[lane] = lane ? x : tau;
+  if (tau != 0.0) {
+    if (lane < L) HEL(W, rho, c0 + lane) = lane ? 0.0 : beta;
+    vs[lane] = x;
+    __syncwarp();
+    const int r = rho + 1 + lane;
+    if (r <= c1) {
+      double* row = &HEL(W, r, c0);  // row[l] = A(r, c0 + l)
+      double a[BW];
+#pragma unroll
+      for (int l = 0; l < BW; ++l) a[l] = row[l];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < BW; l += 2) {
+        w0 = fma(a[l], vs[l], w0);
+        w1 = fma(a[l + 1], vs[l + 1], w1);
+      }
+      const double w = (w0 + w1) * tau;
+#pragma unroll
+      for (int l = 0; l < BW; ++l) row[l] = fma(-w, vs[l], a[l]);
     }
-    r -= cnt;
-    if (r == 0) return false;  // the empty slot after row ii
-    r -= 1;
+    __syncwarp();
   }
-  return false;
+  // ---- left reflector from column c0, applied to columns (c0, c0 + 2 BW - 1]
+  double y = lane < L ? HEL(W, c0 + lane, c0) : 0.0;
+  const double tl = warp_house(y, lane, beta);
+  if (tl != 0.0) {
+    if (lane < L) HEL(W, c0 + lane, c0) = lane ? 0.0 : beta;
+    vs[lane] = y;
+    __syncwarp();
+    const int c = c0 + 1 + lane;
+    if (c < n) {
+      double* col = &HEL(W, c0, c);  // col[l * (HB - 1)] = A(c0 + l, c)
+      double a[BW];
+#pragma unroll
+      for (int l = 0; l < BW; ++l) a[l] = col[l * (HB - 1)];
+      double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < BW; l += 2) {
+        w0 = fma(vs[l], a[l], w0);
+        w1 = fma(vs[l + 1], a[l + 1], w1);
+      }
+      const double w = (w0 + w1) * tl;
+#pragma unroll
+      for (int l = 0; l < BW; ++l) col[l * (HB - 1)] = fma(-w, vs[l], a[l]);
+    }
+    __syncwarp();
+  }
 }
 
-__host__ __device__ __forceinline__ int64_t chase_slots(int64_t n) {
-  const int64_t nfull = n - BW > 0 ? n - BW : 0;
-  int64_t e = nfull * BW;
-  for (int64_t ii = nfull; ii + 2 <= n - 1; ++ii) e += (n - 2 - ii) + 1;
-  return e;
-}
-
-__host__ __device__ __forceinline__ int chase_maxlen(int64_t n) {
-  return n >= 3 ? int(2 + 2 * ((n - 3) / BW)) : 1;
-}
-
-__host__ __device__ __forceinline__ int chase_logmax(int64_t n) {
-  return n >= 3 ? int(2 + (n - 3) / BW) : 1;
-}
-
-constexpr int BULGE_WARPS = 16;
-
-// Band (bandwidth 16) -> upper bidiagonal by Givens bulge chasing, one CTA
-// per slice with the band (+ one fill diagonal on each side) in shared
-// memory.  Row i's extra entries are annihilated outermost first by a column
-// rotation whose fill below the diagonal is chased down by alternating row /
-// column rotations in steps of 16.  Chases run as a wavefront: slot e starts
-// at time lag*e on warp e % 16, one rotation per warp per time step, a CTA
-// barrier between steps.  Footprints of chases >= 2 steps apart on the same
-// row (and >= 6 steps apart across a row boundary) are disjoint, so every
-// entry sees the same sequence of updates as in the sequential algorithm and
-// the chases commute.  Vector jobs log each chase's column rotations.
-__global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P) {
+template <bool GMEM>
+__global__ void __launch_bounds__(512) svd_bulge_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* W = reinterpret_cast<double*>(smem_raw);
+  __shared__ double vsh[16][32];
   __shared__ int64_t cur;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = P.n, NP = P.NP;
-  const int nn = int(n);
-  const int64_t nslot = chase_slots(n);
-  const int maxlen = chase_maxlen(n);
-  const int lmax = chase_logmax(n);
-  int lag = (maxlen + 1 + BULGE_WARPS - 1) / BULGE_WARPS;
-  if (lag < 3) lag = 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int n = int(P.n);
+  const int64_t NP = P.NP;
+  double* W = GMEM ? P.hbbuf + int64_t(blockIdx.x) * (n + BW) * HB : reinterpret_cast<double*>(smem_raw);
+  const int64_t kmax = hb_kmax(n), T = hb_steps(n);
   for (;;) {
     if (threadIdx.x == 0) cur = int64_t(atomicAdd(&P.counter[2], 1ull));
     __syncthreads();
@@ -1451,107 +1500,27 @@ __global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P
     if (P.flags[si]) continue;
     long long t0 = clock64();
     const double* band = P.bandbuf + si * (BW + 1) * NP;
-    for (int64_t e = threadIdx.x; e < n * BWS; e += blockDim.x) {
-      const int64_t i = e / BWS, k = e % BWS;
-      const int64_t d = k - 1;
-      W[e] = (d >= 0 && d <= BW && i + d < n) ? band[d * NP + i] : 0.0;
+    for (int64_t e = threadIdx.x; e < int64_t(n + BW) * HB; e += blockDim.x) {
+      const int r = int(e / HB), d = int(e % HB) - HOFF;
+      W[e] = (d >= 0 && d <= BW && r + d < n) ? band[d * NP + r] : 0.0;
     }
     __syncthreads();
-    double* lcs = P.rotcs ? P.rotcs + si * P.rotcap * 2 : nullptr;
-    int32_t* lcol = P.rotcol ? P.rotcol + si * P.rotcap : nullptr;
-    int32_t* lcnt = P.rotcs ? reinterpret_cast<int32_t*>(P.rotcnt) + si * nslot : nullptr;
-    // per-warp chase state
-    int64_t e = warp;
-    int ci = 0, cj = 0, rr = 0, phase = -1, nlog = 0;  // phase -1: not started
-    const int64_t tend = int64_t(lag) * (nslot + BULGE_WARPS) + maxlen + 2;
-    for (int64_t t = 0; t < tend; ++t) {
-      if (e < nslot && t >= lag * e) {
-        if (phase < 0) {
-          if (!chase_slot(e, nn, ci, cj)) {  // empty slot: nothing to do
-            if (lcnt && lane == 0) lcnt[e] = 0;
-            e += BULGE_WARPS;
-            goto barrier;
-          }
-          phase = 0;
-          nlog = 0;
-        }
-        {
-          double c, s;
-          bool done = false;
-          if (phase == 0) {  // column rotation (cj-1, cj) on rows ci .. cj
-            givens(BEL(W, ci, cj - 1), BEL(W, ci, cj), c, s);
-            __syncwarp();
-            if (s == 0.0) {
-              done = true;
-            } else {
-              const int r = ci + lane;
-              if (r <= cj) {
-                const double a = BEL(W, r, cj - 1), b = BEL(W, r, cj);
-                BEL(W, r, cj - 1) = c * a + s * b;
-                BEL(W, r, cj) = lane ? -s * a + c * b : 0.0;
-              }
-              if (lcs && lane == 0) {
-                const int64_t q = e * lmax + nlog;
-                lcs[2 * q] = c;
-                lcs[2 * q + 1] = s;
-                lcol[q] = cj;
-              }
-              ++nlog;
-              rr = cj;
-              phase = 1;
-            }
-          } else if (phase == 1) {  // row rotation (rr-1, rr) annihilating the fill at (rr, rr-1)
-            givens(BEL(W, rr - 1, rr - 1), BEL(W, rr, rr - 1), c, s);
-            __syncwarp();
-            if (s != 0.0) {
-              const int cend = (rr + BW < nn - 1) ? rr + BW : nn - 1;
-              const int col = rr - 1 + lane;
-              if (col <= cend) {
-                const double a = BEL(W, rr - 1, col), b = BEL(W, rr, col);
-                BEL(W, rr - 1, col) = c * a + s * b;
-                BEL(W, rr, col) = lane ? -s * a + c * b : 0.0;
-              }
-            }
-            if (rr + BW >= nn) done = true;
-            else phase = 2;
-          } else {  // column rotation (cc-1, cc) annihilating the fill at (rr-1, cc)
-            const int cc = rr + BW;
-            givens(BEL(W, rr - 1, cc - 1), BEL(W, rr - 1, cc), c, s);
-            __syncwarp();
-            if (s == 0.0) {
-              done = true;
-            } else {
-              const int r2 = rr - 1 + lane;
-              if (r2 <= cc) {
-                const double a = BEL(W, r2, cc - 1), b = BEL(W, r2, cc);
-                BEL(W, r2, cc - 1) = c * a + s * b;
-                BEL(W, r2, cc) = lane ? -s * a + c * b : 0.0;
-              }
-              if (lcs && lane == 0) {
-                const int64_t q = e * lmax + nlog;
-                lcs[2 * q] = c;
-                lcs[2 * q + 1] = s;
-                lcol[q] = cc;
-              }
-              ++nlog;
-              rr = cc;
-              phase = 1;
-            }
-          }
-          if (done) {
-            if (lcnt && lane == 0) lcnt[e] = nlog;
-            e += BULGE_WARPS;
-            phase = -1;
-          }
-        }
+    double* lg = P.hhlog ? P.hhlog + si * P.hhcap : nullptr;
+    for (int64_t t = 0; t < T; ++t) {
+      // this warp's sweeps: i == warp (mod nw), 3 i <= t < 3 i + K_i
+      int64_t i = t / 3;
+      i -= ((i - warp) % nw + nw) % nw;
+      for (; i >= 0 && t - 3 * i < kmax; i -= nw) {
+        const int64_t k = t - 3 * i;
+        if (k < hb_tasks(n, i))
+          hb_task(W, n, int(i), int(k), lane, vsh[warp], lg ? lg + (i * kmax + k) * HLOG : nullptr);
       }
-    barrier:
       __syncthreads();
     }
     double* de = P.debuf + si * 2 * NP;
-    for (int64_t i = threadIdx.x; i < NP; i += blockDim.x) {
-      de[i] = i < n ? BEL(W, i, i) : 0.0;
-      de[NP + i] = i + 1 < n ? BEL(W, i, i + 1) : 0.0;
+    for (int64_t q = threadIdx.x; q < NP; q += blockDim.x) {
+      de[q] = q < n ? HEL(W, int(q), int(q)) : 0.0;
+      de[NP + q] = q + 1 < n ? HEL(W, int(q), int(q) + 1) : 0.0;
     }
     __syncthreads();
     long long t1 = clock64();
@@ -1566,17 +1535,9 @@ __global__ void __launch_bounds__(BULGE_WARPS * 32) svd_bulge_kernel(SvdParams P
 // T_GK - x I) - n.  One thread per (slice, sigma_j), sigma_j the j-th
 // largest; interval shrunk to 2u * max(sigma_j, 1e-3 * bound).
 // ----------------------------------------------------------------------
-// 1/q from the MUFU approximation plus two Newton steps (relative error
-// ~1e-15): a Sturm pivot computed this way is the exact pivot of T_GK with
-// off-diagonals perturbed by a few ulps, which is all the count needs.
-__device__ __forceinline__ double rcp_nr(double q) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  double e = fma(-q, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-q, r, 1.0);
-  return fma(r, e, r);
-}
+// Pivots use rcp_nr (relative error ~1e-15): a Sturm pivot computed this
+// way is the exact pivot of T_GK with off-diagonals perturbed by a few ulps,
+// which is all the count needs.
 
 __device__ __forceinline__ int count_below(const double* d, const double* e, int n, double x,
                                            double pivmin) {
@@ -2011,11 +1972,8 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
       }
     }
     // ---- (2) back-transformation, 32 vectors per pass
-    const int64_t nslot = chase_slots(n);
-    const int lmax = chase_logmax(n);
-    const int32_t* rcnt = reinterpret_cast<const int32_t*>(P.rotcnt) + si * nslot;
-    const double* rcs = P.rotcs + si * P.rotcap * 2;
-    const int32_t* rcol = P.rotcol + si * P.rotcap;
+    const int64_t kmax = hb_kmax(n);
+    const double* lg = P.hhlog + si * P.hhcap;
     const double* rv = P.rvlog + si * npan * (BW * NP + BW * BW);
     for (int64_t j0 = 0; j0 < k; j0 += P.btw) {
       const int64_t j = j0 + lane;
@@ -2025,40 +1983,26 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
         for (int64_t q = 0; q < n; ++q) mine[q] = Vb[j * RP + q];
       __syncwarp();
       if (act) {
-        // chases in reverse order, each chase's column rotations in reverse
-        // (a chase's rotations act on distinct column pairs, 16 apart, so
-        //  four at a time are loaded, rotated and stored without hazards)
-        for (int64_t e = nslot - 1; e >= 0; --e) {
-          int q = rcnt[e] - 1;
-          const int64_t tb = e * lmax;
-          for (; q >= 3; q -= 4) {
-            double c[4], s[4], a[4], b[4];
-            int col[4];
+        // bulge-chase right reflectors, last applied first: x <- H x
+        for (int64_t i = n - 3; i >= 0; --i) {
+          for (int64_t kk = hb_tasks(n, i) - 1; kk >= 0; --kk) {
+            const double* h = lg + (i * kmax + kk) * HLOG;
+            const double tau = h[0];
+            if (tau == 0.0) continue;
+            const int64_t c0 = i + kk * BW + 1;
+            const int L = int(n - c0 < BW ? n - c0 : BW);
+            double hv[BW];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int64_t t = tb + q - u;
-              c[u] = rcs[2 * t];
-              s[u] = rcs[2 * t + 1];
-              col[u] = rcol[t];
-            }
+            for (int l = 1; l < BW; ++l) hv[l] = h[l];
+            double w = mine[c0];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              a[u] = mine[col[u] - 1];
-              b[u] = mine[col[u]];
-            }
+            for (int l = 1; l < BW; ++l)
+              if (l < L) w = fma(hv[l], mine[c0 + l], w);
+            w *= tau;
+            mine[c0] -= w;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              mine[col[u] - 1] = c[u] * a[u] - s[u] * b[u];
-              mine[col[u]] = s[u] * a[u] + c[u] * b[u];
-            }
-          }
-          for (; q >= 0; --q) {
-            const int64_t t = tb + q;
-            const double c = rcs[2 * t], s = rcs[2 * t + 1];
-            const int col = rcol[t];
-            const double a = mine[col - 1], b = mine[col];
-            mine[col - 1] = c * a - s * b;
-            mine[col] = s * a + c * b;
+            for (int l = 1; l < BW; ++l)
+              if (l < L) mine[c0 + l] = fma(-w, hv[l], mine[c0 + l]);
           }
         }
         for (int64_t pk = npan - 2; pk >= 0; --pk) {
@@ -2308,7 +2252,9 @@ struct Plan {
   int ns;
   size_t jsmem, rsmem, bsmem;
   int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages;
-  int64_t rotcap, count;
+  int64_t hhcap, count;
+  bool hb_gmem;
+  int hb_threads;
   size_t vsmem, tsmem;
   size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
       off_vsel, off_ii, total;
@@ -2338,7 +2284,7 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.ns = 1;
   while (g.ns < g.n) g.ns <<= 1;
   g.jsmem = jacobi_smem_bytes(g.ns);
-  g.bidiag = g_tune_mode == 1 && g.LP <= QR_MAX_LP;
+  g.bidiag = g_tune_mode >= 1 && g.LP <= QR_MAX_LP;
   {
     const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
     const size_t ring = size_t(GW) * XS * sizeof(double);
@@ -2370,7 +2316,10 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   // (the state-keeping truncated job always receives the values pass's s,
   //  so its workspace has exactly the values-state layout)
   g.internal_s = g.wantv && !have_s && !g.by_slice;
-  g.bsmem = size_t(g.NP) * BWS * sizeof(double);
+  g.bsmem = size_t(g.n + BW) * HB * sizeof(double);
+  g.hb_threads = 32 * hb_warps(g.n);
+  g.hb_gmem = g_tune_mode == 2 || g.bsmem > size_t(220 * 1024);
+  if (g.hb_gmem) g.bsmem = 0;
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
   STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -2397,13 +2346,14 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     const int64_t work = count * g.n;
     g.ii_threads = int(work < int64_t(sms) * 128 ? work : int64_t(sms) * 128);
     g.ii_threads = int(round_up(g.ii_threads < 1 ? 1 : g.ii_threads, 128));  // whole blocks
-    g.rotcap = chase_slots(g.n) * chase_logmax(g.n);
+    g.hhcap = (g.n >= 3 ? (g.n - 2) : 1) * hb_kmax(g.n) * HLOG;
   }
   if (g.bidiag) {
     rc = occupancy((const void*)svd_reduce_kernel, TPB, g.rsmem, &per);
     if (rc) return rc;
     g.slots_r = clampc(int64_t(sms) * per);
-    rc = occupancy((const void*)svd_bulge_kernel, BULGE_WARPS * 32, g.bsmem, &per);
+    rc = occupancy(g.hb_gmem ? (const void*)svd_bulge_kernel<true> : (const void*)svd_bulge_kernel<false>,
+                   g.hb_threads, g.bsmem, &per);
     if (rc) return rc;
     g.slots_b = clampc(int64_t(sms) * per);
     int64_t bb = (count * g.n + 127) / 128;
@@ -2426,9 +2376,9 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.off_s = take(g.internal_s ? size_t(nslices) * g.n * sizeof(double) : 0);
   const size_t npan = size_t(g.NP / BW);
   g.off_rv = take(g.logs ? size_t(count) * npan * (BW * g.NP + BW * BW) * sizeof(double) : 0);
-  g.off_rcs = take(g.logs ? size_t(count) * g.rotcap * 2 * sizeof(double) : 0);
-  g.off_rcol = take(g.logs ? size_t(count) * g.rotcap * sizeof(int32_t) : 0);
-  g.off_rcnt = take(g.logs ? size_t(count) * chase_slots(g.n) * sizeof(int32_t) : 0);
+  g.off_rcs = take(g.logs ? size_t(count) * g.hhcap * sizeof(double) : 0);
+  g.off_rcol = take(g.hb_gmem ? size_t(g.slots_b) * (g.n + BW) * HB * sizeof(double) : 0);
+  g.off_rcnt = take(0);
   g.off_vsel = take(g.logs ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
   g.off_ii = take(g.logs ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
   g.total = off;
@@ -2541,6 +2491,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.bidiag = pl.bidiag;
   P.wtwo = pl.wtwo;
   P.by_slice = pl.by_slice;
+  P.hbbuf = reinterpret_cast<double*>(base + pl.off_rcol);
   P.stats = g_stats_on;
   // Jacobi convergence: every |cos(x_i, x_j)| <= L * eps (LAPACK dgesvj uses M*EPS).
   P.tol = double(pl.L > 32 ? pl.L : 32) * DBL_EPSILON;
@@ -2548,10 +2499,8 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.max_inner = g_tune_inner;
   if (pl.logs) {
     P.rvlog = reinterpret_cast<double*>(base + pl.off_rv);
-    P.rotcs = reinterpret_cast<double*>(base + pl.off_rcs);
-    P.rotcol = reinterpret_cast<int32_t*>(base + pl.off_rcol);
-    P.rotcnt = reinterpret_cast<int64_t*>(base + pl.off_rcnt);
-    P.rotcap = pl.rotcap;
+    P.hhlog = reinterpret_cast<double*>(base + pl.off_rcs);
+    P.hhcap = pl.hhcap;
     P.vsel = reinterpret_cast<double*>(base + pl.off_vsel);
     P.iiscr = reinterpret_cast<double*>(base + pl.off_ii);
     P.btw = pl.btw;
@@ -2559,7 +2508,8 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   if (pl.run_front) {
     svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
-    svd_bulge_kernel<<<pl.slots_b, BULGE_WARPS * 32, pl.bsmem, st>>>(P);
+    if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(P);
+    else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
     STARM_LAUNCH_CHECK();

@@ -1,0 +1,22 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list:
+per-kernel totals for the LAST step of run_step.py (launches after the
+midpoint), in ms."""
+import collections
+import csv
+import sys
+
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+hdr = rows[0]
+ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+ids = hdr.index("ID")
+data = [(int(r[ids]), r[ki], float(r[vi].replace(",", ""))) for r in rows[1:] if r[vi]]
+unit = rows[1][hdr.index("Metric Unit")] if len(rows) > 1 else ""
+scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(unit, 1e-6)
+half = data[len(data) // 2:] if len(sys.argv) < 3 else data
+tot = collections.OrderedDict()
+for _, k, v in half:
+    name = k.split("(")[0].split("::")[-1][:60]
+    tot[name] = tot.get(name, 0.0) + v * scale
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print(f"{v:9.3f} ms  {k}")
+print(f"{sum(tot.values()):9.3f} ms  total ({len(half)} launches)")
