@@ -1365,9 +1365,9 @@ __host__ __device__ __forceinline__ int64_t hb_kmax(int64_t n) { return n >= 3 ?
 __host__ __device__ __forceinline__ int64_t hb_steps(int64_t n) {
   return n >= 3 ? 3 * (n - 3) + hb_tasks(n, n - 3) : 0;
 }
-__host__ __device__ __forceinline__ int hb_warps(int64_t n) {  // concurrent sweeps <= ceil(kmax / 3)
+__host__ __device__ __forceinline__ int hb_warps(int64_t n, int cap) {  // ceil(kmax / 3) sweeps overlap
   const int64_t w = (hb_kmax(n) + 2) / 3;
-  return int(w < 1 ? 1 : (w > 16 ? 16 : w));
+  return int(w < 1 ? 1 : (w > cap ? cap : w));
 }
 __device__ __forceinline__ double& HEL(double* W, int r, int c) { return W[r * (HB - 1) + c + HOFF]; }
 
@@ -1420,17 +1420,19 @@ __device__ __forceinline__ double warp_house(double& x, int lane, double& beta) 
 // One task of the chase (see above).  The window has BW zero rows of
 // padding below row n - 1, so the reflector loops run over all BW entries
 // with v_l = 0 beyond L and constant offsets from one base pointer.
-__device__ __forceinline__ void hb_task(double* W, int n, int i, int k, int lane, double* vs,
-                                        double* lg) {
+// Inactive warps (act false) run the shuffles on zeros and touch nothing, so
+// every warp reaches each shuffle converged.
+__device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act, int lane,
+                                        double* vs, double* lg) {
   const int c0 = i + k * BW + 1;
   const int c1 = min(c0 + BW - 1, n - 1);
-  const int L = c1 - c0 + 1;
+  const int L = act ? c1 - c0 + 1 : 0;
   const int rho = k ? c0 - BW : i;
   double beta;
   // ---- right reflector from row rho, applied to rows (rho, c1]
   double x = lane < L ? HEL(W, rho, c0 + lane) : 0.0;
   const double tau = warp_house(x, lane, beta);
-  if (lg && lane < BW) lg[lane] = lane ? x : tau;
+  if (act && lg && lane < BW) lg[lane] = lane ? x : tau;
   if (tau != 0.0) {
     if (lane < L) HEL(W, rho, c0 + lane) = lane ? 0.0 : beta;
     vs[lane] = x;
@@ -1481,9 +1483,9 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, int lane
 }
 
 template <bool GMEM>
-__global__ void __launch_bounds__(512) svd_bulge_kernel(SvdParams P) {
+__global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double vsh[16][32];
+  __shared__ double vsh[32][32];
   __shared__ int64_t cur;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int n = int(P.n);
@@ -1506,14 +1508,27 @@ __global__ void __launch_bounds__(512) svd_bulge_kernel(SvdParams P) {
     }
     __syncthreads();
     double* lg = P.hhlog ? P.hhlog + si * P.hhcap : nullptr;
+    // this warp runs sweeps i == warp (mod nw); sweep i is active at steps
+    // [3 i, 3 i + K_i).  With 3 nw >= kmax a warp has at most one active
+    // sweep; otherwise (n > 96 BW) older sweeps are finished in extra passes.
+    int cur = -1, next = warp;
     for (int64_t t = 0; t < T; ++t) {
-      // this warp's sweeps: i == warp (mod nw), 3 i <= t < 3 i + K_i
-      int64_t i = t / 3;
-      i -= ((i - warp) % nw + nw) % nw;
-      for (; i >= 0 && t - 3 * i < kmax; i -= nw) {
-        const int64_t k = t - 3 * i;
-        if (k < hb_tasks(n, i))
-          hb_task(W, n, int(i), int(k), lane, vsh[warp], lg ? lg + (i * kmax + k) * HLOG : nullptr);
+      if (3 * int64_t(next) == t) {
+        cur = next;
+        next += nw;
+      }
+      if (!GMEM || 3 * nw >= kmax) {
+        const int k = int(t - 3 * int64_t(cur));
+        const bool act = cur >= 0 && k < hb_tasks(n, cur);
+        hb_task(W, n, act ? cur : 0, act ? k : 0, act, lane, vsh[warp],
+                lg ? lg + (int64_t(act ? cur : 0) * kmax + (act ? k : 0)) * HLOG : nullptr);
+      } else {
+        for (int i = cur; i >= 0 && t - 3 * int64_t(i) < kmax; i -= nw) {
+          const int k = int(t - 3 * int64_t(i));
+          const bool act = k < hb_tasks(n, i);
+          hb_task(W, n, act ? i : 0, act ? k : 0, act, lane, vsh[warp],
+                  lg ? lg + (int64_t(i) * kmax + k) * HLOG : nullptr);
+        }
       }
       __syncthreads();
     }
@@ -2317,8 +2332,8 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   //  so its workspace has exactly the values-state layout)
   g.internal_s = g.wantv && !have_s && !g.by_slice;
   g.bsmem = size_t(g.n + BW) * HB * sizeof(double);
-  g.hb_threads = 32 * hb_warps(g.n);
-  g.hb_gmem = g_tune_mode == 2 || g.bsmem > size_t(220 * 1024);
+  g.hb_gmem = g_tune_mode == 2 || g.bsmem > size_t(216 * 1024);
+  g.hb_threads = 32 * hb_warps(g.n, g.hb_gmem ? 32 : 16);
   if (g.hb_gmem) g.bsmem = 0;
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
