@@ -612,17 +612,21 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
 // 16 panel columns, so the BLAS2 column steps touch no shared memory; only
 // the 16 reductions per column and the pivot row go through it.
 template <int RPT>
-__device__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
-                                 int64_t nrows) {
+__device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
+                                              int64_t nrows) {
+  // Register-resident panel, column loop NOT unrolled: b[i][c] holds panel
+  // column j + c of this thread's rows, so every column runs the same code
+  // (column 0 is factored, then the window shifts left by one).  Keeps the
+  // instruction footprint of the 16 columns at one column's worth.
   const int tid = threadIdx.x;
-  double a[RPT][BW];
+  double b[RPT][BW];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int64_t r = tid + i * TPB;
 #pragma unroll
-    for (int c = 0; c < BW; ++c) a[i][c] = (r < nrows) ? pan[c * prs + r] : 0.0;
+    for (int c = 0; c < BW; ++c) b[i][c] = (r < nrows) ? pan[c * prs + r] : 0.0;
   }
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < BW; ++j) {
     const int64_t pr = k0 + j;
     const int par = j & 1;  // double-buffered pivot row / sums: 2 barriers per column
@@ -634,18 +638,18 @@ __device__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64
       const int64_t r = tid + i * TPB;
       if (r == pr) {
 #pragma unroll
-        for (int c = 0; c < BW; ++c) q.prow[par][c] = a[i][c];
+        for (int c = 0; c < BW; ++c) q.prow[par][c] = b[i][c];
       }
       if (r > pr) {
-        const double x = a[i][j];
+        const double x = b[i][0];
         acc[0] = fma(x, x, acc[0]);
 #pragma unroll
-        for (int c = j + 1; c < BW; ++c) acc[c] = fma(x, a[i][c], acc[c]);
+        for (int c = 1; c < BW; ++c) acc[c] = fma(x, b[i][c], acc[c]);
       }
     }
     reduce16(acc, q.red, q.psum[par]);
     // every thread derives the reflector (dlarfg) redundantly
-    const double alpha = q.prow[par][j];
+    const double alpha = q.prow[par][0];
     const double xn2 = q.psum[par][0];
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (xn2 > 0.0) {
@@ -657,25 +661,25 @@ __device__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64
     if (tau != 0.0) {
       double tw[BW];
 #pragma unroll
-      for (int c = j + 1; c < BW; ++c) tw[c] = tau * fma(scal, q.psum[par][c], q.prow[par][c]);
+      for (int c = 1; c < BW; ++c) tw[c] = tau * fma(scal, q.psum[par][c], q.prow[par][c]);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int64_t r = tid + i * TPB;
         if (r >= pr) {
-          const double vr = (r == pr) ? 1.0 : a[i][j] * scal;
+          const double vr = (r == pr) ? 1.0 : b[i][0] * scal;
 #pragma unroll
-          for (int c = j + 1; c < BW; ++c) a[i][c] = fma(-vr, tw[c], a[i][c]);
-          a[i][j] = (r == pr) ? beta : vr;
+          for (int c = 1; c < BW; ++c) b[i][c] = fma(-vr, tw[c], b[i][c]);
+          b[i][0] = (r == pr) ? beta : vr;
         }
       }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int64_t r = tid + i * TPB;
-    if (r < nrows) {
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t r = tid + i * TPB;
+      if (r < nrows) pan[j * prs + r] = b[i][0];
 #pragma unroll
-      for (int c = 0; c < BW; ++c) pan[c * prs + r] = a[i][c];
+      for (int c = 0; c + 1 < BW; ++c) b[i][c] = b[i][c + 1];
+      b[i][BW - 1] = 0.0;
     }
   }
   __syncthreads();
