@@ -464,41 +464,58 @@ __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, cons
 
 // Copy slice into X (LP x NP, ld LP), transposing when m < p; zero padding.
 // Returns flag: 0 ok, 1 all-zero, 2 non-finite.
-__device__ int load_slice(const SvdParams& P, const double* A, double* X, double* tile) {
+__device__ int load_slice(const SvdParams& P, const double* __restrict__ A, double* __restrict__ X,
+                          double* tile) {
+  // Batched so that every thread keeps LB loads in flight (the copy is
+  // HBM-latency bound otherwise).
+  constexpr int LB = 16;
   const int tid = threadIdx.x;
   const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP;
   int bad = 0, nonzero = 0;
   if (!P.transposed) {
-    for (int64_t c = 0; c < NP; ++c) {
-      for (int64_t r = tid; r < LP; r += TPB) {
-        double x = 0.0;
-        if (r < L && c < n) {
-          x = A[r + c * P.m];
-          bad |= !isfinite(x);
-          nonzero |= (x != 0.0);
-        }
-        X[r + c * LP] = x;
+    const int64_t total = LP * NP;
+    for (int64_t e0 = 0; e0 < total; e0 += int64_t(TPB) * LB) {
+      double v[LB];
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int64_t e = e0 + tid + int64_t(u) * TPB;
+        const int64_t r = e % LP, c = e / LP;
+        v[u] = (e < total && r < L && c < n) ? A[r + c * P.m] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int64_t e = e0 + tid + int64_t(u) * TPB;
+        bad |= !isfinite(v[u]);
+        nonzero |= (v[u] != 0.0);
+        if (e < total) X[e] = v[u];
       }
     }
   } else {
+    // 32 (columns of X) x 128 (rows of X) tiles through shared memory
     for (int64_t c0 = 0; c0 < NP; c0 += 32) {
-      for (int64_t r0 = 0; r0 < LP; r0 += 32) {
-        for (int e = tid; e < 1024; e += TPB) {
+      for (int64_t r0 = 0; r0 < LP; r0 += 128) {
+        double v[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int e = tid + u * TPB;
           const int cc = e & 31, rr = e >> 5;
           const int64_t c = c0 + cc, r = r0 + rr;
-          double x = 0.0;
-          if (r < L && c < n) {
-            x = A[c + r * P.m];
-            bad |= !isfinite(x);
-            nonzero |= (x != 0.0);
-          }
-          tile[rr * 33 + cc] = x;
+          v[u] = (r < L && c < n) ? A[c + r * P.m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int e = tid + u * TPB;
+          bad |= !isfinite(v[u]);
+          nonzero |= (v[u] != 0.0);
+          tile[(e >> 5) * 33 + (e & 31)] = v[u];
         }
         __syncthreads();
-        for (int e = tid; e < 1024; e += TPB) {
-          const int rr = e & 31, cc = e >> 5;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int e = tid + u * TPB;
+          const int rr = e & 127, cc = e >> 7;
           const int64_t c = c0 + cc, r = r0 + rr;
-          if (c < NP) X[r + c * LP] = tile[rr * 33 + cc];
+          if (c < NP && r < LP) X[r + c * LP] = tile[rr * 33 + cc];
         }
         __syncthreads();
       }
@@ -611,9 +628,12 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
 // Register-resident variant: thread t owns rows t + i*TPB (i < RPT) of all
 // 16 panel columns, so the BLAS2 column steps touch no shared memory; only
 // the 16 reductions per column and the pivot row go through it.
+// The panel is read straight from global memory: element (r, c) =
+// src[r * sr + c * sc] for lo <= r < nrows, 0 otherwise (all loads in flight).
 template <int RPT>
 __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
-                                              int64_t nrows) {
+                                              int64_t nrows, const double* src, int64_t sr,
+                                              int64_t sc, int64_t lo) {
   // Register-resident panel, column loop NOT unrolled: b[i][c] holds panel
   // column j + c of this thread's rows, so every column runs the same code
   // (column 0 is factored, then the window shifts left by one).  Keeps the
@@ -623,8 +643,9 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     const int64_t r = tid + i * TPB;
+    const bool in = r >= lo && r < nrows;
 #pragma unroll
-    for (int c = 0; c < BW; ++c) b[i][c] = (r < nrows) ? pan[c * prs + r] : 0.0;
+    for (int c = 0; c < BW; ++c) b[i][c] = in ? src[r * sr + c * sc] : 0.0;
   }
 #pragma unroll 1
   for (int j = 0; j < BW; ++j) {
@@ -685,14 +706,21 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
   __syncthreads();
 }
 
-__device__ void panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows) {
+__device__ void panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows,
+                                 const double* src, int64_t sr, int64_t sc, int64_t lo) {
   const int64_t rpt = (nrows + TPB - 1) / TPB;
   switch (rpt) {
-    case 1: panel_factor_reg<1>(q, pan, prs, k0, nrows); break;
-    case 2: panel_factor_reg<2>(q, pan, prs, k0, nrows); break;
-    case 3: panel_factor_reg<3>(q, pan, prs, k0, nrows); break;
-    case 4: panel_factor_reg<4>(q, pan, prs, k0, nrows); break;
-    default: panel_factor(q, pan, prs, k0, nrows); break;
+    case 1: panel_factor_reg<1>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 2: panel_factor_reg<2>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 3: panel_factor_reg<3>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 4: panel_factor_reg<4>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    default:
+      for (int c = 0; c < BW; ++c)
+        for (int64_t r = threadIdx.x; r < prs; r += TPB)
+          pan[c * prs + r] = (r >= lo && r < nrows) ? src[r * sr + c * sc] : 0.0;
+      __syncthreads();
+      panel_factor(q, pan, prs, k0, nrows);
+      break;
   }
 }
 
@@ -1244,10 +1272,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     if (P.L > P.n) {
       for (int64_t k0 = 0; k0 < NP; k0 += BW) {
         const int64_t kc = (k0 / RCH) * RCH;
-        for (int c = 0; c < BW; ++c)
-          for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < LP ? X[r + (k0 + c) * LP] : 0.0;
-        __syncthreads();
-        { long long _a = clock64(); panel_factor_any(q, pan, prs, k0, LP); pf += clock64() - _a; }
+        { long long _a = clock64(); panel_factor_any(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
         if (tid < BW * BW) {
           const int c = tid / BW, r = tid % BW;
           if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
@@ -1273,10 +1298,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
       const int64_t kc = (k / RCH) * RCH;
-      for (int c = 0; c < BW; ++c)
-        for (int64_t r = tid; r < prs; r += TPB) pan[c * prs + r] = r < RP ? X[r + (k + c) * LP] : 0.0;
-      __syncthreads();
-      { long long _a = clock64(); panel_factor_any(q, pan, prs, k, RP); pf += clock64() - _a; }
+      { long long _a = clock64(); panel_factor_any(q, pan, prs, k, RP, X + k * LP, 1, LP, 0); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;
         if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
@@ -1294,13 +1316,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
-      for (int64_t j = tid; j < prs; j += TPB) {
-        const bool in = (j >= j0 && j < NP);
-#pragma unroll
-        for (int c = 0; c < BW; ++c) pan[c * prs + j] = in ? X[(k + c) + j * LP] : 0.0;
-      }
-      __syncthreads();
-      { long long _a = clock64(); panel_factor_any(q, pan, prs, j0, NP); pf += clock64() - _a; }
+      { long long _a = clock64(); panel_factor_any(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
         if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
