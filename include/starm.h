@@ -81,6 +81,16 @@ size_t starm_last_error(char* buf, size_t len);
 int starm_ttm_f64(const double* src, const double* mat, double* dst, int64_t rows,
                   int64_t inner, int64_t batch, int64_t out_cols, void* stream);
 
+/* ------------------------------------------------------- K1b fast DCT
+ * The DCT transform of the reference (transforms.py dct matrix applied by
+ * the mode-k product, ttm.py:87-104) computed in O(n log n) per fiber:
+ * the same (rows, n, batch) column-major view as starm_ttm_f64 with
+ * inner = out_cols = n, and mat = the orthonormal DCT-II matrix
+ * (inverse = 0) or its transpose, the DCT-III (inverse = 1).  n must be a
+ * power of two in [2, 4096] (STARM_UNSUPPORTED otherwise); src != dst. */
+int starm_dct_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
+                  int inverse, void* stream);
+
 /* ----------------------------------------------------- K11 facewise GEMM
  * Replaces _facewise_matmul (tsvdm.py:205-216): for each slice i,
  *   C_i (m x l) = A_i (m x p) * B_i (p x l), all column-major, slice
@@ -90,8 +100,12 @@ int starm_facewise_gemm_f64(const double* a, const double* b, double* c, int64_t
 
 /* ------------------------------------------------------ K3-K6 slice SVD
  * Replaces _slice_svd/LAPACK dgesvd over slices (slicesvd.py:42-62 and the
- * three drivers named by `job`).  One CTA per slice runs a blocked
- * one-sided Jacobi SVD (Gram tiles on FP64 DMMA) in a global workspace.
+ * three drivers named by `job`).  Slices whose 16-column panel fits in
+ * shared memory take the bidiagonal path: Householder QR + band reduction
+ * (FP64 DMMA compact-WY updates), Householder bulge chasing to upper
+ * bidiagonal, bisection for sigma, inverse iteration + back-transformation
+ * for vectors.  Others run a blocked one-sided Jacobi SVD (Gram tiles on
+ * DMMA).  One CTA per slice, persistent grids, global workspace.
  *
  *  ahat       (m, p, nslices) column-major input, never modified.
  *  slice_ids  optional device int64 list of slices to factor (count

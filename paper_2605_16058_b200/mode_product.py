@@ -6,6 +6,11 @@ column-major buffer is ``batch`` row-major (inner x rows) blocks and the
 kernel computes dst[b] = M @ src[b] for all b in a single grid.  The
 variant and thread arguments are validated exactly like the reference and
 then have no further effect.
+
+Structured transforms take exact shortcuts of the same linear map: the DCT
+kind (power-of-two extent <= 4096) runs the O(n log n) FFT-based DCT-II /
+DCT-III kernel (starm_dct_f64) instead of the dense product, and the
+identity kind is a device copy (the dense product with I is exact).
 """
 
 from __future__ import annotations
@@ -17,7 +22,7 @@ import numpy as np
 
 from . import _native as nat
 from .tensors import DenseTensor, DeviceTensor, as_device
-from .transform_set import Transform, TransformSet
+from .transform_set import DCT, IDENTITY, Transform, TransformSet
 
 __all__ = ["BATCHED", "LOOP", "PARFOR", "VARIANTS", "TTMPlan", "ttm", "ttm_inverse",
            "to_transform_domain", "from_transform_domain", "ttm_device"]
@@ -98,6 +103,28 @@ def ttm_device(x: DeviceTensor, mode: int, op, out_cols: int, inner: int) -> Dev
     return out
 
 
+def _fast_kind(m, n):
+    if isinstance(m, Transform):
+        if m.kind == DCT and 2 <= n <= 4096 and (n & (n - 1)) == 0:
+            return DCT
+        if m.kind == IDENTITY:
+            return IDENTITY
+    return None
+
+
+def structured_device(x: DeviceTensor, mode: int, kind: str, inverse: bool) -> DeviceTensor:
+    """Mode-``mode`` product with a DCT (DCT-II, or DCT-III when inverse) or
+    identity transform without the dense matrix."""
+    plan = TTMPlan.for_dims(x.dims, mode, x.dims[mode])
+    out = DeviceTensor.empty(x.dims, x.device)
+    if kind == IDENTITY:
+        out.data.copy_(x.data)
+        return out
+    nat.call("starm_dct_f64", x.data.data_ptr(), out.data.data_ptr(), plan.rows, plan.inner,
+             plan.batch, int(bool(inverse)), nat.stream_ptr(x.device))
+    return out
+
+
 def _shape(m):
     if isinstance(m, Transform):
         return m.matrix.shape
@@ -127,6 +154,9 @@ def ttm(t, mode, m, variant=BATCHED, threads=1):
         raise ValueError(f"matrix has {shape[1]} columns, mode {mode} extent is {t.dims[mode]}")
 
     def go(x):
+        kind = _fast_kind(m, x.dims[mode])
+        if kind is not None:
+            return structured_device(x, mode, kind, inverse=False)
         op, j, n = _matrix_operand(m, x.device)
         return ttm_device(x, mode, op, j, n)
 
@@ -142,6 +172,9 @@ def ttm_inverse(t, mode, m, variant=BATCHED, threads=1):
         raise ValueError(f"matrix of shape {shape} cannot undo mode {mode} of extent {t.dims[mode]}")
 
     def go(x):
+        kind = _fast_kind(m, x.dims[mode])
+        if kind is not None:
+            return structured_device(x, mode, kind, inverse=True)
         op, j, n = _matrix_operand(m, x.device, transpose=True)
         return ttm_device(x, mode, op, j, n)
 
@@ -151,6 +184,10 @@ def ttm_inverse(t, mode, m, variant=BATCHED, threads=1):
 def forward_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
     out = x
     for k, tr in enumerate(ts, start=2):
+        kind = _fast_kind(tr, out.dims[k])
+        if kind is not None:
+            out = structured_device(out, k, kind, inverse=False)
+            continue
         op, j, n = _matrix_operand(tr, x.device)
         out = ttm_device(out, k, op, j, n)
     return out
@@ -159,6 +196,10 @@ def forward_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
 def inverse_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
     out = x
     for k in range(len(ts) + 1, 1, -1):
+        kind = _fast_kind(ts[k - 2], out.dims[k])
+        if kind is not None:
+            out = structured_device(out, k, kind, inverse=True)
+            continue
         op, j, n = _matrix_operand(ts[k - 2], x.device, transpose=True)
         out = ttm_device(out, k, op, j, n)
     return out

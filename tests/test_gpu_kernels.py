@@ -50,6 +50,40 @@ def test_ttm_large_dct_round_trip():
     assert abs(ahat.frobenius_norm() - t.frobenius_norm()) <= 1e-12 * t.frobenius_norm()
 
 
+@pytest.mark.parametrize("dims,mode", [((37, 41, 2), 2), ((5, 3, 4), 2), ((3, 7, 8, 3), 2),
+                                       ((2, 5, 3, 64), 3), ((9, 11, 1024), 2),
+                                       ((3, 2, 2048), 2), ((2, 3, 4096), 2), ((1, 1, 16), 2)])
+def test_fast_dct_matches_dense_product(dims, mode):
+    # the DCT kind takes the FFT path (starm_dct_f64).  Oracles: the
+    # reference's dense mode-k product with its DCT matrix (whose cos entries
+    # carry ~n * 1e-16 absolute error, so that comparison is loosened with n)
+    # and scipy's FFT-based orthonormal DCT-II (tight).
+    import scipy.fft
+    a = random_array(dims, 17 + sum(dims))
+    t = sb.DenseTensor(a)
+    n = dims[mode]
+    lg = max(1.0, math.log2(n))
+    tr = sb.dct_matrix(n)
+    got = sb.ttm(t, mode, tr)
+    ref = oracle.ttm(a, mode, oracle.dct_matrix(n))
+    assert rel_error(ref, got.array) <= 1e-16 * n + 1e-14
+    exact = scipy.fft.dct(a, type=2, norm="ortho", axis=mode)
+    assert rel_error(exact, got.array) <= 2e-16 * lg + 1e-16
+    back = sb.ttm_inverse(got, mode, tr)
+    assert rel_error(a, back.array) <= 2e-16 * lg + 1e-16
+    ref_back = oracle.ttm(ref, mode, oracle.dct_matrix(n).T)
+    assert rel_error(ref_back, back.array) <= 2e-16 * n + 1e-14
+
+
+def test_fast_dct_rejects_non_power_of_two():
+    from paper_2605_16058_b200 import _native as nat
+    import torch
+    x = torch.zeros(3 * 12, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    with pytest.raises(ValueError, match="power-of-two"):
+        nat.call("starm_dct_f64", x.data_ptr(), y.data_ptr(), 3, 12, 1, 0, nat.stream_ptr())
+
+
 # ------------------------------------------------------------- slice SVD (K3-K6)
 
 @pytest.mark.parametrize("dims", SHAPES)
