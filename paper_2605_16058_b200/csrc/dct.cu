@@ -9,8 +9,11 @@
 // Two real fibers share one complex FFT (real / imaginary parts).  One CTA
 // transforms 2 P fibers (consecutive rows of one batch block, so global
 // accesses are 16 P-byte runs per time index) with radix-2 DIT stages in
-// shared memory; twiddles come from sincospi in the prologue.  n must be a
-// power of two; the launcher returns STARM_UNSUPPORTED otherwise.
+// shared memory; twiddle tables (sincospi) are built once per device and n
+// in a small library-owned allocation.  n must be a power of two <= 4096;
+// the launcher returns STARM_UNSUPPORTED otherwise.
+#include <mutex>
+
 #include "common.cuh"
 
 namespace starm {
@@ -28,19 +31,41 @@ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
 
 __device__ __forceinline__ int bitrev(int x, int bits) { return int(__brev(unsigned(x)) >> (32 - bits)); }
 
-// P complex sequences of length n in z[p * n + i]; tw[m] = e^{-+2 pi i m / n}.
-__device__ void fft_stages(cplx* z, const cplx* tw, int n, int logn, int P) {
-  const int half_total = P * (n >> 1);
-  for (int s = 0; s < logn; ++s) {
+// Twiddle tables per (device, n), built once by dct_tables_kernel:
+//   tw[m] = e^{-2 pi i m / n} (m < n/2),  pw[j] = (cos, sin)(pi j / 2n) (j < n).
+__global__ void dct_tables_kernel(cplx* tw, cplx* pw, int n) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    double sv, cv;
+    if (m < n / 2) {
+      sincospi(2.0 * m / n, &sv, &cv);
+      tw[m] = {cv, -sv};
+    }
+    sincospi(0.5 * m / n, &sv, &cv);
+    pw[m] = {cv, sv};
+  }
+}
+
+// P complex sequences of length N = 2^LOGN in z[p * N + i], bit-reversed
+// input; radix-2 DIT stages (conjugate twiddles when INVERSE).
+// fibre pairs per CTA: 4 up to n = 1024, then shared memory limits it
+__host__ __device__ constexpr int dct_pairs(int logn) { return logn <= 10 ? 4 : (logn == 11 ? 2 : 1); }
+
+template <int LOGN, bool INVERSE>
+__device__ __forceinline__ void fft_stages(cplx* z, const cplx* tw) {
+  constexpr int N = 1 << LOGN, H = N >> 1;
+  constexpr int half_total = dct_pairs(LOGN) * H;
+#pragma unroll 1
+  for (int s = 0; s < LOGN; ++s) {
     const int h = 1 << s;
-    const int step = n >> (s + 1);  // twiddle stride
     for (int q = threadIdx.x; q < half_total; q += blockDim.x) {
-      const int p = q / (n >> 1), qq = q % (n >> 1);
+      const int p = q >> (LOGN - 1), qq = q & (H - 1);
       const int k = qq & (h - 1);
       const int i0 = ((qq >> s) << (s + 1)) + k;
-      cplx* zp = z + p * n;
+      cplx* zp = z + p * N;
+      cplx w = tw[k << (LOGN - 1 - s)];
+      if (INVERSE) w.im = -w.im;
       const cplx a = zp[i0];
-      const cplx b = cmul(zp[i0 + h], tw[k * step]);
+      const cplx b = cmul(zp[i0 + h], w);
       zp[i0] = {a.re + b.re, a.im + b.im};
       zp[i0 + h] = {a.re - b.re, a.im - b.im};
     }
@@ -48,92 +73,154 @@ __device__ void fft_stages(cplx* z, const cplx* tw, int n, int logn, int P) {
   }
 }
 
-template <bool INVERSE>
+template <int LOGN, bool INVERSE>
 __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restrict__ src,
                                                           double* __restrict__ dst, int64_t rows,
-                                                          int n, int logn, int64_t batch, int P) {
+                                                          int64_t batch,
+                                                          const cplx* __restrict__ gtw,
+                                                          const cplx* __restrict__ gpw) {
+  constexpr int N = 1 << LOGN;
+  constexpr int P = dct_pairs(LOGN);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* z = reinterpret_cast<cplx*>(smem_raw);  // [P][n]
-  cplx* tw = z + int64_t(P) * n;                // [n / 2] FFT twiddles
-  cplx* pw = tw + (n >> 1);                     // [n] e^{-i pi j / 2n} (cos, sin)
-  const int F = 2 * P;
+  cplx* z = reinterpret_cast<cplx*>(smem_raw);  // [P][N]
+  cplx* tw = z + P * N;                         // [N / 2]
+  constexpr int F = 2 * P;
   const int64_t tiles_per_b = (rows + F - 1) / F;
-  const int64_t tile = blockIdx.x;
-  const int64_t b = tile / tiles_per_b;
-  const int64_t r0 = (tile % tiles_per_b) * F;
-  const int64_t base = b * rows * n;
-  const double c0 = sqrt(1.0 / n), c1 = sqrt(2.0 / n);
-  for (int m = threadIdx.x; m < (n >> 1); m += blockDim.x) {
-    double sv, cv;
-    sincospi(2.0 * m / n, &sv, &cv);
-    tw[m] = {cv, INVERSE ? sv : -sv};
-  }
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double sv, cv;
-    sincospi(0.5 * j / n, &sv, &cv);
-    pw[j] = {cv, sv};
-  }
+  const int64_t b = blockIdx.x / tiles_per_b;
+  const int64_t r0 = (blockIdx.x % tiles_per_b) * F;
+  const int64_t base = b * rows * N;
+  const double c0 = sqrt(1.0 / N), c1 = sqrt(2.0 / N);
+  for (int m = threadIdx.x; m < N / 2; m += blockDim.x) tw[m] = gtw[m];
+  constexpr int U = 8;  // loads in flight per thread
+  const int total = F * N;
   if (!INVERSE) {
     // load x (fibers f = 2p + {0,1}) into bit-reversed Makhoul order
-    for (int64_t e = threadIdx.x; e < int64_t(F) * n; e += blockDim.x) {
-      const int f = int(e % F), t = int(e / F);
-      const int64_t r = r0 + f;
-      const double x = r < rows ? src[base + r + int64_t(t) * rows] : 0.0;
-      const int pos = (t & 1) ? n - 1 - (t >> 1) : (t >> 1);
-      double* zp = reinterpret_cast<double*>(z + (f >> 1) * n + bitrev(pos, logn));
-      zp[f & 1] = x;
+    for (int e0 = 0; e0 < total; e0 += U * DCT_THREADS) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * DCT_THREADS + threadIdx.x;
+        const int f = e % F, t = e / F;
+        const int64_t r = r0 + f;
+        v[u] = (e < total && r < rows) ? src[base + r + int64_t(t) * rows] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * DCT_THREADS + threadIdx.x;
+        if (e < total) {
+          const int f = e % F, t = e / F;
+          const int pos = (t & 1) ? N - 1 - (t >> 1) : (t >> 1);
+          reinterpret_cast<double*>(z + (f >> 1) * N + bitrev(pos, LOGN))[f & 1] = v[u];
+        }
+      }
     }
     __syncthreads();
-    fft_stages(z, tw, n, logn, P);
+    fft_stages<LOGN, false>(z, tw);
     // split the pair, post-twiddle, scale, store (consecutive threads: consecutive fibers)
-    for (int64_t e = threadIdx.x; e < int64_t(F) * n; e += blockDim.x) {
-      const int f = int(e % F), j = int(e / F);
+    for (int e = threadIdx.x; e < total; e += DCT_THREADS) {
+      const int f = e % F, j = e / F;
       const int64_t r = r0 + f;
       if (r >= rows) continue;
-      const cplx* zp = z + (f >> 1) * n;
-      const cplx zj = zp[j], zn = zp[(n - j) & (n - 1)];
+      const cplx* zp = z + (f >> 1) * N;
+      const cplx zj = zp[j], zn = zp[(N - j) & (N - 1)];
       cplx v;
       if ((f & 1) == 0) {
         v = {0.5 * (zj.re + zn.re), 0.5 * (zj.im - zn.im)};  // (Z_j + conj Z_{n-j}) / 2
       } else {
         v = {0.5 * (zj.im + zn.im), 0.5 * (zn.re - zj.re)};  // (Z_j - conj Z_{n-j}) / 2i
       }
-      const cplx w = pw[j];
+      const cplx w = gpw[j];
       const double xr = fma(w.re, v.re, w.im * v.im);  // Re(e^{-i theta} v)
       dst[base + r + int64_t(j) * rows] = (j ? c1 : c0) * xr;
     }
   } else {
     // V^f_j = e^{i theta_j} (Y_j / c_j - i Y_{n-j} / c_{n-j}); z = V^a + i V^b
-    for (int64_t e = threadIdx.x; e < int64_t(P) * n; e += blockDim.x) {
-      const int p = int(e % P), j = int(e / P);  // consecutive threads: consecutive fibers
+    const double ic0 = 1.0 / c0, ic1 = 1.0 / c1;
+    for (int e = threadIdx.x; e < P * N; e += DCT_THREADS) {
+      const int p = e % P, j = e / P;  // consecutive threads: consecutive fibers
       double ya = 0.0, yb = 0.0, yna = 0.0, ynb = 0.0;
       const int64_t ra = r0 + 2 * p, rb = ra + 1;
-      const int64_t oj = base + int64_t(j) * rows, on = base + int64_t(n - j) * rows;
+      const int64_t oj = base + int64_t(j) * rows, on = base + int64_t(N - j) * rows;
+      const double sj = j ? ic1 : ic0;
       if (ra < rows) {
-        ya = src[oj + ra] / (j ? c1 : c0);
-        if (j) yna = src[on + ra] / c1;
+        ya = src[oj + ra] * sj;
+        if (j) yna = src[on + ra] * ic1;
       }
       if (rb < rows) {
-        yb = src[oj + rb] / (j ? c1 : c0);
-        if (j) ynb = src[on + rb] / c1;
+        yb = src[oj + rb] * sj;
+        if (j) ynb = src[on + rb] * ic1;
       }
-      const cplx w = pw[j];  // (cos theta, sin theta): e^{+i theta}
+      const cplx w = gpw[j];  // e^{+i theta}
       const cplx va = cmul(w, {ya, -yna});
       const cplx vb = cmul(w, {yb, -ynb});
-      z[p * n + bitrev(j, logn)] = {va.re - vb.im, va.im + vb.re};
+      z[p * N + bitrev(j, LOGN)] = {va.re - vb.im, va.im + vb.re};
     }
     __syncthreads();
-    fft_stages(z, tw, n, logn, P);
-    const double inv = 1.0 / n;
-    for (int64_t e = threadIdx.x; e < int64_t(F) * n; e += blockDim.x) {
-      const int f = int(e % F), t = int(e / F);
+    fft_stages<LOGN, true>(z, tw);
+    const double inv = 1.0 / N;
+    for (int e = threadIdx.x; e < total; e += DCT_THREADS) {
+      const int f = e % F, t = e / F;
       const int64_t r = r0 + f;
       if (r >= rows) continue;
-      const int pos = (t & 1) ? n - 1 - (t >> 1) : (t >> 1);
-      const cplx zz = z[(f >> 1) * n + pos];
+      const int pos = (t & 1) ? N - 1 - (t >> 1) : (t >> 1);
+      const cplx zz = z[(f >> 1) * N + pos];
       dst[base + r + int64_t(t) * rows] = ((f & 1) ? zz.im : zz.re) * inv;
     }
   }
+}
+
+struct DctTables {
+  cplx* tw[13] = {};
+  cplx* pw[13] = {};
+};
+
+std::mutex g_dct_mu;
+DctTables g_dct_tables[64];  // per device ordinal
+
+int dct_tables(int logn, const cplx** tw, const cplx** pw, cudaStream_t st) {
+  int dev = 0;
+  STARM_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("starm_dct_f64: device ordinal out of range");
+    return STARM_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lk(g_dct_mu);
+  DctTables& t = g_dct_tables[dev];
+  if (!t.tw[logn]) {
+    const int n = 1 << logn;
+    cplx *a = nullptr, *b = nullptr;
+    STARM_CUDA_TRY(cudaMalloc(&a, sizeof(cplx) * (n / 2 > 0 ? n / 2 : 1)));
+    STARM_CUDA_TRY(cudaMalloc(&b, sizeof(cplx) * n));
+    dct_tables_kernel<<<(n + 255) / 256, 256, 0, st>>>(a, b, n);
+    STARM_LAUNCH_CHECK();
+    STARM_CUDA_TRY(cudaStreamSynchronize(st));
+    t.tw[logn] = a;
+    t.pw[logn] = b;
+  }
+  *tw = t.tw[logn];
+  *pw = t.pw[logn];
+  return STARM_OK;
+}
+
+template <int LOGN>
+int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool inverse,
+               cudaStream_t st) {
+  constexpr int N = 1 << LOGN;
+  constexpr int P = dct_pairs(LOGN);
+  const size_t smem = (size_t(P) * N + N / 2) * sizeof(cplx);
+  const int64_t tiles = (rows + 2 * P - 1) / (2 * P) * batch;
+  if (tiles > int64_t(0x7fffffff)) {
+    set_error("starm_dct_f64: too many fibers for one launch");
+    return STARM_UNSUPPORTED;
+  }
+  const cplx *tw = nullptr, *pw = nullptr;
+  const int rc = dct_tables(LOGN, &tw, &pw, st);
+  if (rc) return rc;
+  auto kern = inverse ? dct_kernel<LOGN, true> : dct_kernel<LOGN, false>;
+  STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, batch, tw, pw);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
 }
 
 }  // namespace
@@ -150,19 +237,20 @@ extern "C" int starm_dct_f64(const double* src, double* dst, int64_t rows, int64
     set_error("starm_dct_f64: the fast path needs a power-of-two length in [2, 4096]");
     return STARM_UNSUPPORTED;
   }
-  int logn = 0;
-  while ((int64_t(1) << logn) < n) ++logn;
-  const int P = n <= 1024 ? 4 : (n == 2048 ? 2 : 1);
-  const size_t smem = (size_t(P) * n + n / 2 + n) * sizeof(cplx);
-  const int64_t tiles = (rows + 2 * P - 1) / (2 * P) * batch;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (inverse) {
-    STARM_CUDA_TRY(cudaFuncSetAttribute(dct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dct_kernel<true><<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, int(n), logn, batch, P);
-  } else {
-    STARM_CUDA_TRY(cudaFuncSetAttribute(dct_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dct_kernel<false><<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, int(n), logn, batch, P);
+  const bool inv = inverse != 0;
+  switch (n) {
+    case 2: return launch_dct<1>(src, dst, rows, batch, inv, st);
+    case 4: return launch_dct<2>(src, dst, rows, batch, inv, st);
+    case 8: return launch_dct<3>(src, dst, rows, batch, inv, st);
+    case 16: return launch_dct<4>(src, dst, rows, batch, inv, st);
+    case 32: return launch_dct<5>(src, dst, rows, batch, inv, st);
+    case 64: return launch_dct<6>(src, dst, rows, batch, inv, st);
+    case 128: return launch_dct<7>(src, dst, rows, batch, inv, st);
+    case 256: return launch_dct<8>(src, dst, rows, batch, inv, st);
+    case 512: return launch_dct<9>(src, dst, rows, batch, inv, st);
+    case 1024: return launch_dct<10>(src, dst, rows, batch, inv, st);
+    case 2048: return launch_dct<11>(src, dst, rows, batch, inv, st);
+    default: return launch_dct<12>(src, dst, rows, batch, inv, st);
   }
-  STARM_LAUNCH_CHECK();
-  return STARM_OK;
 }
