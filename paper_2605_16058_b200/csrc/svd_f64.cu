@@ -1594,44 +1594,144 @@ __device__ __forceinline__ int count_below(const double* d, const double* e, int
   return neg - n;
 }
 
+// Sturm count of T_GK - x I plus the log-derivatives of f(x) = det(T_GK - x I):
+// with pivots q_i (q_0 = -x, q_i = -x - b_{i-1}^2 / q_{i-1}),
+//   G = f'/f = sum q_i'/q_i,  H = -(f'/f)' = sum (q_i'/q_i)^2 - q_i''/q_i.
+__device__ __forceinline__ int count_lag(const double* d, const double* e, int n, double x,
+                                         double pivmin, double& G, double& H) {
+  int neg = 0;
+  double q = -x, dq = -1.0, d2 = 0.0;
+  G = 0.0;
+  H = 0.0;
+  neg += (q < 0.0);
+  for (int k = 0; k < 2 * n - 1; ++k) {
+    const double b = (k & 1) ? e[k >> 1] : d[k >> 1];
+    if (fabs(q) < pivmin) q = -pivmin;
+    const double r = rcp_nr(q);
+    const double g = dq * r;
+    G += g;
+    H = fma(g, g, fma(-d2, r, H));
+    const double t = b * b * r;
+    const double tr = t * r;
+    d2 = tr * fma(-2.0 * dq, g, d2);  // b^2 r^2 (q'' - 2 q'^2 r)
+    dq = fma(tr, dq, -1.0);
+    q = -x - t;
+    neg += (q < 0.0);
+  }
+  if (fabs(q) < pivmin) q = -pivmin;
+  const double r = rcp_nr(q);
+  const double g = dq * r;
+  G += g;
+  H = fma(g, g, fma(-d2, r, H));
+  return neg - n;
+}
+
+// sigma_j: bisection on Sturm counts until [lo, hi) isolates it (count(lo) =
+// target, count(hi) = target + 1), then Laguerre's method on det(T_GK - x I)
+// (cubically convergent; T_GK is real-rooted, and the branch is chosen by
+// the count so the iterate moves toward the bracketed root), safeguarded by
+// the bracket, which every evaluation tightens.  Clusters that never
+// isolate, and Laguerre runs that do not converge, finish by bisection to
+// 2u * max(sigma, 1e-3 * bound).  The phases are warp-uniform (a lane waits
+// for the warp before the next phase) so bisection and Laguerre steps never
+// diverge inside a warp.
 __global__ void svd_bisect_kernel(SvdParams P) {
   const int64_t n = P.n, NP = P.NP;
   const int64_t total = P.count * n;
-  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
-       g += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t it = g / n, j = g % n;
+  const double N2 = 2.0 * double(n);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; w * 32 < total; w += warps) {
+    const int64_t g = w * 32 + lane;
+    const bool valid = g < total;
+    const int64_t it = valid ? g / n : 0, j = valid ? g % n : 0;
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
-    const int flag = P.flags[si];
-    if (flag == 2) continue;
-    double sigma = 0.0;
+    const int flag = valid ? P.flags[si] : 1;
+    const double* d = P.debuf + si * 2 * NP;
+    const double* e = d + NP;
+    double bound = 0.0, amax = 0.0;
     if (flag == 0) {
-      const double* d = P.debuf + si * 2 * NP;
-      const double* e = d + NP;
-      double bound = 0.0, amax = 0.0;
       for (int64_t k = 0; k < n; ++k) {
         const double dk = fabs(d[k]), ek = (k + 1 < n) ? fabs(e[k]) : 0.0;
         const double ekm = k > 0 ? fabs(e[k - 1]) : 0.0;
         bound = fmax(bound, fmax(dk + ek, dk + ekm));
         amax = fmax(amax, fmax(dk, ek));
       }
-      if (bound > 0.0) {
-        const double pivmin = fmax(DBL_MIN, amax * amax * 1e-300);
-        const int64_t target = n - 1 - j;  // want count_below(x) <= target
-        double lo = 0.0, hi = bound * (1.0 + 4.0 * DBL_EPSILON) + DBL_MIN;
-        for (int iter = 0; iter < 120; ++iter) {
+    }
+    const double pivmin = fmax(DBL_MIN, amax * amax * 1e-300);
+    const int64_t target = n - 1 - j;  // want count_below(x) <= target
+    double lo = 0.0, hi = bound * (1.0 + 4.0 * DBL_EPSILON) + DBL_MIN;
+    int64_t clo = 0, chi = n;
+    double sigma = 0.0, x = 0.0;
+    int state = (flag == 0 && bound > 0.0) ? 0 : 3;  // 0 isolate, 1 Laguerre, 2 bisect, 3 done
+    auto converged = [&]() {
+      const double mid = 0.5 * (lo + hi);
+      return !(mid > lo && mid < hi) || hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, 1e-3 * bound);
+    };
+    // ---- phase A: bisection until isolated
+    while (__any_sync(0xffffffffu, state == 0)) {
+      if (state == 0) {
+        if (converged()) {
+          sigma = 0.5 * (lo + hi);
+          state = 3;
+        } else if (clo == target && chi == target + 1) {
+          x = 0.5 * (lo + hi);
+          state = 1;
+        } else {
           const double mid = 0.5 * (lo + hi);
-          if (!(mid > lo && mid < hi)) break;
-          if (hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, 1e-3 * bound)) break;
-          if (count_below(d, e, int(n), mid, pivmin) <= target)
+          const int64_t c = count_below(d, e, int(n), mid, pivmin);
+          if (c <= target) {
             lo = mid;
-          else
+            clo = c;
+          } else {
             hi = mid;
+            chi = c;
+          }
         }
-        sigma = 0.5 * (lo + hi);
       }
     }
-    P.s[j + slice * n] = sigma;
+    // ---- phase B: Laguerre inside the bracket
+    for (int lt = 0; lt < 16 && __any_sync(0xffffffffu, state == 1); ++lt) {
+      if (state == 1) {
+        double G, H;
+        const int64_t c = count_lag(d, e, int(n), x, pivmin, G, H);
+        const bool below = c <= target;  // x below sigma_j: step up
+        if (below) {
+          lo = x;
+          clo = c;
+        } else {
+          hi = x;
+          chi = c;
+        }
+        const double disc = sqrt(fmax((N2 - 1.0) * fma(N2, H, -G * G), 0.0));
+        const double den = below ? G - disc : G + disc;
+        double xn = den != 0.0 ? x - N2 / den : 0.5 * (lo + hi);
+        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(xn), 1e-3 * bound);
+        if (fabs(xn - x) <= tol || hi - lo <= tol) {
+          sigma = (xn >= lo && xn <= hi) ? xn : x;
+          state = 3;
+        } else {
+          if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+          x = xn;
+        }
+      }
+    }
+    if (state == 1) state = 2;
+    // ---- phase C: bisection to the end for the rest
+    while (__any_sync(0xffffffffu, state == 2)) {
+      if (state == 2) {
+        if (converged()) {
+          sigma = 0.5 * (lo + hi);
+          state = 3;
+        } else {
+          const double mid = 0.5 * (lo + hi);
+          if (count_below(d, e, int(n), mid, pivmin) <= target) lo = mid;
+          else hi = mid;
+        }
+      }
+    }
+    if (valid && flag != 2) P.s[j + slice * n] = sigma;
   }
 }
 
