@@ -130,8 +130,10 @@ size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t nslices, int64_t 
 /* Tuning / diagnostics (process-wide; a value < 0 leaves a knob unchanged):
  * inner Jacobi sweeps per pair step (default 1), sweep cap (60), values
  * path (1 = QR + band reduction + bulge chasing + bisection whenever a
- * 16-column panel of the slice fits in shared memory, 0 = Jacobi only),
- * kernel counters on/off.  starm_svd_stats copies 16 counters (slices,
+ * 16-column panel of the slice fits in shared memory, 0 = Jacobi only,
+ * 2 = as 1 with the bulge-chase window in global memory, 3 = diagnostic
+ * for timing the band-reduction kernel alone: the call returns after it
+ * with undefined outputs), kernel counters on/off.  starm_svd_stats copies 16 counters (slices,
  * sweeps, pairs, rotated pairs, cycles in gram / eig / apply / qr /
  * finalize / load / band / bulge) to host memory, synchronising the device. */
 int starm_svd_tune(int max_inner, int max_sweeps, int mode, int stats);

@@ -731,12 +731,15 @@ __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64
   const int tile = warp & 3, half = warp >> 2;
   const int ti = tile >> 1, tj = tile & 1;
   double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
-  int u = 0;
-  for (int64_t r0 = kc + half * 4; r0 < LP; r0 += 8, u = (u + 1) & 3) {
-    const double a = pan[(ti * 8 + gq) * prs + r0 + tq];
-    const double b = pan[(tj * 8 + gq) * prs + r0 + tq];
-    dmma884(d0[u], d1[u], a, b);
+  const double* pa = pan + (ti * 8 + gq) * prs + tq;
+  const double* pb = pan + (tj * 8 + gq) * prs + tq;
+  const int lp = int(LP);
+  int r0 = int(kc) + half * 4;
+  for (; r0 + 24 < lp; r0 += 32) {  // four independent accumulators (constant indices)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma884(d0[u], d1[u], pa[r0 + 8 * u], pb[r0 + 8 * u]);
   }
+  for (; r0 < lp; r0 += 8) dmma884(d0[0], d1[0], pa[r0], pb[r0]);
   q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq] = (d0[0] + d0[1]) + (d0[2] + d0[3]);
   q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq + 1] = (d1[0] + d1[1]) + (d1[2] + d1[3]);
   __syncthreads();
@@ -960,37 +963,47 @@ constexpr int CS16 = 20;    // column stride of a staged 16-row chunk
 
 // C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
 // rows [kc, nrows) in 16-row chunks dealt round-robin to the warps.
+// Index math is 32-bit with per-lane base pointers (a slice slot is < 2^31
+// elements), so the loops are DMMA / LDS / cp.async with few integer ops.
 template <bool TWO>
-__device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs,
-                                  double* X, int64_t ld, int64_t nrows, int64_t NP, int64_t kc,
-                                  int64_t c0) {
+__device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs64,
+                                  double* X, int64_t ld64, int64_t nrows64, int64_t NP64,
+                                  int64_t kc64, int64_t c064) {
   constexpr int WR = TWO ? WREG : WREG1;
+  constexpr int NW = TPB / 32;
+  const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
+  const int kc = int(kc64), c0 = int(c064);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   double* wr = wbase + warp * WR;  // [TWO ? 2 : 1][32 * CS16]
-  const int64_t nck = (nrows - kc) / 16;
-  auto stage = [&](int64_t ck, int b) {
-    const int64_t r0 = kc + ck * 16;
-    double* dst = wr + b * (GW * CS16);
+  const int nck = (nrows - kc) / 16;
+  // staging: lane copies rows (sr2, sr2 + 1) of columns scol + 4 i, i < 8
+  const int scol = lane >> 3, sr2 = (lane & 7) * 2;
+  double* xl = X + (c0 + scol) * ld + kc + sr2;  // + 16 ck + 4 i ld
+  const int nin = (NP - c0 - scol + 3) >> 2;     // columns scol + 4 i < NP - c0  <=>  i < nin
+  auto stage = [&](int ck, int b) {
+    double* dst = wr + b * (GW * CS16) + scol * CS16 + sr2;
+    const double* srcp = xl + ck * 16;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int qq = lane + 32 * i;
-      const int col = qq >> 3, r2 = (qq & 7) * 2;
-      const bool in = c0 + col < NP;
-      cp_async16(dst + col * CS16 + r2, in ? X + r0 + r2 + (c0 + col) * ld : X, in ? 16 : 0);
+      const bool in = i < nin;
+      cp_async16(dst + 4 * i * CS16, in ? srcp + 4 * i * ld : X, in ? 16 : 0);
     }
     cp_async_commit();
   };
+  // A fragments of V^T: V[r][a*8+gq] = pan[(a*8+gq) prs + r]
+  const double* pa0 = pan + gq * prs + kc + tq;
+  const double* pa1 = pa0 + 8 * prs;
   // ---- Y = V^T C  (16 x 32): every warp accumulates all 8 tiles over its chunks
   double y[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) y[a][b][0] = y[a][b][1] = 0.0;
-  int64_t ck = warp;
+  int ck = warp;
   if (ck < nck) stage(ck, 0);
-  for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
-    const int64_t nx = ck + TPB / 32;
+  for (int it = 0; ck < nck; ck += NW, ++it) {
+    const int nx = ck + NW;
     if (!TWO && it > 0) stage(ck, 0);
     if (TWO && nx < nck) {
       stage(nx, (it + 1) & 1);
@@ -999,15 +1012,15 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
       cp_async_wait<0>();
     }
     __syncwarp();
-    const double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
-    const int64_t r0 = kc + ck * 16;
+    const double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16) + gq * CS16 + tq;
+    const int ro = ck * 16;
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       double av[2], bv[4];
+      av[0] = pa0[ro + k4 * 4];
+      av[1] = pa1[ro + k4 * 4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = pan[(a * 8 + gq) * prs + r0 + k4 * 4 + tq];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = cs[(b * 8 + gq) * CS16 + k4 * 4 + tq];
+      for (int b = 0; b < 4; ++b) bv[b] = cs[b * 8 * CS16 + k4 * 4];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -1017,20 +1030,20 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   }
   // ---- deterministic cross-warp sum (fixed warp order) into q.y
   {
-    double* part = wr;  // 16 x 32 row-major partial of this warp
+    double* part = wr + gq * GW + 2 * tq;  // 16 x 32 row-major partial of this warp
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        part[(a * 8 + gq) * GW + b * 8 + 2 * tq] = y[a][b][0];
-        part[(a * 8 + gq) * GW + b * 8 + 2 * tq + 1] = y[a][b][1];
+        part[a * 8 * GW + b * 8] = y[a][b][0];
+        part[a * 8 * GW + b * 8 + 1] = y[a][b][1];
       }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < BW * GW; e += TPB) {
     double sacc = 0.0;
 #pragma unroll
-    for (int w = 0; w < TPB / 32; ++w) sacc += wbase[w * WR + e];
+    for (int w = 0; w < NW; ++w) sacc += wbase[w * WR + e];
     q.y[(e / GW) * GS + (e % GW)] = sacc;
   }
   __syncthreads();
@@ -1042,11 +1055,18 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
     q.z[c * ZS + i] = sacc;
   }
   __syncthreads();
-  // ---- C -= V Z per chunk, warp-private
+  // ---- C -= V Z per chunk, warp-private.  A fragments V[r0+a*8+gq][k4*4+tq]
+  const double* pv = pan + tq * prs + kc + gq;  // + k4*4 prs + ro + a*8
+  const double* zb = q.z + gq * ZS + tq;         // + b*8 ZS + k4*4
+  double zf[4][4];                                // B fragments of Z, loop-invariant
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) zf[k4][b] = zb[b * 8 * ZS + k4 * 4];
   ck = warp;
   if (ck < nck) stage(ck, 0);
-  for (int it = 0; ck < nck; ck += TPB / 32, ++it) {
-    const int64_t nx = ck + TPB / 32;
+  for (int it = 0; ck < nck; ck += NW, ++it) {
+    const int nx = ck + NW;
     if (!TWO && it > 0) stage(ck, 0);
     if (TWO && nx < nck) {
       stage(nx, (it + 1) & 1);
@@ -1055,8 +1075,8 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
       cp_async_wait<0>();
     }
     __syncwarp();
-    double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
-    const int64_t r0 = kc + ck * 16;
+    double* csb = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
+    const int ro = ck * 16;
     double acc[2][4][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -1064,32 +1084,29 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
     for (int k4 = 0; k4 < BW / 4; ++k4) {
-      double av[2], bv[4];
+      double av[2];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = pan[(k4 * 4 + tq) * prs + r0 + a * 8 + gq];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = q.z[(b * 8 + gq) * ZS + k4 * 4 + tq];
+      for (int a = 0; a < 2; ++a) av[a] = pv[k4 * 4 * prs + ro + a * 8];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], zf[k4][b]);
     }
+    double* cw = csb + 2 * tq * CS16 + gq;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        cs[(b * 8 + 2 * tq) * CS16 + a * 8 + gq] -= acc[a][b][0];
-        cs[(b * 8 + 2 * tq + 1) * CS16 + a * 8 + gq] -= acc[a][b][1];
+        cw[b * 8 * CS16 + a * 8] -= acc[a][b][0];
+        cw[b * 8 * CS16 + CS16 + a * 8] -= acc[a][b][1];
       }
     __syncwarp();
+    const double* cr = csb + scol * CS16 + sr2;
+    double* xw = xl + ro;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int qq = lane + 32 * i;
-      const int col = qq >> 3, r2 = (qq & 7) * 2;
-      if (c0 + col < NP)
-        *reinterpret_cast<double2*>(X + r0 + r2 + (c0 + col) * ld) =
-            *reinterpret_cast<const double2*>(cs + col * CS16 + r2);
-    }
+    for (int i = 0; i < 8; ++i)
+      if (i < nin)
+        *reinterpret_cast<double2*>(xw + 4 * i * ld) = *reinterpret_cast<const double2*>(cr + 4 * i * CS16);
     __syncwarp();
   }
   cp_async_wait<0>();
@@ -1098,122 +1115,130 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
 
 // LQ half-step update, warp-private:  C <- C (I - V T V^T) for columns
 // [j0, NP) and rows [rmin, nrows) of A (ld).  Each warp owns 8-row tiles
-// (rows rc + 8*t, t = warp, warp+8, ...) end to end: Y = C V, Z = Y T and
-// C -= Z V^T never leave the warp.  V[j][c] = pan2[c * prs + j].
+// (rows rc + 8*t, t = warp, warp+8, ...) end to end: Y = C V, Z = Y T (on
+// DMMA) and C -= Z V^T never leave the warp.  V[j][c] = pan2[c * prs + j].
 constexpr int CS8 = 12;  // column stride of a staged 8-row tile
 
 template <bool TWO>
-__device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2, int64_t prs,
-                               double* A, int64_t ld, int64_t nrows, int64_t NP, int64_t rc,
-                               int64_t rmin, int64_t j0) {
+__device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2, int64_t prs64,
+                               double* A, int64_t ld64, int64_t nrows64, int64_t NP64, int64_t rc64,
+                               int64_t rmin64, int64_t j064) {
   constexpr int WR = TWO ? WREG : WREG1;
+  constexpr int NW = TPB / 32;
+  const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
+  const int rc = int(rc64), rmin = int(rmin64), j0 = int(j064);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  double* wr = wbase + warp * WR;            // ring [TWO ? 2 : 1][32 * CS8]
+  double* wr = wbase + warp * WR;              // ring [TWO ? 2 : 1][32 * CS8]
   double* zs = wr + (TWO ? 2 : 1) * GW * CS8;  // Y / Z scratch [16 * CS8]
-  const double* Tm = q.t;
-  const int64_t nblk = (NP - j0 + GW - 1) / GW;
-  const int64_t ntile = (nrows - rc) / 8;
-  auto stage = [&](int64_t r0, int64_t b, int slot) {
-    const int64_t jb = j0 + b * GW;
-    double* dst = wr + slot * (GW * CS8);
+  const int nblk = (NP - j0 + GW - 1) / GW;
+  const int ntile = (nrows - rc) / 8;
+  // staging: lane copies rows (sr2, sr2 + 1) of columns scol + 8 i, i < 4
+  const int scol = lane >> 2, sr2 = (lane & 3) * 2;
+  double* al = A + (j0 + scol) * ld + sr2;  // + r0 + (32 b + 8 i) ld
+  auto stage = [&](int r0, int b, int slot) {
+    double* dst = wr + slot * (GW * CS8) + scol * CS8 + sr2;
+    const double* srcp = al + r0 + b * GW * ld;
+    const int lim = NP - j0 - b * GW - scol;  // column scol + 8 i in range  <=>  8 i < lim
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int qq = lane + 32 * i;
-      const int col = qq >> 2, r2 = (qq & 3) * 2;
-      const bool in = jb + col < NP;
-      cp_async16(dst + col * CS8 + r2, in ? A + r0 + r2 + (jb + col) * ld : A, in ? 16 : 0);
+      const bool in = 8 * i < lim;
+      cp_async16(dst + 8 * i * CS8, in ? srcp + 8 * i * ld : A, in ? 16 : 0);
     }
     cp_async_commit();
   };
-  for (int64_t tile = warp; tile < ntile; tile += TPB / 32) {
-    const int64_t r0 = rc + tile * 8;
+  const double* pvy = pan2 + gq * prs + j0 + tq;  // Y pass B: V[jb+k4*4+tq][ct*8+gq]
+  const double* pvz = pan2 + tq * prs + j0 + gq;  // Z pass B: V[jb+c*8+gq][k4*4+tq]
+  // T as B fragments (T[k][n], n = ct*8+gq, k = k4*4+tq), loop-invariant
+  double tf[4][2];
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4)
+#pragma unroll
+    for (int ct = 0; ct < 2; ++ct) tf[k4][ct] = q.t[(k4 * 4 + tq) * 17 + ct * 8 + gq];
+  for (int tile = warp; tile < ntile; tile += NW) {
+    const int r0 = rc + tile * 8;
     if (r0 + 8 <= rmin) continue;  // rows above the panel are final
     // ---- Y = C V (8 x 16)
     double y[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [ct][k4&1][e]
     stage(r0, 0, 0);
-    for (int64_t b = 0; b < nblk; ++b) {
+    for (int b = 0; b < nblk; ++b) {
       if (!TWO && b > 0) stage(r0, b, 0);
       if (TWO && b + 1 < nblk) {
-        stage(r0, b + 1, int((b + 1) & 1));
+        stage(r0, b + 1, (b + 1) & 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      const double* cs = wr + (TWO ? (b & 1) : 0) * (GW * CS8);
-      const int64_t jb = j0 + b * GW;
+      const double* cs = wr + (TWO ? (b & 1) : 0) * (GW * CS8) + tq * CS8 + gq;
+      const double* pb = pvy + b * GW;
 #pragma unroll
       for (int k4 = 0; k4 < GW / 4; ++k4) {
-        const double a = cs[(k4 * 4 + tq) * CS8 + gq];
+        const double a = cs[k4 * 4 * CS8];
 #pragma unroll
         for (int ct = 0; ct < 2; ++ct)
-          dmma884(y[ct][k4 & 1][0], y[ct][k4 & 1][1], a,
-                  pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
+          dmma884(y[ct][k4 & 1][0], y[ct][k4 & 1][1], a, pb[ct * 8 * prs + k4 * 4]);
       }
       __syncwarp();
     }
-    // ---- Z = Y T (8 x 16): Y -> zs (row-major 8 x 16), Z -> zs as A fragments
+    // ---- Z = Y T (8 x 16) on DMMA: Y -> zs row-major, Z -> zs column-major (A fragments)
 #pragma unroll
     for (int ct = 0; ct < 2; ++ct) {
       zs[gq * 16 + ct * 8 + 2 * tq] = y[ct][0][0] + y[ct][1][0];
       zs[gq * 16 + ct * 8 + 2 * tq + 1] = y[ct][0][1] + y[ct][1][1];
     }
     __syncwarp();
-    double zv[4];
+    double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = lane + 32 * u;  // 128 outputs
-      const int r = e & 7, c = e >> 3;
-      double sacc = 0.0;
-      for (int l = 0; l <= c; ++l) sacc += zs[r * 16 + l] * Tm[l * 17 + c];
-      zv[u] = sacc;
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const double a = zs[gq * 16 + k4 * 4 + tq];
+#pragma unroll
+      for (int ct = 0; ct < 2; ++ct) dmma884(z[ct][0], z[ct][1], a, tf[k4][ct]);
     }
     __syncwarp();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = lane + 32 * u;
-      const int r = e & 7, c = e >> 3;
-      zs[c * CS8 + r] = zv[u];
+    for (int ct = 0; ct < 2; ++ct) {
+      zs[(ct * 8 + 2 * tq) * CS8 + gq] = z[ct][0];
+      zs[(ct * 8 + 2 * tq + 1) * CS8 + gq] = z[ct][1];
     }
     __syncwarp();
+    double zf[4];
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) zf[k4] = zs[(k4 * 4 + tq) * CS8 + gq];
     // ---- C -= Z V^T, block by block
     stage(r0, 0, 0);
-    for (int64_t b = 0; b < nblk; ++b) {
+    for (int b = 0; b < nblk; ++b) {
       if (!TWO && b > 0) stage(r0, b, 0);
       if (TWO && b + 1 < nblk) {
-        stage(r0, b + 1, int((b + 1) & 1));
+        stage(r0, b + 1, (b + 1) & 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      double* cs = wr + (TWO ? (b & 1) : 0) * (GW * CS8);
-      const int64_t jb = j0 + b * GW;
+      double* csb = wr + (TWO ? (b & 1) : 0) * (GW * CS8);
+      const double* pb = pvz + b * GW;
       double acc[4][2];
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
 #pragma unroll
-      for (int k4 = 0; k4 < BW / 4; ++k4) {
-        const double a = zs[(k4 * 4 + tq) * CS8 + gq];
+      for (int k4 = 0; k4 < BW / 4; ++k4)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          dmma884(acc[c][0], acc[c][1], a, pan2[(k4 * 4 + tq) * prs + jb + c * 8 + gq]);
-      }
+        for (int c = 0; c < 4; ++c) dmma884(acc[c][0], acc[c][1], zf[k4], pb[k4 * 4 * prs + c * 8]);
+      double* cw = csb + 2 * tq * CS8 + gq;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        cs[(c * 8 + 2 * tq) * CS8 + gq] -= acc[c][0];
-        cs[(c * 8 + 2 * tq + 1) * CS8 + gq] -= acc[c][1];
+        cw[c * 8 * CS8] -= acc[c][0];
+        cw[c * 8 * CS8 + CS8] -= acc[c][1];
       }
       __syncwarp();
+      const double* cr = csb + scol * CS8 + sr2;
+      double* aw = al + r0 + b * GW * ld;
+      const int lim = NP - j0 - b * GW - scol;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int qq = lane + 32 * i;
-        const int col = qq >> 2, r2 = (qq & 3) * 2;
-        if (jb + col < NP)
-          *reinterpret_cast<double2*>(A + r0 + r2 + (jb + col) * ld) =
-              *reinterpret_cast<const double2*>(cs + col * CS8 + r2);
-      }
+      for (int i = 0; i < 4; ++i)
+        if (8 * i < lim)
+          *reinterpret_cast<double2*>(aw + 8 * i * ld) = *reinterpret_cast<const double2*>(cr + 8 * i * CS8);
       __syncwarp();
     }
   }
@@ -2397,7 +2422,10 @@ struct Plan {
 
 int g_tune_inner = 1;
 int g_tune_sweeps = 60;
-int g_tune_mode = 1;  // 1 = bidiagonal values path when the panel fits, 0 = Jacobi only
+// 1 = bidiagonal values path when the panel fits, 0 = Jacobi only, 2 = bidiagonal
+// with the bulge-chase window in global memory, 3 = diagnostic: the values
+// pass stops after the reduce kernel (outputs undefined; for timing it alone)
+int g_tune_mode = 1;
 int g_stats_on = 0;
 
 int occupancy(const void* fn, int threads, size_t smem, int* per_sm) {
@@ -2643,6 +2671,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   if (pl.run_front) {
     svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
+    if (g_tune_mode == 3) return STARM_OK;
     if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(P);
     else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
