@@ -53,6 +53,9 @@ def parse():
                     help="slices in the CPU sample (0 = auto, ~10-20 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nt", type=int, default=DIMS[2], help="time steps (default 1024 = c2)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N>1: shard ONE c2 tensor over the ranks (fibre all-to-all, strong "
+                         "scaling) instead of N independent replicas")
     return ap.parse_args()
 
 
@@ -399,10 +402,99 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """One c2 tensor sharded over the ranks (paper_2605_16058_b200/sharded.py):
+    fibre-local DCT, all-to-all to slice ownership, per-rank values pass,
+    all-gathered sigma, replicated threshold, truncated factors."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"),
+                 ("WORLD_SIZE", "1")):
+        os.environ.setdefault(k, v)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    import paper_2605_16058_b200 as sb
+    from paper_2605_16058_b200 import _native as nat
+    from paper_2605_16058_b200.sharded import (DeviceOps, ShardPlan, reconstruct_sharded,
+                                               relative_error_sharded, scatter_fibres,
+                                               tsvdm_tolerance_sharded)
+    a = make_input(args.nt, seed=0)  # the same tensor on every rank
+    m, p, n = a.shape
+    in_bytes = a.size * 8
+    plan = ShardPlan(m, p, n, world, rank)
+    blk = scatter_fibres(a, plan).reshape(-1, order="F")
+    del a
+    pinned = torch.empty(blk.size, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = blk
+    x = pinned.to(dev)
+    ops = DeviceOps(sb.dct_matrix(n), dev)
+
+    def step(src):
+        return tsvdm_tolerance_sharded(src, plan, ops, EPS, dist)
+
+    for _ in range(max(args.warmup, 1)):
+        res = step(x)
+    torch.cuda.synchronize()
+    lib = nat.load()
+    lib.starm_launch_count_reset()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            res = step(x)
+        e1.record()
+        e1.synchronize()
+    launches = lib.starm_launch_count_reset() // max(args.steps, 1)
+    tt = torch.tensor([e0.elapsed_time(e1) / 1e3], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_dev = float(tt.item())
+    rec = reconstruct_sharded(res, plan, ops, dist)
+    realised = relative_error_sharded(x, rec, dist)
+    del rec
+    if not (realised < EPS and abs(realised - res.relative_error) <= 1e-8):
+        raise SystemExit(f"bench: invalid sharded result: {realised} vs {res.relative_error}")
+    # e2e: this rank's fibre block from pinned host memory every step
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = step(pinned.to(dev, non_blocking=True))
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": args.steps * in_bytes / t_dev / 1e9, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (configs.config2, seed 0, one tensor sharded over the ranks)",
+            "config": {"workload": "c2: 361x720x1024 f64, DCT-II over time, tolerance 1e-2, "
+                                   "fibre-sharded transform + all-to-all to slice ownership",
+                       "global_batch": 1, "seq_len": n, "parallelism": f"sharded x{world}"},
+            "e2e": {"value": args.steps * in_bytes / t_e2e / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 8 * (n + 3)},
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "result": {"total_rank": int(res.ranks.sum()), "relative_error": res.relative_error,
+                       "realised_error": realised},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.sharded:
+        run_sharded(args)
     else:
         run_ours(args)
 

@@ -1,10 +1,13 @@
 """Slice-wise thin SVDs on the B200 (reference slicesvd.py).
 
-All factorizations run in the batched one-sided Jacobi kernel
-(csrc/svd_f64.cu) through ``starm_svd_f64``; the reference's two threading
-strategies (``slices-parallel`` / ``svd-parallel``, slicesvd.py:65-77) are
-validated and then map to the same persistent grid.  Inputs are never
-modified: the kernel factors a private workspace copy of each slice.
+All factorizations run in the batched slice-SVD kernels (csrc/svd_f64.cu)
+through ``starm_svd_f64``: Householder QR + band reduction + bulge chasing
++ bisection/Laguerre for sigma, inverse iteration + back-transformation for
+vectors, and a blocked one-sided Jacobi kernel for slices too tall for the
+shared-memory panel.  The reference's two threading strategies
+(``slices-parallel`` / ``svd-parallel``, slicesvd.py:65-77) are validated
+and then map to the same persistent grids.  Inputs are never modified: the
+kernels factor a private workspace copy of each slice.
 """
 
 from __future__ import annotations
