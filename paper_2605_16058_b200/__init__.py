@@ -14,7 +14,7 @@ from .compress import (COMPUTE_EFFICIENT, MEMORY_EFFICIENT, METHOD_FIXED_RANK, M
                        TOLERANCE_STRATEGIES, TRUNCATE, CompressedTensor, StageClock,
                        ThresholdResult, TSVDMResult, compression_ratio, compute_threshold,
                        full_tsvdm, reconstruct, relative_error_device, starm_product,
-                       tsvdm_fixed_rank, tsvdm_tolerance)
+                       tsvdm_fixed_rank, tsvdm_tolerance, tsvdm_tolerance_stream)
 from .mode_product import (BATCHED, LOOP, PARFOR, TTMPlan, from_transform_domain,
                            to_transform_domain, ttm, ttm_inverse)
 from .slice_svd import (SLICES_PARALLEL, SVD_PARALLEL, DeviceFactors, SliceSVDSet,
@@ -37,5 +37,5 @@ __all__ = [
     "from_transform_domain", "full_tsvdm", "identity_transform", "linear_index", "multi_index",
     "orthonormality_residual", "reconstruct", "refold", "relative_error_device", "starm_product",
     "svd_all_slices", "svd_truncated_slices", "svd_values_only", "to_transform_domain",
-    "tsvdm_fixed_rank", "tsvdm_tolerance", "ttm", "ttm_inverse", "validate_transform",
+    "tsvdm_fixed_rank", "tsvdm_tolerance", "tsvdm_tolerance_stream", "ttm", "ttm_inverse", "validate_transform",
 ]

@@ -32,7 +32,8 @@ __all__ = [
     "TRUNCATE", "COMPUTE_EFFICIENT", "MEMORY_EFFICIENT", "TOLERANCE_STRATEGIES",
     "METHOD_FIXED_RANK", "METHOD_TOLERANCE", "StageClock", "ThresholdResult",
     "compute_threshold", "TSVDMResult", "CompressedTensor", "starm_product", "full_tsvdm",
-    "tsvdm_fixed_rank", "tsvdm_tolerance", "reconstruct", "compression_ratio",
+    "tsvdm_fixed_rank", "tsvdm_tolerance", "tsvdm_tolerance_stream", "reconstruct",
+    "compression_ratio",
     "threshold_device", "relative_error_device",
 ]
 
@@ -392,6 +393,54 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
         clock.mark("pack")
     tau, discarded, total, _ = summary
     return _finish(a, ts, factors, METHOD_TOLERANCE, epsilon, discarded, total, host)
+
+
+def tsvdm_tolerance_stream(tensors, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT,
+                           device=None):
+    """Compress a sequence of host tensors (DenseTensor, same transform set)
+    with ``tsvdm_tolerance``, yielding one host CompressedTensor per input in
+    order.  The host-to-device copy of tensor k+1 runs on a copy stream while
+    tensor k is compressed (two device input buffers, event-ordered reuse),
+    so for pinned inputs a stream of tensors costs ~max(copy, compute) per
+    tensor instead of copy + compute.  Results are identical to calling
+    ``tsvdm_tolerance`` on each tensor."""
+    import torch
+    dev = nat.require_cuda(device)
+    copy_stream = torch.cuda.Stream(dev)
+    bufs, ready, free, keep = [None, None], [None, None], [None, None], [None, None]
+
+    def issue(t, b):
+        if not isinstance(t, DenseTensor):
+            raise TypeError(f"expected DenseTensor inputs, got {type(t).__name__}")
+        ts.check_dims(t.dims)
+        src = torch.from_numpy(np.ascontiguousarray(t.data))
+        if bufs[b] is None or bufs[b].numel() != src.numel():
+            bufs[b] = torch.empty(src.numel(), dtype=torch.float64, device=dev)
+        with torch.cuda.stream(copy_stream):
+            if free[b] is not None:
+                copy_stream.wait_event(free[b])
+            bufs[b].copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        ready[b], keep[b] = ev, src
+
+    it = iter(tensors)
+    cur = next(it, None)
+    if cur is None:
+        return
+    issue(cur, 0)
+    b = 0
+    while cur is not None:
+        nxt = next(it, None)
+        if nxt is not None:
+            issue(nxt, 1 - b)  # overlaps the compression of ``cur``
+        torch.cuda.current_stream(dev).wait_event(ready[b])
+        c = tsvdm_tolerance(DeviceTensor(bufs[b], cur.dims), ts, epsilon, strategy)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        free[b] = ev
+        yield c.to_host()
+        cur, b = nxt, 1 - b
 
 
 def _state_fits(x) -> bool:

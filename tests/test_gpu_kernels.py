@@ -335,3 +335,18 @@ def test_full_tsvdm_lossless():
         ts = sb.TransformSet.build(dims, "dct")
         res = sb.full_tsvdm(t, ts)
         assert rel_error(a, res.reconstruct().array) <= 1e-11
+
+
+def test_tolerance_stream_equals_per_tensor_calls():
+    dims = (30, 44, 16)
+    ts = sb.TransformSet.build(dims, "dct")
+    hosts = [sb.DenseTensor(random_array(dims, 40 + k)) for k in range(3)]
+    got = list(sb.tsvdm_tolerance_stream(hosts, ts, 0.2))
+    assert len(got) == 3
+    for h, c in zip(hosts, got):
+        ref = sb.tsvdm_tolerance(h, ts, 0.2)
+        assert np.array_equal(c.ranks, ref.ranks)
+        assert np.array_equal(c.factors.u_data, ref.factors.u_data)
+        assert np.array_equal(c.factors.g_data, ref.factors.g_data)
+        assert c.discarded_energy == ref.discarded_energy and c.total_energy == ref.total_energy
+    assert list(sb.tsvdm_tolerance_stream([], ts, 0.2)) == []
