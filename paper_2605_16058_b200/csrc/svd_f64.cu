@@ -2075,19 +2075,11 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   }
 }
 
-// One warp per slice: (1) Gram-Schmidt twice of the k bidiagonal vectors in
-// order (a vanished vector is replaced by a canonical basis vector), then
-// (2) back-transformation v <- P1 P2 v: the logged bulge-chasing column
-// rotations in reverse order, then the band-reduction LQ reflectors
-// (I - V T V^T) from the last panel to the first.  Vectors are processed 32
-// at a time, one per lane, staged in shared memory.
-__global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* vm = reinterpret_cast<double*>(smem_raw);  // [P.btw][ls]
+// One warp per slice: Gram-Schmidt twice of the k bidiagonal vectors in
+// order (a vanished vector is replaced by a canonical basis vector).
+__global__ void __launch_bounds__(32) svd_orth_kernel(SvdParams P) {
   const int lane = threadIdx.x;
   const int64_t n = P.n, NP = P.NP, RP = P.RP;
-  const int64_t npan = NP / BW;
-  const int64_t ls = n | 1;  // odd lane stride: conflict-free column access
   for (;;) {
     int64_t it = 0;
     if (lane == 0) it = int64_t(atomicAdd(&P.counter[3], 1ull));
@@ -2098,7 +2090,6 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
     const int64_t slice = P.ids ? P.ids[it] : it;
     const int64_t k = kout_of(P, slice);
     double* Vb = P.vsel + si * RP * NP;
-    // ---- (1) orthonormalise the bidiagonal vectors (CGS2 with fallback)
     for (int64_t j = 0; j < k; ++j) {
       double* vj = Vb + j * RP;
       int64_t basis = 0;
@@ -2131,71 +2122,130 @@ __global__ void __launch_bounds__(32) svd_backtransform_kernel(SvdParams P) {
         __syncwarp();
       }
     }
-    // ---- (2) back-transformation, 32 vectors per pass
-    const int64_t kmax = hb_kmax(n);
+  }
+}
+
+// Back-transformation v <- P1 P2 v of one right vector per warp: the bulge
+// chase's right reflectors in reverse order, then the band reduction's LQ
+// panels (I - V T V^T) from the last to the first.  The tasks of one sweep
+// act on disjoint 16-column ranges, so lane k applies task k of the sweep
+// (sweeps in reverse, a __syncwarp between them; each lane's next record is
+// prefetched into registers during the current sweep); the LQ panels are
+// applied warp-cooperatively (lanes split the rows, butterfly-reduced
+// V^T x).  The vector lives in shared memory with a skewed index
+// (q + q / 16) so the lanes' 16-element ranges fall in distinct banks.
+constexpr int BT_WARPS = 4;
+__host__ __device__ __forceinline__ int64_t bt_stride(int64_t n) { return n + n / 16 + 48; }
+__device__ __forceinline__ int sx(int q) { return q + (q >> 4); }
+
+__global__ void __launch_bounds__(BT_WARPS * 32) svd_backtransform_kernel(SvdParams P, int64_t items) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = int(P.n);
+  const int64_t NP = P.NP, RP = P.RP;
+  const int npan = int(NP / BW);
+  const int64_t stride = bt_stride(n);
+  double* x = reinterpret_cast<double*>(smem_raw) + warp * stride;
+  const int64_t kmax = hb_kmax(n);
+  const int64_t nwarps = int64_t(gridDim.x) * BT_WARPS;
+  for (int64_t g = int64_t(blockIdx.x) * BT_WARPS + warp; g < items; g += nwarps) {
+    const int64_t it = g / n, j = g % n;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    if (j >= kout_of(P, slice)) continue;
+    double* vg = P.vsel + si * RP * NP + j * RP;
+    for (int q = lane; q < stride; q += 32) x[q] = 0.0;
+    __syncwarp();
+    for (int q = lane; q < n; q += 32) x[sx(q)] = vg[q];
+    __syncwarp();
+    // ---- bulge-chase reflectors, last sweep first; lane = task
     const double* lg = P.hhlog + si * P.hhcap;
-    const double* rv = P.rvlog + si * npan * (BW * NP + BW * BW);
-    for (int64_t j0 = 0; j0 < k; j0 += P.btw) {
-      const int64_t j = j0 + lane;
-      const bool act = lane < P.btw && j < k;
-      double* mine = vm + lane * ls;
-      if (act)
-        for (int64_t q = 0; q < n; ++q) mine[q] = Vb[j * RP + q];
+    double rec[BW], nxt[BW];
+#pragma unroll
+    for (int l = 0; l < BW; ++l) rec[l] = nxt[l] = 0.0;
+    if (n >= 3 && lane < hb_tasks(n, n - 3)) {
+      const double* h = lg + (int64_t(n - 3) * kmax + lane) * HLOG;
+#pragma unroll
+      for (int l = 0; l < BW; ++l) rec[l] = h[l];
+    }
+    for (int i = n - 3; i >= 0; --i) {
+      const int K = int(hb_tasks(n, i));
+      if (i > 0 && lane < hb_tasks(n, i - 1)) {
+        const double* h = lg + (int64_t(i - 1) * kmax + lane) * HLOG;
+#pragma unroll
+        for (int l = 0; l < BW; ++l) nxt[l] = h[l];
+      }
+      for (int kb = 0; kb < K; kb += 32) {  // tasks of one sweep are disjoint
+        const int k = kb + lane;
+        double r[BW];
+        if (kb == 0) {
+#pragma unroll
+          for (int l = 0; l < BW; ++l) r[l] = rec[l];
+        } else if (k < K) {
+          const double* h = lg + (int64_t(i) * kmax + k) * HLOG;
+#pragma unroll
+          for (int l = 0; l < BW; ++l) r[l] = h[l];
+        }
+        if (k < K && r[0] != 0.0) {
+          const int c0 = i + k * BW + 1;
+          const int base = sx(c0), b16 = BW - (c0 & 15);  // skew steps by one at l = b16
+          double xv[BW];
+#pragma unroll
+          for (int l = 0; l < BW; ++l) xv[l] = x[base + l + (l >= b16)];
+          double w0 = xv[0], w1 = 0.0;
+#pragma unroll
+          for (int l = 1; l < BW; l += 2) {
+            w1 = fma(r[l], xv[l], w1);
+            if (l + 1 < BW) w0 = fma(r[l + 1], xv[l + 1], w0);
+          }
+          const double w = (w0 + w1) * r[0];
+          x[base] = xv[0] - w;
+#pragma unroll
+          for (int l = 1; l < BW; ++l) x[base + l + (l >= b16)] = fma(-w, r[l], xv[l]);
+        }
+      }
       __syncwarp();
-      if (act) {
-        // bulge-chase right reflectors, last applied first: x <- H x
-        for (int64_t i = n - 3; i >= 0; --i) {
-          for (int64_t kk = hb_tasks(n, i) - 1; kk >= 0; --kk) {
-            const double* h = lg + (i * kmax + kk) * HLOG;
-            const double tau = h[0];
-            if (tau == 0.0) continue;
-            const int64_t c0 = i + kk * BW + 1;
-            const int L = int(n - c0 < BW ? n - c0 : BW);
-            double hv[BW];
 #pragma unroll
-            for (int l = 1; l < BW; ++l) hv[l] = h[l];
-            double w = mine[c0];
+      for (int l = 0; l < BW; ++l) rec[l] = nxt[l];
+    }
+    // ---- LQ panels of the band reduction, last first
+    const double* rv = P.rvlog + si * int64_t(npan) * (BW * NP + BW * BW);
+    for (int pk = npan - 2; pk >= 0; --pk) {
+      const double* Vp = rv + int64_t(pk) * (BW * NP + BW * BW);  // V[c][q], q < NP
+      const double* Tp = Vp + BW * NP;                              // T[a][b]
+      const int jlo = pk * BW + BW;
+      double y[BW];
 #pragma unroll
-            for (int l = 1; l < BW; ++l)
-              if (l < L) w = fma(hv[l], mine[c0 + l], w);
-            w *= tau;
-            mine[c0] -= w;
+      for (int c = 0; c < BW; ++c) y[c] = 0.0;
+      for (int q = jlo + lane; q < n; q += 32) {
+        const double xq = x[sx(q)];
 #pragma unroll
-            for (int l = 1; l < BW; ++l)
-              if (l < L) mine[c0 + l] = fma(-w, hv[l], mine[c0 + l]);
-          }
-        }
-        for (int64_t pk = npan - 2; pk >= 0; --pk) {
-          const double* Vp = rv + pk * (BW * NP + BW * BW);  // V[c][jj], jj < NP
-          const double* Tp = Vp + BW * NP;                     // T[a][b]
-          const int64_t jlo = pk * BW + BW;                    // V rows start at the LQ pivots
-          double y[BW];
+        for (int c = 0; c < BW; ++c) y[c] = fma(Vp[c * NP + q], xq, y[c]);
+      }
 #pragma unroll
-          for (int c = 0; c < BW; ++c) y[c] = 0.0;
-          for (int64_t q = jlo; q < n; ++q) {
-            const double x = mine[q];
+      for (int c = 0; c < BW; ++c) {
 #pragma unroll
-            for (int c = 0; c < BW; ++c) y[c] = fma(Vp[c * NP + q], x, y[c]);
-          }
-          double zz[BW];
+        for (int o = 16; o > 0; o >>= 1) y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
+      }
+      double zz[BW];
 #pragma unroll
-          for (int a = 0; a < BW; ++a) {
-            double acc = 0.0;
+      for (int a = 0; a < BW; ++a) {
+        double acc = 0.0;
 #pragma unroll
-            for (int b = 0; b < BW; ++b) acc = fma(Tp[a * BW + b], y[b], acc);
-            zz[a] = acc;
-          }
-          for (int64_t q = jlo; q < n; ++q) {
-            double acc = mine[q];
+        for (int b = 0; b < BW; ++b) acc = fma(Tp[a * BW + b], y[b], acc);
+        zz[a] = acc;
+      }
+      for (int q = jlo + lane; q < n; q += 32) {
+        double acc = x[sx(q)];
 #pragma unroll
-            for (int c = 0; c < BW; ++c) acc = fma(-Vp[c * NP + q], zz[c], acc);
-            mine[q] = acc;
-          }
-        }
-        for (int64_t q = 0; q < RP; ++q) Vb[j * RP + q] = q < n ? mine[q] : 0.0;
+        for (int c = 0; c < BW; ++c) acc = fma(-Vp[c * NP + q], zz[c], acc);
+        x[sx(q)] = acc;
       }
       __syncwarp();
     }
+    for (int q = lane; q < RP; q += 32) vg[q] = q < n ? x[sx(q)] : 0.0;
+    __syncwarp();
   }
 }
 
@@ -2499,13 +2549,11 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     if (rc) return rc;
     g.slots_v = clampc(int64_t(sms) * per);
     g.slots_j = g.slots_v;  // vecout uses the X slots
-    const int64_t ls = g.n | 1;
-    int64_t tw = int64_t(200 * 1024) / (ls * 8);
-    g.btw = int(tw > 32 ? 32 : (tw < 1 ? 1 : tw));
-    g.tsmem = size_t(g.btw) * ls * sizeof(double);
-    rc = occupancy((const void*)svd_backtransform_kernel, 32, g.tsmem, &per);
+    g.slots_t = clampc(int64_t(sms) * 8);  // CGS2 warps (one per slice)
+    g.tsmem = size_t(BT_WARPS) * bt_stride(g.n) * sizeof(double);
+    rc = occupancy((const void*)svd_backtransform_kernel, BT_WARPS * 32, g.tsmem, &per);
     if (rc) return rc;
-    g.slots_t = clampc(int64_t(sms) * per);
+    g.btw = per;  // back-transform CTAs per SM
     const int64_t work = count * g.n;
     g.ii_threads = int(work < int64_t(sms) * 128 ? work : int64_t(sms) * 128);
     g.ii_threads = int(round_up(g.ii_threads < 1 ? 1 : g.ii_threads, 128));  // whole blocks
@@ -2681,7 +2729,18 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   if (pl.run_vec) {
     svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n);
     STARM_LAUNCH_CHECK();
-    svd_backtransform_kernel<<<pl.slots_t, 32, pl.tsmem, st>>>(P);
+    svd_orth_kernel<<<pl.slots_t, 32, 0, st>>>(P);
+    STARM_LAUNCH_CHECK();
+    {
+      const int64_t items = count * pl.n;
+      int64_t blocks = (items + BT_WARPS - 1) / BT_WARPS;
+      int dev = 0, sms = 0;
+      STARM_CUDA_TRY(cudaGetDevice(&dev));
+      STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const int64_t cap = int64_t(sms) * pl.btw * 4;
+      if (blocks > cap) blocks = cap;
+      svd_backtransform_kernel<<<unsigned(blocks), BT_WARPS * 32, pl.tsmem, st>>>(P, items);
+    }
     STARM_LAUNCH_CHECK();
     svd_vecout_kernel<<<pl.slots_v, TPB, pl.jsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
