@@ -56,8 +56,8 @@ constexpr int CS_TILE = 1024;
 __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long long* vbits,
                                                            int64_t count, double eps, double* w,
                                                            double* v_out, ThState* st) {
-  __shared__ double tile[2][CS_TILE];
-  __shared__ double wt[2][CS_TILE];
+  __shared__ __align__(16) double tile[2][CS_TILE];
+  __shared__ __align__(16) double wt[2][CS_TILE];
   __shared__ double acc_sh;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* v = reinterpret_cast<const double*>(vbits);
@@ -84,29 +84,54 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
         if (t == 0) {
           acc = tl[0];
           wl[0] = acc;
-          k = 1;
-        }
-        double nx[8];
-        if (k + 8 <= len) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) nx[q] = tl[k + q];
-        }
-        for (; k + 8 <= len; k += 8) {
-          double cur[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) cur[q] = nx[q];
-          if (k + 16 <= len) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) nx[q] = tl[k + 8 + q];
+          for (k = 1; k < 8 && k < len; ++k) {
+            acc = __dadd_rn(acc, tl[k]);
+            wl[k] = acc;
           }
+        }
+        // two register banks of 8: loads of one bank overlap the other's
+        // dependent adds; running sums leave as 16-byte pairs
+        auto chain8 = [&](const double (&c)[8], int k0) {
           double w8[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            acc = __dadd_rn(acc, cur[q]);
+            acc = __dadd_rn(acc, c[q]);
             w8[q] = acc;
           }
 #pragma unroll
-          for (int q = 0; q < 8; ++q) wl[k + q] = w8[q];
+          for (int q = 0; q < 8; q += 2)
+            *reinterpret_cast<double2*>(wl + k0 + q) = make_double2(w8[q], w8[q + 1]);
+        };
+        double ra[8], rb[8];
+        if (k + 8 <= len) {
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(tl + k + q);
+            ra[q] = v2.x;
+            ra[q + 1] = v2.y;
+          }
+        }
+        for (; k + 16 <= len; k += 16) {
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(tl + k + 8 + q);
+            rb[q] = v2.x;
+            rb[q + 1] = v2.y;
+          }
+          chain8(ra, k);
+          if (k + 24 <= len) {
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+              const double2 v2 = *reinterpret_cast<const double2*>(tl + k + 16 + q);
+              ra[q] = v2.x;
+              ra[q + 1] = v2.y;
+            }
+          }
+          chain8(rb, k + 8);
+        }
+        if (k + 8 <= len) {
+          chain8(ra, k);
+          k += 8;
         }
         for (; k < len; ++k) {
           acc = __dadd_rn(acc, tl[k]);
@@ -114,13 +139,23 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
         }
       }
     } else {
-      if (t + 1 < ntiles) {  // prefetch the next tile
+      if (t + 1 < ntiles) {  // prefetch the next tile: all loads in flight at once
         const int len = tlen(t + 1);
         const int64_t base = (t + 1) * CS_TILE;
-        for (int k = lane; k < len; k += 32) {
-          const double x = v[base + k];
-          tile[b ^ 1][k] = x;
-          if (v_out) v_out[base + k] = x;
+        constexpr int PER = CS_TILE / 32;
+        double x[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          x[u] = k < len ? v[base + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          if (k < len) {
+            tile[b ^ 1][k] = x[u];
+            if (v_out) v_out[base + k] = x[u];
+          }
         }
       }
       if (t > 0) {  // running sums of the previous tile out
