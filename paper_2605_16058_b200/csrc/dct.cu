@@ -45,29 +45,55 @@ __global__ void dct_tables_kernel(cplx* tw, cplx* pw, int n) {
   }
 }
 
-// P complex sequences of length N = 2^LOGN in z[p * N + i], bit-reversed
-// input; radix-2 DIT stages (conjugate twiddles when INVERSE).
 // fibre pairs per CTA: 4 up to n = 1024, then shared memory limits it
 __host__ __device__ constexpr int dct_pairs(int logn) { return logn <= 10 ? 4 : (logn == 11 ? 2 : 1); }
 
+// P complex sequences of length N = 2^LOGN in z[p * N + i], bit-reversed
+// input; DIT stages fused in pairs (radix 4: 4 loads, 4 twiddle products,
+// 8 additions, 4 stores per item, one barrier per pair), plus one radix-2
+// stage first when LOGN is odd.  Conjugate twiddles when INVERSE.
 template <int LOGN, bool INVERSE>
 __device__ __forceinline__ void fft_stages(cplx* z, const cplx* tw) {
   constexpr int N = 1 << LOGN, H = N >> 1;
-  constexpr int half_total = dct_pairs(LOGN) * H;
-#pragma unroll 1
-  for (int s = 0; s < LOGN; ++s) {
-    const int h = 1 << s;
-    for (int q = threadIdx.x; q < half_total; q += blockDim.x) {
+  constexpr int P = dct_pairs(LOGN);
+  int s = 0;
+  if (LOGN & 1) {  // radix-2 stage with h = 1 (twiddle 1)
+    for (int q = threadIdx.x; q < P * H; q += blockDim.x) {
       const int p = q >> (LOGN - 1), qq = q & (H - 1);
+      cplx* zp = z + p * N + 2 * qq;
+      const cplx a = zp[0], b = zp[1];
+      zp[0] = {a.re + b.re, a.im + b.im};
+      zp[1] = {a.re - b.re, a.im - b.im};
+    }
+    __syncthreads();
+    s = 1;
+  }
+#pragma unroll 1
+  for (; s < LOGN; s += 2) {
+    const int h = 1 << s;
+    constexpr int Q = N >> 2;
+    for (int q = threadIdx.x; q < P * Q; q += blockDim.x) {
+      const int p = q >> (LOGN - 2), qq = q & (Q - 1);
       const int k = qq & (h - 1);
-      const int i0 = ((qq >> s) << (s + 1)) + k;
+      const int i0 = ((qq >> s) << (s + 2)) + k;
       cplx* zp = z + p * N;
-      cplx w = tw[k << (LOGN - 1 - s)];
-      if (INVERSE) w.im = -w.im;
-      const cplx a = zp[i0];
-      const cplx b = cmul(zp[i0 + h], w);
-      zp[i0] = {a.re + b.re, a.im + b.im};
-      zp[i0 + h] = {a.re - b.re, a.im - b.im};
+      cplx w1 = tw[k << (LOGN - 1 - s)];  // W_{2h}^k
+      cplx w2 = tw[k << (LOGN - 2 - s)];  // W_{4h}^k
+      if (INVERSE) {
+        w1.im = -w1.im;
+        w2.im = -w2.im;
+      }
+      // W_{4h}^{k+h} = W_{4h}^k * (-i) forward, * (+i) inverse
+      const cplx w3 = INVERSE ? cplx{-w2.im, w2.re} : cplx{w2.im, -w2.re};
+      const cplx a0 = zp[i0], a1 = cmul(zp[i0 + h], w1);
+      const cplx a2 = zp[i0 + 2 * h], a3 = cmul(zp[i0 + 3 * h], w1);
+      const cplx b0 = {a0.re + a1.re, a0.im + a1.im}, b1 = {a0.re - a1.re, a0.im - a1.im};
+      const cplx b2 = cmul(cplx{a2.re + a3.re, a2.im + a3.im}, w2);
+      const cplx b3 = cmul(cplx{a2.re - a3.re, a2.im - a3.im}, w3);
+      zp[i0] = {b0.re + b2.re, b0.im + b2.im};
+      zp[i0 + 2 * h] = {b0.re - b2.re, b0.im - b2.im};
+      zp[i0 + h] = {b1.re + b3.re, b1.im + b3.im};
+      zp[i0 + 3 * h] = {b1.re - b3.re, b1.im - b3.im};
     }
     __syncthreads();
   }
