@@ -132,12 +132,10 @@ size_t jacobi_smem_bytes(int ns) {
 
 struct __align__(16) QrSmemFixed {
   double t[BW * 17];
-  double sg[2][BW * 17];
+  double sg[4][BW * 17];  // per row-quarter partial Gram (NT / 128 used)
   double y[BW * GS];
   double z[GW * ZS];
-  double yr[RCH * 17];
-  double zr[BW * XS];
-  double red[TPB / 32][BW];
+  double red[16][BW];     // per-warp partials (NT / 32 used)
   double sums[BW];
   double wv[BW];
   double tau[BW];
@@ -464,6 +462,7 @@ __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, cons
 
 // Copy slice into X (LP x NP, ld LP), transposing when m < p; zero padding.
 // Returns flag: 0 ok, 1 all-zero, 2 non-finite.
+template <int NT>
 __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, double* __restrict__ X,
                           double* tile) {
   // Batched so that every thread keeps LB loads in flight (the copy is
@@ -474,17 +473,17 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
   int bad = 0, nonzero = 0;
   if (!P.transposed) {
     const int64_t total = LP * NP;
-    for (int64_t e0 = 0; e0 < total; e0 += int64_t(TPB) * LB) {
+    for (int64_t e0 = 0; e0 < total; e0 += int64_t(NT) * LB) {
       double v[LB];
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
-        const int64_t e = e0 + tid + int64_t(u) * TPB;
+        const int64_t e = e0 + tid + int64_t(u) * NT;
         const int64_t r = e % LP, c = e / LP;
         v[u] = (e < total && r < L && c < n) ? A[r + c * P.m] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
-        const int64_t e = e0 + tid + int64_t(u) * TPB;
+        const int64_t e = e0 + tid + int64_t(u) * NT;
         bad |= !isfinite(v[u]);
         nonzero |= (v[u] != 0.0);
         if (e < total) X[e] = v[u];
@@ -492,27 +491,28 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
     }
   } else {
     // 32 (columns of X) x 128 (rows of X) tiles through shared memory
+    constexpr int LT = 4096 / NT;
     for (int64_t c0 = 0; c0 < NP; c0 += 32) {
       for (int64_t r0 = 0; r0 < LP; r0 += 128) {
-        double v[LB];
+        double v[LT];
 #pragma unroll
-        for (int u = 0; u < LB; ++u) {
-          const int e = tid + u * TPB;
+        for (int u = 0; u < LT; ++u) {
+          const int e = tid + u * NT;
           const int cc = e & 31, rr = e >> 5;
           const int64_t c = c0 + cc, r = r0 + rr;
           v[u] = (r < L && c < n) ? A[c + r * P.m] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < LB; ++u) {
-          const int e = tid + u * TPB;
+        for (int u = 0; u < LT; ++u) {
+          const int e = tid + u * NT;
           bad |= !isfinite(v[u]);
           nonzero |= (v[u] != 0.0);
           tile[(e >> 5) * 33 + (e & 31)] = v[u];
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < LB; ++u) {
-          const int e = tid + u * TPB;
+        for (int u = 0; u < LT; ++u) {
+          const int e = tid + u * NT;
           const int rr = e & 127, cc = e >> 7;
           const int64_t c = c0 + cc, r = r0 + rr;
           if (c < NP && r < LP) X[r + c * LP] = tile[rr * 33 + cc];
@@ -536,8 +536,8 @@ __device__ __forceinline__ double& PAN(double* pan, int64_t prs, int c, int64_t 
 
 // Sum 16 per-thread partials over the CTA: butterfly inside each warp (16
 // shuffles leave lanes 2v, 2v+1 holding warp-sum v), then 8 warp partials.
-__device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[TPB / 32][BW],
-                                         double* out) {
+template <int NT>
+__device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[16][BW], double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double v8[8], v4[4], v2[2], v1;
   const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
@@ -570,7 +570,7 @@ __device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[TPB / 
   if (threadIdx.x < BW) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < TPB / 32; ++w) s += red[w][threadIdx.x];
+    for (int w = 0; w < NT / 32; ++w) s += red[w][threadIdx.x];
     out[threadIdx.x] = s;
   }
   __syncthreads();
@@ -579,6 +579,7 @@ __device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[TPB / 
 // Unblocked Householder on panel columns [0,16) of pan (rows k0.., ld prs):
 // LAPACK dlarfg/dlarf per column.  Leaves R (upper) in rows <= k0+j and v
 // below; tau in q.tau.
+template <int NT>
 __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t LP) {
   const int tid = threadIdx.x;
   for (int j = 0; j < BW; ++j) {
@@ -586,14 +587,14 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
     double acc[BW];
 #pragma unroll
     for (int c = 0; c < BW; ++c) acc[c] = 0.0;
-    for (int64_t r = pr + 1 + tid; r < LP; r += TPB) {
+    for (int64_t r = pr + 1 + tid; r < LP; r += NT) {
       const double x = PAN(pan, prs, j, r);
       acc[0] = fma(x, x, acc[0]);
 #pragma unroll
       for (int c = 1; c < BW; ++c)
         if (c > j) acc[c] = fma(x, PAN(pan, prs, c, r), acc[c]);
     }
-    reduce16(acc, q.red, q.sums);
+    reduce16<NT>(acc, q.red, q.sums);
     if (tid == 0) {
       const double alpha = PAN(pan, prs, j, pr);
       const double xn2 = q.sums[0];
@@ -611,7 +612,7 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
     __syncthreads();
     const double tau = q.tau[j], scal = q.scal[0], beta = q.scal[1];
     if (tau != 0.0) {
-      for (int64_t r = pr + tid; r < LP; r += TPB) {
+      for (int64_t r = pr + tid; r < LP; r += NT) {
         const double x = PAN(pan, prs, j, r);
         const double vr = (r == pr) ? 1.0 : x * scal;
         const double tv = tau * vr;
@@ -630,7 +631,7 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
 // the 16 reductions per column and the pivot row go through it.
 // The panel is read straight from global memory: element (r, c) =
 // src[r * sr + c * sc] for lo <= r < nrows, 0 otherwise (all loads in flight).
-template <int RPT>
+template <int NT, int RPT>
 __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
                                               int64_t nrows, const double* src, int64_t sr,
                                               int64_t sc, int64_t lo) {
@@ -642,7 +643,7 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
   double b[RPT][BW];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int64_t r = tid + i * TPB;
+    const int64_t r = tid + i * NT;
     const bool in = r >= lo && r < nrows;
 #pragma unroll
     for (int c = 0; c < BW; ++c) b[i][c] = in ? src[r * sr + c * sc] : 0.0;
@@ -656,7 +657,7 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
     for (int c = 0; c < BW; ++c) acc[c] = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int64_t r = tid + i * TPB;
+      const int64_t r = tid + i * NT;
       if (r == pr) {
 #pragma unroll
         for (int c = 0; c < BW; ++c) q.prow[par][c] = b[i][c];
@@ -668,7 +669,7 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
         for (int c = 1; c < BW; ++c) acc[c] = fma(x, b[i][c], acc[c]);
       }
     }
-    reduce16(acc, q.red, q.psum[par]);
+    reduce16<NT>(acc, q.red, q.psum[par]);
     // every thread derives the reflector (dlarfg) redundantly
     const double alpha = q.prow[par][0];
     const double xn2 = q.psum[par][0];
@@ -685,7 +686,7 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
       for (int c = 1; c < BW; ++c) tw[c] = tau * fma(scal, q.psum[par][c], q.prow[par][c]);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        const int64_t r = tid + i * TPB;
+        const int64_t r = tid + i * NT;
         if (r >= pr) {
           const double vr = (r == pr) ? 1.0 : b[i][0] * scal;
 #pragma unroll
@@ -696,7 +697,7 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
     }
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int64_t r = tid + i * TPB;
+      const int64_t r = tid + i * NT;
       if (r < nrows) pan[j * prs + r] = b[i][0];
 #pragma unroll
       for (int c = 0; c + 1 < BW; ++c) b[i][c] = b[i][c + 1];
@@ -706,26 +707,31 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
   __syncthreads();
 }
 
+template <int NT>
 __device__ void panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows,
                                  const double* src, int64_t sr, int64_t sc, int64_t lo) {
-  const int64_t rpt = (nrows + TPB - 1) / TPB;
+  const int64_t rpt = (nrows + NT - 1) / NT;
   switch (rpt) {
-    case 1: panel_factor_reg<1>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 2: panel_factor_reg<2>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 3: panel_factor_reg<3>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 4: panel_factor_reg<4>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 1: panel_factor_reg<NT, 1>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 2: panel_factor_reg<NT, 2>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 3: panel_factor_reg<NT, 3>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 4: panel_factor_reg<NT, 4>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
     default:
       for (int c = 0; c < BW; ++c)
-        for (int64_t r = threadIdx.x; r < prs; r += TPB)
+        for (int64_t r = threadIdx.x; r < prs; r += NT)
           pan[c * prs + r] = (r >= lo && r < nrows) ? src[r * sr + c * sc] : 0.0;
       __syncthreads();
-      panel_factor(q, pan, prs, k0, nrows);
+      panel_factor<NT>(q, pan, prs, k0, nrows);
       break;
   }
 }
 
 // S = V^T V (16x16) on DMMA; V = explicit panel (zeros above, 1 on pivots).
+// Warp w computes Gram tile (w & 3) over the rows of quarter w >> 2 (NT /
+// 128 quarters interleaved in 4-row groups).
+template <int NT>
 __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64_t kc, int64_t LP) {
+  constexpr int NH = NT / 128, STEP = 4 * NH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int tile = warp & 3, half = warp >> 2;
@@ -735,11 +741,11 @@ __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64
   const double* pb = pan + (tj * 8 + gq) * prs + tq;
   const int lp = int(LP);
   int r0 = int(kc) + half * 4;
-  for (; r0 + 24 < lp; r0 += 32) {  // four independent accumulators (constant indices)
+  for (; r0 + 3 * STEP < lp; r0 += 4 * STEP) {  // four independent accumulators
 #pragma unroll
-    for (int u = 0; u < 4; ++u) dmma884(d0[u], d1[u], pa[r0 + 8 * u], pb[r0 + 8 * u]);
+    for (int u = 0; u < 4; ++u) dmma884(d0[u], d1[u], pa[r0 + STEP * u], pb[r0 + STEP * u]);
   }
-  for (; r0 < lp; r0 += 8) dmma884(d0[0], d1[0], pa[r0], pb[r0]);
+  for (; r0 < lp; r0 += STEP) dmma884(d0[0], d1[0], pa[r0], pb[r0]);
   q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq] = (d0[0] + d0[1]) + (d0[2] + d0[3]);
   q.sg[half][(ti * 8 + gq) * 17 + tj * 8 + 2 * tq + 1] = (d1[0] + d1[1]) + (d1[2] + d1[3]);
   __syncthreads();
@@ -751,21 +757,16 @@ __device__ void panel_gram(QrSmemFixed& q, const double* pan, int64_t prs, int64
     q.t[i * 17 + i] = q.tau[i];
     for (int j = i + 1; j < BW; ++j) {
       double acc = 0.0;
-      for (int l = i; l < j; ++l) acc += q.t[i * 17 + l] * (q.sg[0][l * 17 + j] + q.sg[1][l * 17 + j]);
+      for (int l = i; l < j; ++l) {
+        double sg = q.sg[0][l * 17 + j];
+#pragma unroll
+        for (int h = 1; h < NH; ++h) sg += q.sg[h][l * 17 + j];
+        acc += q.t[i * 17 + l] * sg;
+      }
       q.t[i * 17 + j] = -q.tau[j] * acc;
     }
   }
   __syncthreads();
-}
-
-// cp.async multi-stage ring of 64 x 32 chunks (nst stages, runtime 2..4).
-__device__ __forceinline__ void cp_wait_dyn(int pending) {
-  switch (pending) {
-    case 0: cp_async_wait<0>(); break;
-    case 1: cp_async_wait<1>(); break;
-    case 2: cp_async_wait<2>(); break;
-    default: cp_async_wait<3>(); break;
-  }
 }
 
 struct Ring {
@@ -773,184 +774,6 @@ struct Ring {
   int nst;
   __device__ __forceinline__ double* buf(int64_t i) const { return base + (i % nst) * (GW * XS); }
 };
-
-// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
-// rows kc..nrows (multiple of RCH); V = explicit panel in shared memory.
-__device__ void trailing_update(QrSmemFixed& q, const Ring& ring, const double* pan, int64_t prs,
-                                double* X, int64_t ld, int64_t nrows, int64_t NP, int64_t kc,
-                                int64_t c0) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int64_t nch = (nrows - kc) / RCH;
-  const int nst = ring.nst;
-  // ---- Y = V^T C (16 x 32): warp -> tile (ti = warp>>2, tj = warp&3)
-  {
-    const int ti = warp >> 2, tj = warp & 3;
-    // four independent accumulator pairs break the DMMA dependency chain
-    double ya[4] = {0.0, 0.0, 0.0, 0.0}, yb[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int s = 0; s < nst - 1; ++s) {
-      if (s < nch) stage_cols(ring.buf(s), X, ld, kc + s * RCH, c0, NP);
-      else cp_async_commit();
-    }
-    for (int64_t ch = 0; ch < nch; ++ch) {
-      cp_wait_dyn(nst - 2);
-      __syncthreads();
-      const int64_t nx = ch + nst - 1;
-      if (nx < nch) stage_cols(ring.buf(nx), X, ld, kc + nx * RCH, c0, NP);
-      else cp_async_commit();
-      const double* cs = ring.buf(ch);
-      const int64_t r0 = kc + ch * RCH;
-      const double* va = pan + (ti * 8 + gq) * prs + r0 + tq;
-      const double* cb = cs + (tj * 8 + gq) * XS + tq;
-#pragma unroll
-      for (int k4 = 0; k4 < RCH / 4; ++k4) dmma884(ya[k4 & 3], yb[k4 & 3], va[k4 * 4], cb[k4 * 4]);
-    }
-    cp_async_wait<0>();
-    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq] = (ya[0] + ya[1]) + (ya[2] + ya[3]);
-    q.y[(ti * 8 + gq) * GS + tj * 8 + 2 * tq + 1] = (yb[0] + yb[1]) + (yb[2] + yb[3]);
-  }
-  __syncthreads();
-  // ---- Z = T^T Y (16 x 32), stored column-major (stride ZS) for B fragments
-  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
-    const int i = e & 15, c = e >> 4;
-    double acc = 0.0;
-    for (int l = 0; l <= i; ++l) acc += q.t[l * 17 + i] * q.y[l * GS + c];
-    q.z[c * ZS + i] = acc;
-  }
-  __syncthreads();
-  // ---- C -= V Z, streamed again
-  for (int s = 0; s < nst - 1; ++s) {
-    if (s < nch) stage_cols(ring.buf(s), X, ld, kc + s * RCH, c0, NP);
-    else cp_async_commit();
-  }
-  for (int64_t ch = 0; ch < nch; ++ch) {
-    cp_wait_dyn(nst - 2);
-    __syncthreads();
-    const int64_t nx = ch + nst - 1;
-    if (nx < nch) stage_cols(ring.buf(nx), X, ld, kc + nx * RCH, c0, NP);
-    else cp_async_commit();
-    double* cs = ring.buf(ch);
-    const int64_t r0 = kc + ch * RCH;
-    double acc[4][2];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < BW / 4; ++k4) {
-      const double a = pan[(k4 * 4 + tq) * prs + r0 + warp * 8 + gq];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        dmma884(acc[c][0], acc[c][1], a, q.z[(c * 8 + gq) * ZS + k4 * 4 + tq]);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      cs[(c * 8 + 2 * tq) * XS + warp * 8 + gq] -= acc[c][0];
-      cs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] -= acc[c][1];
-    }
-    __syncthreads();
-    store_cols(X, ld, r0, c0, NP, cs);
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-}
-
-// Store rows >= rmin of a staged 64 x 32 chunk (rmin even).
-__device__ __forceinline__ void store_cols_from(double* M, int64_t ld, int64_t r0, int64_t col0,
-                                                int64_t ncols, const double* buf, int64_t rmin) {
-#pragma unroll
-  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
-    const int c = threadIdx.x + q * TPB;
-    const int col = c >> 5;
-    const int r2 = (c & 31) * 2;
-    if (col0 + col < ncols && r0 + r2 >= rmin)
-      *reinterpret_cast<double2*>(M + r0 + r2 + (col0 + col) * ld) =
-          *reinterpret_cast<const double2*>(buf + col * XS + r2);
-  }
-}
-
-// LQ half-step update of the band reduction:  C <- C (I - V T V^T) for
-// columns [j0, NP) and rows [rmin, nrows) of A (ld), chunks starting at rc.
-// V[j][c] = pan2[c * prs + j] (explicit, zero outside [j0 + c, NP)).
-__device__ void right_update(QrSmemFixed& q, const Ring& ring, const double* pan2, int64_t prs,
-                             double* A, int64_t ld, int64_t nrows, int64_t NP, int64_t rc,
-                             int64_t rmin, int64_t j0) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int nst = ring.nst;
-  const int64_t nblk = (NP - j0 + GW - 1) / GW;
-  for (int64_t r0 = rc; r0 < nrows; r0 += RCH) {
-    // ---- Y = C V (64 x 16): warp -> row tile `warp`, column tiles 0..1
-    double y[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [ct][k4&1][e]
-    for (int s = 0; s < nst - 1; ++s) {
-      if (s < nblk) stage_cols(ring.buf(s), A, ld, r0, j0 + s * GW, NP);
-      else cp_async_commit();
-    }
-    for (int64_t b = 0; b < nblk; ++b) {
-      cp_wait_dyn(nst - 2);
-      __syncthreads();
-      const int64_t nx = b + nst - 1;
-      if (nx < nblk) stage_cols(ring.buf(nx), A, ld, r0, j0 + nx * GW, NP);
-      else cp_async_commit();
-      const double* cs = ring.buf(b);
-      const int64_t jb = j0 + b * GW;
-#pragma unroll
-      for (int k4 = 0; k4 < GW / 4; ++k4) {
-        const double a = cs[(k4 * 4 + tq) * XS + warp * 8 + gq];
-#pragma unroll
-        for (int ct = 0; ct < 2; ++ct)
-          dmma884(y[ct][k4 & 1][0], y[ct][k4 & 1][1], a,
-                  pan2[(ct * 8 + gq) * prs + jb + k4 * 4 + tq]);
-      }
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int ct = 0; ct < 2; ++ct) {
-      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq] = y[ct][0][0] + y[ct][1][0];
-      q.yr[(warp * 8 + gq) * 17 + ct * 8 + 2 * tq + 1] = y[ct][0][1] + y[ct][1][1];
-    }
-    __syncthreads();
-    // ---- Z = Y T (64 x 16), column-major (stride XS) for A fragments
-    for (int e = tid; e < RCH * BW; e += TPB) {
-      const int r = e & 63, c = e >> 6;
-      double acc = 0.0;
-      for (int l = 0; l <= c; ++l) acc += q.yr[r * 17 + l] * q.t[l * 17 + c];
-      q.zr[c * XS + r] = acc;
-    }
-    __syncthreads();
-    // ---- C -= Z V^T, column block by column block
-    for (int s = 0; s < nst - 1; ++s) {
-      if (s < nblk) stage_cols(ring.buf(s), A, ld, r0, j0 + s * GW, NP);
-      else cp_async_commit();
-    }
-    for (int64_t b = 0; b < nblk; ++b) {
-      cp_wait_dyn(nst - 2);
-      __syncthreads();
-      const int64_t nx = b + nst - 1;
-      if (nx < nblk) stage_cols(ring.buf(nx), A, ld, r0, j0 + nx * GW, NP);
-      else cp_async_commit();
-      double* cs = ring.buf(b);
-      const int64_t jb = j0 + b * GW;
-      double acc[4][2];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
-#pragma unroll
-      for (int k4 = 0; k4 < BW / 4; ++k4) {
-        const double a = q.zr[(k4 * 4 + tq) * XS + warp * 8 + gq];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          dmma884(acc[c][0], acc[c][1], a, pan2[(k4 * 4 + tq) * prs + jb + c * 8 + gq]);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        cs[(c * 8 + 2 * tq) * XS + warp * 8 + gq] -= acc[c][0];
-        cs[(c * 8 + 2 * tq + 1) * XS + warp * 8 + gq] -= acc[c][1];
-      }
-      __syncthreads();
-      store_cols_from(A, ld, r0, jb, NP, cs, rmin);
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------------
 // Warp-private streaming trailing updates (no CTA barrier per chunk).
@@ -965,12 +788,12 @@ constexpr int CS16 = 20;    // column stride of a staged 16-row chunk
 // rows [kc, nrows) in 16-row chunks dealt round-robin to the warps.
 // Index math is 32-bit with per-lane base pointers (a slice slot is < 2^31
 // elements), so the loops are DMMA / LDS / cp.async with few integer ops.
-template <bool TWO>
+template <int NT, bool TWO>
 __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs64,
                                   double* X, int64_t ld64, int64_t nrows64, int64_t NP64,
                                   int64_t kc64, int64_t c064) {
   constexpr int WR = TWO ? WREG : WREG1;
-  constexpr int NW = TPB / 32;
+  constexpr int NW = NT / 32;
   const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
   const int kc = int(kc64), c0 = int(c064);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1040,7 +863,7 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
       }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
+  for (int e = threadIdx.x; e < BW * GW; e += NT) {
     double sacc = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) sacc += wbase[w * WR + e];
@@ -1048,7 +871,7 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   }
   __syncthreads();
   // ---- Z = T^T Y (16 x 32), column-major (stride ZS) for B fragments
-  for (int e = threadIdx.x; e < BW * GW; e += TPB) {
+  for (int e = threadIdx.x; e < BW * GW; e += NT) {
     const int i = e & 15, c = e >> 4;
     double sacc = 0.0;
     for (int l = 0; l <= i; ++l) sacc += q.t[l * 17 + i] * q.y[l * GS + c];
@@ -1119,12 +942,12 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
 // DMMA) and C -= Z V^T never leave the warp.  V[j][c] = pan2[c * prs + j].
 constexpr int CS8 = 12;  // column stride of a staged 8-row tile
 
-template <bool TWO>
+template <int NT, bool TWO>
 __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2, int64_t prs64,
                                double* A, int64_t ld64, int64_t nrows64, int64_t NP64, int64_t rc64,
                                int64_t rmin64, int64_t j064) {
   constexpr int WR = TWO ? WREG : WREG1;
-  constexpr int NW = TPB / 32;
+  constexpr int NW = NT / 32;
   const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
   const int rc = int(rc64), rmin = int(rmin64), j0 = int(j064);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1247,10 +1070,11 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
 }
 
 // Panel -> explicit V (zeros above the pivot, 1 on it) for rows [0, prs).
+template <int NT>
 __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0, int64_t nrows) {
   for (int c = 0; c < BW; ++c) {
     double* col = pan + c * prs;
-    for (int64_t r = threadIdx.x; r < prs; r += TPB) {
+    for (int64_t r = threadIdx.x; r < prs; r += NT) {
       if (r < k0 + c || r >= nrows) col[r] = 0.0;
       else if (r == k0 + c) col[r] = 1.0;
     }
@@ -1264,7 +1088,8 @@ __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0,
 //   upper band (bandwidth 16) by alternating 16-column QR and 16-row LQ
 //   panels (compact-WY updates on DMMA, nst-stage cp.async ring) -> the 17
 //   diagonals of B to bandbuf.  Vector jobs also log P1's panels (V, T).
-__global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
   const int64_t LP = P.LP, NP = P.NP, RP = P.RP, n = P.n;
@@ -1285,7 +1110,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
-    const int flag = load_slice(P, P.A + slice * P.m * P.p, X, ring.buf(0));
+    const int flag = load_slice<NT>(P, P.A + slice * P.m * P.p, X, ring.buf(0));
     if (tid == 0) {
       P.flags[si] = flag;
       if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
@@ -1297,68 +1122,68 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     if (P.L > P.n) {
       for (int64_t k0 = 0; k0 < NP; k0 += BW) {
         const int64_t kc = (k0 / RCH) * RCH;
-        { long long _a = clock64(); panel_factor_any(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
+        { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
         if (tid < BW * BW) {
           const int c = tid / BW, r = tid % BW;
           if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
         }
         __syncthreads();
         if (k0 + BW < NP) {
-          explicit_v(pan, prs, k0, LP);
-          panel_gram(q, pan, prs, kc, LP);
+          explicit_v<NT>(pan, prs, k0, LP);
+          panel_gram<NT>(q, pan, prs, kc, LP);
           long long _a = clock64();
           for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
-            P.wtwo ? trailing_update_w<true>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0)
-                   : trailing_update_w<false>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
+            P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0)
+                   : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
           tr += clock64() - _a;
         }
         __syncthreads();
       }
       // keep only R (upper triangle of the leading NP x NP block)
       for (int64_t c = 0; c < NP; ++c)
-        for (int64_t r = c + 1 + tid; r < LP; r += TPB) X[r + c * LP] = 0.0;
+        for (int64_t r = c + 1 + tid; r < LP; r += NT) X[r + c * LP] = 0.0;
       __syncthreads();
     }
     long long t2 = clock64();
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
       const int64_t kc = (k / RCH) * RCH;
-      { long long _a = clock64(); panel_factor_any(q, pan, prs, k, RP, X + k * LP, 1, LP, 0); pf += clock64() - _a; }
+      { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k, RP, X + k * LP, 1, LP, 0); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;
         if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
       }
       __syncthreads();
       if (k + BW >= NP) break;
-      explicit_v(pan, prs, k, RP);
-      panel_gram(q, pan, prs, kc, RP);
+      explicit_v<NT>(pan, prs, k, RP);
+      panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
         for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
-          P.wtwo ? trailing_update_w<true>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0)
-                 : trailing_update_w<false>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
+          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0)
+                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
         tr += clock64() - _a;
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
-      { long long _a = clock64(); panel_factor_any(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
+      { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
       if (tid < BW * BW) {
         const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
         if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
       }
       __syncthreads();
-      explicit_v(pan, prs, j0, NP);
-      panel_gram(q, pan, prs, (j0 / 8) * 8, NP);
+      explicit_v<NT>(pan, prs, j0, NP);
+      panel_gram<NT>(q, pan, prs, (j0 / 8) * 8, NP);
       if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
         double* dst = P.rvlog + (si * (NP / BW) + k / BW) * (BW * NP + BW * BW);
         for (int c = 0; c < BW; ++c)
-          for (int64_t jj = tid; jj < NP; jj += TPB) dst[c * NP + jj] = pan[c * prs + jj];
+          for (int64_t jj = tid; jj < NP; jj += NT) dst[c * NP + jj] = pan[c * prs + jj];
         if (tid < BW * BW) dst[BW * NP + tid] = q.t[(tid / BW) * 17 + (tid % BW)];
       }
       {
         long long _a = clock64();
-        if (P.wtwo) right_update_w<true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
-        else right_update_w<false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        if (P.wtwo) right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        else right_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         ru += clock64() - _a;
       }
       __syncthreads();
@@ -1366,7 +1191,7 @@ __global__ void __launch_bounds__(TPB) svd_reduce_kernel(SvdParams P) {
     // ---------------- the 17 diagonals of the band
     double* band = P.bandbuf + si * (BW + 1) * NP;
     for (int d = 0; d <= BW; ++d)
-      for (int64_t i = tid; i < NP; i += TPB) band[d * NP + i] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
+      for (int64_t i = tid; i < NP; i += NT) band[d * NP + i] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
     __syncthreads();
     long long t3 = clock64();
     stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
@@ -2317,7 +2142,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
       ldt = RP;
       rows = RP;
     } else {
-      flag = load_slice(P, A, Xslot, sm.xs[0]);
+      flag = load_slice<TPB>(P, A, Xslot, sm.xs[0]);
       T = Xslot;
       ldt = LP;
       rows = LP;
@@ -2455,6 +2280,7 @@ struct Plan {
   int64_t L, n, LP, NP, RP;
   int job;                  // effective job after the fallback mapping
   bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, wtwo;
+  int reduce_nt;
   bool logs;                // right-side transformation logs (vector machinery buffers)
   bool run_front;           // reduce / bulge / bisect
   bool run_vec;             // inverse iteration / back-transform / output
@@ -2471,6 +2297,12 @@ struct Plan {
 };
 
 int g_tune_inner = 1;
+// reduce-kernel CTA size: 0 = automatic, else 256 or 512 (env STARM_REDUCE_THREADS)
+int g_reduce_threads = [] {
+  const char* e = getenv("STARM_REDUCE_THREADS");
+  const int v = e ? atoi(e) : 256;
+  return (v == 0 || v == 256 || v == 512) ? v : 256;
+}();
 int g_tune_sweeps = 60;
 // 1 = bidiagonal values path when the panel fits, 0 = Jacobi only, 2 = bidiagonal
 // with the bulge-chase window in global memory, 3 = diagnostic: the values
@@ -2502,15 +2334,21 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
     const size_t ring = size_t(GW) * XS * sizeof(double);
     g.qr_stages = 2;
-    size_t extra = size_t(g.qr_stages) * ring;
-    const size_t wreg = size_t(TPB / 32) * WREG * sizeof(double);
-    const size_t wreg1 = size_t(TPB / 32) * WREG1 * sizeof(double);
-    // two-stage warp rings when they fit next to the panel, else one stage
-    g.wtwo = fixed + (wreg > extra ? wreg : extra) <= size_t(227 * 1024);
-    const size_t w = g.wtwo ? wreg : wreg1;
-    if (w > extra) extra = w;
-    g.rsmem = fixed + extra;
-    if (g.rsmem > size_t(227 * 1024)) g.bidiag = false;  // panel does not fit: Jacobi path
+    auto smem_for = [&](int nt, bool two) {
+      size_t extra = size_t(g.qr_stages) * ring;
+      const size_t w = size_t(nt / 32) * (two ? WREG : WREG1) * sizeof(double);
+      return fixed + (w > extra ? w : extra);
+    };
+    const size_t cap = size_t(227 * 1024);
+    // 16 warps (single-stage rings) when they fit next to the panel, else 8
+    // warps with two-stage rings when those fit, else one stage
+    int nt = g_reduce_threads;
+    if (nt == 0) nt = smem_for(512, false) <= cap ? 512 : 256;
+    if (nt == 512 && smem_for(512, false) > cap) nt = 256;
+    g.reduce_nt = nt;
+    g.wtwo = smem_for(nt, true) <= cap;
+    g.rsmem = smem_for(nt, g.wtwo);
+    if (g.rsmem > cap) g.bidiag = false;  // panel does not fit: Jacobi path
   }
   // Without the bidiagonal path the state-keeping jobs degrade to the plain
   // ones (the Jacobi kernel recomputes).
@@ -2560,7 +2398,8 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.hhcap = (g.n >= 3 ? (g.n - 2) : 1) * hb_kmax(g.n) * HLOG;
   }
   if (g.bidiag) {
-    rc = occupancy((const void*)svd_reduce_kernel, TPB, g.rsmem, &per);
+    rc = g.reduce_nt == 512 ? occupancy((const void*)svd_reduce_kernel<512>, 512, g.rsmem, &per)
+                            : occupancy((const void*)svd_reduce_kernel<256>, 256, g.rsmem, &per);
     if (rc) return rc;
     g.slots_r = clampc(int64_t(sms) * per);
     rc = occupancy(g.hb_gmem ? (const void*)svd_bulge_kernel<true> : (const void*)svd_bulge_kernel<false>,
@@ -2717,7 +2556,8 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     P.btw = pl.btw;
   }
   if (pl.run_front) {
-    svd_reduce_kernel<<<pl.slots_r, TPB, pl.rsmem, st>>>(P);
+    if (pl.reduce_nt == 512) svd_reduce_kernel<512><<<pl.slots_r, 512, pl.rsmem, st>>>(P);
+    else svd_reduce_kernel<256><<<pl.slots_r, 256, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     if (g_tune_mode == 3) return STARM_OK;
     if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(P);

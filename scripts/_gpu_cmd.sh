@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "dct or ttm or tolerance" 2>&1 | tail -3
-timeout 300 python scripts/run_step.py > gpurun_out/rs.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/run_step.py > /dev/null 2>&1; cat gpurun_out/rs.log
+STARM_REDUCE_THREADS=512 timeout 900 python -m pytest tests/test_gpu_kernels.py -m gpu -x -q 2>&1 | tail -2
+STARM_REDUCE_THREADS=256 timeout 300 python scripts/time_reduce.py 2>&1 | tail -1
+STARM_REDUCE_THREADS=512 timeout 300 python scripts/time_reduce.py 2>&1 | tail -1
+STARM_REDUCE_THREADS=512 timeout 300 python scripts/run_step.py 2>&1 | tail -1
