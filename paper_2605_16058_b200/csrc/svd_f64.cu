@@ -784,153 +784,172 @@ constexpr int WREG = 1280;  // doubles per warp (two-stage ring)
 constexpr int WREG1 = 640;  // single-stage variant for panels too tall for WREG
 constexpr int CS16 = 20;    // column stride of a staged 16-row chunk
 
-// C <- (I - V T^T V^T) C for columns [c0, c0+32) of X (ld, NP columns),
-// rows [kc, nrows) in 16-row chunks dealt round-robin to the warps.
-// Index math is 32-bit with per-lane base pointers (a slice slot is < 2^31
-// elements), so the loops are DMMA / LDS / cp.async with few integer ops.
+// C <- (I - V T^T V^T) C for all columns [c_start, NP) of X (ld), 32-column
+// blocks in turn, rows [kc, nrows) in 16-row chunks dealt round-robin to the
+// warps.  Per block: Y = V^T C (pass 1), a cross-warp sum and Z = T^T Y, then
+// C -= V Z (pass 2).  Each warp walks one flat sequence of chunk loads
+// (block, pass, chunk) through its cp.async ring, so the first chunk of
+// pass 2 and of the next block are already in flight during the barriers of
+// the reduction.  Index math is 32-bit with per-lane base pointers.
 template <int NT, bool TWO>
 __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* pan, int64_t prs64,
                                   double* X, int64_t ld64, int64_t nrows64, int64_t NP64,
-                                  int64_t kc64, int64_t c064) {
+                                  int64_t kc64, int64_t cs64) {
   constexpr int WR = TWO ? WREG : WREG1;
   constexpr int NW = NT / 32;
   const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
-  const int kc = int(kc64), c0 = int(c064);
+  const int kc = int(kc64), c_start = int(cs64);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   double* wr = wbase + warp * WR;  // [TWO ? 2 : 1][32 * CS16]
   const int nck = (nrows - kc) / 16;
+  const int my = nck > warp ? (nck - warp + NW - 1) / NW : 0;  // chunks of this warp per pass
+  const int nb = (NP - c_start + GW - 1) / GW;
+  const int total = nb * 2 * my;
   // staging: lane copies rows (sr2, sr2 + 1) of columns scol + 4 i, i < 8
   const int scol = lane >> 3, sr2 = (lane & 7) * 2;
-  double* xl = X + (c0 + scol) * ld + kc + sr2;  // + 16 ck + 4 i ld
-  const int nin = (NP - c0 - scol + 3) >> 2;     // columns scol + 4 i < NP - c0  <=>  i < nin
-  auto stage = [&](int ck, int b) {
-    double* dst = wr + b * (GW * CS16) + scol * CS16 + sr2;
-    const double* srcp = xl + ck * 16;
+  auto slot_of = [&](int sq) { return TWO ? (sq & 1) : 0; };
+  auto issue = [&](int sq) {
+    const int b = sq / (2 * my), i = (sq % (2 * my)) % my;
+    const int c0 = c_start + b * GW;
+    const int nin = (NP - c0 - scol + 3) >> 2;
+    double* dst = wr + slot_of(sq) * (GW * CS16) + scol * CS16 + sr2;
+    const double* srcp = X + (c0 + scol) * ld + kc + sr2 + (warp + i * NW) * 16;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const bool in = i < nin;
-      cp_async16(dst + 4 * i * CS16, in ? srcp + 4 * i * ld : X, in ? 16 : 0);
+    for (int u = 0; u < 8; ++u) {
+      const bool in = u < nin;
+      cp_async16(dst + 4 * u * CS16, in ? srcp + 4 * u * ld : X, in ? 16 : 0);
     }
     cp_async_commit();
   };
-  // A fragments of V^T: V[r][a*8+gq] = pan[(a*8+gq) prs + r]
-  const double* pa0 = pan + gq * prs + kc + tq;
+  // before computing step sq: (two-stage) put sq + 1 in flight, wait for sq
+  auto begin = [&](int sq) {
+    if (TWO && sq + 1 < total) {
+      issue(sq + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+  };
+  // after computing step sq: (one stage) the slot is free, load sq + 1 --
+  // except after the last chunk of pass 1, whose slot takes the partial Y
+  auto end = [&](int sq) {
+    __syncwarp();
+    if (!TWO && sq + 1 < total && (sq % (2 * my)) != my - 1) issue(sq + 1);
+  };
+  // slot holding warp w's partial Y after pass 1 of block b: the slot of its
+  // last pass-1 chunk (free; the two-stage prefetch went to the other one)
+  auto part_off = [&](int w, int b) {
+    const int myw = nck > w ? (nck - w + NW - 1) / NW : 0;
+    return myw ? slot_of(b * 2 * myw + myw - 1) * (GW * CS16) : 0;
+  };
+  const double* pa0 = pan + gq * prs + kc + tq;  // A fragments of V^T
   const double* pa1 = pa0 + 8 * prs;
-  // ---- Y = V^T C  (16 x 32): every warp accumulates all 8 tiles over its chunks
-  double y[2][4][2];
+  const double* pv = pan + tq * prs + kc + gq;   // A fragments of V
+  const double* zb = q.z + gq * ZS + tq;
+  if (total > 0) issue(0);
+  for (int b = 0; b < nb; ++b) {
+    const int c0 = c_start + b * GW;
+    // ---- pass 1: Y = V^T C (16 x 32), all 8 tiles per warp over its chunks
+    double y[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) y[a][b][0] = y[a][b][1] = 0.0;
-  int ck = warp;
-  if (ck < nck) stage(ck, 0);
-  for (int it = 0; ck < nck; ck += NW, ++it) {
-    const int nx = ck + NW;
-    if (!TWO && it > 0) stage(ck, 0);
-    if (TWO && nx < nck) {
-      stage(nx, (it + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+      for (int t = 0; t < 4; ++t) y[a][t][0] = y[a][t][1] = 0.0;
+    for (int i = 0; i < my; ++i) {
+      const int sq = b * 2 * my + i;
+      begin(sq);
+      const double* cs = wr + slot_of(sq) * (GW * CS16) + gq * CS16 + tq;
+      const int ro = (warp + i * NW) * 16;
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        double av[2], bv[4];
+        av[0] = pa0[ro + k4 * 4];
+        av[1] = pa1[ro + k4 * 4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bv[t] = cs[t * 8 * CS16 + k4 * 4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dmma884(y[a][t][0], y[a][t][1], av[a], bv[t]);
+      }
+      end(sq);
     }
-    __syncwarp();
-    const double* cs = wr + (TWO ? (it & 1) : 0) * (GW * CS16) + gq * CS16 + tq;
-    const int ro = ck * 16;
-#pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4) {
-      double av[2], bv[4];
-      av[0] = pa0[ro + k4 * 4];
-      av[1] = pa1[ro + k4 * 4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = cs[b * 8 * CS16 + k4 * 4];
+    // ---- deterministic cross-warp sum (fixed warp order) into q.y
+    {
+      double* part = wr + part_off(warp, b) + gq * GW + 2 * tq;
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(y[a][b][0], y[a][b][1], av[a], bv[b]);
+        for (int t = 0; t < 4; ++t) {
+          part[a * 8 * GW + t * 8] = y[a][t][0];
+          part[a * 8 * GW + t * 8 + 1] = y[a][t][1];
+        }
     }
-    __syncwarp();
-  }
-  // ---- deterministic cross-warp sum (fixed warp order) into q.y
-  {
-    double* part = wr + gq * GW + 2 * tq;  // 16 x 32 row-major partial of this warp
+    __syncthreads();
+    for (int e = threadIdx.x; e < BW * GW; e += NT) {
+      double sacc = 0.0;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        part[a * 8 * GW + b * 8] = y[a][b][0];
-        part[a * 8 * GW + b * 8 + 1] = y[a][b][1];
-      }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < BW * GW; e += NT) {
-    double sacc = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) sacc += wbase[w * WR + e];
-    q.y[(e / GW) * GS + (e % GW)] = sacc;
-  }
-  __syncthreads();
-  // ---- Z = T^T Y (16 x 32), column-major (stride ZS) for B fragments
-  for (int e = threadIdx.x; e < BW * GW; e += NT) {
-    const int i = e & 15, c = e >> 4;
-    double sacc = 0.0;
-    for (int l = 0; l <= i; ++l) sacc += q.t[l * 17 + i] * q.y[l * GS + c];
-    q.z[c * ZS + i] = sacc;
-  }
-  __syncthreads();
-  // ---- C -= V Z per chunk, warp-private.  A fragments V[r0+a*8+gq][k4*4+tq]
-  const double* pv = pan + tq * prs + kc + gq;  // + k4*4 prs + ro + a*8
-  const double* zb = q.z + gq * ZS + tq;         // + b*8 ZS + k4*4
-  double zf[4][4];                                // B fragments of Z, loop-invariant
-#pragma unroll
-  for (int k4 = 0; k4 < 4; ++k4)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) zf[k4][b] = zb[b * 8 * ZS + k4 * 4];
-  ck = warp;
-  if (ck < nck) stage(ck, 0);
-  for (int it = 0; ck < nck; ck += NW, ++it) {
-    const int nx = ck + NW;
-    if (!TWO && it > 0) stage(ck, 0);
-    if (TWO && nx < nck) {
-      stage(nx, (it + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+      for (int w = 0; w < NW; ++w) sacc += wbase[w * WR + part_off(w, b) + e];
+      q.y[(e / GW) * GS + (e % GW)] = sacc;
     }
-    __syncwarp();
-    double* csb = wr + (TWO ? (it & 1) : 0) * (GW * CS16);
-    const int ro = ck * 16;
-    double acc[2][4][2];
+    __syncthreads();
+    if (!TWO && my > 0) issue(b * 2 * my + my);  // first chunk of pass 2
+    // ---- Z = T^T Y (16 x 32), column-major (stride ZS) for B fragments
+    for (int e = threadIdx.x; e < BW * GW; e += NT) {
+      const int ii = e & 15, c = e >> 4;
+      double sacc = 0.0;
+      for (int l = 0; l <= ii; ++l) sacc += q.t[l * 17 + ii] * q.y[l * GS + c];
+      q.z[c * ZS + ii] = sacc;
+    }
+    __syncthreads();
+    double zf[4][4];  // B fragments of Z
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int k4 = 0; k4 < 4; ++k4)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < BW / 4; ++k4) {
-      double av[2];
-#pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = pv[k4 * 4 * prs + ro + a * 8];
+      for (int t = 0; t < 4; ++t) zf[k4][t] = zb[t * 8 * ZS + k4 * 4];
+    // ---- pass 2: C -= V Z per chunk
+    const int nin = (NP - c0 - scol + 3) >> 2;
+    double* xl = X + (c0 + scol) * ld + kc + sr2;
+    for (int i = 0; i < my; ++i) {
+      const int sq = b * 2 * my + my + i;
+      begin(sq);
+      double* csb = wr + slot_of(sq) * (GW * CS16);
+      const int ro = (warp + i * NW) * 16;
+      double acc[2][4][2];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], zf[k4][b]);
-    }
-    double* cw = csb + 2 * tq * CS16 + gq;
+        for (int t = 0; t < 4; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+      for (int k4 = 0; k4 < BW / 4; ++k4) {
+        double av[2];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        cw[b * 8 * CS16 + a * 8] -= acc[a][b][0];
-        cw[b * 8 * CS16 + CS16 + a * 8] -= acc[a][b][1];
+        for (int a = 0; a < 2; ++a) av[a] = pv[k4 * 4 * prs + ro + a * 8];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dmma884(acc[a][t][0], acc[a][t][1], av[a], zf[k4][t]);
       }
-    __syncwarp();
-    const double* cr = csb + scol * CS16 + sr2;
-    double* xw = xl + ro;
+      double* cw = csb + 2 * tq * CS16 + gq;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nin)
-        *reinterpret_cast<double2*>(xw + 4 * i * ld) = *reinterpret_cast<const double2*>(cr + 4 * i * CS16);
-    __syncwarp();
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          cw[t * 8 * CS16 + a * 8] -= acc[a][t][0];
+          cw[t * 8 * CS16 + CS16 + a * 8] -= acc[a][t][1];
+        }
+      __syncwarp();
+      const double* cr = csb + scol * CS16 + sr2;
+      double* xw = xl + ro;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < nin)
+          *reinterpret_cast<double2*>(xw + 4 * u * ld) = *reinterpret_cast<const double2*>(cr + 4 * u * CS16);
+      end(sq);
+    }
+    __syncthreads();  // q.z is rewritten by the next block
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -1132,9 +1151,8 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
           explicit_v<NT>(pan, prs, k0, LP);
           panel_gram<NT>(q, pan, prs, kc, LP);
           long long _a = clock64();
-          for (int64_t c0 = k0 + BW; c0 < NP; c0 += GW)
-            P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0)
-                   : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, c0);
+          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
+                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
           tr += clock64() - _a;
         }
         __syncthreads();
@@ -1159,9 +1177,8 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
       panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
-        for (int64_t c0 = k + BW; c0 < NP; c0 += GW)
-          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0)
-                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, c0);
+        P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
+               : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
         tr += clock64() - _a;
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)

@@ -1,4 +1,4 @@
-STARM_REDUCE_THREADS=512 timeout 900 python -m pytest tests/test_gpu_kernels.py -m gpu -x -q 2>&1 | tail -2
-STARM_REDUCE_THREADS=256 timeout 300 python scripts/time_reduce.py 2>&1 | tail -1
-STARM_REDUCE_THREADS=512 timeout 300 python scripts/time_reduce.py 2>&1 | tail -1
-STARM_REDUCE_THREADS=512 timeout 300 python scripts/run_step.py 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_kernels.py -m gpu -x -q 2>&1 | tail -2
+timeout 300 python scripts/time_reduce.py 2>&1 | tail -1
+timeout 300 python scripts/probe_reduce.py 2>&1 | tail -1
+timeout 300 python scripts/run_step.py 2>&1 | tail -1
