@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native as nat
 from .mode_product import BATCHED, VARIANTS, forward_device, inverse_device
-from .slice_svd import (SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
+from .slice_svd import (check_status, SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
                         VariableRankFactors, pack_offsets_device, svd_full_device,
                         svd_truncated_device, svd_values_device)
 from .tensors import DenseTensor, DeviceTensor, as_device
@@ -379,16 +379,20 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
         # fits comfortably (always for compute-efficient); otherwise refactor
         # the rank>0 slices (memory-efficient in the reference's sense).
         keep = strategy == COMPUTE_EFFICIENT or _state_fits(ahat3)
+        pending = []  # device status pairs, read back with the next D2H
         with clock.stage("stage1-svd"):
             if keep:
-                s, state = svd_values_device(ahat3, keep_state=True)
+                s, state = svd_values_device(ahat3, keep_state=True, defer=pending)
             else:
-                s, state = svd_values_device(ahat3), None
+                s, state = svd_values_device(ahat3, defer=pending), None
         with clock.stage("threshold"):
             ranks, scal, j, _, _ = threshold_device(s, r, n, epsilon)
-            summary = _summary(ranks, scal)
+            summary = _summary(ranks, scal, pending)
+        pending = []
         with clock.stage("stage2-svd"):
-            factors, _ = svd_truncated_device(ahat3, ranks, summary[3], state=state)
+            factors, _ = svd_truncated_device(ahat3, ranks, summary[3], state=state, defer=pending)
+            if pending:
+                check_status(torch.cat(pending).cpu().numpy())
         del state
         clock.mark("pack")
     tau, discarded, total, _ = summary
@@ -448,14 +452,19 @@ def _state_fits(x) -> bool:
     import torch
     from .slice_svd import state_bytes
     free, _ = torch.cuda.mem_get_info(x.device)
+    free += torch.cuda.memory_reserved(x.device) - torch.cuda.memory_allocated(x.device)
     return state_bytes(x) < free // 4
 
 
-def _summary(ranks, scal):
-    """One small D2H: (tau, discarded, total, sum of ranks)."""
+def _summary(ranks, scal, pending=()):
+    """One small D2H: (tau, discarded, total, sum of ranks) plus any deferred
+    SVD status pairs, which are checked here."""
     import torch
-    packed = torch.cat([scal, ranks.sum().reshape(1).to(torch.float64)])
-    h = packed.cpu().numpy()
+    parts = [scal, ranks.sum().reshape(1).to(torch.float64)]
+    parts += [st.to(torch.float64) for st in pending]
+    h = torch.cat(parts).cpu().numpy()
+    if pending:
+        check_status(h[4:].astype(np.int64))
     return float(h[0]), float(h[1]), float(h[2]), int(h[3])
 
 

@@ -161,11 +161,14 @@ def _raise_slice_status(status_host, what):
 
 
 def _svd_launch(x: DeviceTensor, job, ids=None, s=None, u=None, v=None, ranks=None, u_off=None,
-                g_off=None, u_data=None, g_data=None, ws=None):
+                g_off=None, u_data=None, g_data=None, ws=None, defer=None):
     """One call of starm_svd_f64 over ``ids`` (device int64, or None for every
     slice).  Returns the workspace (which carries the per-slice state after a
     VALUES_STATE job).  Work is scheduled on persistent grids; the scratch is
-    per resident CTA except for the per-slice factorisation state."""
+    per resident CTA except for the per-slice factorisation state.  With a
+    ``defer`` list the device status pair is appended to it instead of being
+    read back here (the caller checks it with ``check_status`` at its next
+    synchronisation point, before any result is returned)."""
     import torch
     m, p, r, n = _geometry(x)
     dev = x.device
@@ -183,8 +186,17 @@ def _svd_launch(x: DeviceTensor, job, ids=None, s=None, u=None, v=None, ranks=No
              nat.ptr(u), nat.ptr(v), nat.ptr(ranks), nat.ptr(u_off), nat.ptr(g_off),
              nat.ptr(u_data), nat.ptr(g_data), status.data_ptr(), ws.data_ptr(), ws.numel(),
              nat.stream_ptr(dev))
-    _raise_slice_status(status.cpu().numpy(), "slice SVD")
+    if defer is not None:
+        defer.append(status)
+    else:
+        _raise_slice_status(status.cpu().numpy(), "slice SVD")
     return ws
+
+
+def check_status(statuses_host):
+    """Raise for the first failing deferred status pair (host int values)."""
+    for i in range(0, len(statuses_host), 2):
+        _raise_slice_status(statuses_host[i:i + 2], "slice SVD")
 
 
 class SvdState:
@@ -202,16 +214,16 @@ def state_bytes(x: DeviceTensor) -> int:
     return int(nat.load().starm_svd_workspace_bytes(m, p, n, n, nat.SVD_VALUES_STATE))
 
 
-def svd_values_device(x: DeviceTensor, keep_state=False):
+def svd_values_device(x: DeviceTensor, keep_state=False, defer=None):
     """(r, N) singular values as a column-major torch tensor (flat r*N); with
     ``keep_state`` also returns the SvdState for svd_truncated_device."""
     import torch
     m, p, r, n = _geometry(x)
     s = torch.empty(r * n, dtype=torch.float64, device=x.device)
     if keep_state:
-        ws = _svd_launch(x, nat.SVD_VALUES_STATE, s=s)
+        ws = _svd_launch(x, nat.SVD_VALUES_STATE, s=s, defer=defer)
         return s, SvdState(ws, s)
-    _svd_launch(x, nat.SVD_VALUES, s=s)
+    _svd_launch(x, nat.SVD_VALUES, s=s, defer=defer)
     return s
 
 
@@ -236,7 +248,7 @@ def pack_offsets_device(ranks_dev, m, p):
 
 
 def svd_truncated_device(x: DeviceTensor, ranks_dev, total_rank, ids=None, keep_values=False,
-                         state=None):
+                         state=None, defer=None):
     """Packed leading-rank factors.  ``ids`` lists the slices to factor
     (device int64); by default all slices with rank > 0, or every slice
     when ``keep_values``.  With ``state`` (from svd_values_device(...,
@@ -249,17 +261,20 @@ def svd_truncated_device(x: DeviceTensor, ranks_dev, total_rank, ids=None, keep_
     u_data = torch.empty(max(total_rank * m, 1), dtype=torch.float64, device=dev)
     g_data = torch.empty(max(total_rank * p, 1), dtype=torch.float64, device=dev)
     s = torch.empty(r * n, dtype=torch.float64, device=dev) if keep_values else None
-    if not keep_values and ids is None:
+    if state is not None and not keep_values:
+        pass  # the state pass walks every slice by index and skips rank-0 ones (no host sync)
+    elif not keep_values and ids is None:
         ids = torch.nonzero(ranks_dev > 0).reshape(-1).to(torch.int64)
     if keep_values:
         ids = None
     if ids is None or ids.numel() > 0:
         if state is not None and not keep_values:
             _svd_launch(x, nat.SVD_TRUNCATED_STATE, ids=ids, s=state.s, ranks=ranks_dev,
-                        u_off=u_off, g_off=g_off, u_data=u_data, g_data=g_data, ws=state.ws)
+                        u_off=u_off, g_off=g_off, u_data=u_data, g_data=g_data, ws=state.ws,
+                        defer=defer)
         else:
             _svd_launch(x, nat.SVD_TRUNCATED, ids=ids, s=s, ranks=ranks_dev, u_off=u_off,
-                        g_off=g_off, u_data=u_data, g_data=g_data)
+                        g_off=g_off, u_data=u_data, g_data=g_data, defer=defer)
     factors = DeviceFactors(m, p, ranks_dev, u_off, g_off, u_data[: total_rank * m],
                             g_data[: total_rank * p], total_rank)
     return factors, s
