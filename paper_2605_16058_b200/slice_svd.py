@@ -221,6 +221,13 @@ def svd_values_device(x: DeviceTensor, keep_state=False, defer=None):
     m, p, r, n = _geometry(x)
     s = torch.empty(r * n, dtype=torch.float64, device=x.device)
     if keep_state:
+        lib = nat.load()
+        if (lib.starm_svd_workspace_bytes(m, p, n, n, nat.SVD_VALUES_STATE)
+                == lib.starm_svd_workspace_bytes(m, p, n, n, nat.SVD_VALUES)):
+            # slices outside the bidiagonal path (Jacobi kernel) keep no
+            # state: the truncated pass refactors them
+            _svd_launch(x, nat.SVD_VALUES, s=s, defer=defer)
+            return s, None
         ws = _svd_launch(x, nat.SVD_VALUES_STATE, s=s, defer=defer)
         return s, SvdState(ws, s)
     _svd_launch(x, nat.SVD_VALUES, s=s, defer=defer)

@@ -1,4 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | python -c "
-import json,sys; d=json.loads(sys.stdin.read())
-for k in ['value','ms_per_step','e2e','stages_ms','gpu_launches']: print(k, d.get(k))"
+timeout 900 python scripts/run_config.py c5 2 tol 2>&1 | tail -5

@@ -43,6 +43,8 @@ elif name == "c5":
     xdev = inverse_device(xh, ts)
     del xh
     run = lambda x: sb.tsvdm_fixed_rank(x, ts, 16)
+    if len(sys.argv) > 3 and sys.argv[3] == "tol":
+        run = lambda x: sb.tsvdm_tolerance(x, ts, 1e-4)
 else:
     raise SystemExit(f"unknown config {name}")
 if a is not None:

@@ -350,3 +350,20 @@ def test_tolerance_stream_equals_per_tensor_calls():
         assert np.array_equal(c.factors.g_data, ref.factors.g_data)
         assert c.discarded_energy == ref.discarded_energy and c.total_energy == ref.total_energy
     assert list(sb.tsvdm_tolerance_stream([], ts, 0.2)) == []
+
+
+@pytest.mark.parametrize("strategy", ["memory-efficient", "compute-efficient"])
+def test_tolerance_on_jacobi_path_slices(strategy):
+    # slices taller than the shared-memory panel (L > 1344) run the Jacobi
+    # kernel, which keeps no factorisation state: the two-pass schedule must
+    # fall back to refactoring (c5's 8192 x 64 slices take this path)
+    dims = (1500, 24, 6)
+    a = random_array(dims, 77)
+    ts = sb.TransformSet.build(dims, "dct")
+    got = sb.tsvdm_tolerance(sb.DenseTensor(a), ts, 0.05, strategy=strategy)
+    ref = oracle.tsvdm_tolerance(a, [oracle.dct_matrix(6)], 0.05)
+    assert np.array_equal(got.ranks, ref["ranks"])
+    assert abs(got.discarded_energy - ref["discarded_energy"]) <= 1e-12 * ref["total_energy"]
+    rec = sb.reconstruct(got)
+    err = np.linalg.norm(rec.array - a) / np.linalg.norm(a)
+    assert abs(err - got.relative_error()) <= 1e-8
