@@ -35,6 +35,8 @@
 #include <float.h>
 #include <limits.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace starm {
@@ -72,7 +74,9 @@ struct SvdParams {
   double* u_data;
   double* g_data;
   int32_t* status;
-  unsigned long long* counter;  // [0] qr kernel, [1] jacobi kernel
+  unsigned long long* counter;  // [0] reduce, [1] jacobi / vecout, [2] bulge, [3] orth, [8 + c] bulge chunk c
+  int64_t lo, hi;               // bulge / bisect: list positions [lo, hi) of this launch
+  int cctr;                     // bulge: counter index of this launch
   double* xslots;               // per-CTA X (LP x NP)
   double* wslots;               // per-CTA V (RP x NP), vector jobs
   double* rbuf;                 // per-slice R (RP x NP), QR path with vectors
@@ -1380,11 +1384,11 @@ __global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams 
   double* W = GMEM ? P.hbbuf + int64_t(blockIdx.x) * (n + BW) * HB : reinterpret_cast<double*>(smem_raw);
   const int64_t kmax = hb_kmax(n), T = hb_steps(n);
   for (;;) {
-    if (threadIdx.x == 0) cur = int64_t(atomicAdd(&P.counter[2], 1ull));
+    if (threadIdx.x == 0) cur = P.lo + int64_t(atomicAdd(&P.counter[P.cctr], 1ull));
     __syncthreads();
     const int64_t it = cur;
     __syncthreads();
-    if (it >= P.count) break;
+    if (it >= P.hi) break;
     const int64_t si = state_index(P, it);
     if (P.flags[si]) continue;
     long long t0 = clock64();
@@ -1504,13 +1508,15 @@ __device__ __forceinline__ int count_lag(const double* d, const double* e, int n
 // diverge inside a warp.
 __global__ void svd_bisect_kernel(SvdParams P) {
   const int64_t n = P.n, NP = P.NP;
-  const int64_t total = P.count * n;
+  const int64_t total = P.hi * n;  // items [lo n, hi n)
   const double N2 = 2.0 * double(n);
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; w * 32 < total; w += warps) {
+  const int64_t w0 = (P.lo * n) >> 5;  // warp-aligned start (earlier items are skipped)
+  for (int64_t w = w0 + ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5); w * 32 < total;
+       w += warps) {
     const int64_t g = w * 32 + lane;
-    const bool valid = g < total;
+    const bool valid = g < total && g >= P.lo * n;
     const int64_t it = valid ? g / n : 0, j = valid ? g % n : 0;
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
@@ -2288,7 +2294,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
 
 __global__ void reset_status_kernel(int32_t* status, unsigned long long* counters) {
   if (threadIdx.x < 2) status[threadIdx.x] = INT32_MAX;
-  if (threadIdx.x < 4) counters[threadIdx.x] = 0ull;
+  counters[threadIdx.x] = 0ull;  // 32 counters
 }
 
 // ---------------------------------------------------------------- host side
@@ -2485,6 +2491,33 @@ extern "C" int starm_svd_stats(unsigned long long* host16, int reset) {
   return STARM_OK;
 }
 
+namespace starm {
+namespace {
+// Library-owned side stream + events per device for the chunked bulge /
+// sigma overlap (created on first use, never destroyed).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, ev[16] = {};
+};
+std::mutex g_side_mu;
+SideStream g_side[64];
+
+SideStream* side_stream() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream& x = g_side[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    for (auto& e : x.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return &x;
+}
+}  // namespace
+}  // namespace starm
+
 extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
                              const int64_t* slice_ids, int64_t count, int job, double* s,
                              double* u, double* v, const int64_t* ranks, const int64_t* u_off,
@@ -2557,6 +2590,9 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
   P.use_qr = pl.use_qr;
   P.bidiag = pl.bidiag;
   P.wtwo = pl.wtwo;
+  P.lo = 0;
+  P.hi = count;
+  P.cctr = 2;
   P.by_slice = pl.by_slice;
   P.hbbuf = reinterpret_cast<double*>(base + pl.off_rcol);
   P.stats = g_stats_on;
@@ -2577,11 +2613,38 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     else svd_reduce_kernel<256><<<pl.slots_r, 256, pl.rsmem, st>>>(P);
     STARM_LAUNCH_CHECK();
     if (g_tune_mode == 3) return STARM_OK;
-    if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(P);
-    else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(P);
-    STARM_LAUNCH_CHECK();
-    svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(P);
-    STARM_LAUNCH_CHECK();
+    // Bulge chase and sigma in NCH slice chunks: sigma of chunk c (FP64-pipe
+    // bound, no shared memory) runs on a side stream next to the bulge chase
+    // of chunk c + 1 (latency bound, one CTA per SM); fork / join by events,
+    // so stream capture sees an ordinary fork-join.
+    const int nch = count >= 4 * int64_t(pl.slots_b) ? 4 : 1;
+    SideStream* ss = nch > 1 ? side_stream() : nullptr;
+    if (nch > 1 && !ss) return STARM_CUDA;
+    if (ss) {
+      STARM_CUDA_TRY(cudaEventRecord(ss->fork, st));
+      STARM_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    }
+    for (int c = 0; c < nch; ++c) {
+      SvdParams Pc = P;
+      Pc.lo = count * c / nch;
+      Pc.hi = count * (c + 1) / nch;
+      Pc.cctr = nch > 1 ? 8 + c : 2;
+      if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(Pc);
+      else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(Pc);
+      STARM_LAUNCH_CHECK();
+      if (ss) {
+        STARM_CUDA_TRY(cudaEventRecord(ss->ev[c], st));
+        STARM_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[c], 0));
+        svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, ss->s>>>(Pc);
+      } else {
+        svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(Pc);
+      }
+      STARM_LAUNCH_CHECK();
+    }
+    if (ss) {
+      STARM_CUDA_TRY(cudaEventRecord(ss->join, ss->s));
+      STARM_CUDA_TRY(cudaStreamWaitEvent(st, ss->join, 0));
+    }
   }
   if (pl.run_vec) {
     svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n);
