@@ -33,6 +33,7 @@
 // counters; workspace is per resident CTA (plus one n x n R per slice on the
 // QR path).
 #include <float.h>
+#include <math_constants.h>
 #include <limits.h>
 
 #include <mutex>
@@ -466,14 +467,16 @@ __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, cons
 
 // Copy slice into X (LP x NP, ld LP), transposing when m < p; zero padding.
 // Returns flag: 0 ok, 1 all-zero, 2 non-finite.
+// Rows [row0, row0 + rows) of X (= A, or A^T when transposed) into the X
+// slot (LP x NP, ld LP); rows < 0 means all P.L rows.
 template <int NT>
 __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, double* __restrict__ X,
-                          double* tile) {
+                          double* tile, int64_t row0 = 0, int64_t rows = -1) {
   // Batched so that every thread keeps LB loads in flight (the copy is
   // HBM-latency bound otherwise).
   constexpr int LB = 16;
   const int tid = threadIdx.x;
-  const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP;
+  const int64_t L = rows < 0 ? P.L : rows, n = P.n, LP = P.LP, NP = P.NP;
   int bad = 0, nonzero = 0;
   if (!P.transposed) {
     const int64_t total = LP * NP;
@@ -483,7 +486,7 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
       for (int u = 0; u < LB; ++u) {
         const int64_t e = e0 + tid + int64_t(u) * NT;
         const int64_t r = e % LP, c = e / LP;
-        v[u] = (e < total && r < L && c < n) ? A[r + c * P.m] : 0.0;
+        v[u] = (e < total && r < L && c < n) ? A[(row0 + r) + c * P.m] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
@@ -504,7 +507,7 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
           const int e = tid + u * NT;
           const int cc = e & 31, rr = e >> 5;
           const int64_t c = c0 + cc, r = r0 + rr;
-          v[u] = (r < L && c < n) ? A[c + r * P.m] : 0.0;
+          v[u] = (r < L && c < n) ? A[c + (row0 + r) * P.m] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < LT; ++u) {
@@ -1105,6 +1108,38 @@ __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0,
   __syncthreads();
 }
 
+// Householder QR of the tall X (LP rows, NP columns, ld LP) in 16-column
+// panels with compact-WY trailing updates; leaves R in the leading NP x NP
+// block and zeros below it.
+template <int NT>
+__device__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double* pan, int64_t prs,
+                         double* wbase, double* X, long long& pf, long long& tr) {
+  const int64_t LP = P.LP, NP = P.NP;
+  const int tid = threadIdx.x;
+  for (int64_t k0 = 0; k0 < NP; k0 += BW) {
+    const int64_t kc = (k0 / RCH) * RCH;
+    { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
+    if (tid < BW * BW) {
+      const int c = tid / BW, r = tid % BW;
+      if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+    }
+    __syncthreads();
+    if (k0 + BW < NP) {
+      explicit_v<NT>(pan, prs, k0, LP);
+      panel_gram<NT>(q, pan, prs, kc, LP);
+      long long _a = clock64();
+      P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
+             : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
+      tr += clock64() - _a;
+    }
+    __syncthreads();
+  }
+  // keep only R (upper triangle of the leading NP x NP block)
+  for (int64_t c = 0; c < NP; ++c)
+    for (int64_t r = c + 1 + tid; r < LP; r += NT) X[r + c * LP] = 0.0;
+  __syncthreads();
+}
+
 // Load / factorisation kernel (one CTA per slice, persistent):
 //   X (L x n) -> [Householder QR if L > n] -> n x n matrix A (upper
 //   triangular R or X itself) -> band reduction  A = Q1 B P1^T  with B
@@ -1142,30 +1177,7 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
     long long t1 = clock64();
     long long pf = 0, tr = 0, ru = 0;
     // ---------------- QR of the tall X (rows LP)
-    if (P.L > P.n) {
-      for (int64_t k0 = 0; k0 < NP; k0 += BW) {
-        const int64_t kc = (k0 / RCH) * RCH;
-        { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
-        if (tid < BW * BW) {
-          const int c = tid / BW, r = tid % BW;
-          if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
-        }
-        __syncthreads();
-        if (k0 + BW < NP) {
-          explicit_v<NT>(pan, prs, k0, LP);
-          panel_gram<NT>(q, pan, prs, kc, LP);
-          long long _a = clock64();
-          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
-                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
-          tr += clock64() - _a;
-        }
-        __syncthreads();
-      }
-      // keep only R (upper triangle of the leading NP x NP block)
-      for (int64_t c = 0; c < NP; ++c)
-        for (int64_t r = c + 1 + tid; r < LP; r += NT) X[r + c * LP] = 0.0;
-      __syncthreads();
-    }
+    if (P.L > P.n) qr_phase<NT>(P, q, pan, prs, wbase, X, pf, tr);
     long long t2 = clock64();
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
@@ -1221,6 +1233,51 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
     stat_add(P, ST_CYC_PFACT, (unsigned long long)pf);
     stat_add(P, ST_CYC_TRAIL, (unsigned long long)tr);
     stat_add(P, ST_CYC_RIGHT, (unsigned long long)ru);
+  }
+}
+
+// TSQR first level for tall-skinny slices whose 16-column panel does not
+// fit in shared memory (e.g. 8192 x 64): block b of a slice is rows
+// [b BR, (b + 1) BR) of X; its Householder QR (qr_phase) leaves R_b, which
+// goes to rows [b NP, b NP + NP) of the slice's stacked matrix S (SP x n,
+// column-major).  S^T S = X^T X, so the bidiagonal path on S gives X's sigma
+// and right vectors; the left vectors are formed from X itself (vecout).
+template <int NT>
+__global__ void __launch_bounds__(NT) svd_tsqr_kernel(SvdParams P, double* S, int64_t BR,
+                                                       int64_t nbk, int64_t SP) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
+  const int64_t LP = P.LP, NP = P.NP, n = P.n;
+  const int64_t prs = LP + 36;
+  double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
+  const Ring ring{pan + BW * prs, P.qr_stages};
+  double* wbase = pan + BW * prs;
+  __shared__ int64_t cur;
+  const int tid = threadIdx.x;
+  double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
+  long long pf = 0, tr = 0;
+  for (;;) {
+    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[5], 1ull));
+    __syncthreads();
+    const int64_t item = cur;
+    __syncthreads();
+    if (item >= P.count * nbk) break;
+    const int64_t it = item / nbk, b = item % nbk;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int64_t row0 = b * BR, rows = P.L - row0 < BR ? P.L - row0 : BR;
+    const int flag = load_slice<NT>(P, P.A + slice * P.m * P.p, X, ring.buf(0), row0, rows);
+    double* Sd = S + slice * SP * n + b * NP;  // rows b NP .., ld SP
+    if (flag == 2) {  // non-finite: poison the block so the stacked pass names the slice
+      for (int64_t e = tid; e < NP * n; e += NT) Sd[(e % NP) + (e / NP) * SP] = CUDART_NAN;
+      __syncthreads();
+      continue;
+    }
+    if (flag == 0) qr_phase<NT>(P, q, pan, prs, wbase, X, pf, tr);
+    for (int64_t e = tid; e < NP * n; e += NT) {
+      const int64_t r = e % NP, c = e / NP;
+      Sd[r + c * SP] = (flag == 0 && r <= c) ? X[r + c * LP] : 0.0;
+    }
+    __syncthreads();
   }
 }
 
@@ -2459,6 +2516,67 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   return STARM_OK;
 }
 
+// TSQR route for tall-skinny slices whose panel does not fit in shared memory
+// (L padded > QR_MAX_LP, n <= 256): row blocks of BR = 1024 rows are reduced
+// to their R factors (svd_tsqr_kernel) into a stacked SP x n matrix per slice
+// (SP = ceil(L / BR) * NP <= QR_MAX_LP), the bidiagonal path runs on that, and
+// vecout forms the left vectors from the original slices.  Workspace: the
+// inner plan's layout first (so a state-keeping pair sees the same offsets),
+// then S, the block-QR X slots and the vecout X slots.
+struct TsqrPlan {
+  bool on = false;
+  int64_t BR = 0, nbk = 0, SP = 0, LPo = 0, blk_L = 0;
+  int slots_q = 0;
+  Plan inner{}, blk{};
+  size_t off_S = 0, off_q = 0, off_vx = 0, total = 0;
+};
+
+int make_tsqr_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, bool have_s,
+                   TsqrPlan* tp) {
+  TsqrPlan t{};
+  const int64_t L = m > p ? m : p, n = m < p ? m : p;
+  const int64_t LP0 = round_up(L, RCH);
+  if (g_tune_mode >= 1 && g_tune_mode != 3 && LP0 > QR_MAX_LP && n <= 256) {
+    t.BR = 1024;
+    t.nbk = (L + t.BR - 1) / t.BR;
+    int64_t NP = round_up(n, BW);
+    if (NP < GW) NP = GW;
+    t.SP = t.nbk * NP;
+    if (t.SP <= QR_MAX_LP && t.SP > n) {
+      int rc = make_plan(t.SP, n, count, nslices, job, have_s, &t.inner);
+      if (rc != STARM_OK) return rc;
+      rc = make_plan(t.BR, n, count, nslices, STARM_SVD_VALUES, false, &t.blk);
+      if (rc != STARM_OK) return rc;
+      if (t.inner.bidiag && t.blk.bidiag && t.blk.reduce_nt == 256) {
+        int dev = 0, sms = 0, per = 0;
+        STARM_CUDA_TRY(cudaGetDevice(&dev));
+        STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        rc = occupancy((const void*)svd_tsqr_kernel<256>, 256, t.blk.rsmem, &per);
+        if (rc != STARM_OK) return rc;
+        const int64_t items = t.inner.count * t.nbk;
+        t.slots_q = int(int64_t(sms) * per < items ? int64_t(sms) * per : items);
+        if (t.slots_q < 1) t.slots_q = 1;
+        t.on = true;
+        t.blk_L = L;
+        t.LPo = LP0;
+        size_t off = (t.inner.total + 255) & ~size_t(255);
+        auto take = [&](size_t bytes) {
+          const size_t o = off;
+          off += (bytes + 255) & ~size_t(255);
+          return o;
+        };
+        t.off_S = take(size_t(nslices) * t.SP * n * sizeof(double));
+        t.off_q = take(size_t(t.slots_q) * t.blk.LP * t.blk.NP * sizeof(double));
+        const bool vec = t.inner.run_vec || t.inner.by_slice;
+        t.off_vx = take(vec ? size_t(t.inner.slots_v) * LP0 * t.inner.NP * sizeof(double) : 0);
+        t.total = off;
+      }
+    }
+  }
+  *tp = t;
+  return STARM_OK;
+}
+
 }  // namespace
 }  // namespace starm
 
@@ -2468,6 +2586,9 @@ extern "C" size_t starm_svd_workspace_bytes(int64_t m, int64_t p, int64_t nslice
                                             int job) {
   if (m < 1 || p < 1 || nslices < 1) return 0;
   if (count < 1 || count > nslices) count = nslices;
+  TsqrPlan tp;
+  if (make_tsqr_plan(m, p, count, nslices, job, false, &tp) != STARM_OK) return 0;
+  if (tp.on) return tp.total;
   Plan pl;
   if (make_plan(m, p, count, nslices, job, false, &pl) != STARM_OK) return 0;
   return pl.total;
@@ -2518,36 +2639,22 @@ SideStream* side_stream() {
 }  // namespace
 }  // namespace starm
 
-extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
-                             const int64_t* slice_ids, int64_t count, int job, double* s,
-                             double* u, double* v, const int64_t* ranks, const int64_t* u_off,
-                             const int64_t* g_off, double* u_data, double* g_data,
-                             int32_t* status, void* ws, size_t ws_bytes, void* stream) {
-  STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "svd: extents must be positive");
-  STARM_CHECK_ARG(job >= STARM_SVD_VALUES && job <= STARM_SVD_TRUNCATED_STATE,
-                  "svd: unknown job %d", job);
-  const int64_t r = m < p ? m : p;
-  if (r > MAX_NS) {
-    set_error("svd: min(m, p) = %lld exceeds the supported %d", (long long)r, MAX_NS);
-    return STARM_UNSUPPORTED;
-  }
-  STARM_CHECK_ARG(ahat && status && ws, "svd: null pointer");
-  STARM_CHECK_ARG((job != STARM_SVD_VALUES && job != STARM_SVD_VALUES_STATE) || s,
-                  "svd: values jobs need s");
-  STARM_CHECK_ARG(job != STARM_SVD_FULL || (s && u && v), "svd: full job needs s, u, v");
-  STARM_CHECK_ARG((job != STARM_SVD_TRUNCATED && job != STARM_SVD_TRUNCATED_STATE) ||
-                      (ranks && u_off && g_off && u_data && g_data),
-                  "svd: truncated jobs need ranks, offsets and packed buffers");
-  STARM_CHECK_ARG(job != STARM_SVD_TRUNCATED_STATE || s,
-                  "svd: the state-keeping truncated job needs the values pass's s");
-  STARM_CHECK_ARG(job != STARM_SVD_VALUES_STATE || !slice_ids,
-                  "svd: the state-keeping values job factors every slice (slice_ids must be NULL)");
-  if (!slice_ids) count = nslices;
-  cudaStream_t st = as_stream(stream);
-  unsigned long long* counters = reinterpret_cast<unsigned long long*>(ws);
-  reset_status_kernel<<<1, 32, 0, st>>>(status, counters);
-  STARM_LAUNCH_CHECK();
-  if (count <= 0) return STARM_OK;
+namespace starm {
+namespace {
+// Left-vector source for the TSQR route: vecout forms U from the original
+// slices (X V / sigma) while everything else ran on the stacked R factors.
+struct VecOverride {
+  const double* A;
+  int64_t m, p, L, LP;
+  int transposed;
+  double* xslots;
+};
+
+int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const int64_t* slice_ids,
+             int64_t count, int job, double* s, double* u, double* v, const int64_t* ranks,
+             const int64_t* u_off, const int64_t* g_off, double* u_data, double* g_data,
+             int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st,
+             unsigned long long* counters, const VecOverride* vo) {
   Plan pl;
   int rc = make_plan(m, p, count, nslices, job, s != nullptr, &pl);
   if (rc != STARM_OK) return rc;
@@ -2662,7 +2769,17 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
       svd_backtransform_kernel<<<unsigned(blocks), BT_WARPS * 32, pl.tsmem, st>>>(P, items);
     }
     STARM_LAUNCH_CHECK();
-    svd_vecout_kernel<<<pl.slots_v, TPB, pl.jsmem, st>>>(P);
+    SvdParams Pv = P;
+    if (vo) {
+      Pv.A = vo->A;
+      Pv.m = vo->m;
+      Pv.p = vo->p;
+      Pv.L = vo->L;
+      Pv.LP = vo->LP;
+      Pv.transposed = vo->transposed;
+      Pv.xslots = vo->xslots;
+    }
+    svd_vecout_kernel<<<pl.slots_v, TPB, pl.jsmem, st>>>(Pv);
     STARM_LAUNCH_CHECK();
   }
   if (pl.run_jacobi) {
@@ -2673,4 +2790,75 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     STARM_LAUNCH_CHECK();
   }
   return STARM_OK;
+}
+}  // namespace
+}  // namespace starm
+
+extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t nslices,
+                             const int64_t* slice_ids, int64_t count, int job, double* s,
+                             double* u, double* v, const int64_t* ranks, const int64_t* u_off,
+                             const int64_t* g_off, double* u_data, double* g_data,
+                             int32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(m >= 1 && p >= 1 && nslices >= 1, "svd: extents must be positive");
+  STARM_CHECK_ARG(job >= STARM_SVD_VALUES && job <= STARM_SVD_TRUNCATED_STATE,
+                  "svd: unknown job %d", job);
+  const int64_t r = m < p ? m : p;
+  if (r > MAX_NS) {
+    set_error("svd: min(m, p) = %lld exceeds the supported %d", (long long)r, MAX_NS);
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG(ahat && status && ws, "svd: null pointer");
+  STARM_CHECK_ARG((job != STARM_SVD_VALUES && job != STARM_SVD_VALUES_STATE) || s,
+                  "svd: values jobs need s");
+  STARM_CHECK_ARG(job != STARM_SVD_FULL || (s && u && v), "svd: full job needs s, u, v");
+  STARM_CHECK_ARG((job != STARM_SVD_TRUNCATED && job != STARM_SVD_TRUNCATED_STATE) ||
+                      (ranks && u_off && g_off && u_data && g_data),
+                  "svd: truncated jobs need ranks, offsets and packed buffers");
+  STARM_CHECK_ARG(job != STARM_SVD_TRUNCATED_STATE || s,
+                  "svd: the state-keeping truncated job needs the values pass's s");
+  STARM_CHECK_ARG(job != STARM_SVD_VALUES_STATE || !slice_ids,
+                  "svd: the state-keeping values job factors every slice (slice_ids must be NULL)");
+  if (!slice_ids) count = nslices;
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(ws);
+  reset_status_kernel<<<1, 32, 0, st>>>(status, counters);
+  STARM_LAUNCH_CHECK();
+  if (count <= 0) return STARM_OK;
+  TsqrPlan tp;
+  int rc = make_tsqr_plan(m, p, count, nslices, job, s != nullptr, &tp);
+  if (rc != STARM_OK) return rc;
+  if (!tp.on)
+    return svd_core(ahat, m, p, nslices, slice_ids, count, job, s, u, v, ranks, u_off, g_off, u_data,
+                    g_data, status, ws, ws_bytes, st, counters, nullptr);
+  STARM_CHECK_ARG(ws_bytes >= tp.total, "svd: workspace too small (%zu < %zu)", ws_bytes, tp.total);
+  char* base = reinterpret_cast<char*>(ws);
+  double* S = reinterpret_cast<double*>(base + tp.off_S);
+  {  // first level: R of every row block into S
+    SvdParams Q{};
+    Q.A = ahat;
+    Q.m = m;
+    Q.p = p;
+    Q.N = nslices;
+    Q.ids = slice_ids;
+    Q.count = count;
+    Q.status = status;
+    Q.counter = counters;
+    Q.xslots = reinterpret_cast<double*>(base + tp.off_q);
+    Q.qr_stages = tp.blk.qr_stages;
+    Q.L = tp.blk_L;
+    Q.n = tp.blk.n;
+    Q.LP = tp.blk.LP;
+    Q.NP = tp.blk.NP;
+    Q.RP = tp.blk.RP;
+    Q.transposed = m < p;
+    Q.wtwo = tp.blk.wtwo;
+    Q.stats = g_stats_on;
+    svd_tsqr_kernel<256><<<tp.slots_q, 256, tp.blk.rsmem, st>>>(Q, S, tp.BR, tp.nbk, tp.SP);
+    STARM_LAUNCH_CHECK();
+  }
+  const int64_t n = m < p ? m : p;
+  VecOverride vo{ahat, m, p, tp.blk_L, tp.LPo, m < p ? 1 : 0,
+                 reinterpret_cast<double*>(base + tp.off_vx)};
+  return svd_core(S, tp.SP, n, nslices, slice_ids, count, job, s, u, v, ranks, u_off, g_off, u_data,
+                  g_data, status, ws, tp.inner.total, st, counters, &vo);
 }

@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [(5, 3, 4), (3, 5, 2, 3), (7, 7, 6), (1, 4, 3), (4, 1, 2), (33, 17, 5), (17, 33, 4),
           (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3),
-          (300, 257, 2), (257, 300, 2), (361, 720, 1), (1024, 1024, 2), (900, 1100, 1)]
+          (300, 257, 2), (257, 300, 2), (361, 720, 1), (1024, 1024, 2), (900, 1100, 1),
+          (2100, 40, 2), (40, 2100, 2), (8192, 64, 2), (5000, 130, 1)]
 
 
 # ------------------------------------------------------------------ TTM (K1)
@@ -353,10 +354,10 @@ def test_tolerance_stream_equals_per_tensor_calls():
 
 
 @pytest.mark.parametrize("strategy", ["memory-efficient", "compute-efficient"])
-def test_tolerance_on_jacobi_path_slices(strategy):
-    # slices taller than the shared-memory panel (L > 1344) run the Jacobi
-    # kernel, which keeps no factorisation state: the two-pass schedule must
-    # fall back to refactoring (c5's 8192 x 64 slices take this path)
+def test_tolerance_on_tall_skinny_slices(strategy):
+    # slices taller than the shared-memory panel (L > 1344): row-block TSQR
+    # into stacked R factors, then the bidiagonal path (c5's 8192 x 64
+    # slices take this route); both tolerance strategies
     dims = (1500, 24, 6)
     a = random_array(dims, 77)
     ts = sb.TransformSet.build(dims, "dct")
