@@ -1112,7 +1112,7 @@ __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0,
 // panels with compact-WY trailing updates; leaves R in the leading NP x NP
 // block and zeros below it.
 template <int NT>
-__device__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double* pan, int64_t prs,
+__device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double* pan, int64_t prs,
                          double* wbase, double* X, long long& pf, long long& tr) {
   const int64_t LP = P.LP, NP = P.NP;
   const int tid = threadIdx.x;
@@ -1685,20 +1685,38 @@ __device__ void gemm_xv(const SvdParams& P, JacobiSmem& sm, const double* A, con
         double* xs = sm.xs[0];
         double* wt = sm.w[0];
         // X tile: rows r0..r0+63, cols kk..kk+31 -> xs[col*XS + row]
-        for (int e = tid; e < GW * RCH; e += TPB) {
+        // (all loads of a tile are issued before any store: one latency per tile)
+        constexpr int XN = GW * RCH / TPB, WN = GW * GW / TPB;
+        double xv[XN], wv[WN];
+#pragma unroll
+        for (int u = 0; u < XN; ++u) {
+          const int e = tid + u * TPB;
           int col, row;
           if (P.transposed) { col = e & 31; row = e >> 5; }   // consecutive col -> contiguous A
           else { row = e & 63; col = e >> 6; }                // consecutive row -> contiguous A
           const int64_t r = r0 + row, c = kk + col;
-          double x = 0.0;
-          if (r < L && c < n) x = P.transposed ? A[c + r * P.m] : A[r + c * P.m];
-          xs[col * XS + row] = x;
+          xv[u] = (r < L && c < n) ? (P.transposed ? A[c + r * P.m] : A[r + c * P.m]) : 0.0;
         }
         // W tile: W[kk+i][idx[kb+j]] -> wt[j*WS + i]
-        for (int e = tid; e < GW * GW; e += TPB) {
+#pragma unroll
+        for (int u = 0; u < WN; ++u) {
+          const int e = tid + u * TPB;
           const int i = e & 31, j = e >> 5;
           const int64_t jj = kb + j;
-          wt[j * WS + i] = (jj < k) ? V[(kk + i) + int64_t(idx[jj]) * RP] : 0.0;
+          wv[u] = (jj < k) ? V[(kk + i) + int64_t(idx[jj]) * RP] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < XN; ++u) {
+          const int e = tid + u * TPB;
+          int col, row;
+          if (P.transposed) { col = e & 31; row = e >> 5; }
+          else { row = e & 63; col = e >> 6; }
+          xs[col * XS + row] = xv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < WN; ++u) {
+          const int e = tid + u * TPB;
+          wt[(e >> 5) * WS + (e & 31)] = wv[u];
         }
         __syncthreads();
         const double* xa = xs + tq * XS + warp * 8 + gq;
@@ -1850,60 +1868,106 @@ __device__ __forceinline__ int64_t kout_of(const SvdParams& P, int64_t slice) {
 // One thread per (slice, cluster head); per-thread scratch of 6 x 2n doubles.
 constexpr int II_CMAX = 32;
 
+// Per-thread scratch vectors are interleaved across the grid's threads
+// (element i of a thread's vector at i * stride), so a warp's accesses to
+// the same index are coalesced; the recurrences carry their state in
+// registers and prefetch the next step's operands.
+struct Strided {
+  double* p;
+  int64_t s;
+  __device__ __forceinline__ double& operator[](int64_t i) const { return p[i * s]; }
+};
+
+// LU with partial pivoting of T_GK - lam I (zero diagonal, off-diagonals
+// b_k = d0, e0, d1, ...; LAPACK dgttrf): outputs the reciprocal pivots rdd,
+// super-diagonals du, du2, multipliers dl and the interchange flags z.
 __device__ void ii_factor(const double* bd, const double* be, int64_t N2, double lam, double pert,
-                          double* dd, double* du, double* du2, double* dl, double* z) {
-  for (int64_t i = 0; i < N2; ++i) {
-    dd[i] = -lam;
-    du[i] = (i + 1 < N2) ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0;
-    du2[i] = 0.0;
-  }
+                          Strided rdd, Strided du, Strided du2, Strided dl, Strided z) {
+  auto b_at = [&](int64_t i) { return (i & 1) ? be[i >> 1] : bd[i >> 1]; };
+  double cdd = -lam;                         // dd[i] as modified so far
+  double cdu = N2 > 1 ? b_at(0) : 0.0;       // du[i] as modified so far
+  double bn = N2 > 2 ? b_at(1) : 0.0;        // original b_{i+1}
   for (int64_t i = 0; i + 1 < N2; ++i) {
-    // original sub-diagonal (T is symmetric); du[i] may already hold fill
-    const double sub = (i & 1) ? be[i >> 1] : bd[i >> 1];
-    if (fabs(dd[i]) >= fabs(sub)) {
-      if (dd[i] == 0.0) dd[i] = pert;
-      const double fact = sub / dd[i];
-      dl[i] = fact;
-      dd[i + 1] -= fact * du[i];
-      z[i] = 0.0;
+    const double bi = b_at(i);               // original sub-diagonal
+    const double bnext = (i + 2 < N2) ? bn : 0.0;
+    const double bpre = (i + 3 < N2) ? b_at(i + 2) : 0.0;  // prefetch for the next step
+    double ddi, dui, du2i, dli, zi, ndd, ndu;
+    if (fabs(cdd) >= fabs(bi)) {
+      ddi = cdd == 0.0 ? pert : cdd;
+      const double fact = bi / ddi;
+      dli = fact;
+      dui = cdu;
+      du2i = 0.0;
+      zi = 0.0;
+      ndd = -lam - fact * cdu;
+      ndu = bnext;
     } else {
-      const double fact = dd[i] / sub;
-      dd[i] = sub;
-      dl[i] = fact;
-      const double temp = du[i];
-      du[i] = dd[i + 1];
-      dd[i + 1] = temp - fact * dd[i + 1];
-      if (i + 2 < N2) {
-        du2[i] = du[i + 1];
-        du[i + 1] = -fact * du[i + 1];
-      }
-      z[i] = 1.0;
+      const double fact = cdd / bi;
+      ddi = bi;
+      dli = fact;
+      dui = -lam;                            // the old dd[i + 1]
+      ndd = cdu - fact * (-lam);
+      du2i = bnext;
+      ndu = -fact * bnext;
+      zi = 1.0;
     }
+    rdd[i] = 1.0 / ddi;
+    du[i] = dui;
+    du2[i] = du2i;
+    dl[i] = dli;
+    z[i] = zi;
+    cdd = ndd;
+    cdu = ndu;
+    bn = bpre;
   }
-  if (dd[N2 - 1] == 0.0) dd[N2 - 1] = pert;
+  rdd[N2 - 1] = 1.0 / (cdd == 0.0 ? pert : cdd);
 }
 
-__device__ void ii_solve(int64_t N2, const double* dd, const double* du, const double* du2,
-                         const double* dl, const double* z, double* x) {
-  for (int64_t i = 0; i + 1 < N2; ++i) {  // apply L and the row interchanges
-    if (z[i] != 0.0) {
-      const double t = x[i];
-      x[i] = x[i + 1];
-      x[i + 1] = t - dl[i] * x[i + 1];
-    } else {
-      x[i + 1] -= dl[i] * x[i];
+__device__ void ii_solve(int64_t N2, Strided rdd, Strided du, Strided du2, Strided dl, Strided z,
+                         Strided x) {
+  // apply L and the row interchanges (x[i + 1] carried in a register)
+  double xi = x[0];
+  double xn = N2 > 1 ? x[1] : 0.0;
+  double dli = N2 > 1 ? dl[0] : 0.0, zi = N2 > 1 ? z[0] : 0.0;
+  for (int64_t i = 0; i + 1 < N2; ++i) {
+    double dln = 0.0, zn = 0.0, xnn = 0.0;
+    if (i + 2 < N2) {
+      dln = dl[i + 1];
+      zn = z[i + 1];
+      xnn = x[i + 2];
     }
+    double xo, xc;
+    if (zi != 0.0) {
+      xo = xn;
+      xc = xi - dli * xn;
+    } else {
+      xo = xi;
+      xc = xn - dli * xi;
+    }
+    x[i] = xo;
+    xi = xc;
+    xn = xnn;
+    dli = dln;
+    zi = zn;
   }
-  // U has diagonal dd, super du, second super du2
-  x[N2 - 1] /= dd[N2 - 1];
-  if (N2 > 1) x[N2 - 2] = (x[N2 - 2] - du[N2 - 2] * x[N2 - 1]) / dd[N2 - 2];
-  for (int64_t i = N2 - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
+  // U has diagonal dd (reciprocals rdd), super du, second super du2
+  double x1 = xi * rdd[N2 - 1];
+  x[N2 - 1] = x1;
+  if (N2 < 2) return;
+  double x0 = (x[N2 - 2] - du[N2 - 2] * x1) * rdd[N2 - 2];
+  x[N2 - 2] = x0;
+  for (int64_t i = N2 - 3; i >= 0; --i) {
+    const double xv = (x[i] - du[i] * x0 - du2[i] * x1) * rdd[i];
+    x[i] = xv;
+    x1 = x0;
+    x0 = xv;
+  }
 }
 
 // x -= (x.z / z.z) z for the T_GK eigenvector z of a previous cluster member
 // (v = stored right vector, sig its shift; u = B v / sig, 0 when sig == 0).
 __device__ void ii_orth(const double* bd, const double* be, int64_t n, const double* v, double sig,
-                        double* x) {
+                        Strided x) {
   const double rs = sig > 0.0 ? 1.0 / sig : 0.0;
   double dot = 0.0, nz = 0.0;
   for (int64_t i = 0; i < n; ++i) {
@@ -1926,13 +1990,13 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   const int64_t n = P.n, NP = P.NP, RP = P.RP, N2 = 2 * P.n;
   const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  double* scr = P.iiscr + gtid * 5 * 2 * NP;
-  double* dd = scr;
-  double* du = dd + 2 * NP;
-  double* du2 = du + 2 * NP;
-  double* dl = du2 + 2 * NP;  // multipliers
-  double* z = dl + 2 * NP;    // 1.0 where rows i, i+1 were interchanged
-  double* x = P.iiscr + nthreads * 5 * 2 * NP + gtid * 2 * NP;  // the iterate
+  const int64_t vl = 2 * NP;  // vector length in the interleaved scratch
+  Strided rdd{P.iiscr + gtid, nthreads};
+  Strided du{P.iiscr + 1 * vl * nthreads + gtid, nthreads};
+  Strided du2{P.iiscr + 2 * vl * nthreads + gtid, nthreads};
+  Strided dl{P.iiscr + 3 * vl * nthreads + gtid, nthreads};  // multipliers
+  Strided z{P.iiscr + 4 * vl * nthreads + gtid, nthreads};   // 1.0 where rows i, i+1 swapped
+  Strided x{P.iiscr + 5 * vl * nthreads + gtid, nthreads};   // the iterate
   for (int64_t g = gtid; g < total_work; g += nthreads) {
     const int64_t it = g / n, j = g % n;
     const int64_t si = state_index(P, it);
@@ -1958,12 +2022,12 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
       double lam = sv[jj];
       if (jj > j && lam > lprev - 10.0 * pert) lam = lprev - 10.0 * pert;  // separate equal shifts
       lprev = lam;
-      ii_factor(bd, be, N2, lam, pert, dd, du, du2, dl, z);
+      ii_factor(bd, be, N2, lam, pert, rdd, du, du2, dl, z);
       for (int64_t i = 0; i < N2; ++i)
         x[i] = 1.0 + 0.25 * double(((i + 1) * 7919 + (jj + 1) * 104729) % 97) / 97.0;
       for (int iter = 0; iter < 3; ++iter) {
         for (int64_t q = j; q < jj; ++q) ii_orth(bd, be, n, P.vsel + si * RP * NP + q * RP, sv[q], x);
-        ii_solve(N2, dd, du, du2, dl, z, x);
+        ii_solve(N2, rdd, du, du2, dl, z, x);
         double nrm = 0.0;
         for (int64_t i = 0; i < N2; ++i) nrm = fmax(nrm, fabs(x[i]));
         const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;

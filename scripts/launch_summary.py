@@ -1,6 +1,6 @@
 """Summarise an ncu --metrics gpu__time_duration.sum CSV launch list:
-per-kernel totals for the LAST step of run_step.py (launches after the
-midpoint), in ms."""
+per-kernel totals for the LAST step of run_step.py (launches from the last
+transform launch on), in ms."""
 import collections
 import csv
 import sys
@@ -12,7 +12,9 @@ ids = hdr.index("ID")
 data = [(int(r[ids]), r[ki], float(r[vi].replace(",", ""))) for r in rows[1:] if r[vi]]
 unit = rows[1][hdr.index("Metric Unit")] if len(rows) > 1 else ""
 scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(unit, 1e-6)
-half = data[len(data) // 2:] if len(sys.argv) < 3 else data
+# the last step starts at the last transform launch (dct / gemm kernel)
+starts = [i for i, (_, k, _) in enumerate(data) if "dct_kernel" in k or "gemm_f64" in k]
+half = data[starts[-1]:] if starts and len(sys.argv) < 3 else data
 tot = collections.OrderedDict()
 for _, k, v in half:
     name = k.split("(")[0].split("::")[-1][:60]
