@@ -1868,10 +1868,11 @@ __device__ __forceinline__ int64_t kout_of(const SvdParams& P, int64_t slice) {
 // One thread per (slice, cluster head); per-thread scratch of 6 x 2n doubles.
 constexpr int II_CMAX = 32;
 
-// Per-thread scratch vectors are interleaved across the grid's threads
-// (element i of a thread's vector at i * stride), so a warp's accesses to
-// the same index are coalesced; the recurrences carry their state in
-// registers and prefetch the next step's operands.
+// Per-thread scratch vectors are interleaved within a warp (element i of a
+// lane's vector at i * 32 + lane), so a warp's accesses to the same index
+// are one coalesced line and each warp walks its own region sequentially;
+// the recurrences carry their state in registers and prefetch the next
+// step's operands.
 struct Strided {
   double* p;
   int64_t s;
@@ -1880,87 +1881,123 @@ struct Strided {
 
 // LU with partial pivoting of T_GK - lam I (zero diagonal, off-diagonals
 // b_k = d0, e0, d1, ...; LAPACK dgttrf): outputs the reciprocal pivots rdd,
-// super-diagonals du, du2, multipliers dl and the interchange flags z.
+// super-diagonals du, du2, multipliers dl and the interchange flags z.  The
+// sequential recurrence runs from registers in blocks of IB steps whose
+// operands are loaded (and results stored) together.
+constexpr int IB = 8;
+
 __device__ void ii_factor(const double* bd, const double* be, int64_t N2, double lam, double pert,
                           Strided rdd, Strided du, Strided du2, Strided dl, Strided z) {
-  auto b_at = [&](int64_t i) { return (i & 1) ? be[i >> 1] : bd[i >> 1]; };
-  double cdd = -lam;                         // dd[i] as modified so far
-  double cdu = N2 > 1 ? b_at(0) : 0.0;       // du[i] as modified so far
-  double bn = N2 > 2 ? b_at(1) : 0.0;        // original b_{i+1}
-  for (int64_t i = 0; i + 1 < N2; ++i) {
-    const double bi = b_at(i);               // original sub-diagonal
-    const double bnext = (i + 2 < N2) ? bn : 0.0;
-    const double bpre = (i + 3 < N2) ? b_at(i + 2) : 0.0;  // prefetch for the next step
-    double ddi, dui, du2i, dli, zi, ndd, ndu;
-    if (fabs(cdd) >= fabs(bi)) {
-      ddi = cdd == 0.0 ? pert : cdd;
-      const double fact = bi / ddi;
-      dli = fact;
-      dui = cdu;
-      du2i = 0.0;
-      zi = 0.0;
-      ndd = -lam - fact * cdu;
-      ndu = bnext;
-    } else {
-      const double fact = cdd / bi;
-      ddi = bi;
-      dli = fact;
-      dui = -lam;                            // the old dd[i + 1]
-      ndd = cdu - fact * (-lam);
-      du2i = bnext;
-      ndu = -fact * bnext;
-      zi = 1.0;
+  auto b_at = [&](int64_t i) { return i < N2 - 1 ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0; };
+  double cdd = -lam;                    // dd[i] as modified so far
+  double cdu = b_at(0);                 // du[i] as modified so far
+  for (int64_t i0 = 0; i0 + 1 < N2; i0 += IB) {
+    double bb[IB + 1];
+#pragma unroll
+    for (int u = 0; u <= IB; ++u) bb[u] = b_at(i0 + u);  // original b_i .. b_{i+IB}
+    double o_rdd[IB], o_du[IB], o_du2[IB], o_dl[IB], o_z[IB];
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = i0 + u;
+      o_rdd[u] = o_du[u] = o_du2[u] = o_dl[u] = o_z[u] = 0.0;
+      if (i + 1 < N2) {
+        const double bi = bb[u], bnext = bb[u + 1];  // b_{N2-1} = 0 by b_at
+        double ddi, ndd, ndu;
+        if (fabs(cdd) >= fabs(bi)) {
+          ddi = cdd == 0.0 ? pert : cdd;
+          const double fact = bi / ddi;
+          o_dl[u] = fact;
+          o_du[u] = cdu;
+          ndd = -lam - fact * cdu;
+          ndu = bnext;
+        } else {
+          const double fact = cdd / bi;
+          ddi = bi;
+          o_dl[u] = fact;
+          o_du[u] = -lam;  // the old dd[i + 1]
+          ndd = cdu + fact * lam;
+          o_du2[u] = bnext;
+          ndu = -fact * bnext;
+          o_z[u] = 1.0;
+        }
+        o_rdd[u] = 1.0 / ddi;
+        cdd = ndd;
+        cdu = ndu;
+      }
     }
-    rdd[i] = 1.0 / ddi;
-    du[i] = dui;
-    du2[i] = du2i;
-    dl[i] = dli;
-    z[i] = zi;
-    cdd = ndd;
-    cdu = ndu;
-    bn = bpre;
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = i0 + u;
+      if (i + 1 < N2) {
+        rdd[i] = o_rdd[u];
+        du[i] = o_du[u];
+        du2[i] = o_du2[u];
+        dl[i] = o_dl[u];
+        z[i] = o_z[u];
+      }
+    }
   }
   rdd[N2 - 1] = 1.0 / (cdd == 0.0 ? pert : cdd);
 }
 
 __device__ void ii_solve(int64_t N2, Strided rdd, Strided du, Strided du2, Strided dl, Strided z,
                          Strided x) {
-  // apply L and the row interchanges (x[i + 1] carried in a register)
+  // forward: apply L and the row interchanges; x[i] carried in a register
   double xi = x[0];
-  double xn = N2 > 1 ? x[1] : 0.0;
-  double dli = N2 > 1 ? dl[0] : 0.0, zi = N2 > 1 ? z[0] : 0.0;
-  for (int64_t i = 0; i + 1 < N2; ++i) {
-    double dln = 0.0, zn = 0.0, xnn = 0.0;
-    if (i + 2 < N2) {
-      dln = dl[i + 1];
-      zn = z[i + 1];
-      xnn = x[i + 2];
+  for (int64_t i0 = 0; i0 + 1 < N2; i0 += IB) {
+    double dlv[IB], zv[IB], xv[IB];
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = i0 + u;
+      const bool in = i + 1 < N2;
+      dlv[u] = in ? dl[i] : 0.0;
+      zv[u] = in ? z[i] : 0.0;
+      xv[u] = in ? x[i + 1] : 0.0;
     }
-    double xo, xc;
-    if (zi != 0.0) {
-      xo = xn;
-      xc = xi - dli * xn;
-    } else {
-      xo = xi;
-      xc = xn - dli * xi;
+    double xo[IB];
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      if (i0 + u + 1 >= N2) break;  // the chain must stop at the last row
+      if (zv[u] != 0.0) {
+        xo[u] = xv[u];
+        xi = xi - dlv[u] * xv[u];
+      } else {
+        xo[u] = xi;
+        xi = xv[u] - dlv[u] * xi;
+      }
     }
-    x[i] = xo;
-    xi = xc;
-    xn = xnn;
-    dli = dln;
-    zi = zn;
+#pragma unroll
+    for (int u = 0; u < IB; ++u)
+      if (i0 + u + 1 < N2) x[i0 + u] = xo[u];
   }
-  // U has diagonal dd (reciprocals rdd), super du, second super du2
-  double x1 = xi * rdd[N2 - 1];
+  // backward: U has diagonal 1/rdd, super du, second super du2
+  double x1 = xi * rdd[N2 - 1];  // x[N2 - 1]
   x[N2 - 1] = x1;
   if (N2 < 2) return;
   double x0 = (x[N2 - 2] - du[N2 - 2] * x1) * rdd[N2 - 2];
   x[N2 - 2] = x0;
-  for (int64_t i = N2 - 3; i >= 0; --i) {
-    const double xv = (x[i] - du[i] * x0 - du2[i] * x1) * rdd[i];
-    x[i] = xv;
-    x1 = x0;
-    x0 = xv;
+  for (int64_t i1 = N2 - 3; i1 >= 0; i1 -= IB) {  // block i1, i1 - 1, ..., i1 - IB + 1
+    double xv[IB], duv[IB], du2v[IB], rv[IB];
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = i1 - u;
+      const bool in = i >= 0;
+      xv[u] = in ? x[i] : 0.0;
+      duv[u] = in ? du[i] : 0.0;
+      du2v[u] = in ? du2[i] : 0.0;
+      rv[u] = in ? rdd[i] : 0.0;
+    }
+    double xo[IB];
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const double v = (xv[u] - duv[u] * x0 - du2v[u] * x1) * rv[u];
+      xo[u] = v;
+      x1 = x0;
+      x0 = v;
+    }
+#pragma unroll
+    for (int u = 0; u < IB; ++u)
+      if (i1 - u >= 0) x[i1 - u] = xo[u];
   }
 }
 
@@ -1990,15 +2027,20 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
   const int64_t n = P.n, NP = P.NP, RP = P.RP, N2 = 2 * P.n;
   const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t vl = 2 * NP;  // vector length in the interleaved scratch
-  Strided rdd{P.iiscr + gtid, nthreads};
-  Strided du{P.iiscr + 1 * vl * nthreads + gtid, nthreads};
-  Strided du2{P.iiscr + 2 * vl * nthreads + gtid, nthreads};
-  Strided dl{P.iiscr + 3 * vl * nthreads + gtid, nthreads};  // multipliers
-  Strided z{P.iiscr + 4 * vl * nthreads + gtid, nthreads};   // 1.0 where rows i, i+1 swapped
-  Strided x{P.iiscr + 5 * vl * nthreads + gtid, nthreads};   // the iterate
+  // scratch interleaved within each warp (element i of lane l at i * 32 + l):
+  // coalesced per index, sequential per warp (TLB-friendly)
+  const int64_t vl = 2 * NP;
+  double* wscr = P.iiscr + (gtid >> 5) * (6 * vl * 32) + (gtid & 31);
+  Strided rdd{wscr, 32};
+  Strided du{wscr + 1 * vl * 32, 32};
+  Strided du2{wscr + 2 * vl * 32, 32};
+  Strided dl{wscr + 3 * vl * 32, 32};  // multipliers
+  Strided z{wscr + 4 * vl * 32, 32};   // 1.0 where rows i, i+1 swapped
+  Strided x{wscr + 5 * vl * 32, 32};   // the iterate
   for (int64_t g = gtid; g < total_work; g += nthreads) {
-    const int64_t it = g / n, j = g % n;
+    // vector index major: the few real items (j < k) of every slice come first
+    // and spread over all threads / warps
+    const int64_t j = g / P.count, it = g % P.count;
     const int64_t si = state_index(P, it);
     if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
@@ -2118,7 +2160,9 @@ __global__ void __launch_bounds__(BT_WARPS * 32) svd_backtransform_kernel(SvdPar
   const int64_t kmax = hb_kmax(n);
   const int64_t nwarps = int64_t(gridDim.x) * BT_WARPS;
   for (int64_t g = int64_t(blockIdx.x) * BT_WARPS + warp; g < items; g += nwarps) {
-    const int64_t it = g / n, j = g % n;
+    // vector index major: the few real items (j < k) of every slice come first
+    // and spread over all threads / warps
+    const int64_t j = g / P.count, it = g % P.count;
     const int64_t si = state_index(P, it);
     if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
