@@ -2136,129 +2136,178 @@ __global__ void __launch_bounds__(32) svd_orth_kernel(SvdParams P) {
   }
 }
 
-// Back-transformation v <- P1 P2 v of one right vector per warp: the bulge
-// chase's right reflectors in reverse order, then the band reduction's LQ
-// panels (I - V T V^T) from the last to the first.  The tasks of one sweep
-// act on disjoint 16-column ranges, so lane k applies task k of the sweep
-// (sweeps in reverse, a __syncwarp between them; each lane's next record is
-// prefetched into registers during the current sweep); the LQ panels are
-// applied warp-cooperatively (lanes split the rows, butterfly-reduced
-// V^T x).  The vector lives in shared memory with a skewed index
-// (q + q / 16) so the lanes' 16-element ranges fall in distinct banks.
-constexpr int BT_WARPS = 4;
+// Back-transformation v <- P1 P2 v of the right vectors: the bulge chase's
+// right reflectors in reverse order, then the band reduction's LQ panels
+// (I - V T V^T) from the last to the first.  One CTA per (slice, group of G
+// vectors), one warp per vector.  Every log record is staged into shared
+// memory once per CTA (cp.async, one sweep ahead) and applied by all G
+// warps, so the logs are read once per group rather than once per vector.
+// The tasks of one sweep act on disjoint 16-column ranges: lane k applies
+// task k (chunks of 32 tasks), a CTA barrier between sweeps.  The LQ panels
+// are streamed in 128-row chunks, each warp forming V^T x (butterfly
+// reduced), T (V^T x), then x -= V z.  Vectors live in shared memory with a
+// skewed index (q + q / 16) so the lanes' 16-element ranges fall in
+// distinct banks; records are padded to 17 doubles for the same reason.
+constexpr int BT_REC = 17;   // padded record stride
+constexpr int BT_ROWS = 64;  // LQ panel rows per staged chunk (double-buffered)
 __host__ __device__ __forceinline__ int64_t bt_stride(int64_t n) { return n + n / 16 + 48; }
+__host__ __device__ __forceinline__ size_t bt_smem(int64_t n, int g) {
+  return (size_t(g) * bt_stride(n) + 2 * size_t(hb_kmax(n)) * BT_REC + 2 * BW * BT_ROWS + BW * BW) *
+         sizeof(double);
+}
 __device__ __forceinline__ int sx(int q) { return q + (q >> 4); }
 
-__global__ void __launch_bounds__(BT_WARPS * 32) svd_backtransform_kernel(SvdParams P, int64_t items) {
+__global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int G) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nthr = blockDim.x;
   const int n = int(P.n);
   const int64_t NP = P.NP, RP = P.RP;
   const int npan = int(NP / BW);
   const int64_t stride = bt_stride(n);
-  double* x = reinterpret_cast<double*>(smem_raw) + warp * stride;
-  const int64_t kmax = hb_kmax(n);
-  const int64_t nwarps = int64_t(gridDim.x) * BT_WARPS;
-  for (int64_t g = int64_t(blockIdx.x) * BT_WARPS + warp; g < items; g += nwarps) {
-    // vector index major: the few real items (j < k) of every slice come first
-    // and spread over all threads / warps
-    const int64_t j = g / P.count, it = g % P.count;
+  const int kmax = int(hb_kmax(n));
+  double* xs = reinterpret_cast<double*>(smem_raw);    // [G][stride]
+  double* rb = xs + G * stride;                        // [2][kmax * BT_REC] sweep records
+  double* vc = rb + 2 * kmax * BT_REC;                 // [2][BW][BT_ROWS] LQ chunks
+  double* ts = vc + 2 * BW * BT_ROWS;                  // [BW * BW] LQ T
+  double* x = xs + warp * stride;
+  const int ngroups = (n + G - 1) / G;
+  for (int64_t cta = blockIdx.x; cta < P.count * ngroups; cta += gridDim.x) {
+    const int64_t it = cta / ngroups;
+    const int grp = int(cta % ngroups);
     const int64_t si = state_index(P, it);
     if (P.flags[si]) continue;
     const int64_t slice = P.ids ? P.ids[it] : it;
-    if (j >= kout_of(P, slice)) continue;
-    double* vg = P.vsel + si * RP * NP + j * RP;
+    const int kv = int(kout_of(P, slice));
+    const int j0 = grp * G;
+    if (j0 >= kv) continue;
+    const int j = j0 + warp;
+    const bool act = j < kv;
+    double* vg = P.vsel + si * RP * NP + int64_t(j) * RP;
     for (int q = lane; q < stride; q += 32) x[q] = 0.0;
     __syncwarp();
-    for (int q = lane; q < n; q += 32) x[sx(q)] = vg[q];
-    __syncwarp();
-    // ---- bulge-chase reflectors, last sweep first; lane = task
+    if (act)
+      for (int q = lane; q < n; q += 32) x[sx(q)] = vg[q];
+    // ---- bulge-chase reflectors, last sweep first
     const double* lg = P.hhlog + si * P.hhcap;
-    double rec[BW], nxt[BW];
-#pragma unroll
-    for (int l = 0; l < BW; ++l) rec[l] = nxt[l] = 0.0;
-    if (n >= 3 && lane < hb_tasks(n, n - 3)) {
-      const double* h = lg + (int64_t(n - 3) * kmax + lane) * HLOG;
-#pragma unroll
-      for (int l = 0; l < BW; ++l) rec[l] = h[l];
-    }
-    for (int i = n - 3; i >= 0; --i) {
+    auto stage = [&](int i, int buf) {  // records of sweep i -> rb[buf]
       const int K = int(hb_tasks(n, i));
-      if (i > 0 && lane < hb_tasks(n, i - 1)) {
-        const double* h = lg + (int64_t(i - 1) * kmax + lane) * HLOG;
-#pragma unroll
-        for (int l = 0; l < BW; ++l) nxt[l] = h[l];
+      double* dst = rb + buf * kmax * BT_REC;
+      const double* src = lg + int64_t(i) * kmax * HLOG;
+      for (int e = threadIdx.x; e < K * HLOG; e += nthr) {  // padded rows: 8-byte copies
+        const int k = e / HLOG, h = e % HLOG;
+        cp_async8(dst + k * BT_REC + h, src + k * HLOG + h);
       }
-      for (int kb = 0; kb < K; kb += 32) {  // tasks of one sweep are disjoint
-        const int k = kb + lane;
-        double r[BW];
-        if (kb == 0) {
+      cp_async_commit();
+    };
+    if (n >= 3) stage(n - 3, (n - 3) & 1);
+    for (int i = n - 3; i >= 0; --i) {
+      if (i > 0) {
+        stage(i - 1, (i - 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const int K = int(hb_tasks(n, i));
+      const double* rbuf = rb + (i & 1) * kmax * BT_REC;
+      if (act) {
+        for (int kb = 0; kb < K; kb += 32) {  // tasks of one sweep are disjoint
+          const int k = kb + lane;
+          if (k < K) {
+            const double* r = rbuf + k * BT_REC;
+            const double tau = r[0];
+            if (tau != 0.0) {
+              const int c0 = i + k * BW + 1;
+              const int base = sx(c0), b16 = BW - (c0 & 15);  // skew steps by one at l = b16
+              double xv[BW];
 #pragma unroll
-          for (int l = 0; l < BW; ++l) r[l] = rec[l];
-        } else if (k < K) {
-          const double* h = lg + (int64_t(i) * kmax + k) * HLOG;
+              for (int l = 0; l < BW; ++l) xv[l] = x[base + l + (l >= b16)];
+              double w0 = xv[0], w1 = 0.0;
 #pragma unroll
-          for (int l = 0; l < BW; ++l) r[l] = h[l];
-        }
-        if (k < K && r[0] != 0.0) {
-          const int c0 = i + k * BW + 1;
-          const int base = sx(c0), b16 = BW - (c0 & 15);  // skew steps by one at l = b16
-          double xv[BW];
+              for (int l = 1; l < BW; l += 2) {
+                w1 = fma(r[l], xv[l], w1);
+                if (l + 1 < BW) w0 = fma(r[l + 1], xv[l + 1], w0);
+              }
+              const double w = (w0 + w1) * tau;
+              x[base] = xv[0] - w;
 #pragma unroll
-          for (int l = 0; l < BW; ++l) xv[l] = x[base + l + (l >= b16)];
-          double w0 = xv[0], w1 = 0.0;
-#pragma unroll
-          for (int l = 1; l < BW; l += 2) {
-            w1 = fma(r[l], xv[l], w1);
-            if (l + 1 < BW) w0 = fma(r[l + 1], xv[l + 1], w0);
+              for (int l = 1; l < BW; ++l) x[base + l + (l >= b16)] = fma(-w, r[l], xv[l]);
+            }
           }
-          const double w = (w0 + w1) * r[0];
-          x[base] = xv[0] - w;
-#pragma unroll
-          for (int l = 1; l < BW; ++l) x[base + l + (l >= b16)] = fma(-w, r[l], xv[l]);
         }
       }
-      __syncwarp();
-#pragma unroll
-      for (int l = 0; l < BW; ++l) rec[l] = nxt[l];
+      __syncthreads();  // rb[i & 1] is restaged two sweeps later
     }
-    // ---- LQ panels of the band reduction, last first
+    // ---- LQ panels of the band reduction, last first.  Per panel one flat
+    // sequence of 2 nq chunk loads (pass 1: V^T x, pass 2: x -= V z) through
+    // a two-buffer cp.async ring.
     const double* rv = P.rvlog + si * int64_t(npan) * (BW * NP + BW * BW);
     for (int pk = npan - 2; pk >= 0; --pk) {
       const double* Vp = rv + int64_t(pk) * (BW * NP + BW * BW);  // V[c][q], q < NP
-      const double* Tp = Vp + BW * NP;                              // T[a][b]
       const int jlo = pk * BW + BW;
-      double y[BW];
+      const int nq = (n - jlo + BT_ROWS - 1) / BT_ROWS;
+      if (nq <= 0) continue;
+      auto issue = [&](int t) {
+        const int q0 = jlo + (t % nq) * BT_ROWS;
+        double* dst = vc + (t & 1) * BW * BT_ROWS;
+        for (int e = threadIdx.x; e < BW * (BT_ROWS / 2); e += nthr) {
+          const int c = e / (BT_ROWS / 2), r2 = (e % (BT_ROWS / 2)) * 2;
+          const int left = n - (q0 + r2);
+          const int bytes = left >= 2 ? 16 : (left == 1 ? 8 : 0);
+          cp_async16(dst + c * BT_ROWS + r2, bytes ? Vp + int64_t(c) * NP + q0 + r2 : Vp, bytes);
+        }
+        cp_async_commit();
+      };
+      for (int e = threadIdx.x; e < BW * BW; e += nthr) ts[e] = Vp[BW * NP + e];
+      issue(0);
+      double y[BW], zz[BW];
 #pragma unroll
       for (int c = 0; c < BW; ++c) y[c] = 0.0;
-      for (int q = jlo + lane; q < n; q += 32) {
-        const double xq = x[sx(q)];
+      for (int t = 0; t < 2 * nq; ++t) {
+        if (t + 1 < 2 * nq) {
+          issue(t + 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* cb = vc + (t & 1) * BW * BT_ROWS;
+        const int q0 = jlo + (t % nq) * BT_ROWS;
+        if (t == nq) {  // pass 1 done: y = V^T x (warp sum), z = T y
 #pragma unroll
-        for (int c = 0; c < BW; ++c) y[c] = fma(Vp[c * NP + q], xq, y[c]);
+          for (int c = 0; c < BW; ++c) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
+          }
+#pragma unroll
+          for (int a = 0; a < BW; ++a) {
+            double acc = 0.0;
+#pragma unroll
+            for (int b2 = 0; b2 < BW; ++b2) acc = fma(ts[a * BW + b2], y[b2], acc);
+            zz[a] = acc;
+          }
+        }
+        if (act) {
+          for (int r = lane; r < BT_ROWS && q0 + r < n; r += 32) {
+            if (t < nq) {
+              const double xq = x[sx(q0 + r)];
+#pragma unroll
+              for (int c = 0; c < BW; ++c) y[c] = fma(cb[c * BT_ROWS + r], xq, y[c]);
+            } else {
+              double acc = x[sx(q0 + r)];
+#pragma unroll
+              for (int c = 0; c < BW; ++c) acc = fma(-cb[c * BT_ROWS + r], zz[c], acc);
+              x[sx(q0 + r)] = acc;
+            }
+          }
+        }
+        __syncthreads();  // the buffer is refilled two steps later
       }
-#pragma unroll
-      for (int c = 0; c < BW; ++c) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) y[c] += __shfl_xor_sync(0xffffffffu, y[c], o);
-      }
-      double zz[BW];
-#pragma unroll
-      for (int a = 0; a < BW; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < BW; ++b) acc = fma(Tp[a * BW + b], y[b], acc);
-        zz[a] = acc;
-      }
-      for (int q = jlo + lane; q < n; q += 32) {
-        double acc = x[sx(q)];
-#pragma unroll
-        for (int c = 0; c < BW; ++c) acc = fma(-Vp[c * NP + q], zz[c], acc);
-        x[sx(q)] = acc;
-      }
-      __syncwarp();
     }
-    for (int q = lane; q < RP; q += 32) vg[q] = q < n ? x[sx(q)] : 0.0;
     __syncwarp();
+    if (act)
+      for (int q = lane; q < RP; q += 32) vg[q] = q < n ? x[sx(q)] : 0.0;
+    __syncthreads();
   }
 }
 
@@ -2475,7 +2524,7 @@ struct Plan {
   bool by_slice;            // state kept per slice across calls
   int ns;
   size_t jsmem, rsmem, bsmem;
-  int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages;
+  int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages, bt_g;
   int64_t hhcap, count;
   bool hb_gmem;
   int hb_threads;
@@ -2576,8 +2625,10 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.slots_v = clampc(int64_t(sms) * per);
     g.slots_j = g.slots_v;  // vecout uses the X slots
     g.slots_t = clampc(int64_t(sms) * 8);  // CGS2 warps (one per slice)
-    g.tsmem = size_t(BT_WARPS) * bt_stride(g.n) * sizeof(double);
-    rc = occupancy((const void*)svd_backtransform_kernel, BT_WARPS * 32, g.tsmem, &per);
+    g.bt_g = 8;  // vectors (warps) per back-transform CTA
+    while (g.bt_g > 1 && bt_smem(g.n, g.bt_g) > size_t(200 * 1024)) --g.bt_g;
+    g.tsmem = bt_smem(g.n, g.bt_g);
+    rc = occupancy((const void*)svd_backtransform_kernel, 32 * g.bt_g, g.tsmem, &per);
     if (rc) return rc;
     g.btw = per;  // back-transform CTAs per SM
     const int64_t work = count * g.n;
@@ -2867,14 +2918,15 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
     svd_orth_kernel<<<pl.slots_t, 32, 0, st>>>(P);
     STARM_LAUNCH_CHECK();
     {
-      const int64_t items = count * pl.n;
-      int64_t blocks = (items + BT_WARPS - 1) / BT_WARPS;
+      // one CTA per (slice, group of bt_g vectors); groups beyond a slice's
+      // rank exit at once
+      int64_t blocks = count * ((pl.n + pl.bt_g - 1) / pl.bt_g);
       int dev = 0, sms = 0;
       STARM_CUDA_TRY(cudaGetDevice(&dev));
       STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const int64_t cap = int64_t(sms) * pl.btw * 4;
+      const int64_t cap = int64_t(sms) * pl.btw * 8;
       if (blocks > cap) blocks = cap;
-      svd_backtransform_kernel<<<unsigned(blocks), BT_WARPS * 32, pl.tsmem, st>>>(P, items);
+      svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g);
     }
     STARM_LAUNCH_CHECK();
     SvdParams Pv = P;
