@@ -1,7 +1,7 @@
 # Builds the sm_100a C-ABI library in-tree (it travels to the GPU box with gpurun).
 NVCC     ?= /usr/local/cuda/bin/nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_2605_16058_b200/csrc
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 $(NVEXTRA) -Xcompiler -fPIC -Iinclude -Ipaper_2605_16058_b200/csrc
 SRCS     := $(wildcard paper_2605_16058_b200/csrc/*.cu)
 OBJS     := $(SRCS:paper_2605_16058_b200/csrc/%.cu=build/%.o)
 LIB      := paper_2605_16058_b200/libstarm.so

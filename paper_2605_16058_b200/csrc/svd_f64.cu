@@ -1095,6 +1095,293 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------
+// Register-resident team updates (one HBM/L2 read + one write per element
+// per panel instead of two reads + one write through an SMEM ring).
+//
+// The warps form teams of TW in {1, 2, 4, 8}; a team owns one 8-column group
+// (left update) or one 8-row tile (right update) at a time and holds it in
+// registers across both passes: each warp keeps up to TT 8x8 blocks of it,
+// two doubles per lane, in a layout that is at once the B fragment of pass 1
+// and the accumulator of pass 2 (the k index of pass 1 and the output index
+// of pass 2 are permuted by sigma(j) = (j >> 1) + 4 (j & 1) so the two
+// coincide).  The team sums its partial Y through SMEM (fixed warp order:
+// deterministic), every warp forms Z on DMMA, and pass 2 accumulates -Z V^T
+// straight into the held block.  TW is the smallest team whose registers
+// cover the rows (columns); beyond 8 * TT blocks the caller uses the ring
+// path.
+// ---------------------------------------------------------------------
+constexpr int TTL = 24;  // 8x8 blocks per warp held in registers (left update)
+constexpr int TTR = 16;  // (right update: more live addresses)
+
+__device__ __forceinline__ int64_t round_up16(int64_t v) { return (v + 15) & ~int64_t(15); }
+
+__device__ __forceinline__ void team_sync(int team, int tw) {
+  if (tw == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(tw * 32) : "memory");
+}
+
+template <int NT, int TT>
+__device__ __forceinline__ int team_width(int blocks) {
+  int tw = 1;
+  while (tw < NT / 32 && tw * TT < blocks) tw <<= 1;
+  return tw * TT >= blocks ? tw : 0;
+}
+
+// C <- (I - V T^T V^T) C on rows [r0, nrows) x columns [c_start, NP) of X
+// (ld); V = pan (rows from r0, explicit: zero above the pivots), T = q.t.
+// ybuf: 2 x NT/32 x 128 doubles.  Returns false (nothing done) when the rows
+// exceed the register capacity.
+template <int NT, int tw>
+__device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, const double* pan, int prs,
+                                                double* X, int ld, int ntiles, int NP, int r0, int c_start) {
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
+  const int my = wit < ntiles ? (ntiles - wit + tw - 1) / tw : 0;
+  const int ngroups = (NP - c_start) >> 3;
+  const int sg = (gq >> 1) + 4 * (gq & 1);
+  double tf[4][2];  // T[4kk + tq][8h + gq] (B fragments, loop invariant)
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + gq];
+  const int rw = r0 + wit * 8;
+  constexpr int ts = tw * 8;  // first row of this warp's tiles, tile stride
+  const double* pA = pan + gq * prs + rw + tq;       // V[row tq (+4)][col gq (+8)]
+  const double* pB = pan + 2 * tq * prs + rw + sg;   // V[row sigma(gq)][col 2tq (+8h+e)]
+  const int rows_bytes = (ntiles * 8) * 8;
+#ifdef STARM_TEAM_PROBE
+  long long tp[5] = {0, 0, 0, 0, 0};
+  long long tq0 = clock64();
+#endif
+  int it = 0;
+  for (int g = team; g < ngroups; g += nteams, ++it) {
+    // warm L2 with the team's next column group (one bulk prefetch per column)
+    if (wit == 0 && lane < 8 && g + nteams < ngroups)
+      bulk_prefetch_l2(X + (c_start + 8 * (g + nteams) + lane) * ld + r0, rows_bytes);
+    double* xc = X + (c_start + 8 * g + gq) * ld + rw + tq;  // C[row tq / tq+4][col gq]
+    double c[TTL][2];
+#pragma unroll
+    for (int i = 0; i < TTL; ++i)
+      if (i < my) {
+        c[i][0] = xc[i * ts];
+        c[i][1] = xc[i * ts + 4];
+      } else {
+        c[i][0] = c[i][1] = 0.0;  // (ends the block's liveness across groups)
+      }
+#ifdef STARM_TEAM_PROBE
+    long long tq1 = clock64();
+    {
+      double dsum = 0.0;
+#pragma unroll
+      for (int i = 0; i < TTL; ++i) asm volatile("add.f64 %0, %0, %1;" : "+d"(dsum) : "d"(c[i][1]));
+      asm volatile("add.f64 %0, %0, %0;" : "+d"(dsum));
+    }
+    long long tq2 = clock64();
+#endif
+    // pass 1: Y = V^T C (16 x 8); lane accumulates Y[8h + gq][2tq + e] in
+    // four independent chains per half
+    double y[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[h][u][0] = y[h][u][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < TTL; ++i)
+      if (i < my) {
+        const double* pa = pA + i * ts;
+        double va[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) va[v] = pa[(v >> 1) * 8 * prs + 4 * (v & 1)];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            dmma884n(y[h][(2 * i + ks) & 3][0], y[h][(2 * i + ks) & 3][1], va[h * 2 + ks], c[i][ks]);
+      }
+    double* yb = ybuf + (it & 1) * NW * 128;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        yb[warp * 128 + (8 * h + gq) * 8 + 2 * tq + e] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
+#ifdef STARM_TEAM_PROBE
+    long long tq3 = clock64();
+#endif
+    team_sync(team, tw);
+#ifdef STARM_TEAM_PROBE
+    long long tq4 = clock64();
+#endif
+    // Z^T = Y^T T (8 x 16): A[gq][tq] of k-step kk = Y[4kk + tq][gq];
+    // lane ends with Z[8h + 2tq + e][gq]
+    double zt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const double* tb = yb + team * tw * 128;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < tw; ++w) a += tb[w * 128 + (4 * kk + tq) * 8 + gq];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) dmma884n(zt[h][0], zt[h][1], a, tf[kk][h]);
+    }
+    // pass 2: C^T += (-Z^T) V^T with k = 8h + 2tq + e (k-step 2h + e);
+    // k-step-major so consecutive DMMAs update different blocks
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const double nz = -zt[kk >> 1][kk & 1];
+      const double* pb = pB + (8 * (kk >> 1) + (kk & 1)) * prs;
+#pragma unroll
+      for (int i = 0; i < TTL; ++i)
+        if (i < my) dmma884n(c[i][0], c[i][1], nz, pb[i * ts]);
+    }
+#pragma unroll
+    for (int i = 0; i < TTL; ++i)
+      if (i < my) {
+        xc[i * ts] = c[i][0];
+        xc[i * ts + 4] = c[i][1];
+      }
+#ifdef STARM_TEAM_PROBE
+    long long tq5 = clock64();
+    tp[0] += tq1 - tq0;  // previous group's stores issued -> loads issued
+    tp[1] += tq2 - tq1;  // load wait
+    tp[2] += tq3 - tq2;  // pass 1
+    tp[3] += tq4 - tq3;  // team barrier
+    tp[4] += tq5 - tq4;  // Z + pass 2 + stores issued
+    tq0 = tq5;
+#endif
+  }
+#ifdef STARM_TEAM_PROBE
+  if (lane == 0 && warp == 0) {
+    atomicAdd(&g_stats[ST_CYC_GRAM], (unsigned long long)tp[1]);
+    atomicAdd(&g_stats[ST_CYC_EIG], (unsigned long long)tp[2]);
+    atomicAdd(&g_stats[ST_CYC_APPLY], (unsigned long long)tp[3]);
+    atomicAdd(&g_stats[ST_CYC_FINAL], (unsigned long long)tp[4]);
+    atomicAdd(&g_stats[ST_CYC_PMISC], (unsigned long long)tp[0]);
+  }
+#endif
+}
+
+template <int NT>
+__device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan, int prs, double* X,
+                                 int ld, int nrows, int NP, int r0, int c_start) {
+  const int ntiles = (nrows - r0) >> 3;
+  switch (team_width<NT, TTL>(ntiles)) {
+    case 1: team_left_update_t<NT, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
+    case 2: team_left_update_t<NT, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
+    case 4: team_left_update_t<NT, 4>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
+    case 8: team_left_update_t<NT, 8>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
+    default: return false;
+  }
+  __syncthreads();
+  return true;
+}
+
+// C <- C (I - V T V^T) on rows [rmin, nrows) x columns [j0, NP) of A (ld);
+// V[j][c] = pan2[c * prs + j] (explicit, zero left of the pivots).
+template <int NT, int tw>
+__device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, const double* pan2, int prs,
+                                                 double* A, int ld, int nrows, int nch, int rmin, int j0) {
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
+  const int my = wit < nch ? (nch - wit + tw - 1) / tw : 0;
+  const int ntile = (nrows - rmin) >> 3;
+  const int sg = (gq >> 1) + 4 * (gq & 1);
+  double tf[4][2];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + gq];
+  const int cw = j0 + wit * 8;
+  constexpr int cs = tw * 8;        // first column of this warp's chunks, chunk stride
+  const double* pB1 = pan2 + gq * prs + cw + tq;      // V[col tq (+4e)][8h + gq]
+  const double* pB2 = pan2 + 2 * tq * prs + cw + sg;  // V[col sigma(gq)][8h + 2tq + e]
+  int it = 0;
+  for (int t = team; t < ntile; t += nteams, ++it) {
+    double* xr = A + (cw + tq) * ld + rmin + 8 * t + gq;  // C[row gq][col tq / tq+4]
+    int ld4 = 4 * ld, ldc = cs * ld;
+    asm volatile("" : "+r"(ld4), "+r"(ldc));  // keep the per-chunk offsets out of the loop-invariant set
+    double c[TTR][2];
+#pragma unroll
+    for (int i = 0; i < TTR; ++i)
+      if (i < my) {
+        c[i][0] = xr[i * ldc];
+        c[i][1] = xr[i * ldc + ld4];
+      } else {
+        c[i][0] = c[i][1] = 0.0;
+      }
+    // pass 1: Y = C V (8 x 16); lane accumulates Y[gq][8h + 2tq + e]
+    double y[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[h][u][0] = y[h][u][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < TTR; ++i)
+      if (i < my) {
+        const double* pb = pB1 + i * cs;
+        double va[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) va[v] = pb[(v >> 1) * 8 * prs + 4 * (v & 1)];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            dmma884n(y[h][(2 * i + e) & 3][0], y[h][(2 * i + e) & 3][1], c[i][e], va[h * 2 + e]);
+      }
+    double* yb = ybuf + (it & 1) * NW * 128;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        yb[warp * 128 + gq * 16 + 8 * h + 2 * tq + e] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
+    team_sync(team, tw);
+    // Z = Y T (8 x 16): A[gq][tq] of k-step kk = Y[gq][4kk + tq]; lane ends
+    // with Z[gq][8h + 2tq + e]
+    double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const double* tb = yb + team * tw * 128;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < tw; ++w) a += tb[w * 128 + gq * 16 + 4 * kk + tq];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) dmma884n(z[h][0], z[h][1], a, tf[kk][h]);
+    }
+    // pass 2: C += (-Z) V^T with k = 8h + 2tq + e, k-step-major
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const double nz = -z[kk >> 1][kk & 1];
+      const double* pb = pB2 + (8 * (kk >> 1) + (kk & 1)) * prs;
+#pragma unroll
+      for (int i = 0; i < TTR; ++i)
+        if (i < my) dmma884n(c[i][0], c[i][1], nz, pb[i * cs]);
+    }
+#pragma unroll
+    for (int i = 0; i < TTR; ++i)
+      if (i < my) {
+        xr[i * ldc] = c[i][0];
+        xr[i * ldc + ld4] = c[i][1];
+      }
+  }
+}
+
+template <int NT>
+__device__ bool team_right_update(QrSmemFixed& q, double* ybuf, const double* pan2, int prs, double* A,
+                                  int ld, int nrows, int NP, int rmin, int j0) {
+  const int nch = (NP - j0) >> 3;
+  switch (team_width<NT, TTR>(nch)) {
+    case 1: team_right_update_t<NT, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
+    case 2: team_right_update_t<NT, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
+    case 4: team_right_update_t<NT, 4>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
+    case 8: team_right_update_t<NT, 8>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
+    default: return false;
+  }
+  __syncthreads();
+  return true;
+}
+
 // Panel -> explicit V (zeros above the pivot, 1 on it) for rows [0, prs).
 template <int NT>
 __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0, int64_t nrows) {
@@ -1113,7 +1400,7 @@ __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0,
 // block and zeros below it.
 template <int NT>
 __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double* pan, int64_t prs,
-                         double* wbase, double* X, long long& pf, long long& tr) {
+                         double* wbase, double* X, int64_t live, long long& pf, long long& tr) {
   const int64_t LP = P.LP, NP = P.NP;
   const int tid = threadIdx.x;
   for (int64_t k0 = 0; k0 < NP; k0 += BW) {
@@ -1128,8 +1415,10 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
       explicit_v<NT>(pan, prs, k0, LP);
       panel_gram<NT>(q, pan, prs, kc, LP);
       long long _a = clock64();
-      P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
-             : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
+      if (!team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
+                                int(k0 + BW)))
+        P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
+               : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
       tr += clock64() - _a;
     }
     __syncthreads();
@@ -1147,7 +1436,7 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
 //   panels (compact-WY updates on DMMA, nst-stage cp.async ring) -> the 17
 //   diagonals of B to bandbuf.  Vector jobs also log P1's panels (V, T).
 template <int NT>
-__global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
+__global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
   const int64_t LP = P.LP, NP = P.NP, RP = P.RP, n = P.n;
@@ -1177,7 +1466,7 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
     long long t1 = clock64();
     long long pf = 0, tr = 0, ru = 0;
     // ---------------- QR of the tall X (rows LP)
-    if (P.L > P.n) qr_phase<NT>(P, q, pan, prs, wbase, X, pf, tr);
+    if (P.L > P.n) qr_phase<NT>(P, q, pan, prs, wbase, X, round_up16(P.L), pf, tr);
     long long t2 = clock64();
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
@@ -1193,8 +1482,10 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
       panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
-        P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
-               : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
+        if (!team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
+                                  int(k + BW)))
+          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
+                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
         tr += clock64() - _a;
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
@@ -1215,8 +1506,12 @@ __global__ void __launch_bounds__(NT) svd_reduce_kernel(SvdParams P) {
       }
       {
         long long _a = clock64();
-        if (P.wtwo) right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
-        else right_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        if (team_right_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0))) {
+        } else if (P.wtwo) {
+          right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        } else {
+          right_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+        }
         ru += clock64() - _a;
       }
       __syncthreads();
@@ -1272,7 +1567,7 @@ __global__ void __launch_bounds__(NT) svd_tsqr_kernel(SvdParams P, double* S, in
       __syncthreads();
       continue;
     }
-    if (flag == 0) qr_phase<NT>(P, q, pan, prs, wbase, X, pf, tr);
+    if (flag == 0) qr_phase<NT>(P, q, pan, prs, wbase, X, LP, pf, tr);
     for (int64_t e = tid; e < NP * n; e += NT) {
       const int64_t r = e % NP, c = e / NP;
       Sd[r + c * SP] = (flag == 0 && r <= c) ? X[r + c * LP] : 0.0;
