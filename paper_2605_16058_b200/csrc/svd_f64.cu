@@ -1096,23 +1096,52 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
 }
 
 // ---------------------------------------------------------------------
-// Register-resident team updates (one HBM/L2 read + one write per element
-// per panel instead of two reads + one write through an SMEM ring).
+// Register-resident team updates (one HBM/L2 read + one write of every
+// trailing block per panel).
 //
 // The warps form teams of TW in {1, 2, 4, 8}; a team owns one 8-column group
 // (left update) or one 8-row tile (right update) at a time and holds it in
-// registers across both passes: each warp keeps up to TT 8x8 blocks of it,
-// two doubles per lane, in a layout that is at once the B fragment of pass 1
-// and the accumulator of pass 2 (the k index of pass 1 and the output index
-// of pass 2 are permuted by sigma(j) = (j >> 1) + 4 (j & 1) so the two
-// coincide).  The team sums its partial Y through SMEM (fixed warp order:
-// deterministic), every warp forms Z on DMMA, and pass 2 accumulates -Z V^T
-// straight into the held block.  TW is the smallest team whose registers
-// cover the rows (columns); beyond 8 * TT blocks the caller uses the ring
-// path.
+// registers across both passes: each warp keeps up to TT 8x8 blocks, two
+// doubles per lane, in a layout that is at once the B (A) fragment of
+// pass 1 and the accumulator of pass 2 (pass 1 sums over the rows (columns)
+// in the order the lane holds them; pass 2's k index is permuted to
+// pi(h, e, t) = 8h + t + 4e, which the T fragments of Z absorb).  While a
+// group is processed, the warp's blocks of its next group stream into a
+// per-warp SMEM stage by cp.async, so the global latency hides behind the
+// DMMA work.  The team sums its partial Y through SMEM in a fixed warp
+// order (deterministic), every warp forms Z on DMMA, and pass 2 accumulates
+// -Z V^T straight into the held blocks.  TW is the smallest team whose
+// registers cover the rows (columns); beyond 8 * TT blocks the caller falls
+// back to the ring path.
+//
+// SMEM (after the panel): ybuf 2 x NW x 128 doubles, then the stage
+// NW x TT x 64 doubles.
 // ---------------------------------------------------------------------
-constexpr int TTL = 24;  // 8x8 blocks per warp held in registers (left update)
-constexpr int TTR = 16;  // (right update: more live addresses)
+constexpr int TT = 16;  // 8x8 blocks per warp held in registers
+constexpr int YB = 144;  // doubles per warp partial of Y (padded: conflict-free 16-byte reads)
+constexpr int TEAM_SMEM_DOUBLES = 2 * 8 * YB + 8 * TT * 64;  // for 8 warps
+
+// Team sum of the warps' partial Y (fixed warp order): lane gets the four
+// values Y[4kk + tq][gq] (left) / Y[gq][4kk + tq] (right), stored at
+// gq * 18 + tq * 4 + kk of every warp's block.
+template <int tw>
+__device__ __forceinline__ void team_ysum(const double* tb, int gq, int tq, double (&a)[4]) {
+  const double* src = tb + gq * 18 + tq * 4;
+  double2 s0 = *reinterpret_cast<const double2*>(src), s1 = *reinterpret_cast<const double2*>(src + 2);
+#pragma unroll
+  for (int w = 1; w < tw; ++w) {
+    const double2 u0 = *reinterpret_cast<const double2*>(src + w * YB);
+    const double2 u1 = *reinterpret_cast<const double2*>(src + w * YB + 2);
+    s0.x += u0.x;
+    s0.y += u0.y;
+    s1.x += u1.x;
+    s1.y += u1.y;
+  }
+  a[0] = s0.x;
+  a[1] = s0.y;
+  a[2] = s1.x;
+  a[3] = s1.y;
+}
 
 __device__ __forceinline__ int64_t round_up16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
@@ -1121,17 +1150,26 @@ __device__ __forceinline__ void team_sync(int team, int tw) {
   else asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(tw * 32) : "memory");
 }
 
-template <int NT, int TT>
+template <int NT>
 __device__ __forceinline__ int team_width(int blocks) {
   int tw = 1;
   while (tw < NT / 32 && tw * TT < blocks) tw <<= 1;
   return tw * TT >= blocks ? tw : 0;
 }
 
-// C <- (I - V T^T V^T) C on rows [r0, nrows) x columns [c_start, NP) of X
-// (ld); V = pan (rows from r0, explicit: zero above the pivots), T = q.t.
-// ybuf: 2 x NT/32 x 128 doubles.  Returns false (nothing done) when the rows
-// exceed the register capacity.
+// T as B fragments of Z^T = Y^T T' / Z = Y T' with T'[l][8h + 2t + e] =
+// T[l][8h + t + 4e]: tf[kk][h] = T[4kk + tq][8h + phi(gq)], phi(j) = (j >> 1) + 4 (j & 1).
+__device__ __forceinline__ void load_tf(const QrSmemFixed& q, double (&tf)[4][2], int gq, int tq) {
+  const int ph = (gq >> 1) + 4 * (gq & 1);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + ph];
+}
+
+// C <- (I - V T^T V^T) C on rows [r0, r0 + 8 ntiles) x columns [c_start, NP)
+// of X (ld); V = pan (explicit: zero above the pivots), T = q.t.
+// Lane (gq, tq) holds C[2tq + ks][gq] of each block (ks = 0, 1).
 template <int NT, int tw>
 __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, const double* pan, int prs,
                                                 double* X, int ld, int ntiles, int NP, int r0, int c_start) {
@@ -1140,133 +1178,98 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
   const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
   const int my = wit < ntiles ? (ntiles - wit + tw - 1) / tw : 0;
   const int ngroups = (NP - c_start) >> 3;
-  const int sg = (gq >> 1) + 4 * (gq & 1);
-  double tf[4][2];  // T[4kk + tq][8h + gq] (B fragments, loop invariant)
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + gq];
+  double tf[4][2];
+  load_tf(q, tf, gq, tq);
   const int rw = r0 + wit * 8;
-  constexpr int ts = tw * 8;  // first row of this warp's tiles, tile stride
-  const double* pA = pan + gq * prs + rw + tq;       // V[row tq (+4)][col gq (+8)]
-  const double* pB = pan + 2 * tq * prs + rw + sg;   // V[row sigma(gq)][col 2tq (+8h+e)]
-  const int rows_bytes = (ntiles * 8) * 8;
-#ifdef STARM_TEAM_PROBE
-  long long tp[5] = {0, 0, 0, 0, 0};
-  long long tq0 = clock64();
-#endif
+  constexpr int ts = tw * 8;                        // row stride between a warp's blocks
+  const double* pA = pan + gq * prs + rw + 2 * tq;  // V[row 2tq (+ks)][col gq (+8h)]
+  const double* pB = pan + tq * prs + rw + gq;      // V[row gq][col tq (+8h+4e)]
+  double* st = ybuf + 2 * NW * YB + warp * (TT * 64) + 2 * lane;  // stage slot i: st + 64 i
+  auto issue = [&](int g) {
+    const double* src = X + (c_start + 8 * g + gq) * ld + rw + 2 * tq;
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+      if (i < my) cp_async16(st + 64 * i, src + i * ts);
+    cp_async_commit();
+  };
+  if (team < ngroups) issue(team);
   int it = 0;
   for (int g = team; g < ngroups; g += nteams, ++it) {
-    // warm L2 with the team's next column group (one bulk prefetch per column)
-    if (wit == 0 && lane < 8 && g + nteams < ngroups)
-      bulk_prefetch_l2(X + (c_start + 8 * (g + nteams) + lane) * ld + r0, rows_bytes);
-    double* xc = X + (c_start + 8 * g + gq) * ld + rw + tq;  // C[row tq / tq+4][col gq]
-    double c[TTL][2];
+    cp_async_wait<0>();
+    double c[TT][2];
 #pragma unroll
-    for (int i = 0; i < TTL; ++i)
+    for (int i = 0; i < TT; ++i)
       if (i < my) {
-        c[i][0] = xc[i * ts];
-        c[i][1] = xc[i * ts + 4];
+        const double2 v = *reinterpret_cast<const double2*>(st + 64 * i);
+        c[i][0] = v.x;
+        c[i][1] = v.y;
       } else {
         c[i][0] = c[i][1] = 0.0;  // (ends the block's liveness across groups)
       }
-#ifdef STARM_TEAM_PROBE
-    long long tq1 = clock64();
-    {
-      double dsum = 0.0;
-#pragma unroll
-      for (int i = 0; i < TTL; ++i) asm volatile("add.f64 %0, %0, %1;" : "+d"(dsum) : "d"(c[i][1]));
-      asm volatile("add.f64 %0, %0, %0;" : "+d"(dsum));
-    }
-    long long tq2 = clock64();
-#endif
+    if (g + nteams < ngroups) issue(g + nteams);  // own slots were just read
     // pass 1: Y = V^T C (16 x 8); lane accumulates Y[8h + gq][2tq + e] in
-    // four independent chains per half
+    // four chains per half
     double y[2][4][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int u = 0; u < 4; ++u) y[h][u][0] = y[h][u][1] = 0.0;
 #pragma unroll
-    for (int i = 0; i < TTL; ++i)
-      if (i < my) {
+    for (int i = 0; i < TT; ++i) {
+      if (i >= my) break;  // (a branch, not predication: predicated-off DMMAs still occupy the pipe)
+      {
         const double* pa = pA + i * ts;
-        double va[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) va[v] = pa[(v >> 1) * 8 * prs + 4 * (v & 1)];
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            dmma884n(y[h][(2 * i + ks) & 3][0], y[h][(2 * i + ks) & 3][1], va[h * 2 + ks], c[i][ks]);
+        for (int h = 0; h < 2; ++h) {
+          const double2 va = *reinterpret_cast<const double2*>(pa + 8 * h * prs);
+          dmma884n(y[h][(2 * i) & 3][0], y[h][(2 * i) & 3][1], va.x, c[i][0]);
+          dmma884n(y[h][(2 * i + 1) & 3][0], y[h][(2 * i + 1) & 3][1], va.y, c[i][1]);
+        }
       }
-    double* yb = ybuf + (it & 1) * NW * 128;
+    }
+    double* yb = ybuf + (it & 1) * NW * YB;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        yb[warp * 128 + (8 * h + gq) * 8 + 2 * tq + e] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
-#ifdef STARM_TEAM_PROBE
-    long long tq3 = clock64();
-#endif
+      for (int e = 0; e < 2; ++e) {  // Y[r = 8h + gq][c = 2tq + e] -> c * 18 + (r & 3) * 4 + (r >> 2)
+        const int r = 8 * h + gq;
+        yb[warp * YB + (2 * tq + e) * 18 + (r & 3) * 4 + (r >> 2)] =
+            (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
+      }
     team_sync(team, tw);
-#ifdef STARM_TEAM_PROBE
-    long long tq4 = clock64();
-#endif
-    // Z^T = Y^T T (8 x 16): A[gq][tq] of k-step kk = Y[4kk + tq][gq];
-    // lane ends with Z[8h + 2tq + e][gq]
+    // Z^T = Y^T T': A[gq][tq] of k-step kk = Y[4kk + tq][gq]; lane ends with
+    // zt[h][e] = Z[8h + tq + 4e][gq]
     double zt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    const double* tb = yb + team * tw * 128;
+    double ya[4];
+    team_ysum<tw>(yb + team * tw * YB, gq, tq, ya);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      double a = 0.0;
+    for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-      for (int w = 0; w < tw; ++w) a += tb[w * 128 + (4 * kk + tq) * 8 + gq];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) dmma884n(zt[h][0], zt[h][1], a, tf[kk][h]);
-    }
-    // pass 2: C^T += (-Z^T) V^T with k = 8h + 2tq + e (k-step 2h + e);
+      for (int h = 0; h < 2; ++h) dmma884n(zt[h][0], zt[h][1], ya[kk], tf[kk][h]);
+    // pass 2: C^T += (-Z^T) V^T, k-step (h, e) <-> k = 8h + tq + 4e,
     // k-step-major so consecutive DMMAs update different blocks
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const double nz = -zt[kk >> 1][kk & 1];
-      const double* pb = pB + (8 * (kk >> 1) + (kk & 1)) * prs;
+      const double* pb = pB + (8 * (kk >> 1) + 4 * (kk & 1)) * prs;
 #pragma unroll
-      for (int i = 0; i < TTL; ++i)
-        if (i < my) dmma884n(c[i][0], c[i][1], nz, pb[i * ts]);
-    }
-#pragma unroll
-    for (int i = 0; i < TTL; ++i)
-      if (i < my) {
-        xc[i * ts] = c[i][0];
-        xc[i * ts + 4] = c[i][1];
+      for (int i = 0; i < TT; ++i) {
+        if (i >= my) break;
+        dmma884n(c[i][0], c[i][1], nz, pb[i * ts]);
       }
-#ifdef STARM_TEAM_PROBE
-    long long tq5 = clock64();
-    tp[0] += tq1 - tq0;  // previous group's stores issued -> loads issued
-    tp[1] += tq2 - tq1;  // load wait
-    tp[2] += tq3 - tq2;  // pass 1
-    tp[3] += tq4 - tq3;  // team barrier
-    tp[4] += tq5 - tq4;  // Z + pass 2 + stores issued
-    tq0 = tq5;
-#endif
+    }
+    double* xc = X + (c_start + 8 * g + gq) * ld + rw + 2 * tq;
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+      if (i < my) *reinterpret_cast<double2*>(xc + i * ts) = make_double2(c[i][0], c[i][1]);
   }
-#ifdef STARM_TEAM_PROBE
-  if (lane == 0 && warp == 0) {
-    atomicAdd(&g_stats[ST_CYC_GRAM], (unsigned long long)tp[1]);
-    atomicAdd(&g_stats[ST_CYC_EIG], (unsigned long long)tp[2]);
-    atomicAdd(&g_stats[ST_CYC_APPLY], (unsigned long long)tp[3]);
-    atomicAdd(&g_stats[ST_CYC_FINAL], (unsigned long long)tp[4]);
-    atomicAdd(&g_stats[ST_CYC_PMISC], (unsigned long long)tp[0]);
-  }
-#endif
 }
 
 template <int NT>
 __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan, int prs, double* X,
                                  int ld, int nrows, int NP, int r0, int c_start) {
   const int ntiles = (nrows - r0) >> 3;
-  switch (team_width<NT, TTL>(ntiles)) {
+  switch (team_width<NT>(ntiles)) {
     case 1: team_left_update_t<NT, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
     case 2: team_left_update_t<NT, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
     case 4: team_left_update_t<NT, 4>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
@@ -1279,6 +1282,7 @@ __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan
 
 // C <- C (I - V T V^T) on rows [rmin, nrows) x columns [j0, NP) of A (ld);
 // V[j][c] = pan2[c * prs + j] (explicit, zero left of the pivots).
+// Lane (gq, tq) holds C[gq][2tq + e] of each block.
 template <int NT, int tw>
 __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, const double* pan2, int prs,
                                                  double* A, int ld, int nrows, int nch, int rmin, int j0) {
@@ -1287,30 +1291,39 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
   const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
   const int my = wit < nch ? (nch - wit + tw - 1) / tw : 0;
   const int ntile = (nrows - rmin) >> 3;
-  const int sg = (gq >> 1) + 4 * (gq & 1);
   double tf[4][2];
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + gq];
+  load_tf(q, tf, gq, tq);
   const int cw = j0 + wit * 8;
-  constexpr int cs = tw * 8;        // first column of this warp's chunks, chunk stride
-  const double* pB1 = pan2 + gq * prs + cw + tq;      // V[col tq (+4e)][8h + gq]
-  const double* pB2 = pan2 + 2 * tq * prs + cw + sg;  // V[col sigma(gq)][8h + 2tq + e]
+  constexpr int cs = tw * 8;                          // column stride between a warp's blocks
+  const double* pB1 = pan2 + gq * prs + cw + 2 * tq;  // V[col 2tq (+e)][8h + gq]
+  const double* pB2 = pan2 + tq * prs + cw + gq;      // V[col gq][8h + tq + 4e]
+  double* st = ybuf + 2 * NW * YB + warp * (TT * 64) + 2 * lane;
+  int ldc = cs * ld;
+  auto issue = [&](int t) {
+    const double* src = A + (cw + 2 * tq) * ld + rmin + 8 * t + gq;
+#pragma unroll
+    for (int i = 0; i < TT; ++i)
+      if (i < my) {
+        cp_async8(st + 64 * i, src + i * ldc);
+        cp_async8(st + 64 * i + 1, src + i * ldc + ld);
+      }
+    cp_async_commit();
+  };
+  if (team < ntile) issue(team);
   int it = 0;
   for (int t = team; t < ntile; t += nteams, ++it) {
-    double* xr = A + (cw + tq) * ld + rmin + 8 * t + gq;  // C[row gq][col tq / tq+4]
-    int ld4 = 4 * ld, ldc = cs * ld;
-    asm volatile("" : "+r"(ld4), "+r"(ldc));  // keep the per-chunk offsets out of the loop-invariant set
-    double c[TTR][2];
+    cp_async_wait<0>();
+    double c[TT][2];
 #pragma unroll
-    for (int i = 0; i < TTR; ++i)
+    for (int i = 0; i < TT; ++i)
       if (i < my) {
-        c[i][0] = xr[i * ldc];
-        c[i][1] = xr[i * ldc + ld4];
+        const double2 v = *reinterpret_cast<const double2*>(st + 64 * i);
+        c[i][0] = v.x;
+        c[i][1] = v.y;
       } else {
         c[i][0] = c[i][1] = 0.0;
       }
+    if (t + nteams < ntile) issue(t + nteams);
     // pass 1: Y = C V (8 x 16); lane accumulates Y[gq][8h + 2tq + e]
     double y[2][4][2];
 #pragma unroll
@@ -1318,51 +1331,54 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
 #pragma unroll
       for (int u = 0; u < 4; ++u) y[h][u][0] = y[h][u][1] = 0.0;
 #pragma unroll
-    for (int i = 0; i < TTR; ++i)
-      if (i < my) {
+    for (int i = 0; i < TT; ++i) {
+      if (i >= my) break;
+      {
         const double* pb = pB1 + i * cs;
-        double va[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) va[v] = pb[(v >> 1) * 8 * prs + 4 * (v & 1)];
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            dmma884n(y[h][(2 * i + e) & 3][0], y[h][(2 * i + e) & 3][1], c[i][e], va[h * 2 + e]);
+        for (int h = 0; h < 2; ++h) {
+          const double2 vb = *reinterpret_cast<const double2*>(pb + 8 * h * prs);
+          dmma884n(y[h][(2 * i) & 3][0], y[h][(2 * i) & 3][1], c[i][0], vb.x);
+          dmma884n(y[h][(2 * i + 1) & 3][0], y[h][(2 * i + 1) & 3][1], c[i][1], vb.y);
+        }
       }
-    double* yb = ybuf + (it & 1) * NW * 128;
+    }
+    double* yb = ybuf + (it & 1) * NW * YB;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        yb[warp * 128 + gq * 16 + 8 * h + 2 * tq + e] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
+      for (int e = 0; e < 2; ++e) {  // Y[r = gq][c = 8h + 2tq + e] -> r * 18 + (c & 3) * 4 + (c >> 2)
+        const int c = 8 * h + 2 * tq + e;
+        yb[warp * YB + gq * 18 + (c & 3) * 4 + (c >> 2)] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
+      }
     team_sync(team, tw);
-    // Z = Y T (8 x 16): A[gq][tq] of k-step kk = Y[gq][4kk + tq]; lane ends
-    // with Z[gq][8h + 2tq + e]
+    // Z = Y T': A[gq][tq] of k-step kk = Y[gq][4kk + tq]; lane ends with
+    // z[h][e] = Z[gq][8h + tq + 4e]
     double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    const double* tb = yb + team * tw * 128;
+    double ya[4];
+    team_ysum<tw>(yb + team * tw * YB, gq, tq, ya);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      double a = 0.0;
+    for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-      for (int w = 0; w < tw; ++w) a += tb[w * 128 + gq * 16 + 4 * kk + tq];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) dmma884n(z[h][0], z[h][1], a, tf[kk][h]);
-    }
-    // pass 2: C += (-Z) V^T with k = 8h + 2tq + e, k-step-major
+      for (int h = 0; h < 2; ++h) dmma884n(z[h][0], z[h][1], ya[kk], tf[kk][h]);
+    // pass 2: C += (-Z) V^T, k-step (h, e) <-> k = 8h + tq + 4e
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const double nz = -z[kk >> 1][kk & 1];
-      const double* pb = pB2 + (8 * (kk >> 1) + (kk & 1)) * prs;
+      const double* pb = pB2 + (8 * (kk >> 1) + 4 * (kk & 1)) * prs;
 #pragma unroll
-      for (int i = 0; i < TTR; ++i)
-        if (i < my) dmma884n(c[i][0], c[i][1], nz, pb[i * cs]);
+      for (int i = 0; i < TT; ++i) {
+        if (i >= my) break;
+        dmma884n(c[i][0], c[i][1], nz, pb[i * cs]);
+      }
     }
+    double* xr = A + (cw + 2 * tq) * ld + rmin + 8 * t + gq;
+    asm volatile("" : "+r"(ldc));
 #pragma unroll
-    for (int i = 0; i < TTR; ++i)
+    for (int i = 0; i < TT; ++i)
       if (i < my) {
         xr[i * ldc] = c[i][0];
-        xr[i * ldc + ld4] = c[i][1];
+        xr[i * ldc + ld] = c[i][1];
       }
   }
 }
@@ -1371,7 +1387,7 @@ template <int NT>
 __device__ bool team_right_update(QrSmemFixed& q, double* ybuf, const double* pan2, int prs, double* A,
                                   int ld, int nrows, int NP, int rmin, int j0) {
   const int nch = (NP - j0) >> 3;
-  switch (team_width<NT, TTR>(nch)) {
+  switch (team_width<NT>(nch)) {
     case 1: team_right_update_t<NT, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
     case 2: team_right_update_t<NT, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
     case 4: team_right_update_t<NT, 4>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
@@ -1415,8 +1431,9 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
       explicit_v<NT>(pan, prs, k0, LP);
       panel_gram<NT>(q, pan, prs, kc, LP);
       long long _a = clock64();
-      if (!team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
-                                int(k0 + BW)))
+      if (!(NT == 256 && P.wtwo &&
+            team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
+                                 int(k0 + BW))))
         P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
                : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
       tr += clock64() - _a;
@@ -1482,8 +1499,9 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
-        if (!team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
-                                  int(k + BW)))
+        if (!(NT == 256 && P.wtwo &&
+              team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
+                                   int(k + BW))))
           P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
                  : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
         tr += clock64() - _a;
@@ -1506,7 +1524,8 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       }
       {
         long long _a = clock64();
-        if (team_right_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0))) {
+        if (NT == 256 && P.wtwo &&
+            team_right_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0))) {
         } else if (P.wtwo) {
           right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         } else {
@@ -2868,7 +2887,9 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.qr_stages = 2;
     auto smem_for = [&](int nt, bool two) {
       size_t extra = size_t(g.qr_stages) * ring;
-      const size_t w = size_t(nt / 32) * (two ? WREG : WREG1) * sizeof(double);
+      size_t w = size_t(nt / 32) * (two ? WREG : WREG1) * sizeof(double);
+      if (nt == 256 && two && w < size_t(TEAM_SMEM_DOUBLES) * sizeof(double))
+        w = size_t(TEAM_SMEM_DOUBLES) * sizeof(double);  // team updates' Y partials + stage
       return fixed + (w > extra ? w : extra);
     };
     const size_t cap = size_t(227 * 1024);
