@@ -24,11 +24,13 @@ per-slice sample of the same workload; see cpu_sample().
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
 import statistics
 import subprocess
+import threading
 import sys
 import time
 
@@ -142,17 +144,69 @@ def run_reference(args):
 # ------------------------------------------------------------ GPU arm
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled every 200 ms during
+    the timed region, through NVML in a background thread (nvidia-smi's own
+    start-up takes driver locks that stall the stream being timed; NVML is
+    initialised and queried once before the region starts).  Falls back to
+    an ``nvidia-smi -lms 200`` subprocess when pynvml is missing."""
 
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, pci_bus_id=None):
         self.index = index
+        self.pci = pci_bus_id
+        self.samples = []  # (sm_mhz, max_mhz, reason bits)
+        self.lines = []
         self.proc = None
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        if self.pci:
+            try:
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(self.pci)
+            except pynvml.NVMLError:
+                pass
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        if os.environ.get("STARM_BENCH_NO_SMI"):
+            return self
+        try:
+            nv, h = self._nvml_handle()
+        except Exception:
+            return self._enter_smi()
+
+        def query():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except AttributeError:
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return sm, mx, bits
+
+        query()  # warm the NVML path before the region starts
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(query())
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
+        return self
+
+    def _enter_smi(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -160,23 +214,42 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, ValueError):
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def pump():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self.lines.append(line)
+                    first.set()
+            first.set()
+
+        self._thread = threading.Thread(target=pump, daemon=True)
+        self._thread.start()
+        first.wait(timeout=10)
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        self._stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        if self._thread is not None:
+            self._thread.join(timeout=5)
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in getattr(self, "lines", []):
+        for s_mhz, m_mhz, bits in self.samples:
+            sm.append(float(s_mhz))
+            mx = max(mx, float(m_mhz))
+            for nm, bit in self.REASONS:
+                if bits & bit:
+                    reasons.add(nm)
+        names = [nm for nm, _ in self.REASONS]
+        for line in self.lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -189,7 +262,16 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else ("nvidia-smi" if self.lines else None)}
+
+
+def pci_bus_id(torch, dev):
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        return "%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+    except Exception:
+        return None
 
 
 def measured_hbm_peak():
@@ -269,13 +351,22 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed host loop
+    retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
+    with ClockSampler(dev.index, pci_bus_id(torch, dev)) as clk:
         e0.record()
-        for _ in range(args.steps):
+        marks[0].record()
+        for k in range(args.steps):
             c = step()
+            marks[k + 1].record()
         e1.record()
         e1.synchronize()
     torch.cuda.synchronize()
+    gc.enable()
+    alloc_retries = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
+    step_ms = [round(marks[k].elapsed_time(marks[k + 1]), 3) for k in range(args.steps)]
     launches = lib.starm_launch_count_reset() // max(args.steps, 1)
     t_dev = e0.elapsed_time(e1) / 1e3
     if world > 1:
@@ -396,6 +487,7 @@ def run_ours(args):
                                  "achieved": dct_bytes / t_ttm / 1e9, "peak": hbm_peak,
                                  "frac": dct_bytes / t_ttm / 1e9 / hbm_peak}},
             "stages_ms": stages,
+            "step_ms": step_ms, "alloc_retries": alloc_retries,
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "result": {"total_rank": ranks_sum, "relative_error": err, "realised_error": realised},
@@ -448,7 +540,7 @@ def run_sharded(args):
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
+    with ClockSampler(dev.index, pci_bus_id(torch, dev)) as clk:
         e0.record()
         for _ in range(args.steps):
             res = step(x)

@@ -541,6 +541,26 @@ __device__ __forceinline__ double& PAN(double* pan, int64_t prs, int c, int64_t 
   return pan[c * prs + r];
 }
 
+// MUFU rsqrt / rcp refined by Newton steps (FP64 sqrt and division are long
+// library sequences on the dependent path of every Householder step).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+__device__ __forceinline__ double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Sum 16 per-thread partials over the CTA: butterfly inside each warp (16
 // shuffles leave lanes 2v, 2v+1 holding warp-sum v), then 8 warp partials.
 template <int NT>
@@ -575,10 +595,14 @@ __device__ __forceinline__ void reduce16(double (&acc)[BW], double (&red)[16][BW
   if (!(lane & 1)) red[warp][(lane >> 1) & 15] = v1;
   __syncthreads();
   if (threadIdx.x < BW) {
-    double s = 0.0;
+    double v[NT / 32];
 #pragma unroll
-    for (int w = 0; w < NT / 32; ++w) s += red[w][threadIdx.x];
-    out[threadIdx.x] = s;
+    for (int w = 0; w < NT / 32; ++w) v[w] = red[w][threadIdx.x];
+#pragma unroll
+    for (int h = 1; h < NT / 32; h <<= 1)
+#pragma unroll
+      for (int w = 0; w + h < NT / 32; w += 2 * h) v[w] += v[w + h];
+    out[threadIdx.x] = v[0];
   }
   __syncthreads();
 }
@@ -639,79 +663,135 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
 // The panel is read straight from global memory: element (r, c) =
 // src[r * sr + c * sc] for lo <= r < nrows, 0 otherwise (all loads in flight).
 template <int NT, int RPT>
-__device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0,
-                                              int64_t nrows, const double* src, int64_t sr,
-                                              int64_t sc, int64_t lo) {
-  // Register-resident panel, column loop NOT unrolled: b[i][c] holds panel
-  // column j + c of this thread's rows, so every column runs the same code
-  // (column 0 is factored, then the window shifts left by one).  Keeps the
-  // instruction footprint of the 16 columns at one column's worth.
+__device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs64, int64_t k064,
+                                              int64_t nrows64, const double* src, int64_t sr,
+                                              int64_t sc, int64_t lo64) {
+  // Register-resident panel, column loop NOT fully unrolled: b[i][c] holds
+  // panel column j + c of this thread's rows; each loop iteration factors
+  // two columns (0, then 1) and shifts the window left by two, so every
+  // iteration runs the same code (instruction footprint of two columns).
   const int tid = threadIdx.x;
+  const int prs = int(prs64), k0 = int(k064), nrows = int(nrows64), lo = int(lo64);
   double b[RPT][BW];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int64_t r = tid + i * NT;
+    const int r = tid + i * NT;
     const bool in = r >= lo && r < nrows;
 #pragma unroll
-    for (int c = 0; c < BW; ++c) b[i][c] = in ? src[r * sr + c * sc] : 0.0;
+    for (int c = 0; c < BW; ++c) b[i][c] = in ? src[int64_t(r) * sr + c * sc] : 0.0;
   }
-#pragma unroll 1
-  for (int j = 0; j < BW; ++j) {
-    const int64_t pr = k0 + j;
+  // One column step on window column C (the pivot), columns C+1.. updated.
+#ifdef STARM_PF_PROBE
+  long long pt[4] = {0, 0, 0, 0};
+#endif
+  auto step = [&](const int j, const int C) {
+#ifdef STARM_PF_PROBE
+    long long p0 = clock64();
+#endif
+    const int pr = k0 + j;
     const int par = j & 1;  // double-buffered pivot row / sums: 2 barriers per column
     double acc[BW];
 #pragma unroll
     for (int c = 0; c < BW; ++c) acc[c] = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int64_t r = tid + i * NT;
+      const int r = tid + i * NT;
       if (r == pr) {
 #pragma unroll
-        for (int c = 0; c < BW; ++c) q.prow[par][c] = b[i][c];
+        for (int c = 0; c < BW; c += 2)
+          *reinterpret_cast<double2*>(&q.prow[par][c]) =
+              make_double2(c + C < BW ? b[i][c + C] : 0.0, c + 1 + C < BW ? b[i][c + 1 + C] : 0.0);
       }
       if (r > pr) {
-        const double x = b[i][0];
+        const double x = b[i][C];
         acc[0] = fma(x, x, acc[0]);
 #pragma unroll
-        for (int c = 1; c < BW; ++c) acc[c] = fma(x, b[i][c], acc[c]);
+        for (int c = 1; c + C < BW; ++c) acc[c] = fma(x, b[i][c + C], acc[c]);
       }
     }
+#ifdef STARM_PF_PROBE
+    long long p1 = clock64();
+#endif
     reduce16<NT>(acc, q.red, q.psum[par]);
+#ifdef STARM_PF_PROBE
+    long long p2 = clock64();
+#endif
     // every thread derives the reflector (dlarfg) redundantly
-    const double alpha = q.prow[par][0];
-    const double xn2 = q.psum[par][0];
+    double pw[BW], sw[BW];
+#pragma unroll
+    for (int c = 0; c < BW; c += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(&q.prow[par][c]);
+      const double2 s2 = *reinterpret_cast<const double2*>(&q.psum[par][c]);
+      pw[c] = p2.x;
+      pw[c + 1] = p2.y;
+      sw[c] = s2.x;
+      sw[c + 1] = s2.y;
+    }
+    const double alpha = pw[0];
+    const double xn2 = sw[0];
     double tau = 0.0, beta = alpha, scal = 0.0;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+    if (xn2 > 0.0) {  // dlarfg: tau = 1 + |alpha| / nrm, 1 / (alpha - beta) = sign(alpha) / (|alpha| + nrm)
+      const double nrm2 = fma(alpha, alpha, xn2);
+      double rn, nrm;
+      if (nrm2 > 1e-280 && nrm2 < 1e280) {
+        rn = rsqrt_nr(nrm2);
+        nrm = nrm2 * rn;
+      } else {
+        nrm = sqrt(nrm2);
+        rn = 1.0 / nrm;
+      }
+      const double aa = fabs(alpha);
+      beta = -copysign(nrm, alpha);
+      tau = fma(aa, rn, 1.0);
+      scal = copysign(rcp_nr(aa + nrm), alpha);
     }
     if (tid == 0) q.tau[j] = tau;
     if (tau != 0.0) {
       double tw[BW];
 #pragma unroll
-      for (int c = 1; c < BW; ++c) tw[c] = tau * fma(scal, q.psum[par][c], q.prow[par][c]);
+      for (int c = 1; c + C < BW; ++c) tw[c] = tau * fma(scal, sw[c], pw[c]);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        const int64_t r = tid + i * NT;
+        const int r = tid + i * NT;
         if (r >= pr) {
-          const double vr = (r == pr) ? 1.0 : b[i][0] * scal;
+          const double vr = (r == pr) ? 1.0 : b[i][C] * scal;
 #pragma unroll
-          for (int c = 1; c < BW; ++c) b[i][c] = fma(-vr, tw[c], b[i][c]);
-          b[i][0] = (r == pr) ? beta : vr;
+          for (int c = 1; c + C < BW; ++c) b[i][c + C] = fma(-vr, tw[c], b[i][c + C]);
+          b[i][C] = (r == pr) ? beta : vr;
         }
       }
     }
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int64_t r = tid + i * NT;
-      if (r < nrows) pan[j * prs + r] = b[i][0];
+      const int r = tid + i * NT;
+      if (r < nrows) pan[j * prs + r] = b[i][C];
+    }
+#ifdef STARM_PF_PROBE
+    long long p3 = clock64();
+    pt[0] += p1 - p0;
+    pt[1] += p2 - p1;
+    pt[2] += p3 - p2;
+#endif
+  };
+#pragma unroll 1
+  for (int j = 0; j < BW; j += 2) {
+    step(j, 0);
+    step(j + 1, 1);
 #pragma unroll
-      for (int c = 0; c + 1 < BW; ++c) b[i][c] = b[i][c + 1];
-      b[i][BW - 1] = 0.0;
+    for (int i = 0; i < RPT; ++i) {
+#pragma unroll
+      for (int c = 0; c + 2 < BW; ++c) b[i][c] = b[i][c + 2];
+      b[i][BW - 2] = b[i][BW - 1] = 0.0;
     }
   }
   __syncthreads();
+#ifdef STARM_PF_PROBE
+  if (tid == 0) {
+    atomicAdd(&g_stats[ST_CYC_GRAM], (unsigned long long)pt[0]);
+    atomicAdd(&g_stats[ST_CYC_EIG], (unsigned long long)pt[1]);
+    atomicAdd(&g_stats[ST_CYC_APPLY], (unsigned long long)pt[2]);
+  }
+#endif
 }
 
 template <int NT>
@@ -1633,23 +1713,6 @@ __host__ __device__ __forceinline__ int hb_warps(int64_t n, int cap) {  // ceil(
 }
 __device__ __forceinline__ double& HEL(double* W, int r, int c) { return W[r * (HB - 1) + c + HOFF]; }
 
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
-}
-
-__device__ __forceinline__ double rcp_nr(double q) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  double e = fma(-q, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-q, r, 1.0);
-  return fma(r, e, r);
-}
 
 // Warp-wide dlarfg: lanes 0..L-1 hold x (0 beyond); on return x holds v
 // (lane 0: 1, 0 beyond L), beta the new leading entry; returns tau (0: H = I).

@@ -5,6 +5,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
 //        -Iinclude -Ipaper_2605_16058_b200/csrc scripts/micro/team_bench.cu
 //        paper_2605_16058_b200/libstarm.so -o scripts/micro/team_bench
+#include <vector>
 #include "svd_f64.cu"
 
 namespace starm {
@@ -30,6 +31,10 @@ __global__ void __launch_bounds__(NT, 1) bench_left(double* Xall, int LP, int NP
       trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
     } else if (mode == 2) {
       team_right_update<NT>(q, wbase, pan, prs, X, LP, NP, NP, k0 + BW, k0 + BW);
+    } else if (mode == 3) {
+      panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0);
+    } else if (mode == 4) {
+      panel_factor_any<NT>(q, pan, prs, k0, NP, X + k0 * LP, 1, LP, 0);
     }
     __syncthreads();
   }
@@ -46,12 +51,16 @@ int main(int argc, char** argv) {
   double* X;
   long long* cyc;
   cudaMalloc(&X, size_t(nblk) * LP * NP * 8);
-  cudaMemset(X, 0, size_t(nblk) * LP * NP * 8);
+  {
+    std::vector<double> h(size_t(LP) * NP);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = double((i * 2654435761ull) % 1000003) / 1000003.0 - 0.5;
+    for (int b = 0; b < nblk; ++b) cudaMemcpy(X + size_t(b) * LP * NP, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  }
   cudaMalloc(&cyc, nblk * 8);
   const size_t smem = sizeof(QrSmemFixed) + size_t(BW) * (LP + 36) * 8 + size_t(TEAM_SMEM_DOUBLES) * 8;
   cudaFuncSetAttribute(bench_left<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  const char* names[] = {"team left (QR phase)", "ring left (QR phase)", "team right (band)"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* names[] = {"team left (QR phase)", "ring left (QR phase)", "team right (band)", "panel factor (QR phase)", "panel factor (band)"};
+  for (int mode = 0; mode < 5; ++mode) {
     if (only >= 0 && mode != only) continue;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEvent_t a, b;
@@ -68,6 +77,12 @@ int main(int argc, char** argv) {
       double avg = 0;
       for (int i = 0; i < nblk; ++i) avg += h[i];
       avg /= nblk;
+      unsigned long long st[16];
+      cudaMemcpyFromSymbol(st, g_stats, sizeof(st));
+      cudaMemset(cyc, 0, 8);
+      unsigned long long z[16] = {0};
+      cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+      if (rep == 2) printf("   probe per CTA: acc %.3f M, reduce %.3f M, rest %.3f M\n", st[4] / 148e6, st[5] / 148e6, st[6] / 148e6);
       if (rep == 2) printf("%-24s %.3f ms  %.3f Mcycles per CTA  err=%s\n", names[mode], ms, avg / 1e6,
                            cudaGetErrorString(cudaGetLastError()));
     }
