@@ -183,23 +183,24 @@ class ClockSampler:
         except Exception:
             return self._enter_smi()
 
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+
         def query():
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            try:
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            except AttributeError:
-                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            return sm, mx, bits
+            return nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, reasons(h)
 
         query()  # warm the NVML path before the region starts
+        self.query_ms = []
 
         def run():
             while not self._stop.is_set():
+                t0 = time.perf_counter()
                 try:
                     self.samples.append(query())
                 except Exception:
                     pass
+                self.query_ms.append(round(1e3 * (time.perf_counter() - t0), 3))
                 self._stop.wait(0.2)
 
         self._thread = threading.Thread(target=run, daemon=True)
@@ -263,7 +264,8 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm),
-                "source": "nvml" if self.samples else ("nvidia-smi" if self.lines else None)}
+                "source": "nvml" if self.samples else ("nvidia-smi" if self.lines else None),
+                "query_ms": getattr(self, "query_ms", None)}
 
 
 def pci_bus_id(torch, dev):

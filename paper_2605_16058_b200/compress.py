@@ -447,12 +447,22 @@ def tsvdm_tolerance_stream(tensors, ts: TransformSet, epsilon, strategy=MEMORY_E
         cur, b = nxt, 1 - b
 
 
+_HBM_BUDGET = {}  # device index -> bytes this process can hold (free + own reserved), read once
+
+
 def _state_fits(x) -> bool:
-    """True when the per-slice SVD state needs < 1/4 of the free HBM."""
+    """True when the per-slice SVD state needs < 1/4 of the free HBM.
+
+    cudaMemGetInfo occasionally blocks for tens of milliseconds, so it is
+    queried once per device; later calls subtract this process's current
+    allocations from that budget."""
     import torch
     from .slice_svd import state_bytes
-    free, _ = torch.cuda.mem_get_info(x.device)
-    free += torch.cuda.memory_reserved(x.device) - torch.cuda.memory_allocated(x.device)
+    idx = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    if idx not in _HBM_BUDGET:
+        free, _ = torch.cuda.mem_get_info(x.device)
+        _HBM_BUDGET[idx] = free + torch.cuda.memory_reserved(x.device)
+    free = _HBM_BUDGET[idx] - torch.cuda.memory_allocated(x.device)
     return state_bytes(x) < free // 4
 
 
