@@ -10,6 +10,9 @@ there is no CPU fallback.  Host inputs (DenseTensor) come back as host
 outputs; DeviceTensor inputs stay in HBM end to end.
 """
 
+from .codec import (BadMagicError, BenchRow, CodecError, FormatError, TruncatedPayloadError,
+                    UnsupportedDtypeError, UnsupportedVersionError, read_compressed, read_tensor,
+                    write_bench_csv, write_compressed, write_tensor)
 from .compress import (COMPUTE_EFFICIENT, MEMORY_EFFICIENT, METHOD_FIXED_RANK, METHOD_TOLERANCE,
                        TOLERANCE_STRATEGIES, TRUNCATE, CompressedTensor, StageClock,
                        ThresholdResult, TSVDMResult, compression_ratio, compute_threshold,
@@ -28,6 +31,9 @@ from .transform_set import (CUSTOM, DATA_DRIVEN, DCT, IDENTITY, Transform, Trans
 __version__ = "0.1.0"
 
 __all__ = [
+    "BadMagicError", "BenchRow", "CodecError", "FormatError", "TruncatedPayloadError",
+    "UnsupportedDtypeError", "UnsupportedVersionError", "read_compressed", "read_tensor",
+    "write_bench_csv", "write_compressed", "write_tensor",
     "BATCHED", "COMPUTE_EFFICIENT", "CUSTOM", "CompressedTensor", "DATA_DRIVEN", "DCT",
     "DenseTensor", "DeviceFactors", "DeviceTensor", "IDENTITY", "LOOP", "MEMORY_EFFICIENT",
     "METHOD_FIXED_RANK", "METHOD_TOLERANCE", "PARFOR", "SLICES_PARALLEL", "SVD_PARALLEL",
