@@ -18,7 +18,11 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(5, 3, 4), (3, 5, 2, 3), (7, 7, 6), (1, 4, 3), (4, 1, 2), (33, 17, 5), (17, 33, 4),
           (70, 130, 3), (130, 70, 3), (64, 64, 2), (200, 40, 3), (40, 200, 3), (2, 2, 2, 2, 3),
           (300, 257, 2), (257, 300, 2), (361, 720, 1), (1024, 1024, 2), (900, 1100, 1),
-          (2100, 40, 2), (40, 2100, 2), (8192, 64, 2), (5000, 130, 1)]
+          (2100, 40, 2), (40, 2100, 2), (8192, 64, 2), (5000, 130, 1),
+          # around the reduce kernel's update-path switch: L <= 960 keeps the
+          # panel + team stage in SMEM (register team updates, widths 1..8);
+          # longer slices use the SMEM-ring updates
+          (1030, 200, 2), (200, 1030, 1), (520, 480, 1)]
 
 
 # ------------------------------------------------------------------ TTM (K1)
