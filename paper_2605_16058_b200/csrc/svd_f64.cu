@@ -693,15 +693,22 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
     double acc[BW];
 #pragma unroll
     for (int c = 0; c < BW; ++c) acc[c] = 0.0;
+    // pivot row to SMEM: one thread branches in (the predicated form costs
+    // every warp RPT x 8 store slots per column)
+    if (tid == (pr & (NT - 1))) {
+      const int ip = pr / NT;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (i == ip) {
+#pragma unroll
+          for (int c = 0; c < BW; c += 2)
+            *reinterpret_cast<double2*>(&q.prow[par][c]) =
+                make_double2(c + C < BW ? b[i][c + C] : 0.0, c + 1 + C < BW ? b[i][c + 1 + C] : 0.0);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = tid + i * NT;
-      if (r == pr) {
-#pragma unroll
-        for (int c = 0; c < BW; c += 2)
-          *reinterpret_cast<double2*>(&q.prow[par][c]) =
-              make_double2(c + C < BW ? b[i][c + C] : 0.0, c + 1 + C < BW ? b[i][c + 1 + C] : 0.0);
-      }
       if (r > pr) {
         const double x = b[i][C];
         acc[0] = fma(x, x, acc[0]);
