@@ -1725,10 +1725,12 @@ __device__ __forceinline__ double& HEL(double* W, int r, int c) { return W[r * (
 // (lane 0: 1, 0 beyond L), beta the new leading entry; returns tau (0: H = I).
 // sqrt and the two divisions go through MUFU rsqrt/rcp + Newton steps:
 // tau = 1 + |alpha| / norm, 1 / (alpha - beta) = sign(alpha) / (|alpha| + norm).
+// Lanes 16..31 carry a mirror of lanes 0..15 (x of lane l & 15), so the sum
+// needs four butterfly levels and both half-warps end with it.
 __device__ __forceinline__ double warp_house(double& x, int lane, double& beta) {
-  double s2 = lane ? x * x : 0.0;
+  double s2 = (lane & 15) ? x * x : 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  for (int o = 8; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   const double alpha = __shfl_sync(0xffffffffu, x, 0);
   beta = alpha;
   if (s2 == 0.0) return 0.0;
@@ -1762,7 +1764,7 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
   const int rho = k ? c0 - BW : i;
   double beta;
   // ---- right reflector from row rho, applied to rows (rho, c1]
-  double x = lane < L ? HEL(W, rho, c0 + lane) : 0.0;
+  double x = (lane & 15) < L ? HEL(W, rho, c0 + (lane & 15)) : 0.0;  // mirrored halves
   const double tau = warp_house(x, lane, beta);
   if (act && lg && lane < BW) lg[lane] = lane ? x : tau;
   if (tau != 0.0) {
@@ -1788,7 +1790,7 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
     __syncwarp();
   }
   // ---- left reflector from column c0, applied to columns (c0, c0 + 2 BW - 1]
-  double y = lane < L ? HEL(W, c0 + lane, c0) : 0.0;
+  double y = (lane & 15) < L ? HEL(W, c0 + (lane & 15), c0) : 0.0;
   const double tl = warp_house(y, lane, beta);
   if (tl != 0.0) {
     if (lane < L) HEL(W, c0 + lane, c0) = lane ? 0.0 : beta;
@@ -1852,8 +1854,8 @@ __global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams 
       if (!GMEM || 3 * nw >= kmax) {
         const int k = int(t - 3 * int64_t(cur));
         const bool act = cur >= 0 && k < hb_tasks(n, cur);
-        hb_task(W, n, act ? cur : 0, act ? k : 0, act, lane, vsh[warp],
-                lg ? lg + (int64_t(act ? cur : 0) * kmax + (act ? k : 0)) * HLOG : nullptr);
+        if (act)  // (warp-uniform: idle warps go straight to the step barrier)
+          hb_task(W, n, cur, k, true, lane, vsh[warp], lg ? lg + (int64_t(cur) * kmax + k) * HLOG : nullptr);
       } else {
         for (int i = cur; i >= 0 && t - 3 * int64_t(i) < kmax; i -= nw) {
           const int k = int(t - 3 * int64_t(i));
@@ -3276,11 +3278,16 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       STARM_CUDA_TRY(cudaEventRecord(ss->fork, st));
       STARM_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));
     }
+    // chunk sizes in whole waves of the one-CTA-per-SM bulge chase (c2:
+    // 296, 296, 296, 136 = 7 waves, where four equal chunks of 256 take 8),
+    // which also leaves the smallest chunk's sigma as the exposed tail
+    const int64_t per = round_up(ceil_div(count, nch), int64_t(pl.slots_b));
     for (int c = 0; c < nch; ++c) {
       SvdParams Pc = P;
-      Pc.lo = count * c / nch;
-      Pc.hi = count * (c + 1) / nch;
+      Pc.lo = per * c < count ? per * c : count;
+      Pc.hi = per * (c + 1) < count ? per * (c + 1) : count;
       Pc.cctr = nch > 1 ? 8 + c : 2;
+      if (Pc.lo >= Pc.hi) continue;
       if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(Pc);
       else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(Pc);
       STARM_LAUNCH_CHECK();
