@@ -1767,6 +1767,7 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
   double x = (lane & 15) < L ? HEL(W, rho, c0 + (lane & 15)) : 0.0;  // mirrored halves
   const double tau = warp_house(x, lane, beta);
   if (act && lg && lane < BW) lg[lane] = lane ? x : tau;
+  double col0 = 0.0;  // this lane's updated A(rho + 1 + lane, c0)
   if (tau != 0.0) {
     if (lane < L) HEL(W, rho, c0 + lane) = lane ? 0.0 : beta;
     vs[lane] = x;
@@ -1777,20 +1778,22 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
       double a[BW];
 #pragma unroll
       for (int l = 0; l < BW; ++l) a[l] = row[l];
-      double w0 = 0.0, w1 = 0.0;
+      double w4[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: half the dependent depth
 #pragma unroll
-      for (int l = 0; l < BW; l += 2) {
-        w0 = fma(a[l], vs[l], w0);
-        w1 = fma(a[l + 1], vs[l + 1], w1);
-      }
-      const double w = (w0 + w1) * tau;
+      for (int l = 0; l < BW; ++l) w4[l & 3] = fma(a[l], vs[l], w4[l & 3]);
+      const double w = ((w4[0] + w4[1]) + (w4[2] + w4[3])) * tau;
+      col0 = fma(-w, vs[0], a[0]);
+      row[0] = col0;
 #pragma unroll
-      for (int l = 0; l < BW; ++l) row[l] = fma(-w, vs[l], a[l]);
+      for (int l = 1; l < BW; ++l) row[l] = fma(-w, vs[l], a[l]);
     }
     __syncwarp();
   }
-  // ---- left reflector from column c0, applied to columns (c0, c0 + 2 BW - 1]
-  double y = (lane & 15) < L ? HEL(W, c0 + (lane & 15), c0) : 0.0;
+  // ---- left reflector from column c0, applied to columns (c0, c0 + 2 BW - 1].
+  // Its column c0 entries were just produced in registers by lanes
+  // c0 + l - rho - 1 (when the right reflector was applied): shuffle them.
+  const double ysh = __shfl_sync(0xffffffffu, col0, (c0 + (lane & 15) - rho - 1) & 31);
+  double y = (lane & 15) < L ? (tau != 0.0 ? ysh : HEL(W, c0 + (lane & 15), c0)) : 0.0;
   const double tl = warp_house(y, lane, beta);
   if (tl != 0.0) {
     if (lane < L) HEL(W, c0 + lane, c0) = lane ? 0.0 : beta;
@@ -1802,13 +1805,10 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
       double a[BW];
 #pragma unroll
       for (int l = 0; l < BW; ++l) a[l] = col[l * (HB - 1)];
-      double w0 = 0.0, w1 = 0.0;
+      double w4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int l = 0; l < BW; l += 2) {
-        w0 = fma(vs[l], a[l], w0);
-        w1 = fma(vs[l + 1], a[l + 1], w1);
-      }
-      const double w = (w0 + w1) * tl;
+      for (int l = 0; l < BW; ++l) w4[l & 3] = fma(vs[l], a[l], w4[l & 3]);
+      const double w = ((w4[0] + w4[1]) + (w4[2] + w4[3])) * tl;
 #pragma unroll
       for (int l = 0; l < BW; ++l) col[l * (HB - 1)] = fma(-w, vs[l], a[l]);
     }
