@@ -2927,6 +2927,14 @@ int g_reduce_threads = [] {
   return (v == 0 || v == 256 || v == 512) ? v : 256;
 }();
 int g_tune_sweeps = 60;
+// bisection blocks per launch on the side stream (env STARM_BISECT_SIDE_PER_SM, per SM)
+int g_bisect_side_blocks = [] {
+  const char* e = getenv("STARM_BISECT_SIDE_PER_SM");
+  const int per = e ? atoi(e) : 4;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (per >= 1 && per <= 64 ? per : 4) * sms;
+}();
 // 1 = bidiagonal values path when the panel fits, 0 = Jacobi only, 2 = bidiagonal
 // with the bulge-chase window in global memory, 3 = diagnostic: the values
 // pass stops after the reduce kernel (outputs undefined; for timing it alone)
@@ -3294,7 +3302,11 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       if (ss) {
         STARM_CUDA_TRY(cudaEventRecord(ss->ev[c], st));
         STARM_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->ev[c], 0));
-        svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, ss->s>>>(Pc);
+        // beside the bulge chase: at most BISECT_SIDE_PER_SM blocks per SM, so
+        // the next chunk's bulge CTA (27 K registers) always finds room
+        // instead of queueing behind a register file full of bisection warps
+        const int side = pl.bisect_blocks < g_bisect_side_blocks ? pl.bisect_blocks : g_bisect_side_blocks;
+        svd_bisect_kernel<<<side, 128, 0, ss->s>>>(Pc);
       } else {
         svd_bisect_kernel<<<pl.bisect_blocks, 128, 0, st>>>(Pc);
       }
