@@ -1951,16 +1951,19 @@ __device__ __forceinline__ int count_lag(const double* d, const double* e, int n
 // diverge inside a warp.
 __global__ void svd_bisect_kernel(SvdParams P) {
   const int64_t n = P.n, NP = P.NP;
-  const int64_t total = P.hi * n;  // items [lo n, hi n)
+  // one warp per (slice, block of 32 consecutive j): the multisection below
+  // shares probes inside a warp, so the composition of a warp must depend
+  // on the slice alone (sigma bitwise identical whichever job or chunk
+  // computes it)
+  const int64_t jblocks = (n + 31) >> 5;
+  const int64_t wtotal = (P.hi - P.lo) * jblocks;
   const double N2 = 2.0 * double(n);
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  const int64_t w0 = (P.lo * n) >> 5;  // warp-aligned start (earlier items are skipped)
-  for (int64_t w = w0 + ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5); w * 32 < total;
-       w += warps) {
-    const int64_t g = w * 32 + lane;
-    const bool valid = g < total && g >= P.lo * n;
-    const int64_t it = valid ? g / n : 0, j = valid ? g % n : 0;
+  for (int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; w < wtotal; w += warps) {
+    const int64_t jv = (w % jblocks) * 32 + lane;
+    const bool valid = jv < n;
+    const int64_t it = P.lo + w / jblocks, j = valid ? jv : 0;
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     const int flag = valid ? P.flags[si] : 1;
@@ -1985,8 +1988,14 @@ __global__ void svd_bisect_kernel(SvdParams P) {
       const double mid = 0.5 * (lo + hi);
       return !(mid > lo && mid < hi) || hi - lo <= 2.0 * DBL_EPSILON * fmax(lo, 1e-3 * bound);
     };
-    // ---- phase A: bisection until isolated
+    // ---- phase A: cooperative multisection until isolated.  A Sturm count
+    // at x tells every sigma of the slice which side of x it lies on, so
+    // the lanes of a warp (consecutive j of one slice) share their probes:
+    // lanes whose brackets coincide split that bracket into k + 1 parts
+    // with k distinct probes, and every lane tightens its bracket with all
+    // probes of its slice (32 probes per Sturm sweep instead of 1).
     while (__any_sync(0xffffffffu, state == 0)) {
+      bool probe = false;
       if (state == 0) {
         if (converged()) {
           sigma = 0.5 * (lo + hi);
@@ -1995,14 +2004,41 @@ __global__ void svd_bisect_kernel(SvdParams P) {
           x = 0.5 * (lo + hi);
           state = 1;
         } else {
-          const double mid = 0.5 * (lo + hi);
-          const int64_t c = count_below(d, e, int(n), mid, pivmin);
-          if (c <= target) {
-            lo = mid;
-            clo = c;
-          } else {
-            hi = mid;
-            chi = c;
+          probe = true;
+        }
+      }
+      // runs of lanes with the same (slice, bracket) among the probing lanes
+      const double plo = __shfl_up_sync(0xffffffffu, lo, 1), phi = __shfl_up_sync(0xffffffffu, hi, 1);
+      const int64_t pit = __shfl_up_sync(0xffffffffu, it, 1);
+      const bool pprobe = __shfl_up_sync(0xffffffffu, probe, 1);
+      const bool cont = lane > 0 && probe && pprobe && pit == it && plo == lo && phi == hi;
+      const unsigned starts = __ballot_sync(0xffffffffu, !cont);  // run heads (and non-probing lanes)
+      const int head = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+      const unsigned after = starts & ~(0xffffffffu >> (31 - lane));  // heads beyond this lane
+      const int next = after ? __ffs(after) - 1 : 32;
+      const int rank = lane - head, k = next - head;
+      double xp = 0.0;
+      int64_t cp = 0;
+      if (probe) {
+        xp = lo + (hi - lo) * (double(rank + 1) / double(k + 1));
+        if (!(xp > lo && xp < hi)) xp = 0.5 * (lo + hi);
+        cp = count_below(d, e, int(n), xp, pivmin);
+      }
+#pragma unroll 4
+      for (int m = 0; m < 32; ++m) {
+        const double xm = __shfl_sync(0xffffffffu, xp, m);
+        const int64_t cm = __shfl_sync(0xffffffffu, cp, m);
+        const int64_t im = __shfl_sync(0xffffffffu, it, m);
+        const bool pm = __shfl_sync(0xffffffffu, probe, m);
+        if (state == 0 && pm && im == it) {
+          if (cm <= target) {
+            if (xm > lo) {
+              lo = xm;
+              clo = cm;
+            }
+          } else if (xm < hi) {
+            hi = xm;
+            chi = cm;
           }
         }
       }
