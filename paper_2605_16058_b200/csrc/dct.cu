@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
   const int64_t base = b * rows * N;
   const double c0 = sqrt(1.0 / N), c1 = sqrt(2.0 / N);
   for (int m = threadIdx.x; m < N / 2; m += blockDim.x) tw[m] = gtw[m];
-  constexpr int U = 8;  // loads in flight per thread
+  constexpr int U = 16;  // loads in flight per thread
   const int total = F * N;
   if (!INVERSE) {
     // load x (fibers f = 2p + {0,1}) into bit-reversed Makhoul order
