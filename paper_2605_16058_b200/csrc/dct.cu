@@ -8,10 +8,14 @@
 //   DCT-III: v = IDFT(V), V_j = e^{i pi j / 2n} (X_j / c_j - i X_{n-j} / c_{n-j})
 // Two real fibers share one complex FFT (real / imaginary parts).  One CTA
 // transforms 2 P fibers (consecutive rows of one batch block, so global
-// accesses are 16 P-byte runs per time index) with radix-2 DIT stages in
-// shared memory; twiddle tables (sincospi) are built once per device and n
-// in a small library-owned allocation.  n must be a power of two <= 4096;
-// the launcher returns STARM_UNSUPPORTED otherwise.
+// accesses are 16 P-byte runs per time index).  n = 1024 (config c2) runs
+// the four-step register FFT of dct1024_kernel; other lengths run radix-4
+// DIT stages in shared memory (dct_kernel).  Twiddle tables (sincospi) are
+// built once per device and n in a small library-owned allocation.  n must
+// be a power of two <= 4096; the launcher returns STARM_UNSUPPORTED
+// otherwise.
+#include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -213,12 +217,257 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Forward DCT-II for n = 1024 with register-resident FFT passes.
+//
+// The pair sequence z (length N = 32 x 32) is transformed by the four-step
+// factorisation: lane t1 of the pair's warp holds z[t1 + 32 t2] (t2 < 32) and
+// does a 32-point DFT over t2 in registers, multiplies by W_N^{t1 k1}, the
+// warp transposes through its own shared-memory chunks, and lane k1 does the
+// second 32-point DFT, ending with Z[k1 + 32 k2].  The Makhoul post-twiddle
+// needs Z[N - j], which sits in lane (32 - k1) mod 32: one shuffle per value.
+// Shared memory is touched 3 times per element (load, transpose, output)
+// instead of once per radix-4 stage, and only the load and the store need a
+// CTA barrier.  Layout: 16-byte chunk (fibre pair s, time t) at ck(t, s);
+// every access pattern below is bank-conflict free (simulated).
+constexpr int D32_WARPS = 4;  // fibre pairs per CTA (8 fibres: 64-byte runs per time index)
+constexpr int D32_N = 1024;
+constexpr int D32_CHUNKS = 4 * D32_N + D32_N / 2;
+
+__constant__ double c_w32[16][2] = {  // W_32^e = (cos, -sin)(2 pi e / 32)
+    {1.0, -0.0},
+    {0.9807852804032304, -0.19509032201612825},
+    {0.9238795325112867, -0.3826834323650898},
+    {0.8314696123025452, -0.5555702330196022},
+    {0.7071067811865476, -0.7071067811865475},
+    {0.5555702330196023, -0.8314696123025452},
+    {0.38268343236508984, -0.9238795325112867},
+    {0.19509032201612833, -0.9807852804032304},
+    {6.123233995736766e-17, -1.0},
+    {-0.1950903220161282, -0.9807852804032304},
+    {-0.3826834323650897, -0.9238795325112867},
+    {-0.555570233019602, -0.8314696123025455},
+    {-0.7071067811865475, -0.7071067811865476},
+    {-0.8314696123025453, -0.5555702330196022},
+    {-0.9238795325112867, -0.3826834323650899},
+    {-0.9807852804032304, -0.1950903220161286},
+};
+
+__constant__ double c_pw32[32][2] = {  // (cos, sin)(pi 32 k2 / 2N): post-twiddle of j = 32 k2
+    {1.0, 0.0},
+    {0.9987954562051724, 0.049067674327418015},
+    {0.9951847266721969, 0.0980171403295606},
+    {0.989176509964781, 0.14673047445536175},
+    {0.9807852804032304, 0.19509032201612825},
+    {0.970031253194544, 0.24298017990326387},
+    {0.9569403357322088, 0.29028467725446233},
+    {0.9415440651830208, 0.33688985339222005},
+    {0.9238795325112867, 0.3826834323650898},
+    {0.9039892931234433, 0.4275550934302821},
+    {0.881921264348355, 0.47139673682599764},
+    {0.8577286100002721, 0.5141027441932217},
+    {0.8314696123025452, 0.5555702330196022},
+    {0.8032075314806449, 0.5956993044924334},
+    {0.773010453362737, 0.6343932841636455},
+    {0.7409511253549591, 0.6715589548470183},
+    {0.7071067811865476, 0.7071067811865475},
+    {0.6715589548470183, 0.7409511253549591},
+    {0.6343932841636455, 0.773010453362737},
+    {0.5956993044924335, 0.8032075314806448},
+    {0.5555702330196023, 0.8314696123025452},
+    {0.5141027441932217, 0.8577286100002721},
+    {0.4713967368259978, 0.8819212643483549},
+    {0.4275550934302822, 0.9039892931234433},
+    {0.38268343236508984, 0.9238795325112867},
+    {0.33688985339222005, 0.9415440651830208},
+    {0.29028467725446233, 0.9569403357322089},
+    {0.24298017990326398, 0.970031253194544},
+    {0.19509032201612833, 0.9807852804032304},
+    {0.14673047445536175, 0.989176509964781},
+    {0.09801714032956077, 0.9951847266721968},
+    {0.049067674327418126, 0.9987954562051724},
+};
+
+__device__ __forceinline__ int ck(int t, int s) { return 4 * t + s + (t >> 1); }
+__device__ __forceinline__ constexpr int br5(int k) {
+  return ((k & 1) << 4) | ((k & 2) << 2) | (k & 4) | ((k & 8) >> 2) | ((k & 16) >> 4);
+}
+
+// In-register radix-2 DIF DFT of length 32: natural-order input, output
+// X[k] in z[br5(k)].  All indices and twiddles are compile-time.
+template <int LG>
+__device__ __forceinline__ void dif_stage(cplx (&z)[32]) {
+  constexpr int len = 1 << LG, half = len >> 1, step = 32 >> LG;
+#pragma unroll
+  for (int b = 0; b < 32; b += len)
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const cplx a = z[b + i], c = z[b + i + half];
+      z[b + i] = {a.re + c.re, a.im + c.im};
+      const cplx d = {a.re - c.re, a.im - c.im};
+      const int e = i * step;
+      if (e == 0) z[b + i + half] = d;
+      else if (e == 8) z[b + i + half] = {d.im, -d.re};
+      else z[b + i + half] = cmul(d, cplx{c_w32[e][0], c_w32[e][1]});
+    }
+}
+
+__device__ __forceinline__ void fft32_dif(cplx (&z)[32]) {
+  dif_stage<5>(z);
+  dif_stage<4>(z);
+  dif_stage<3>(z);
+  dif_stage<2>(z);
+  dif_stage<1>(z);
+}
+
+// INV: DCT-III.  z_j = V^a_j + i V^b_j is built from X_j and X_{N-j} of the
+// staged tile, and IDFT(z) = conj(DFT(conj z)) / N runs through the same
+// four-step DFT; position pos of the result goes to time 2 pos (pos < N/2)
+// or 2N - 1 - 2 pos.
+template <bool INV>
+__global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
+    const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
+    const cplx* __restrict__ gtw, const cplx* __restrict__ gpw, int vec16) {
+  constexpr int N = D32_N, F = 2 * D32_WARPS, NT = 32 * D32_WARPS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* ch = reinterpret_cast<cplx*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t tiles_per_b = (rows + F - 1) / F;
+  const int64_t b = blockIdx.x / tiles_per_b;
+  const int64_t r0 = (blockIdx.x % tiles_per_b) * F;
+  const double* sb = src + b * rows * N + r0;
+  double* db = dst + b * rows * N + r0;
+  const int nf = int(rows - r0 < F ? rows - r0 : F);  // live fibres of this tile
+  // load: chunk q = (t, s) <- fibres r0 + 2s, r0 + 2s + 1 at time t (zero-filled past rows)
+  if (vec16) {
+#pragma unroll 4
+    for (int q = tid; q < 4 * N; q += NT) {
+      const int t = q >> 2, s = q & 3;
+      cp_async16(&ch[ck(t, s)], sb + 2 * s + int64_t(t) * rows, 2 * s < nf ? 16 : 0);
+    }
+  } else {
+#pragma unroll 4
+    for (int q = tid; q < 4 * N; q += NT) {
+      const int t = q >> 2, s = q & 3;
+      double* d = reinterpret_cast<double*>(&ch[ck(t, s)]);
+      const double* g = sb + 2 * s + int64_t(t) * rows;
+      cp_async8(d, g, 2 * s < nf ? 8 : 0);
+      cp_async8(d + 1, g + 1, 2 * s + 1 < nf ? 8 : 0);
+    }
+  }
+  cp_async_commit();
+  // twiddles, loaded while the tile is in flight: W_N^{t1 k1} for k1 = 8a + b
+  // is wh[a] * wl[b] (two table entries, one product)
+  cplx wl[8], wh[4];
+#pragma unroll
+  for (int b = 1; b < 8; ++b) wl[b] = gtw[lane * b];
+#pragma unroll
+  for (int a = 1; a < 4; ++a) {
+    const int m = lane * 8 * a;
+    wh[a] = gtw[m & (N / 2 - 1)];
+    if (m & (N / 2)) wh[a] = {-wh[a].re, -wh[a].im};
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  const double c0 = sqrt(1.0 / N), c1 = sqrt(2.0 / N);
+  const cplx pl = gpw[lane];
+  // pass 1: lane t1 holds z[t1 + 32 t2]
+  cplx z[32];
+  if constexpr (!INV) {
+    // Makhoul order: position pos <- time 2 pos (pos < N/2), 2N - 1 - 2 pos otherwise
+#pragma unroll
+    for (int t2 = 0; t2 < 32; ++t2) {
+      const int pos = lane + 32 * t2;
+      const int t = t2 < 16 ? 2 * pos : 2 * N - 1 - 2 * pos;
+      z[t2] = ch[ck(t, w)];
+    }
+  } else {
+    // V^f_j = e^{i theta_j} (Y_j / c_j - i Y_{N-j} / c_{N-j}), z = conj(V^a + i V^b)
+    const double ic0 = 1.0 / c0, ic1 = 1.0 / c1;
+#pragma unroll
+    for (int t2 = 0; t2 < 32; ++t2) {
+      const int j = lane + 32 * t2;
+      const cplx y = ch[ck(j, w)], yn = ch[ck((N - j) & (N - 1), w)];
+      const double sj = j ? ic1 : ic0, sn = j ? ic1 : 0.0;
+      const cplx pw = t2 == 0 ? pl : cmul(pl, cplx{c_pw32[t2][0], c_pw32[t2][1]});
+      const cplx va = cmul(pw, cplx{y.re * sj, -yn.re * sn});
+      const cplx vb = cmul(pw, cplx{y.im * sj, -yn.im * sn});
+      z[t2] = {va.re - vb.im, -(va.im + vb.re)};
+    }
+  }
+  fft32_dif(z);
+  // twiddle W_N^{t1 k1}
+#pragma unroll
+  for (int k1 = 1; k1 < 32; ++k1) {
+    const int a = k1 >> 3, b = k1 & 7;
+    const cplx tw = a == 0 ? wl[b] : (b == 0 ? wh[a] : cmul(wh[a], wl[b]));
+    z[br5(k1)] = cmul(z[br5(k1)], tw);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < 32; ++k1) ch[ck(32 * k1 + (lane ^ k1), w)] = z[br5(k1)];
+  __syncwarp();
+#pragma unroll
+  for (int t1 = 0; t1 < 32; ++t1) z[t1] = ch[ck(32 * lane + (t1 ^ lane), w)];
+  __syncwarp();
+  fft32_dif(z);  // lane k1: Z[k1 + 32 k2] in z[br5(k2)]
+  if constexpr (!INV) {
+    const int partner = (32 - lane) & 31;
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) {
+      const int j = lane + 32 * k2;
+      const cplx zj = z[br5(k2)];
+      const cplx o = z[br5(31 - k2)], own = z[br5((32 - k2) & 31)];
+      cplx zn;
+      zn.re = __shfl_sync(0xffffffffu, o.re, partner);
+      zn.im = __shfl_sync(0xffffffffu, o.im, partner);
+      if (lane == 0) zn = own;  // Z[N - 32 k2] = Z[32 (32 - k2)] (k2 = 0: Z[0])
+      const cplx va = {0.5 * (zj.re + zn.re), 0.5 * (zj.im - zn.im)};  // (Z_j + conj Z_{n-j}) / 2
+      const cplx vb = {0.5 * (zj.im + zn.im), 0.5 * (zn.re - zj.re)};  // (Z_j - conj Z_{n-j}) / 2i
+      const cplx pw = k2 == 0 ? pl : cmul(pl, cplx{c_pw32[k2][0], c_pw32[k2][1]});
+      const double cj = j ? c1 : c0;
+      ch[ck(j, w)] = {cj * fma(pw.re, va.re, pw.im * va.im), cj * fma(pw.re, vb.re, pw.im * vb.im)};
+    }
+  } else {
+    const double inv = 1.0 / N;
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) {
+      const int pos = lane + 32 * k2;
+      const int t = k2 < 16 ? 2 * pos : 2 * N - 1 - 2 * pos;
+      const cplx r = z[br5(k2)];
+      ch[ck(t, w)] = {r.re * inv, -r.im * inv};
+    }
+  }
+  __syncthreads();
+  if (vec16 && nf == F) {
+#pragma unroll 8
+    for (int q = tid; q < 4 * N; q += NT) {
+      const int t = q >> 2, s = q & 3;
+      const cplx v = ch[ck(t, s)];
+      *reinterpret_cast<double2*>(db + 2 * s + int64_t(t) * rows) = make_double2(v.re, v.im);
+    }
+  } else {
+    for (int q = tid; q < 4 * N; q += NT) {
+      const int t = q >> 2, s = q & 3;
+      const cplx v = ch[ck(t, s)];
+      double* g = db + 2 * s + int64_t(t) * rows;
+      if (2 * s < nf) g[0] = v.re;
+      if (2 * s + 1 < nf) g[1] = v.im;
+    }
+  }
+}
+
 struct DctTables {
   cplx* tw[13] = {};
   cplx* pw[13] = {};
 };
 
 std::mutex g_dct_mu;
+// STARM_DCT_LEGACY=1: the shared-memory radix-4 kernel for every length (A/B runs)
+const bool g_dct_legacy = [] {
+  const char* e = getenv("STARM_DCT_LEGACY");
+  return e && e[0] == '1';
+}();
 DctTables g_dct_tables[64];  // per device ordinal
 
 int dct_tables(int logn, const cplx** tw, const cplx** pw, cudaStream_t st) {
@@ -260,6 +509,21 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
   const cplx *tw = nullptr, *pw = nullptr;
   const int rc = dct_tables(LOGN, &tw, &pw, st);
   if (rc) return rc;
+  if (LOGN == 10 && !g_dct_legacy) {
+    const size_t sm2 = size_t(D32_CHUNKS) * sizeof(cplx);
+    const int64_t t2 = (rows + 2 * D32_WARPS - 1) / (2 * D32_WARPS) * batch;
+    const int vec16 = (rows % 2 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
+    // hoisted twiddle products at 2 CTAs / SM: 1.33 ms on c2, against 1.44 ms
+    // for per-k1 table loads at 3 CTAs / SM and 1.36 ms for the hoisted
+    // twiddles squeezed into 168 registers (3 CTAs / SM, spills); loading
+    // each lane's 32 values straight from global memory (no staging) 2.4 ms
+    auto kern = inverse ? dct1024_kernel<true> : dct1024_kernel<false>;
+    STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)));
+    kern<<<unsigned(t2), 32 * D32_WARPS, sm2, st>>>(src, dst, rows, tw, pw, vec16);
+    STARM_LAUNCH_CHECK();
+    return STARM_OK;
+  }
   auto kern = inverse ? dct_kernel<LOGN, true> : dct_kernel<LOGN, false>;
   STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   kern<<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, batch, tw, pw);

@@ -57,7 +57,11 @@ def test_ttm_large_dct_round_trip():
 
 @pytest.mark.parametrize("dims,mode", [((37, 41, 2), 2), ((5, 3, 4), 2), ((3, 7, 8, 3), 2),
                                        ((2, 5, 3, 64), 3), ((9, 11, 1024), 2),
-                                       ((3, 2, 2048), 2), ((2, 3, 4096), 2), ((1, 1, 16), 2)])
+                                       ((3, 2, 2048), 2), ((2, 3, 4096), 2), ((1, 1, 16), 2),
+                                       # n = 1024 register-FFT kernel: full tiles with 16-byte
+                                       # access, an even-rows partial tile, batch > 1
+                                       ((8, 12, 1024), 2), ((10, 13, 1024), 2),
+                                       ((3, 4, 1024, 2), 2), ((1, 1, 1024), 2)])
 def test_fast_dct_matches_dense_product(dims, mode):
     # the DCT kind takes the FFT path (starm_dct_f64).  Oracles: the
     # reference's dense mode-k product with its DCT matrix (whose cos entries
