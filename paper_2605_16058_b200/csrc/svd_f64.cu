@@ -2558,6 +2558,168 @@ __global__ void __launch_bounds__(32) svd_orth_kernel(SvdParams P) {
   }
 }
 
+// Blocked variant (RP <= 1024): one CTA (8 warps) per slice.  Vectors are
+// taken 16 at a time into shared memory (W); the block is projected against
+// all earlier, finished vectors Q = V[:, 0:j0] by block-MGS over 64-column
+// chunks of Q, twice (C = Q_c^T W, W -= Q_c C, both on DMMA), then
+// orthonormalised internally (CGS2, one warp per dot product) and written
+// back.  A vector that vanishes (norm <= 1/2 of its unit input) falls back
+// to canonical basis vectors projected against every earlier vector, as the
+// one-warp kernel above.  Vector j depends only on vectors < j (block
+// boundaries at multiples of 16), so the leading k vectors are the same bits
+// whatever the slice's rank.  Work per slice: 4 n k^2 flops on DMMA instead
+// of k^2 dependent warp dot products.
+constexpr int OB = 16;   // vectors per block
+constexpr int OQ = 64;   // earlier vectors per chunk
+constexpr int OCS = 24;  // C row stride (conflict-free B fragments)
+__host__ __device__ __forceinline__ size_t orth_smem(int64_t RP) {
+  return (size_t(OB) * size_t(RP + 4) + size_t(OQ) * OCS + 32) * sizeof(double);
+}
+
+__device__ __forceinline__ double cta_sum256(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const double s = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(256) svd_orth_block_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = int(P.n), rp = int(P.RP), ws = rp + 4;
+  const int64_t NP = P.NP, RP = P.RP;
+  double* W = reinterpret_cast<double*>(smem_raw);  // [OB][ws]: column c at W + c * ws
+  double* Cs = W + OB * ws;                         // [OQ][OCS]
+  double* red = Cs + OQ * OCS;                      // [8] CTA partials
+  double* dots = red + 8;                           // [16]
+  __shared__ int64_t cur;
+  for (;;) {
+    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[3], 1ull));
+    __syncthreads();
+    const int64_t it = cur;
+    __syncthreads();
+    if (it >= P.count) break;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int k = int(kout_of(P, slice));
+    double* Vb = P.vsel + si * RP * NP;
+    int64_t basis = 0;
+    for (int j0 = 0; j0 < k; j0 += OB) {
+      const int kb = min(OB, k - j0);
+      for (int e = tid; e < OB * rp; e += 256) {
+        const int c = e / rp, q = e - c * rp;
+        W[c * ws + q] = (c < kb && q < n) ? Vb[int64_t(j0 + c) * RP + q] : 0.0;
+      }
+      __syncthreads();
+      for (int pass = 0; pass < 2 && j0 > 0; ++pass) {
+        for (int i0 = 0; i0 < j0; i0 += OQ) {
+          {  // Cs[i][c] = sum_q V[q][i0 + i] W[c][q]; warp w: i in [8w, 8w + 8)
+            const int col = i0 + 8 * warp + g;
+            const bool live = col < j0;
+            const double* qa = Vb + int64_t(live ? col : 0) * RP + t;
+            const double* wb = W + g * ws + t;
+            double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < n; r += 4) {
+              const double a = live ? qa[r] : 0.0;
+              dmma884n(d0, d1, a, wb[r]);
+              dmma884n(e0, e1, a, wb[r + 8 * ws]);
+            }
+            double* cr = Cs + (8 * warp + g) * OCS + 2 * t;
+            cr[0] = d0;
+            cr[1] = d1;
+            cr[8] = e0;
+            cr[9] = e1;
+          }
+          __syncthreads();
+          {  // W[c][q] -= sum_i V[q][i0 + i] Cs[i][c]; warp w: row tiles w, w + 8, ...
+            const int nic = min(OQ, j0 - i0);  // a multiple of OB
+            for (int r0 = 8 * warp; r0 < n; r0 += 64) {
+              const double* qa = Vb + int64_t(i0 + t) * RP + r0 + g;
+              const double* cb = Cs + t * OCS + g;
+              double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll 4
+              for (int kk = 0; kk < nic; kk += 4) {
+                const double a = qa[int64_t(kk) * RP];
+                dmma884n(d0, d1, a, cb[kk * OCS]);
+                dmma884n(e0, e1, a, cb[kk * OCS + 8]);
+              }
+              double* wr = W + 2 * t * ws + r0 + g;
+              wr[0] -= d0;
+              wr[ws] -= d1;
+              wr[8 * ws] -= e0;
+              wr[9 * ws] -= e1;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int c = 0; c < kb; ++c) {
+        double* wc = W + c * ws;
+        for (int pass = 0; pass < 2 && c > 0; ++pass) {
+          for (int i = warp; i < c; i += 8) {
+            const double* wi = W + i * ws;
+            double sd = 0.0;
+            for (int q = lane; q < n; q += 32) sd = fma(wi[q], wc[q], sd);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+            if (lane == 0) dots[i] = sd;
+          }
+          __syncthreads();
+          for (int q = tid; q < n; q += 256) {
+            double v = wc[q];
+            for (int i = 0; i < c; ++i) v = fma(-dots[i], W[i * ws + q], v);
+            wc[q] = v;
+          }
+          __syncthreads();
+        }
+        double sq = 0.0;
+        for (int q = tid; q < n; q += 256) sq = fma(wc[q], wc[q], sq);
+        double nr = sqrt(cta_sum256(sq, red));
+        if (!(nr > 0.5)) {
+          // vanished: canonical basis vectors, each projected (3 passes, MGS)
+          // against every earlier vector, until one keeps norm > cthr
+          const int j = j0 + c;
+          const double cthr = 0.5 * sqrt(double(n - j) / double(n));
+          for (int attempt = 1; attempt <= n; ++attempt) {
+            for (int q = tid; q < n; q += 256) wc[q] = (q == basis) ? 1.0 : 0.0;
+            ++basis;
+            __syncthreads();
+            for (int pass = 0; pass < 3; ++pass) {
+              for (int i = 0; i < j; ++i) {
+                const double* vi = i < j0 ? Vb + int64_t(i) * RP : W + (i - j0) * ws;
+                double sd = 0.0;
+                for (int q = tid; q < n; q += 256) sd = fma(vi[q], wc[q], sd);
+                const double dd = cta_sum256(sd, red);
+                for (int q = tid; q < n; q += 256) wc[q] = fma(-dd, vi[q], wc[q]);
+                __syncthreads();
+              }
+            }
+            sq = 0.0;
+            for (int q = tid; q < n; q += 256) sq = fma(wc[q], wc[q], sq);
+            nr = sqrt(cta_sum256(sq, red));
+            if (nr > cthr) break;
+          }
+        }
+        const double inv = nr > 0.0 ? 1.0 / nr : 0.0;
+        for (int q = tid; q < n; q += 256) wc[q] *= inv;
+        __syncthreads();
+      }
+      for (int e = tid; e < kb * rp; e += 256) {
+        const int c = e / rp, q = e - c * rp;
+        if (q < n) Vb[int64_t(j0 + c) * RP + q] = W[c * ws + q];
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Back-transformation v <- P1 P2 v of the right vectors: the bulge chase's
 // right reflectors in reverse order, then the band reduction's LQ panels
 // (I - V T V^T) from the last to the first.  One CTA per (slice, group of G
@@ -2963,6 +3125,11 @@ int g_reduce_threads = [] {
   return (v == 0 || v == 256 || v == 512) ? v : 256;
 }();
 int g_tune_sweeps = 60;
+// STARM_ORTH_WARP=1: the one-warp-per-slice orthonormalisation everywhere (A/B runs)
+const bool g_orth_warp = [] {
+  const char* e = getenv("STARM_ORTH_WARP");
+  return e && e[0] == '1';
+}();
 // bisection blocks per launch on the side stream (env STARM_BISECT_SIDE_PER_SM, per SM)
 int g_bisect_side_blocks = [] {
   const char* e = getenv("STARM_BISECT_SIDE_PER_SM");
@@ -3356,7 +3523,21 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
   if (pl.run_vec) {
     svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n);
     STARM_LAUNCH_CHECK();
-    svd_orth_kernel<<<pl.slots_t, 32, 0, st>>>(P);
+    if (pl.RP <= 1024 && !g_orth_warp) {
+      const size_t osm = orth_smem(pl.RP);
+      int dev = 0, sms = 0;
+      STARM_CUDA_TRY(cudaGetDevice(&dev));
+      STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      STARM_CUDA_TRY(cudaFuncSetAttribute(svd_orth_block_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(osm)));
+      int per = int((227 * 1024) / (osm + 1024));
+      per = per < 1 ? 1 : (per > 4 ? 4 : per);
+      int64_t grid = int64_t(sms) * per;
+      if (grid > count) grid = count;
+      svd_orth_block_kernel<<<unsigned(grid), 256, osm, st>>>(P);
+    } else {
+      svd_orth_kernel<<<pl.slots_t, 32, 0, st>>>(P);
+    }
     STARM_LAUNCH_CHECK();
     {
       // one CTA per (slice, group of bt_g vectors); groups beyond a slice's

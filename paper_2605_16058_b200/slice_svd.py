@@ -321,6 +321,8 @@ def svd_truncated_slices(ahat, ranks, strategy=SLICES_PARALLEL, threads=1, keep_
     import torch
     _check_strategy(strategy, threads)
     m, p, r, n = _geometry(ahat)
+    if isinstance(ranks, torch.Tensor):  # e.g. ThresholdResult.ranks of a device compute_threshold
+        ranks = ranks.cpu().numpy()
     ranks = np.asarray(ranks, dtype=np.int64)
     if ranks.shape != (n,):
         raise ValueError(f"need one rank per slice ({n}), got shape {ranks.shape}")

@@ -2,7 +2,7 @@
 time the compression (device-resident input) and check the realised error
 against the energy identity  relerr^2 = discarded / total  (orthogonal M).
 
-usage: python scripts/run_config.py c3 [reps]
+usage: python scripts/run_config.py c1|c2|c3|c4|c5 [reps] [tol]
 """
 import sys
 import time
@@ -45,6 +45,30 @@ elif name == "c5":
     run = lambda x: sb.tsvdm_fixed_rank(x, ts, 16)
     if len(sys.argv) > 3 and sys.argv[3] == "tol":
         run = lambda x: sb.tsvdm_tolerance(x, ts, 1e-4)
+elif name == "c4":
+    # SURVEY 8c "Config 4 restatement": float32 input upcast to float64 (tensor.py:87), the
+    # non-orthonormal M applied as a raw-matrix ttm, values -> threshold -> truncated factors,
+    # reconstruction with the explicit M^-1 (not M^T)
+    a32, mm, minv = configs.config4()
+    a = np.asfortranarray(a32, dtype=np.float64)  # upcast like the reference (tensor.py:87)
+    del a32
+    eps4 = 1e-3
+
+    def run(x):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        ahat = sb.ttm(x, 2, mm)
+        ev[1].record()
+        s = sb.svd_values_only(ahat)
+        ev[2].record()
+        thr = sb.compute_threshold(s, eps4)
+        ev[3].record()
+        f = sb.svd_truncated_slices(ahat, thr.ranks)
+        ev[4].record()
+        ev[4].synchronize()
+        print("    stages ms: " + ", ".join(f"{k} {ev[i].elapsed_time(ev[i + 1]):.1f}" for i, k in
+                                          enumerate(("ttm", "values", "threshold", "truncated"))))
+        return ahat, thr, f
 else:
     raise SystemExit(f"unknown config {name}")
 if a is not None:
@@ -60,7 +84,26 @@ for i in range(reps):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"  rep {i}: {ms:.1f} ms  total_rank {c.factors.total_rank}", flush=True)
+    tr = c[2].total_rank if name == "c4" else c.factors.total_rank
+    print(f"  rep {i}: {ms:.1f} ms  total_rank {tr}", flush=True)
+if name == "c4":
+    from paper_2605_16058_b200 import _native as nat
+    ahat, thr, f = c
+    m_, p_, n_ = xdev.dims
+    chat = sb.DeviceTensor.empty(xdev.dims, dev)
+    nat.call("starm_unpack_facewise_f64", f.u_data.data_ptr(), f.g_data.data_ptr(),
+             f.ranks_dev.data_ptr(), f.u_off.data_ptr(), f.g_off.data_ptr(), m_, p_, n_,
+             chat.data.data_ptr(), nat.stream_ptr(dev))
+    err_t = relative_error_device(ahat, chat)
+    rec = sb.ttm(chat, 2, minv)
+    err_o = relative_error_device(xdev, rec)
+    pred = float(np.sqrt(thr.discarded_energy / thr.total_energy))
+    print(f"  J {thr.j}  tau {thr.tau:.6g}  sum rank {f.total_rank} of {m_ * n_}")
+    print(f"  transform-domain relerr {err_t:.10g}  predicted {pred:.10g}  diff {abs(err_t - pred):.3g}")
+    print(f"  original-domain relerr {err_o:.10g} (M non-orthonormal: not bounded by eps)")
+    ok = abs(err_t - pred) <= 1e-8 + 1e-6 * pred and err_t <= eps4
+    print("OK" if ok else "MISMATCH")
+    sys.exit(0 if ok else 1)
 rec = reconstruct_device(c, dev)
 err = relative_error_device(xdev, rec)
 pred = float(np.sqrt(c.discarded_energy / c.total_energy))
