@@ -664,7 +664,7 @@ __device__ void panel_factor(QrSmemFixed& q, double* pan, int64_t prs, int64_t k
 // src[r * sr + c * sc] for lo <= r < nrows, 0 otherwise (all loads in flight).
 template <int NT, int RPT>
 __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64_t prs64, int64_t k064,
-                                              int64_t nrows64, const double* src, int64_t sr,
+                                              int64_t nrows64, double* src, int64_t sr,
                                               int64_t sc, int64_t lo64) {
   // Register-resident panel, column loop NOT fully unrolled: b[i][c] holds
   // panel column j + c of this thread's rows; each loop iteration factors
@@ -768,10 +768,15 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
         }
       }
     }
+    // column j is final: pan gets the explicit V column (0 above the pivot,
+    // 1 on it, v below, 0 past nrows) and the R entries (rows k0 .. pr) go
+    // straight back to the source matrix
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int r = tid + i * NT;
-      if (r < nrows) pan[j * prs + r] = b[i][C];
+      const double bv = b[i][C];
+      if (r < prs) pan[j * prs + r] = (r > pr && r < nrows) ? bv : (r == pr ? 1.0 : 0.0);
+      if (r >= k0 && r <= pr) src[int64_t(r) * sr + j * sc] = bv;
     }
 #ifdef STARM_PF_PROBE
     long long p3 = clock64();
@@ -801,22 +806,25 @@ __device__ __noinline__ void panel_factor_reg(QrSmemFixed& q, double* pan, int64
 #endif
 }
 
+// Returns true when the register path ran: then pan already holds the
+// explicit V and R is written back through src; otherwise the caller copies
+// R out of pan and forms V (explicit_v).
 template <int NT>
-__device__ void panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows,
-                                 const double* src, int64_t sr, int64_t sc, int64_t lo) {
+__device__ bool panel_factor_any(QrSmemFixed& q, double* pan, int64_t prs, int64_t k0, int64_t nrows,
+                                 double* src, int64_t sr, int64_t sc, int64_t lo) {
   const int64_t rpt = (nrows + NT - 1) / NT;
   switch (rpt) {
-    case 1: panel_factor_reg<NT, 1>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 2: panel_factor_reg<NT, 2>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 3: panel_factor_reg<NT, 3>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
-    case 4: panel_factor_reg<NT, 4>(q, pan, prs, k0, nrows, src, sr, sc, lo); break;
+    case 1: panel_factor_reg<NT, 1>(q, pan, prs, k0, nrows, src, sr, sc, lo); return true;
+    case 2: panel_factor_reg<NT, 2>(q, pan, prs, k0, nrows, src, sr, sc, lo); return true;
+    case 3: panel_factor_reg<NT, 3>(q, pan, prs, k0, nrows, src, sr, sc, lo); return true;
+    case 4: panel_factor_reg<NT, 4>(q, pan, prs, k0, nrows, src, sr, sc, lo); return true;
     default:
       for (int c = 0; c < BW; ++c)
         for (int64_t r = threadIdx.x; r < prs; r += NT)
           pan[c * prs + r] = (r >= lo && r < nrows) ? src[r * sr + c * sc] : 0.0;
       __syncthreads();
       panel_factor<NT>(q, pan, prs, k0, nrows);
-      break;
+      return false;
   }
 }
 
@@ -1508,14 +1516,17 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
   const int tid = threadIdx.x;
   for (int64_t k0 = 0; k0 < NP; k0 += BW) {
     const int64_t kc = (k0 / RCH) * RCH;
-    { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
-    if (tid < BW * BW) {
-      const int c = tid / BW, r = tid % BW;
-      if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+    bool reg;
+    { long long _a = clock64(); reg = panel_factor_any<NT>(q, pan, prs, k0, LP, X + k0 * LP, 1, LP, 0); pf += clock64() - _a; }
+    if (!reg) {
+      if (tid < BW * BW) {
+        const int c = tid / BW, r = tid % BW;
+        if (r <= c) X[(k0 + r) + (k0 + c) * LP] = pan[c * prs + k0 + r];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (k0 + BW < NP) {
-      explicit_v<NT>(pan, prs, k0, LP);
+      if (!reg) explicit_v<NT>(pan, prs, k0, LP);
       panel_gram<NT>(q, pan, prs, kc, LP);
       long long _a = clock64();
       if (!(NT == 256 && P.wtwo &&
@@ -1575,14 +1586,17 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
       const int64_t kc = (k / RCH) * RCH;
-      { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, k, RP, X + k * LP, 1, LP, 0); pf += clock64() - _a; }
-      if (tid < BW * BW) {
-        const int c = tid / BW, r = tid % BW;
-        if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
+      bool reg;
+      { long long _a = clock64(); reg = panel_factor_any<NT>(q, pan, prs, k, RP, X + k * LP, 1, LP, 0); pf += clock64() - _a; }
+      if (!reg) {
+        if (tid < BW * BW) {
+          const int c = tid / BW, r = tid % BW;
+          if (r <= c) X[(k + r) + (k + c) * LP] = pan[c * prs + k + r];
+        }
+        __syncthreads();
       }
-      __syncthreads();
       if (k + BW >= NP) break;
-      explicit_v<NT>(pan, prs, k, RP);
+      if (!reg) explicit_v<NT>(pan, prs, k, RP);
       panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
@@ -1595,13 +1609,15 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       }
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
-      { long long _a = clock64(); panel_factor_any<NT>(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
-      if (tid < BW * BW) {
-        const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
-        if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
+      { long long _a = clock64(); reg = panel_factor_any<NT>(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
+      if (!reg) {
+        if (tid < BW * BW) {
+          const int c = tid / BW, r = tid % BW;  // R2[r][c] -> A[k+c][j0+r]
+          if (r <= c) X[(k + c) + (j0 + r) * LP] = pan[c * prs + j0 + r];
+        }
+        __syncthreads();
+        explicit_v<NT>(pan, prs, j0, NP);
       }
-      __syncthreads();
-      explicit_v<NT>(pan, prs, j0, NP);
       panel_gram<NT>(q, pan, prs, (j0 / 8) * 8, NP);
       if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
         double* dst = P.rvlog + (si * (NP / BW) + k / BW) * (BW * NP + BW * BW);

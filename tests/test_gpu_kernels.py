@@ -167,6 +167,23 @@ def test_truncated_match_leading_triplets_bitwise():
             assert np.array_equal(f.g_block(i), g)
 
 
+def test_truncated_bitwise_across_orth_blocks():
+    # r = 150: several 16-vector orthonormalisation blocks, earlier vectors
+    # projected in more than one 64-column chunk, partial last blocks
+    dims = (150, 170, 4)
+    a = random_array(dims, 23)
+    t = sb.DenseTensor(a)
+    full = sb.svd_all_slices(t)
+    ranks = np.array([0, 75, 150, 97])
+    f = sb.svd_truncated_slices(t, ranks)
+    for i, k in enumerate(ranks):
+        u = full.u.frontal_slice(i)
+        assert np.linalg.norm(u.T @ u - np.eye(150)) <= 1e-10 * math.sqrt(150)
+        assert np.array_equal(f.u_block(i), u[:, :k])
+        g = full.s[:k, i, None] * full.v.frontal_slice(i)[:, :k].T
+        assert np.array_equal(f.g_block(i), g)
+
+
 def _degenerate_slices():
     """Slices whose singular values repeat exactly: blockdiag(B, B) (the two
     copies decouple in the bidiagonal), U diag(pairs) V^T, and rank-deficient
