@@ -1538,9 +1538,11 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
     }
     __syncthreads();
   }
-  // keep only R (upper triangle of the leading NP x NP block)
-  for (int64_t c = 0; c < NP; ++c)
-    for (int64_t r = c + 1 + tid; r < LP; r += NT) X[r + c * LP] = 0.0;
+  // keep only R (upper triangle of the leading NP x NP block): zero below the
+  // diagonal in the rows the band phase reads (< RP; TSQR masks r <= c itself)
+  const int zr = int(P.RP < LP ? P.RP : LP), lp = int(LP);
+  for (int c = 0; c < int(NP); ++c)
+    for (int r = c + 1 + tid; r < zr; r += NT) X[r + int64_t(c) * lp] = 0.0;
   __syncthreads();
 }
 
@@ -2757,7 +2759,7 @@ __host__ __device__ __forceinline__ size_t bt_smem(int64_t n, int g) {
 }
 __device__ __forceinline__ int sx(int q) { return q + (q >> 4); }
 
-__global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int G) {
+__global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int G, int lq) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nthr = blockDim.x;
   const int n = int(P.n);
@@ -2842,7 +2844,7 @@ __global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int
     // sequence of 2 nq chunk loads (pass 1: V^T x, pass 2: x -= V z) through
     // a two-buffer cp.async ring.
     const double* rv = P.rvlog + si * int64_t(npan) * (BW * NP + BW * BW);
-    for (int pk = npan - 2; pk >= 0; --pk) {
+    for (int pk = lq ? npan - 2 : -1; pk >= 0; --pk) {
       const double* Vp = rv + int64_t(pk) * (BW * NP + BW * BW);  // V[c][q], q < NP
       const int jlo = pk * BW + BW;
       const int nq = (n - jlo + BT_ROWS - 1) / BT_ROWS;
@@ -2907,6 +2909,115 @@ __global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int
     __syncwarp();
     if (act)
       for (int q = lane; q < RP; q += 32) vg[q] = q < n ? x[sx(q)] : 0.0;
+    __syncthreads();
+  }
+}
+
+// LQ panels of the band reduction applied to KB right vectors at once on
+// DMMA (after svd_backtransform_kernel has applied the bulge reflectors):
+// X <- (I - V_p T_p V_p^T) X for p = last .. first, X (n x KB) resident in
+// shared memory, V_p streamed from the panel log.  Per panel: Y = V_p^T X
+// (16 x KB tiles, one per warp, K split in two when KB = 16), Z = T_p Y,
+// X -= V_p Z.  Column v of X depends only on itself, so vector j is the
+// same bits whatever the slice's rank.  4 n^2 flops per vector on DMMA.
+constexpr int LQ_ZS = 40;  // Z row stride (= 8 mod 32: conflict-free B fragments)
+__host__ __device__ __forceinline__ int lq_xs(int64_t n) { return int(((n + 31) / 32) * 32 + 4); }
+__host__ __device__ __forceinline__ size_t lq_smem(int64_t n, int kb) {
+  return (size_t(kb) * lq_xs(n) + 2 * BW * 40 + BW * LQ_ZS + BW * BW) * sizeof(double);
+}
+
+template <int KB>
+__global__ void __launch_bounds__(256) svd_lqapply_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT8 = KB / 8, TILES = 2 * NT8, KS = 8 / TILES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = int(P.n), npan = int(P.NP / BW), xs = lq_xs(P.n);
+  const int64_t NP = P.NP, RP = P.RP;
+  double* X = reinterpret_cast<double*>(smem_raw);  // [KB][xs]: vector v at X + v * xs
+  double* Ys = X + KB * xs;                         // [KS][16][40]
+  double* Zs = Ys + 2 * BW * 40;                    // [16][LQ_ZS]
+  double* Ts = Zs + BW * LQ_ZS;                     // [16][16]
+  const int ngroups = (n + KB - 1) / KB;
+  const int tile = warp % TILES, ks = warp / TILES, mt = tile / NT8, nt = tile % NT8;
+  for (int64_t cta = blockIdx.x; cta < P.count * ngroups; cta += gridDim.x) {
+    const int64_t it = cta / ngroups;
+    const int j0 = int(cta % ngroups) * KB;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int kv = int(kout_of(P, slice));
+    if (j0 >= kv) continue;
+    double* vb = P.vsel + si * RP * NP;
+    for (int e = tid; e < KB * xs; e += 256) {
+      const int v = e / xs, q = e - v * xs;
+      X[e] = (j0 + v < kv && q < n) ? vb[int64_t(j0 + v) * RP + q] : 0.0;
+    }
+    const double* rv = P.rvlog + si * int64_t(npan) * (BW * NP + BW * BW);
+    for (int pk = npan - 2; pk >= 0; --pk) {
+      const double* Vp = rv + int64_t(pk) * (BW * NP + BW * BW);  // V[c][q] at Vp[c * NP + q]
+      const int jlo = pk * BW + BW;                               // V rows < jlo are zero
+      if (jlo >= n) continue;
+      Ts[tid] = Vp[BW * NP + tid];  // T[a][b] at a * 16 + b (256 threads, 256 entries)
+      if (pk > 0 && tid < BW) {     // next panel's live rows -> L2 while this one runs
+        const double* nv = Vp - (BW * NP + BW * BW) + int64_t(tid) * NP;
+        const int lo = (jlo - BW) & ~1, bytes = (n - lo) * 8 & ~15;
+        if (bytes > 0) bulk_prefetch_l2(nv + lo, bytes);
+      }
+      __syncthreads();
+      {  // Y = V^T X: warp -> (mt, nt) tile, rows split KS ways (4-aligned)
+        const int r0 = jlo & ~3, span = ((n - r0 + 4 * KS - 1) / (4 * KS)) * 4;
+        const int rb = r0 + ks * span, re = min(n, rb + span);
+        const double* va = Vp + int64_t(8 * mt + g) * NP + t;
+        const double* xb = X + (8 * nt + g) * xs + t;
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+        int r = rb;
+#pragma unroll 4
+        for (; r + 4 < re; r += 8) {
+          dmma884n(d0, d1, va[r], xb[r]);
+          dmma884n(e0, e1, va[r + 4], xb[r + 4]);
+        }
+        if (r < re) dmma884n(d0, d1, va[r], xb[r]);
+        double* yr = Ys + (ks * BW + 8 * mt + g) * 40 + 8 * nt + 2 * t;
+        yr[0] = d0 + e0;
+        yr[1] = d1 + e1;
+      }
+      __syncthreads();
+      for (int e = tid; e < BW * KB; e += 256) {  // Z = T Y
+        const int a = e / KB, v = e - a * KB;
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < BW; ++b) {
+          double y = Ys[b * 40 + v];
+          if (KS == 2) y += Ys[(BW + b) * 40 + v];
+          acc = fma(Ts[a * BW + b], y, acc);
+        }
+        Zs[a * LQ_ZS + v] = acc;
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int r0 = (jlo & ~7) + 8 * warp; r0 < n; r0 += 64) {  // X -= V Z, 8-row tiles
+        double acc[NT8][2];
+#pragma unroll
+        for (int c = 0; c < NT8; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < BW; kk += 4) {
+          const double a = Vp[int64_t(kk + t) * NP + r0 + g];
+#pragma unroll
+          for (int c = 0; c < NT8; ++c) dmma884n(acc[c][0], acc[c][1], a, Zs[(kk + t) * LQ_ZS + 8 * c + g]);
+        }
+#pragma unroll
+        for (int c = 0; c < NT8; ++c) {
+          X[(8 * c + 2 * t) * xs + r0 + g] -= acc[c][0];
+          X[(8 * c + 2 * t + 1) * xs + r0 + g] -= acc[c][1];
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < KB * int(RP); e += 256) {
+      const int v = e / int(RP), q = e - v * int(RP);
+      if (j0 + v < kv) vb[int64_t(j0 + v) * RP + q] = q < n ? X[v * xs + q] : 0.0;
+    }
     __syncthreads();
   }
 }
@@ -3141,6 +3252,11 @@ int g_reduce_threads = [] {
   return (v == 0 || v == 256 || v == 512) ? v : 256;
 }();
 int g_tune_sweeps = 60;
+// STARM_LQ_WARP=1: LQ panels applied per warp inside the back-transformation (A/B runs)
+const bool g_lq_warp = [] {
+  const char* e = getenv("STARM_LQ_WARP");
+  return e && e[0] == '1';
+}();
 // STARM_ORTH_WARP=1: the one-warp-per-slice orthonormalisation everywhere (A/B runs)
 const bool g_orth_warp = [] {
   const char* e = getenv("STARM_ORTH_WARP");
@@ -3564,7 +3680,25 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       const int64_t cap = int64_t(sms) * pl.btw * 8;
       if (blocks > cap) blocks = cap;
-      svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g);
+      // LQ panels on DMMA over blocks of 32 (n <= 636) or 16 (n <= 1276) vectors
+      // for n > 400 (measured: c4 n = 512 truncated pass 762 -> 733 ms, c3 n =
+      // 1024 420 -> 409 ms); below that the separate launch costs more than
+      // the per-warp panels inside the back-transformation (c2 n = 361: +0.34 ms)
+      const int lkb = (g_lq_warp || pl.n <= 400) ? 0
+                      : (lq_smem(pl.n, 32) <= size_t(200 * 1024) ? 32
+                         : (lq_smem(pl.n, 16) <= size_t(200 * 1024) ? 16 : 0));
+      svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0);
+      STARM_LAUNCH_CHECK();
+      if (lkb) {
+        const size_t lsm = lq_smem(pl.n, lkb);
+        auto lk = lkb == 32 ? svd_lqapply_kernel<32> : svd_lqapply_kernel<16>;
+        STARM_CUDA_TRY(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsm)));
+        int per = int((227 * 1024) / (lsm + 1024));
+        per = per < 1 ? 1 : (per > 4 ? 4 : per);
+        int64_t lb = count * ((pl.n + lkb - 1) / lkb);
+        if (lb > int64_t(sms) * per) lb = int64_t(sms) * per;
+        lk<<<unsigned(lb), 256, lsm, st>>>(P);
+      }
     }
     STARM_LAUNCH_CHECK();
     SvdParams Pv = P;

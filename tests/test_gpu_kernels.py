@@ -167,18 +167,25 @@ def test_truncated_match_leading_triplets_bitwise():
             assert np.array_equal(f.g_block(i), g)
 
 
-def test_truncated_bitwise_across_orth_blocks():
+@pytest.mark.parametrize("dims,ranks", [((150, 170, 4), (0, 75, 150, 97)),
+                                         ((420, 440, 3), (420, 33, 200))])
+def test_truncated_bitwise_across_orth_blocks(dims, ranks):
     # r = 150: several 16-vector orthonormalisation blocks, earlier vectors
-    # projected in more than one 64-column chunk, partial last blocks
-    dims = (150, 170, 4)
+    # projected in more than one 64-column chunk, partial last blocks;
+    # r = 420: also the DMMA LQ back-transformation (n > 400, 32-vector blocks)
     a = random_array(dims, 23)
     t = sb.DenseTensor(a)
     full = sb.svd_all_slices(t)
-    ranks = np.array([0, 75, 150, 97])
+    r = min(dims[0], dims[1])
+    ranks = np.array(ranks)
     f = sb.svd_truncated_slices(t, ranks)
     for i, k in enumerate(ranks):
         u = full.u.frontal_slice(i)
-        assert np.linalg.norm(u.T @ u - np.eye(150)) <= 1e-10 * math.sqrt(150)
+        v = full.v.frontal_slice(i)
+        assert np.linalg.norm(u.T @ u - np.eye(r)) <= 1e-10 * math.sqrt(r)
+        assert np.linalg.norm(v.T @ v - np.eye(r)) <= 1e-10 * math.sqrt(r)
+        sl = t.frontal_slice(i)
+        assert np.linalg.norm(full.reconstruct_slice(i) - sl) <= 1e-12 * np.linalg.norm(sl)
         assert np.array_equal(f.u_block(i), u[:, :k])
         g = full.s[:k, i, None] * full.v.frontal_slice(i)[:, :k].T
         assert np.array_equal(f.g_block(i), g)
