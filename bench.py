@@ -487,7 +487,8 @@ def run_ours(args):
                                          "kernels": "reduce + bulge chase + bisection/Laguerre"},
                          "dct": {"bound": "hbm", "ms": t_ttm * 1e3, "unit": "GB/s",
                                  "achieved": dct_bytes / t_ttm / 1e9, "peak": hbm_peak,
-                                 "frac": dct_bytes / t_ttm / 1e9 / hbm_peak}},
+                                 "frac": dct_bytes / t_ttm / 1e9 / hbm_peak,
+                                 "traffic": profiled_traffic("dct1024_kernel")}},
             "stages_ms": stages,
             "step_ms": step_ms, "alloc_retries": alloc_retries,
             "clocks": clk.summary(),
