@@ -54,16 +54,26 @@ elif name == "c4":
     del a32
     eps4 = 1e-3
 
+    from paper_2605_16058_b200.compress import _summary, threshold_device
+    from paper_2605_16058_b200.slice_svd import svd_truncated_device, svd_values_device
+
     def run(x):
+        # tsvdm_tolerance's memory-efficient schedule (values pass keeping each
+        # slice's factorisation state -> device threshold -> truncated pass from
+        # the state) with the raw M, which a TransformSet would reject
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         ahat = sb.ttm(x, 2, mm)
         ev[1].record()
-        s = sb.svd_values_only(ahat)
+        s, state = svd_values_device(ahat, keep_state=True)
         ev[2].record()
-        thr = sb.compute_threshold(s, eps4)
+        m_, p_, n_ = ahat.dims
+        ranks, scal, j, _, _ = threshold_device(s, min(m_, p_), n_, eps4)
+        tau, disc, tot, total_rank = _summary(ranks, scal)
+        thr = sb.ThresholdResult(None, None, int(j.item()), tau, ranks, disc, tot)
         ev[3].record()
-        f = sb.svd_truncated_slices(ahat, thr.ranks)
+        f, _ = svd_truncated_device(ahat, ranks, total_rank, state=state)
+        del state
         ev[4].record()
         ev[4].synchronize()
         print("    stages ms: " + ", ".join(f"{k} {ev[i].elapsed_time(ev[i + 1]):.1f}" for i, k in
