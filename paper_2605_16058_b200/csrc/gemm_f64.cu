@@ -8,7 +8,7 @@
 // starm_product (tsvdm.py:205-216).
 //
 // Tiling: CTA tile 128 x 64 x 16, 8 warps (4 along M x 2 along N), warp
-// tile 32 x 32 = 4 x 4 DMMA.8x8x4 accumulators (64 FP64 registers).  A 3-stage
+// tile 32 x 32 = 4 x 4 DMMA.8x8x4 accumulators (64 FP64 registers).  A 4-stage
 // cp.async ring stages A[k][m] (m contiguous, +4 pad) and B[n][k] (k
 // contiguous, +4 pad) tiles; the pads make every fragment load
 // bank-conflict free (half-warp lanes (g,t) hit banks 8t+2g / 8g+2t).
@@ -19,7 +19,15 @@
 namespace starm {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
+// c3-shaped transform (scripts/run_gemm.py): BK 16 x 4 stages 32.3 TFLOP/s
+// (2 CTAs / SM), 16 x 3 30.0, 32 x 2 32.0, 32 x 3 25.5 (1 CTA / SM)
+#ifndef GEMM_BK
+#define GEMM_BK 16
+#endif
+#ifndef GEMM_STAGES
+#define GEMM_STAGES 4
+#endif
+constexpr int BM = 128, BN = 64, BK = GEMM_BK, STAGES = GEMM_STAGES, THREADS = 256;
 constexpr int APAD = BM + 4;  // doubles per k-row of the A tile
 constexpr int BPAD = BK + 4;  // doubles per n-column of the B tile
 constexpr int A_TILE = BK * APAD;
