@@ -14,7 +14,7 @@
 //   their bit patterns) -> sequential running sums + lower_bound -> masks for
 //   both candidate rules in C order -> exclusive scans -> order-preserving
 //   compaction -> numpy-pairwise sums of both candidates (one CTA, the
-//   pairwise tree cut at depth 8 into 256 per-thread subtrees and recombined
+//   pairwise tree cut at depth 10 into 1024 per-thread subtrees and recombined
 //   in the same shape) -> tie rule -> per-slice ranks.
 // All products use __dmul_rn so no FMA contraction changes a rounding.
 #include <cub/cub.cuh>
@@ -24,8 +24,11 @@
 namespace starm {
 namespace {
 
-constexpr int PW_THREADS = 256;
-constexpr int PW_DEPTH = 8;  // 2^8 == PW_THREADS
+#ifndef PW_LOG
+#define PW_LOG 10
+#endif
+constexpr int PW_DEPTH = PW_LOG;  // 2^PW_DEPTH == PW_THREADS
+constexpr int PW_THREADS = 1 << PW_DEPTH;
 
 struct ThState {
   double budget;
@@ -264,15 +267,6 @@ __device__ __forceinline__ int64_t pw_split(int64_t n) {
   return n2 - n2 % 8;
 }
 
-// Recombine per-thread subtree sums in the same tree shape.
-__device__ double pw_combine(const double* part, int64_t n, int depth, int path) {
-  if (depth == PW_DEPTH) return part[path];
-  if (n <= 128) return part[path << (PW_DEPTH - depth)];
-  const int64_t n2 = pw_split(n);
-  return __dadd_rn(pw_combine(part, n2, depth + 1, path * 2),
-                   pw_combine(part, n - n2, depth + 1, path * 2 + 1));
-}
-
 __device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
   const int t = threadIdx.x;
   int64_t lo = 0, len = n;
@@ -295,8 +289,31 @@ __device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
   }
   part[t] = owner ? pw_sum(a + lo, len) : 0.0;
   __syncthreads();
-  double res = 0.0;
-  if (t == 0) res = (n == 0) ? 0.0 : __dadd_rn(0.0, pw_combine(part, n, 0, 0));
+  // Recombine bottom-up, one tree level per step, in the tree's own order:
+  // node (d, p) lives at part[p << (D - d)] (its left child's slot), so
+  // every internal node adds its two children in place.  Nodes that were
+  // leaves above the cut (n <= 128) already hold their sum; nodes below such
+  // a leaf do not exist.
+  for (int d = PW_DEPTH - 1; d >= 0; --d) {
+    if (t < (1 << d)) {
+      int64_t l = n;
+      bool exists = true;
+      for (int q = 0; q < d; ++q) {  // replay the splits from the root
+        if (l <= 128) {
+          exists = false;
+          break;
+        }
+        const int64_t n2 = pw_split(l);
+        l = ((t >> (d - 1 - q)) & 1) ? l - n2 : n2;
+      }
+      if (exists && l > 128) {
+        const int i = t << (PW_DEPTH - d);
+        part[i] = __dadd_rn(part[i], part[i + (1 << (PW_DEPTH - d - 1))]);
+      }
+    }
+    __syncthreads();
+  }
+  const double res = (n == 0) ? 0.0 : __dadd_rn(0.0, part[0]);
   __syncthreads();
   return res;
 }
