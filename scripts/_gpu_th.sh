@@ -1,7 +1,3 @@
-for L in 10 8; do
-rm -f build/threshold.o paper_2605_16058_b200/libstarm.so; make -j8 NVEXTRA="-DPW_LOG=$L" > /dev/null 2>&1
-echo "PW_LOG=$L"
 timeout 900 python -m pytest tests -m gpu -x -q -k "threshold or tolerance or tie" 2>&1 | tail -1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/run_step.py > /dev/null 2>&1
 python scripts/launch_summary.py gpurun_out/launches.csv > gpurun_out/ls.txt; grep "pairwise\|cumsum" gpurun_out/ls.txt
-done
