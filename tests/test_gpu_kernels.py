@@ -342,6 +342,30 @@ def test_tolerance_matches_oracle(dims):
             assert rel_error(recs[sb.TRUNCATE].array, recs[strategy].array) <= 1e-10
 
 
+def test_dway_mixed_transforms_tolerance():
+    # a 5-way tensor (the paper's datasets are 5-6-way) with
+    # one transform kind per mode -- DCT (FFT path, n = 64), a custom Haar
+    # matrix (DMMA GEMM path, middle mode: batch > 1) and the identity --
+    # against the oracle: ranks bit-exact, energies, realised error.
+    dims = (48, 40, 64, 6, 3)
+    rng = np.random.default_rng(41)
+    base = rng.standard_normal((48, 40, 4)) @ rng.standard_normal((4, 64 * 6 * 3))
+    a = np.asfortranarray(base.reshape(dims, order="F") + 1e-2 * rng.standard_normal(dims))
+    q, r = np.linalg.qr(rng.standard_normal((6, 6)))
+    haar = sb.Transform(np.asfortranarray(q * np.sign(np.diag(r))), sb.CUSTOM)
+    ts = sb.TransformSet.build(dims, [sb.DCT, haar, sb.IDENTITY])
+    mats = [tr.matrix for tr in ts]
+    t = sb.DenseTensor(a)
+    for eps in (0.3, 0.02):
+        ref = oracle.tsvdm_tolerance(a, mats, eps)
+        c = sb.tsvdm_tolerance(t, ts, eps)
+        assert np.array_equal(c.ranks, ref["ranks"])
+        assert abs(c.discarded_energy - ref["discarded_energy"]) <= 1e-10 * ref["total_energy"]
+        rec = sb.reconstruct(c)
+        err = rel_error(a, rec.array)
+        assert err < eps and abs(c.relative_error() - err) <= 1e-8
+
+
 def test_tolerance_zero_tensor():
     t = sb.DenseTensor.zeros((4, 4, 3))
     ts = sb.TransformSet.build(t.dims, "identity")
