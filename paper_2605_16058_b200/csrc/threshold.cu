@@ -92,8 +92,7 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
             wl[k] = acc;
           }
         }
-        // two register banks of 8: loads of one bank overlap the other's
-        // dependent adds; running sums leave as 16-byte pairs
+        // running sums leave as 16-byte pairs
         auto chain8 = [&](const double (&c)[8], int k0) {
           double w8[8];
 #pragma unroll
@@ -105,35 +104,34 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
           for (int q = 0; q < 8; q += 2)
             *reinterpret_cast<double2*>(wl + k0 + q) = make_double2(w8[q], w8[q + 1]);
         };
-        double ra[8], rb[8];
-        if (k + 8 <= len) {
+        // three banks: each bank's loads are issued two banks (16 dependent
+        // adds, ~128 cycles) before its adds, covering the ~60-cycle
+        // shared-memory latency that a one-bank lead only just covered
+        auto load8 = [&](double (&c)[8], int k0) {
 #pragma unroll
           for (int q = 0; q < 8; q += 2) {
-            const double2 v2 = *reinterpret_cast<const double2*>(tl + k + q);
-            ra[q] = v2.x;
-            ra[q + 1] = v2.y;
+            const double2 v2 = *reinterpret_cast<const double2*>(tl + k0 + q);
+            c[q] = v2.x;
+            c[q + 1] = v2.y;
           }
-        }
-        for (; k + 16 <= len; k += 16) {
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const double2 v2 = *reinterpret_cast<const double2*>(tl + k + 8 + q);
-            rb[q] = v2.x;
-            rb[q + 1] = v2.y;
-          }
+        };
+        double ra[8], rb[8], rc[8];
+        if (k + 8 <= len) load8(ra, k);
+        if (k + 16 <= len) load8(rb, k + 8);
+        for (; k + 24 <= len; k += 24) {
+          load8(rc, k + 16);
           chain8(ra, k);
-          if (k + 24 <= len) {
-#pragma unroll
-            for (int q = 0; q < 8; q += 2) {
-              const double2 v2 = *reinterpret_cast<const double2*>(tl + k + 16 + q);
-              ra[q] = v2.x;
-              ra[q + 1] = v2.y;
-            }
-          }
+          if (k + 32 <= len) load8(ra, k + 24);
           chain8(rb, k + 8);
+          if (k + 40 <= len) load8(rb, k + 32);
+          chain8(rc, k + 16);
         }
         if (k + 8 <= len) {
           chain8(ra, k);
+          k += 8;
+        }
+        if (k + 8 <= len) {
+          chain8(rb, k);
           k += 8;
         }
         for (; k < len; ++k) {
