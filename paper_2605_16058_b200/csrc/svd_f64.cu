@@ -2331,10 +2331,17 @@ __device__ void ii_factor(const double* bd, const double* be, int64_t N2, double
   auto b_at = [&](int64_t i) { return i < N2 - 1 ? ((i & 1) ? be[i >> 1] : bd[i >> 1]) : 0.0; };
   double cdd = -lam;                    // dd[i] as modified so far
   double cdu = b_at(0);                 // du[i] as modified so far
+  // original b_i .. b_{i+IB} of the current block; the next block's are
+  // loaded one block ahead (software pipelining of the read-only inputs)
+  double nb[IB + 1];
+#pragma unroll
+  for (int u = 0; u <= IB; ++u) nb[u] = b_at(u);
   for (int64_t i0 = 0; i0 + 1 < N2; i0 += IB) {
     double bb[IB + 1];
 #pragma unroll
-    for (int u = 0; u <= IB; ++u) bb[u] = b_at(i0 + u);  // original b_i .. b_{i+IB}
+    for (int u = 0; u <= IB; ++u) bb[u] = nb[u];
+#pragma unroll
+    for (int u = 0; u <= IB; ++u) nb[u] = b_at(i0 + IB + u);
     double o_rdd[IB], o_du[IB], o_du2[IB], o_dl[IB], o_z[IB];
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
@@ -2384,16 +2391,29 @@ __device__ void ii_solve(int64_t N2, Strided rdd, Strided du, Strided du2, Strid
                          Strided x) {
   // forward: apply L and the row interchanges; x[i] carried in a register
   double xi = x[0];
+  // block operands loaded one block ahead (the next block never reads an x
+  // this block stores: it reads x[i0 + IB + 1 ..], this one stores x[i0 .. i0 + IB - 1])
+  double ndl[IB], nz[IB], nx[IB];
+  auto fwd_load = [&](int64_t b0) {
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = b0 + u;
+      const bool in = i + 1 < N2;
+      ndl[u] = in ? dl[i] : 0.0;
+      nz[u] = in ? z[i] : 0.0;
+      nx[u] = in ? x[i + 1] : 0.0;
+    }
+  };
+  fwd_load(0);
   for (int64_t i0 = 0; i0 + 1 < N2; i0 += IB) {
     double dlv[IB], zv[IB], xv[IB];
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
-      const int64_t i = i0 + u;
-      const bool in = i + 1 < N2;
-      dlv[u] = in ? dl[i] : 0.0;
-      zv[u] = in ? z[i] : 0.0;
-      xv[u] = in ? x[i + 1] : 0.0;
+      dlv[u] = ndl[u];
+      zv[u] = nz[u];
+      xv[u] = nx[u];
     }
+    fwd_load(i0 + IB);
     double xo[IB];
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
@@ -2416,17 +2436,29 @@ __device__ void ii_solve(int64_t N2, Strided rdd, Strided du, Strided du2, Strid
   if (N2 < 2) return;
   double x0 = (x[N2 - 2] - du[N2 - 2] * x1) * rdd[N2 - 2];
   x[N2 - 2] = x0;
+  double nxv[IB], nduv[IB], ndu2v[IB], nrv[IB];  // next block, loaded one block ahead
+  auto bwd_load = [&](int64_t b1) {
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      const int64_t i = b1 - u;
+      const bool in = i >= 0;
+      nxv[u] = in ? x[i] : 0.0;
+      nduv[u] = in ? du[i] : 0.0;
+      ndu2v[u] = in ? du2[i] : 0.0;
+      nrv[u] = in ? rdd[i] : 0.0;
+    }
+  };
+  bwd_load(N2 - 3);
   for (int64_t i1 = N2 - 3; i1 >= 0; i1 -= IB) {  // block i1, i1 - 1, ..., i1 - IB + 1
     double xv[IB], duv[IB], du2v[IB], rv[IB];
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
-      const int64_t i = i1 - u;
-      const bool in = i >= 0;
-      xv[u] = in ? x[i] : 0.0;
-      duv[u] = in ? du[i] : 0.0;
-      du2v[u] = in ? du2[i] : 0.0;
-      rv[u] = in ? rdd[i] : 0.0;
+      xv[u] = nxv[u];
+      duv[u] = nduv[u];
+      du2v[u] = ndu2v[u];
+      rv[u] = nrv[u];
     }
+    bwd_load(i1 - IB);
     double xo[IB];
 #pragma unroll
     for (int u = 0; u < IB; ++u) {
