@@ -480,14 +480,20 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
   int bad = 0, nonzero = 0;
   if (!P.transposed) {
     const int64_t total = LP * NP;
-    for (int64_t e0 = 0; e0 < total; e0 += int64_t(NT) * LB) {
-      double v[LB];
+    double v[LB], w[LB];  // batch in hand, next batch in flight
+    auto load_batch = [&](double (&d)[LB], int64_t e0) {
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
         const int64_t e = e0 + tid + int64_t(u) * NT;
         const int64_t r = e % LP, c = e / LP;
-        v[u] = (e < total && r < L && c < n) ? A[(row0 + r) + c * P.m] : 0.0;
+        d[u] = (e < total && r < L && c < n) ? A[(row0 + r) + c * P.m] : 0.0;
       }
+    };
+    load_batch(w, 0);
+    for (int64_t e0 = 0; e0 < total; e0 += int64_t(NT) * LB) {
+#pragma unroll
+      for (int u = 0; u < LB; ++u) v[u] = w[u];
+      load_batch(w, e0 + int64_t(NT) * LB);
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
         const int64_t e = e0 + tid + int64_t(u) * NT;
@@ -497,35 +503,42 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
       }
     }
   } else {
-    // 32 (columns of X) x 128 (rows of X) tiles through shared memory
+    // 32 (columns of X) x 128 (rows of X) tiles through shared memory; the
+    // next tile's loads are issued as soon as this tile is in shared memory,
+    // so they fly while this tile is copied out
     constexpr int LT = 4096 / NT;
-    for (int64_t c0 = 0; c0 < NP; c0 += 32) {
-      for (int64_t r0 = 0; r0 < LP; r0 += 128) {
-        double v[LT];
+    const int64_t nrt = (LP + 127) / 128, ntiles = ((NP + 31) / 32) * nrt;
+    double v[LT];
+    auto load_tile = [&](int64_t t) {
+      const int64_t c0 = (t / nrt) * 32, r0 = (t % nrt) * 128;
 #pragma unroll
-        for (int u = 0; u < LT; ++u) {
-          const int e = tid + u * NT;
-          const int cc = e & 31, rr = e >> 5;
-          const int64_t c = c0 + cc, r = r0 + rr;
-          v[u] = (r < L && c < n) ? A[c + (row0 + r) * P.m] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < LT; ++u) {
-          const int e = tid + u * NT;
-          bad |= !isfinite(v[u]);
-          nonzero |= (v[u] != 0.0);
-          tile[(e >> 5) * 33 + (e & 31)] = v[u];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < LT; ++u) {
-          const int e = tid + u * NT;
-          const int rr = e & 127, cc = e >> 7;
-          const int64_t c = c0 + cc, r = r0 + rr;
-          if (c < NP && r < LP) X[r + c * LP] = tile[rr * 33 + cc];
-        }
-        __syncthreads();
+      for (int u = 0; u < LT; ++u) {
+        const int e = tid + u * NT;
+        const int cc = e & 31, rr = e >> 5;
+        const int64_t c = c0 + cc, r = r0 + rr;
+        v[u] = (t < ntiles && r < L && c < n) ? A[c + (row0 + r) * P.m] : 0.0;
       }
+    };
+    load_tile(0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+      const int64_t c0 = (t / nrt) * 32, r0 = (t % nrt) * 128;
+#pragma unroll
+      for (int u = 0; u < LT; ++u) {
+        const int e = tid + u * NT;
+        bad |= !isfinite(v[u]);
+        nonzero |= (v[u] != 0.0);
+        tile[(e >> 5) * 33 + (e & 31)] = v[u];
+      }
+      __syncthreads();
+      load_tile(t + 1);
+#pragma unroll
+      for (int u = 0; u < LT; ++u) {
+        const int e = tid + u * NT;
+        const int rr = e & 127, cc = e >> 7;
+        const int64_t c = c0 + cc, r = r0 + rr;
+        if (c < NP && r < LP) X[r + c * LP] = tile[rr * 33 + cc];
+      }
+      __syncthreads();
     }
   }
   bad = __syncthreads_or(bad);
