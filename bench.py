@@ -387,6 +387,17 @@ def run_ours(args):
     del rec
     if not (realised < EPS and abs(realised - err) <= 1e-8):
         raise SystemExit(f"bench: invalid result: realised error {realised} vs recorded {err}")
+    # reconstruction + relative error, timed separately: facewise
+    # U_i G_i (DMMA), inverse DCT, error sums; device-resident factors
+    er0, er1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    er0.record()
+    for _ in range(3):
+        rec = sb.reconstruct(c)
+        sb.relative_error_device(x, rec)
+        del rec
+    er1.record()
+    er1.synchronize()
+    t_rec = er0.elapsed_time(er1) / 3
 
     # ---- stage split + dominant kernel (values SVD) on one extra step
     clock = sb.StageClock()
@@ -490,6 +501,8 @@ def run_ours(args):
                                  "frac": dct_bytes / t_ttm / 1e9 / hbm_peak,
                                  "traffic": profiled_traffic("dct1024_kernel")}},
             "stages_ms": stages,
+            "reconstruct": {"ms": t_rec, "unit": "GB/s", "value": in_bytes / t_rec / 1e6,
+                            "what": "reconstruct + relative error of the timed result (outside the timed region)"},
             "step_ms": step_ms, "alloc_retries": alloc_retries,
             "clocks": clk.summary(),
             "gpu_launches": launches,

@@ -62,16 +62,19 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const int64_t* ranks, int
 }
 
 // ------------------------------------------------- facewise U_i G_i tiles
-// chat_i (m x p) = U_i (m x k) * G_i (k x p), k = ranks[i] (0 -> zeros).
-constexpr int RT = 64, KC = 16;
+// chat_i (m x p) = U_i (m x k) * G_i (k x p), k = ranks[i] (0 -> zeros), on
+// DMMA: 64 x 64 output tile per CTA, 8 warps of 32 x 16 (4 x 2 m8n8k4
+// accumulators), K in chunks of 16 staged in shared memory with row stride
+// 72 (= 8 mod 32: the (g, t) fragment lanes hit distinct banks).
+constexpr int RT = 64, KC = 16, US = RT + 8;
 
 __global__ void __launch_bounds__(256) unpack_kernel(const double* u_data, const double* g_data,
                                                      const int64_t* ranks, const int64_t* u_off,
                                                      const int64_t* g_off, int64_t m, int64_t p,
                                                      int64_t tiles_m, int64_t tiles_p,
                                                      double* chat) {
-  __shared__ double us[KC][RT];
-  __shared__ double gs[KC][RT + 1];
+  __shared__ double us[KC][US];  // us[k][row]
+  __shared__ double gs[KC][US];  // gs[k][col]
   const int64_t per_slice = tiles_m * tiles_p;
   const int64_t slice = blockIdx.x / per_slice;
   const int64_t tile = blockIdx.x % per_slice;
@@ -80,45 +83,47 @@ __global__ void __launch_bounds__(256) unpack_kernel(const double* u_data, const
   const double* U = u_data + u_off[slice];
   const double* G = g_data + g_off[slice];
   double* C = chat + slice * m * p;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;  // rows 32 wm .., cols 16 wn ..
+  double acc[4][2][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int64_t k0 = 0; k0 < k; k0 += KC) {
     for (int e = threadIdx.x; e < KC * RT; e += 256) {
-      const int kk = e / RT, rr = e % RT;
+      const int kk = e / RT, rr = e % RT;  // U: consecutive threads, consecutive rows
       const int64_t row = m0 + rr, kx = k0 + kk;
       us[kk][rr] = (row < m && kx < k) ? U[row + kx * m] : 0.0;
-      const int cc = e / KC, k2 = e % KC;
+      const int cc = e / KC, k2 = e % KC;  // G: consecutive threads, consecutive k
       const int64_t col = p0 + cc, ky = k0 + k2;
       gs[k2][cc] = (col < p && ky < k) ? G[ky + col * k] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-      double a[4], b[4];
+    for (int k4 = 0; k4 < KC; k4 += 4) {
+      double af[4], bf[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = us[kk][tx * 4 + q];
-        b[q] = gs[kk][ty * 4 + q];
-      }
+      for (int i = 0; i < 4; ++i) af[i] = us[k4 + tq][32 * wm + 8 * i + gq];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int j = 0; j < 2; ++j) bf[j] = gs[k4 + tq][16 * wn + 8 * j + gq];
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884n(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    const int64_t col = p0 + ty * 4 + y;
-    if (col >= p) continue;
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + 32 * wm + 8 * i + gq;
+    if (row >= m) continue;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int64_t row = m0 + tx * 4 + x;
-      if (row < m) C[row + col * m] = acc[x][y];
+    for (int j = 0; j < 2; ++j) {
+      const int64_t col = p0 + 16 * wn + 8 * j + 2 * tq;
+      if (col < p) C[row + col * m] = acc[i][j][0];
+      if (col + 1 < p) C[row + (col + 1) * m] = acc[i][j][1];
     }
   }
 }
