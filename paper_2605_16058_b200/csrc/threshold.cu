@@ -13,9 +13,10 @@
 //   square_keys -> radix sort (64-bit keys: non-negative doubles order like
 //   their bit patterns) -> sequential running sums + lower_bound -> masks for
 //   both candidate rules in C order -> exclusive scans -> order-preserving
-//   compaction -> numpy-pairwise sums of both candidates (one CTA, the
-//   pairwise tree cut at depth 10 into 1024 per-thread subtrees and recombined
-//   in the same shape) -> tie rule -> per-slice ranks.
+//   compaction -> numpy-pairwise sums of both candidates (the pairwise tree
+//   cut at depth 10 into 1024 subtrees per candidate, summed by 64 CTAs of
+//   32 threads, then recombined level by level in the same shape by one CTA)
+//   -> tie rule -> per-slice ranks.
 // All products use __dmul_rn so no FMA contraction changes a rounding.
 #include <cub/cub.cuh>
 
@@ -265,17 +266,14 @@ __device__ __forceinline__ int64_t pw_split(int64_t n) {
   return n2 - n2 % 8;
 }
 
-__device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
-  const int t = threadIdx.x;
+// Subtree t of the pairwise tree cut at depth PW_DEPTH (0 when t is not the
+// owner of a leaf that ends above the cut).
+__device__ double pw_leaf(const double* a, int64_t n, int t) {
   int64_t lo = 0, len = n;
-  bool owner = true;
-  int depth = 0;
-  for (; depth < PW_DEPTH; ++depth) {
+  for (int depth = 0; depth < PW_DEPTH; ++depth) {
     if (len <= 128) {
       // Leaf above the cut: only the all-zero-suffix descendant computes it.
-      const int rest = t & ((1 << (PW_DEPTH - depth)) - 1);
-      owner = (rest == 0);
-      break;
+      return (t & ((1 << (PW_DEPTH - depth)) - 1)) == 0 ? pw_sum(a + lo, len) : 0.0;
     }
     const int64_t n2 = pw_split(len);
     if ((t >> (PW_DEPTH - 1 - depth)) & 1) {
@@ -285,13 +283,16 @@ __device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
       len = n2;
     }
   }
-  part[t] = owner ? pw_sum(a + lo, len) : 0.0;
-  __syncthreads();
-  // Recombine bottom-up, one tree level per step, in the tree's own order:
-  // node (d, p) lives at part[p << (D - d)] (its left child's slot), so
-  // every internal node adds its two children in place.  Nodes that were
-  // leaves above the cut (n <= 128) already hold their sum; nodes below such
-  // a leaf do not exist.
+  return pw_sum(a + lo, len);
+}
+
+// Recombine the PW_THREADS subtree sums in part[] bottom-up, one tree level
+// per step, in the tree's own order: node (d, p) lives at part[p << (D - d)]
+// (its left child's slot), so every internal node adds its two children in
+// place.  Nodes that were leaves above the cut (n <= 128) already hold their
+// sum; nodes below such a leaf do not exist.  One CTA of PW_THREADS threads.
+__device__ double pw_combine_levels(int64_t n, double* part) {
+  const int t = threadIdx.x;
   for (int d = PW_DEPTH - 1; d >= 0; --d) {
     if (t < (1 << d)) {
       int64_t l = n;
@@ -316,16 +317,36 @@ __device__ double pw_sum_parallel(const double* a, int64_t n, double* part) {
   return res;
 }
 
+// The 2 x PW_THREADS subtree sums (both candidate masks), 32 per CTA so the
+// strided per-thread reads spread over many SMs' L1s.
+constexpr int PW_LEAF_CTA = 32;
+__global__ void __launch_bounds__(PW_LEAF_CTA) pairwise_leaves_kernel(const int* fa, const int* fb,
+                                                                      const int* pa, const int* pb,
+                                                                      const double* da,
+                                                                      const double* db, int64_t count,
+                                                                      const ThState* st, double* parts) {
+  if (st->mode < 0) return;
+  const int g = blockIdx.x * PW_LEAF_CTA + threadIdx.x;  // [0, 2 PW_THREADS)
+  const int which = g / PW_THREADS, t = g % PW_THREADS;
+  const int64_t na = count ? int64_t(pa[count - 1]) + fa[count - 1] : 0;
+  const int64_t nb = count ? int64_t(pb[count - 1]) + fb[count - 1] : 0;
+  parts[g] = which ? pw_leaf(db, nb, t) : pw_leaf(da, na, t);
+}
+
 __global__ void __launch_bounds__(PW_THREADS) pairwise_kernel(const int* fa, const int* fb,
                                                                const int* pa, const int* pb,
-                                                               const double* da, const double* db,
-                                                               int64_t count, ThState* st) {
+                                                               int64_t count, const double* parts,
+                                                               ThState* st) {
   __shared__ double part[PW_THREADS];
   if (st->mode < 0) return;
   const int64_t na = count ? int64_t(pa[count - 1]) + fa[count - 1] : 0;
   const int64_t nb = count ? int64_t(pb[count - 1]) + fb[count - 1] : 0;
-  const double sa = pw_sum_parallel(da, na, part);
-  const double sb = pw_sum_parallel(db, nb, part);
+  part[threadIdx.x] = parts[threadIdx.x];
+  __syncthreads();
+  const double sa = pw_combine_levels(na, part);
+  part[threadIdx.x] = parts[PW_THREADS + threadIdx.x];
+  __syncthreads();
+  const double sb = pw_combine_levels(nb, part);
   if (threadIdx.x == 0) {
     st->disc[0] = sa;
     st->disc[1] = sb;
@@ -367,7 +388,7 @@ __global__ void ranks_kernel(const double* s, int64_t r, int64_t N, const ThStat
 }
 
 struct ThLayout {
-  size_t keys, sorted, w, fa, fb, pa, pb, da, db, state, cub, total;
+  size_t keys, sorted, w, fa, fb, pa, pb, da, db, state, parts, cub, total;
   size_t cub_bytes;
 };
 
@@ -389,6 +410,7 @@ ThLayout layout(int64_t count) {
   L.da = take(count * 8);
   L.db = take(count * 8);
   L.state = take(sizeof(ThState));
+  L.parts = take(2 * PW_THREADS * sizeof(double));  // pairwise subtree sums of both candidates
   size_t sort_bytes = 0, scan_bytes = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
                                  (unsigned long long*)nullptr, int(count));
@@ -458,7 +480,11 @@ extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, 
   STARM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cubtmp, cub_bytes, fb, pb, int(count), st));
   scatter_kernel<<<grid, 256, 0, st>>>(s, r, nslices, fa, fb, pa, pb, da, db);
   STARM_LAUNCH_CHECK();
-  pairwise_kernel<<<1, PW_THREADS, 0, st>>>(fa, fb, pa, pb, da, db, count, stt);
+  double* parts = reinterpret_cast<double*>(base + L.parts);
+  pairwise_leaves_kernel<<<2 * PW_THREADS / PW_LEAF_CTA, PW_LEAF_CTA, 0, st>>>(fa, fb, pa, pb, da, db,
+                                                                              count, stt, parts);
+  STARM_LAUNCH_CHECK();
+  pairwise_kernel<<<1, PW_THREADS, 0, st>>>(fa, fb, pa, pb, count, parts, stt);
   STARM_LAUNCH_CHECK();
   ranks_kernel<<<grid_for(nslices), 256, 0, st>>>(s, r, nslices, stt, ranks_out, scal_out, j_out);
   STARM_LAUNCH_CHECK();
