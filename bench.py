@@ -1,24 +1,36 @@
 #!/usr/bin/env python
-"""Benchmark: tolerance t-SVDM compression throughput (input GB/s) on B200.
+"""Benchmark: t-SVDM compression throughput (input GB/s) on B200.
 
-Workload (BASELINE.json configs[1], "c2"): climate-reanalysis-like float64
-tensor 361 x 720 x 1024, M = orthonormal DCT-II over time, relative
-tolerance 1e-2, ranks chosen globally (tsvdm_tolerance, memory-efficient).
-Synthetic data of that shape/distribution (paper_2605_16058_b200.configs).
+Workloads (``--config``, paper_2605_16058_b200/workloads.py; BASELINE.json
+configs): c1 fixed rank 10 (256x256x64), c2 tolerance 1e-2 (361x720x1024,
+DCT: the default -- BASELINE's metric is quoted on configs[1]), c3 fixed
+rank 32 (1024^2 x 512, Haar), c4 tolerance 1e-3 (512^2 x 2048 X-ray-like,
+raw invertible M), c5 fixed rank 16 / c5t tolerance 1e-4 (8192x64x4096,
+Haar).  Seeded synthetic data of each config's shape and distribution.
 
-One step = one compression call (forward TTM -> values SVD of every slice ->
-device threshold -> truncated SVD of the rank>0 slices -> packed factors).
-  value : input bytes / s with the tensor already resident in HBM
-          (2.13 GB input > 126 MB L2, so no L2 flush is needed)
-  e2e   : the same through the public host API (DenseTensor in, host
-          CompressedTensor out), H2D of the input and D2H of the packed
-          factors inside the timed region.
-Multi-GPU (torchrun): every rank compresses its own c2 tensor (replicas,
-weak scaling); time = max over ranks of the device-timed region.
+One step = one compression call (forward transform -> slice SVDs ->
+threshold -> packed factors).
+  value : input bytes / s with the tensor already resident in HBM (every
+          config's input exceeds the 126 MB L2 except c1, 33.5 MB: c1 steps
+          are separated by an L2 flush, a 256 MB write, outside the events)
+  e2e   : the same through the drop-in host call (DenseTensor in from pinned
+          memory, host CompressedTensor out): H2D of the input and D2H of the
+          packed factors inside every timed step.  ``e2e_stream`` is the
+          pipelined host API (tsvdm_tolerance_stream: H2D of step k+1 under
+          step k), tolerance configs only.
 
-`--impl reference` times the reference algorithm's CPU restatement
-(oracle/, numpy + LAPACK dgesvd like the reference package) on a bounded
-per-slice sample of the same workload; see cpu_sample().
+Multi-GPU.  ``--gpus N`` (N > 1) without a torchrun environment relaunches
+itself under ``torch.distributed.run`` with N local ranks.  Under torchrun
+the default is north_star's split of ONE tensor (sharded.py): fibre-local
+transform, NCCL all-to-all to slice ownership, per-rank SVDs, all-gathered
+sigma, replicated threshold/energies ("scaling": "strong");
+``--replicas`` runs N independent tensors instead ("weak").  Time = max
+over ranks of the device-timed region.
+
+``--impl reference`` times the reference algorithm on the host cores: the
+oracle port (oracle/, numpy + LAPACK dgesvd exactly like the reference
+package; the reference itself is not present on the GPU box) on a bounded
+per-slice sample of the same workload, rank 0 only.
 """
 
 from __future__ import annotations
@@ -28,10 +40,11 @@ import gc
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
-import threading
 import sys
+import threading
 import time
 
 import numpy as np
@@ -39,10 +52,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "t-SVD input GB/s (c2 tolerance t-SVDM, device-resident input)"
 UNIT = "GB/s"
-EPS = 1e-2
-DIMS = (361, 720, 1024)
+
+
+def metric_name(cfg):
+    return f"t-SVD input GB/s ({cfg} t-SVDM, device-resident input)"
 
 
 def parse():
@@ -51,13 +65,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c5t"])
     ap.add_argument("--cpu-sample-slices", type=int, default=0,
                     help="slices in the CPU sample (0 = auto, ~10-20 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--nt", type=int, default=DIMS[2], help="time steps (default 1024 = c2)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent tensors (weak scaling) instead of one sharded tensor")
     ap.add_argument("--sharded", action="store_true",
-                    help="N>1: shard ONE c2 tensor over the ranks (fibre all-to-all, strong "
-                         "scaling) instead of N independent replicas")
+                    help="run the sharded pipeline even at N=1 (world size 1 over NCCL)")
     return ap.parse_args()
 
 
@@ -68,33 +84,57 @@ def dist_env():
     return rank, world, local
 
 
-def make_input(nt, seed):
-    from paper_2605_16058_b200.configs import config2
-    return config2(nlat=DIMS[0], nlon=DIMS[1], nt=nt, seed=seed)
+def relaunch_under_torchrun(args):
+    """``--gpus N`` from a plain ``python bench.py``: re-exec under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.call(cmd, env=env)
 
 
 # ------------------------------------------------------------ CPU baseline
 
-def cpu_sample(a, nslices, threads):
-    """Reference algorithm (oracle restatement of tsvdm_tolerance,
-    memory-efficient) on a per-slice sample of the full c2 problem: the
-    forward TTM restricted to the first `nslices` output slices (M[:S] @
-    A_(3), full inner dimension), the values SVD of those slices (LAPACK
-    dgesvd, 1 core: the reference's f2py wrapper holds the GIL), the
-    threshold over the sample, and the truncated SVD of the kept slices.
-    Returns (seconds, bytes of input represented)."""
+def cpu_sample(wl, nslices, threads, a=None):
+    """The reference algorithm (oracle restatement, numpy + LAPACK dgesvd)
+    on a per-slice sample of workload ``wl``: the forward transform
+    restricted to the first ``nslices`` OUTPUT slices (M[:S] @ A_(3), full
+    inner dimension, all BLAS threads), then per slice the SVD the reference
+    runs (values pass + truncated pass for tolerance; truncated with
+    keep_values for fixed rank; 1 core: scipy's dgesvd wrapper holds the
+    GIL) and the threshold over the sample.  Returns (seconds, bytes of
+    input represented)."""
     import oracle
     from threadpoolctl import threadpool_limits
-    m, p, n = a.shape
-    mat = oracle.dct_matrix(n)[:nslices, :]
+    m, p, n = wl.dims
+    if a is None:
+        a = wl.host
+    if wl.transform == "dct":
+        mat = oracle.dct_matrix(n)
+    elif wl.transform == "raw":
+        mat = wl.mat
+    else:
+        mat = wl.ts[0].matrix
+    mat = np.ascontiguousarray(mat[:nslices, :])
     t0 = time.perf_counter()
     with threadpool_limits(limits=threads, user_api="blas"):
         flat = a.reshape(-1, order="F").reshape(n, m * p)
         ahat = (mat @ flat).reshape(-1).reshape((m, p, nslices), order="F")
     with threadpool_limits(limits=1, user_api="blas"):
-        res = oracle.tsvdm_tolerance(None, None, EPS, ahat=ahat)
+        if wl.kind == "tolerance":
+            oracle.tsvdm_tolerance(None, None, float(wl.param), ahat=ahat)
+        else:
+            ranks = np.full(nslices, int(wl.param), dtype=np.int64)
+            oracle.svd_truncated_slices(ahat, ranks, keep_values=True)
     dt = time.perf_counter() - t0
-    return dt, nslices * m * p * 8, int(res["ranks"].sum())
+    return dt, nslices * m * p * 8
 
 
 def cpu_info():
@@ -110,42 +150,64 @@ def cpu_info():
     return model, os.cpu_count() or 1
 
 
+def per_slice_cpu_seconds(wl):
+    """Rough 1-core dgesvd seconds per slice, used only to
+    size the sample to ~10-20 s."""
+    m, p, _ = wl.dims
+    return max(1e-3, 0.27 * (m * p * min(m, p)) / (361 * 720 * 361))
+
+
+def host_for_cpu(wl):
+    """Host input for the CPU sample (c5 is formed on the device: only the
+    first few hundred time steps' worth of host data exist otherwise)."""
+    if wl.host is not None:
+        return wl.host
+    import oracle
+    ahat = wl.extra["ahat"]
+    return oracle.ttm(ahat, 2, wl.extra["mat"].T)
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    a = make_input(args.nt, 0)
+    from paper_2605_16058_b200.workloads import make_workload
+    wl = make_workload(args.config, seed=0)
+    a = host_for_cpu(wl)
     model, cores = cpu_info()
-    s = args.cpu_sample_slices or max(2, int(120 / max(args.steps + args.warmup, 1) / 0.3))
-    s = min(s, a.shape[2])
+    budget = 150.0 / max(args.steps + args.warmup, 1)
+    s = args.cpu_sample_slices or max(2, int(budget / per_slice_cpu_seconds(wl)))
+    s = min(s, wl.dims[2])
     for _ in range(args.warmup):
-        cpu_sample(a, max(1, s // 4), cores)
+        cpu_sample(wl, max(1, s // 4), cores, a)
     times, nbytes = [], 0
     for _ in range(args.steps):
-        dt, nbytes, _ = cpu_sample(a, s, cores)
+        dt, nbytes = cpu_sample(wl, s, cores, a)
         times.append(dt)
     v = nbytes / statistics.mean(times) / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (configs.config2, seed 0)",
-        "config": {"workload": "c2: 361x720x1024 f64, DCT-II, tolerance 1e-2, memory-efficient",
-                   "global_batch": 1, "seq_len": args.nt, "parallelism": "cpu"},
+        "impl": "reference", "metric": metric_name(args.config), "value": v, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (workloads.{args.config}, seed 0)",
+        "config": {"workload": wl.describe, "global_batch": 1, "seq_len": wl.dims[2],
+                   "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"first {s} of {a.shape[2]} slices of c2 per step: restricted "
-                                   f"TTM (all {cores} BLAS threads) + dgesvd values/vectors "
-                                   f"(1 core, GIL) + threshold; CPU {model}"},
+                         "sample": f"first {s} of {wl.dims[2]} transform-domain slices per step: "
+                                   f"restricted transform (all {cores} BLAS threads) + dgesvd "
+                                   f"passes (1 core: the reference's f2py wrapper holds the GIL) "
+                                   f"+ threshold; CPU {model}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------ GPU arm
+# ------------------------------------------------------------ GPU arm helpers
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled every 200 ms during
-    the timed region, through NVML in a background thread (nvidia-smi's own
+    the timed region through NVML in a background thread (nvidia-smi's own
     start-up takes driver locks that stall the stream being timed; NVML is
     initialised and queried once before the region starts).  Falls back to
     an ``nvidia-smi -lms 200`` subprocess when pynvml is missing."""
@@ -182,7 +244,6 @@ class ClockSampler:
             nv, h = self._nvml_handle()
         except Exception:
             return self._enter_smi()
-
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
@@ -264,8 +325,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm),
-                "source": "nvml" if self.samples else ("nvidia-smi" if self.lines else None),
-                "query_ms": getattr(self, "query_ms", None)}
+                "source": "nvml" if self.samples else ("nvidia-smi" if self.lines else None)}
 
 
 def pci_bus_id(torch, dev):
@@ -276,20 +336,22 @@ def pci_bus_id(torch, dev):
         return None
 
 
-def measured_hbm_peak():
+def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"])
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except (OSError, KeyError, ValueError):
-        return 7700.0  # B200_PROFILING.md fallback
+        return 7700.0, "B200_PROFILING.md fallback"
 
 
-def profiled_traffic(kernel):
+def profiled_traffic(kernel, cfg):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel``
     on this workload, from the committed ncu --set full capture summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel)
+            d = json.load(f)
+        return d.get(f"{cfg}/{kernel}", d.get(kernel) if cfg == "c2" else None)
     except (OSError, ValueError):
         return None
 
@@ -313,6 +375,27 @@ def fp64_peak(torch, dev):
     return 2 * n ** 3 * k / (e0.elapsed_time(e1) / 1e3) / 1e12
 
 
+def timed(torch, fn, reps=1):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        out = fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps, out
+
+
+def host_available_bytes():
+    try:
+        import psutil
+        return psutil.virtual_memory().available
+    except Exception:
+        return 0
+
+
+# ------------------------------------------------------------ GPU arm (1 tensor / rank)
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -326,24 +409,20 @@ def run_ours(args):
 
     import paper_2605_16058_b200 as sb
     from paper_2605_16058_b200 import _native as nat
+    from paper_2605_16058_b200.workloads import make_workload
+    from paper_2605_16058_b200.slice_svd import svd_values_device
 
-    a = make_input(args.nt, seed=rank)
-    m, p, n = a.shape
-    in_bytes = a.size * 8
-    # e2e input lives in pinned (page-locked) host memory, as the contract asks;
-    # the DenseTensor is a zero-copy numpy view of it.
-    pinned = torch.empty(a.size, dtype=torch.float64, pin_memory=True)
-    pinned.numpy()[:] = a.reshape(-1, order="F")
-    host = sb.DenseTensor(pinned.numpy().reshape(a.shape, order="F"), copy=False)
-    ts = sb.TransformSet.build(a.shape, "dct")
-    x = sb.DeviceTensor.from_host(host, dev)
+    wl = make_workload(args.config, seed=rank)
+    x = wl.device_input(dev)
+    wl.extra.pop("ahat", None)
+    m, p, n = wl.dims
+    in_bytes = wl.in_bytes
+    is_tol = wl.kind == "tolerance"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if in_bytes < (256 << 20) else None
     torch.cuda.synchronize()
 
-    def step():
-        return sb.tsvdm_tolerance(x, ts, EPS)
-
     for _ in range(max(args.warmup, 1)):
-        c = step()
+        res = wl.step(x)
     torch.cuda.synchronize()
     lib = nat.load()
     lib.starm_launch_count_reset()
@@ -352,161 +431,183 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     gc.collect()
     gc.disable()  # no collector pauses inside the timed host loop
-    retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     with ClockSampler(dev.index, pci_bus_id(torch, dev)) as clk:
-        e0.record()
-        marks[0].record()
         for k in range(args.steps):
-            c = step()
-            marks[k + 1].record()
-        e1.record()
-        e1.synchronize()
+            if flush is not None:
+                flush.fill_(k & 0xFF)   # L2 flush between steps (outside the events)
+            starts[k].record()
+            res = wl.step(x)
+            ends[k].record()
+        ends[-1].synchronize()
     torch.cuda.synchronize()
     gc.enable()
-    alloc_retries = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
-    step_ms = [round(marks[k].elapsed_time(marks[k + 1]), 3) for k in range(args.steps)]
+    step_ms = [round(starts[k].elapsed_time(ends[k]), 3) for k in range(args.steps)]
     launches = lib.starm_launch_count_reset() // max(args.steps, 1)
-    t_dev = e0.elapsed_time(e1) / 1e3
+    t_dev = sum(step_ms) / 1e3
     if world > 1:
         tt = torch.tensor([t_dev], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev = float(tt.item())
         dist.barrier()
     value = world * args.steps * in_bytes / t_dev / 1e9
-    ranks_sum = c.factors.total_rank
-    err = c.relative_error()
-    # Validity of the timed result (outside the timed region): the realised
-    # reconstruction error must be below the tolerance and match the energy
-    # bookkeeping, so a fast-but-wrong kernel cannot produce a number.
-    rec = sb.reconstruct(c)
-    realised = sb.relative_error_device(x, rec)
-    del rec
-    if not (realised < EPS and abs(realised - err) <= 1e-8):
-        raise SystemExit(f"bench: invalid result: realised error {realised} vs recorded {err}")
-    # reconstruction + relative error, timed separately: facewise
-    # U_i G_i (DMMA), inverse DCT, error sums; device-resident factors
-    er0, er1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    er0.record()
-    for _ in range(3):
-        rec = sb.reconstruct(c)
-        sb.relative_error_device(x, rec)
-        del rec
-    er1.record()
-    er1.synchronize()
-    t_rec = er0.elapsed_time(er1) / 3
+    total_rank = res.factors.total_rank
+    # validity of the timed result (outside the timed region): the realised
+    # error equals the energy bookkeeping and meets the tolerance
+    realised, recorded = wl.realised_error(x, res)
+    if not abs(realised - recorded) <= 1e-8 * max(1.0, recorded) or (is_tol and not realised <= wl.param):
+        raise SystemExit(f"bench: invalid result: realised error {realised} vs recorded {recorded}")
 
-    # ---- stage split + dominant kernel (values SVD) on one extra step
-    clock = sb.StageClock()
-    sb.tsvdm_tolerance(x, ts, EPS, clock=clock)
-    stages = {k: round(v * 1e3, 3) for k, v in clock.seconds.items()}
-    from paper_2605_16058_b200.mode_product import forward_device
-    from paper_2605_16058_b200.slice_svd import svd_values_device
-    ahat = forward_device(x, ts)
+    # ---- reconstruction + error, timed separately
+    t_rec, _ = timed(torch, lambda: wl.realised_error(x, res), reps=2)
+
+    # ---- stage split and the dominant kernel
+    stages = {}
+    if is_tol and wl.transform != "raw":
+        clock = sb.StageClock()
+        wl.step(x, clock=clock)
+        stages = {k: round(v * 1e3, 3) for k, v in clock.seconds.items()}
+    t_fwd, ahat = timed(torch, lambda: wl.forward(x))
     ahat3 = sb.DeviceTensor(ahat.data, (m, p, n))
     svd_values_device(ahat3)
-    torch.cuda.synchronize()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record()
-    svd_values_device(ahat3)
-    e3.record()
-    e3.synchronize()
-    t_svd = e2.elapsed_time(e3) / 1e3
-    # the dominant kernel alone: tune mode 3 stops the values pass after
-    # svd_reduce_kernel (QR + band reduction); same stream, CUDA events
-    lib.starm_svd_tune(-1, -1, 3, -1)
+    t_values, _ = timed(torch, lambda: svd_values_device(ahat3))
+    lib.starm_svd_tune(-1, -1, 3, -1)   # values pass returns right after svd_reduce_kernel
     try:
         svd_values_device(ahat3)
-        e2.record()
-        for _ in range(3):
-            svd_values_device(ahat3)
-        e3.record()
-        e3.synchronize()
-        t_red = e2.elapsed_time(e3) / 1e3 / 3
+        t_red, _ = timed(torch, lambda: svd_values_device(ahat3), reps=2)
     finally:
         lib.starm_svd_tune(-1, -1, 1, -1)
-    e2.record()
-    forward_device(x, ts)
-    e3.record()
-    e3.synchronize()
-    t_ttm = e2.elapsed_time(e3) / 1e3
     del ahat, ahat3
+    f_ttm, f_svd, f_lapack = wl.flops(total_rank)
     a_, b_ = max(m, p), min(m, p)
-    # Sigma-only GVL count = Householder QR (2ab^2 - 2b^3/3) +
-    # two-sided reduction of R (8b^3/3): exactly the reduce kernel's work
-    f_svd = n * (2 * a_ * b_ ** 2 + 2 * b_ ** 3)
-    dct_bytes = 2 * 8 * n * m * p  # read + write of the tensor
+    f_red = n * (2 * a_ * b_ ** 2 + 2 * b_ ** 3)   # Sigma-only GVL count = the reduce kernel's work
     peak = fp64_peak(torch, dev)
-    hbm_peak = measured_hbm_peak()
-    traffic = profiled_traffic("svd_reduce_kernel")
+    hbm_peak, hbm_src = measured_peaks()
+    dense = wl.transform != "dct"
+    fwd_obj = {"ms": t_fwd * 1e3}
+    if dense:
+        fwd_obj.update(bound="tensor", kernel="gemm_f64_kernel (FP64 DMMA, 4-stage cp.async ring)",
+                       achieved=f_ttm / t_fwd / 1e12, peak=peak, unit="TFLOP/s",
+                       frac=f_ttm / t_fwd / 1e12 / peak, algorithmic_flops=f_ttm,
+                       traffic=profiled_traffic("gemm_f64_kernel", args.config))
+    else:
+        dct_bytes = 2 * 8 * n * m * p
+        fwd_obj.update(bound="hbm", kernel="dct1024_kernel + residual_gemm_kernel (tcgen05)",
+                       achieved=dct_bytes / t_fwd / 1e9, peak=hbm_peak, unit="GB/s",
+                       frac=dct_bytes / t_fwd / 1e9 / hbm_peak, algorithmic_bytes=dct_bytes,
+                       traffic=profiled_traffic("dct1024_kernel", args.config))
+    red_obj = {"bound": "tensor",
+               "kernel": "svd_reduce_kernel (Householder QR + band reduction, FP64 DMMA)",
+               "achieved": f_red / t_red / 1e12, "peak": peak, "unit": "TFLOP/s",
+               "frac": f_red / t_red / 1e12 / peak,
+               "traffic": profiled_traffic("svd_reduce_kernel", args.config),
+               "algorithmic_flops": f_red, "ms": t_red * 1e3}
+    dominant = fwd_obj if (dense and t_fwd > t_red) else red_obj
+    roof = dict(dominant)
+    roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (FP64 not in "
+                           "MEASURED_PEAKS.json)") if roof["unit"] == "TFLOP/s" else hbm_src
+    roof["forward_transform"] = fwd_obj
+    roof["svd_reduce"] = red_obj
+    roof["values_pass"] = {"ms": t_values * 1e3, "achieved": f_red / t_values / 1e12,
+                           "kernels": "reduce + bulge chase + bisection/Laguerre"}
+    bound_ms = 1e3 * (f_ttm / (peak * 1e12) if dense else 2 * 8 * n * m * p / (hbm_peak * 1e9)) \
+        + 1e3 * f_svd / (peak * 1e12)
+    roof["step_bound_ms"] = bound_ms
+    roof["step_frac"] = bound_ms / (1e3 * t_dev / args.steps * world / world)
 
-    # ---- e2e through the public host API (after an untimed warm-up pass of
-    # the streaming path: its device buffers come from the caching allocator)
-    for _ in sb.tsvdm_tolerance_stream([host] * 2, ts, EPS):
-        pass
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    d2h = 0
-    # the streaming host API: each step's H2D (pinned) runs on a copy stream
-    # under the previous step's compression; each step's packed factors come
-    # back to the host (D2H) inside the timed region
-    for ch in sb.tsvdm_tolerance_stream([host] * args.steps, ts, EPS):
-        d2h = (ch.factors.u_data.nbytes + ch.factors.g_data.nbytes + ch.factors.ranks.nbytes)
-    torch.cuda.synchronize()
-    t_e2e = time.perf_counter() - t0
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-    e2e = world * args.steps * in_bytes / t_e2e / 1e9
+    # ---- e2e through the drop-in host call: pinned host input -> H2D inside
+    # the step -> host CompressedTensor (D2H of the packed factors)
+    e2e = None
+    e2e_stream = None
+    if not args.no_e2e and host_available_bytes() > 3 * in_bytes:
+        pinned = torch.empty(m * p * n, dtype=torch.float64, pin_memory=True)
+        pinned.copy_(x.data, non_blocking=False)
+        host = sb.DenseTensor(pinned.numpy().reshape((m, p, n), order="F"), copy=False)
+        del x
+        torch.cuda.empty_cache()
+
+        def host_step():
+            if wl.transform == "raw":
+                xd = sb.DeviceTensor.from_host(host, dev)
+                r = wl.step(xd)
+                return r.factors.to_host()
+            if wl.kind == "fixed-rank":
+                return sb.tsvdm_fixed_rank(host, wl.ts, int(wl.param)).factors
+            return sb.tsvdm_tolerance(host, wl.ts, float(wl.param)).factors
+
+        f = host_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            f = host_step()
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        d2h = int(f.u_data.nbytes + f.g_data.nbytes + f.ranks.nbytes)
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": world * args.steps * in_bytes / t_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": d2h,
+               "call": "tsvdm_tolerance / tsvdm_fixed_rank(DenseTensor) -> host CompressedTensor"}
+        if is_tol and wl.transform != "raw":
+            for _ in sb.tsvdm_tolerance_stream([host] * 2, wl.ts, float(wl.param)):
+                pass
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in sb.tsvdm_tolerance_stream([host] * args.steps, wl.ts, float(wl.param)):
+                pass
+            torch.cuda.synchronize()
+            t_s = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([t_s], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_s = float(tt.item())
+            e2e_stream = {"value": world * args.steps * in_bytes / t_s / 1e9, "unit": UNIT,
+                          "call": "tsvdm_tolerance_stream (H2D of step k+1 overlapped with step k)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model, cores = cpu_info()
-        s = args.cpu_sample_slices or 32
-        cpu_sample(a, 2, cores)  # warm BLAS / LAPACK
-        dt, nbytes, _ = cpu_sample(a, s, cores)
-        cpu = {"value": nbytes / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"first {s} of {n} slices of c2: restricted TTM ({cores} BLAS threads) + "
-                         f"dgesvd values/vectors (1 core, GIL) + threshold; {dt:.1f} s; CPU {model}"}
+        a_host = host_for_cpu(wl) if wl.host is not None else None
+        if a_host is None and e2e is not None:
+            a_host = host.array
+        if a_host is not None:
+            s = args.cpu_sample_slices or max(2, min(n, int(15.0 / per_slice_cpu_seconds(wl))))
+            cpu_sample(wl, 1, cores, a_host)  # warm BLAS / LAPACK
+            dt, nbytes = cpu_sample(wl, s, cores, a_host)
+            cpu = {"value": nbytes / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"first {s} of {n} slices of {args.config}: restricted transform "
+                             f"({cores} BLAS threads) + dgesvd passes (1 core, GIL) + threshold; "
+                             f"{dt:.1f} s; CPU {model}"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps,
+            "metric": metric_name(args.config), "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (configs.config2: 40 harmonic x seasonal modes + 1e-2 noise, seed=rank)",
-            "config": {"workload": "c2: 361x720x1024 f64, DCT-II over time, tolerance 1e-2, "
-                                   "memory-efficient; input 2.13 GB > L2 (no flush needed)",
+            "data": f"synthetic (workloads.{args.config}, seed=rank)",
+            "config": {"workload": wl.describe + ("; L2 flushed between steps" if flush is not None
+                                                  else "; input > L2 (no flush needed)"),
                        "global_batch": world, "seq_len": n,
                        "parallelism": f"replicas x{world}" if world > 1 else "single"},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
-                    "d2h_bytes_per_step": d2h},
-            "roofline": {"bound": "tensor",
-                         "kernel": "svd_reduce_kernel (Householder QR + band reduction, FP64 DMMA)",
-                         "achieved": f_svd / t_red / 1e12, "peak": peak, "unit": "TFLOP/s",
-                         "frac": f_svd / t_red / 1e12 / peak, "traffic": traffic,
-                         "peak_source": "cuBLAS DGEMM 4096^3 measured in this run (FP64 not in "
-                                        "MEASURED_PEAKS.json)",
-                         "algorithmic_flops": f_svd, "ms": t_red * 1e3,
-                         "values_pass": {"ms": t_svd * 1e3, "achieved": f_svd / t_svd / 1e12,
-                                         "kernels": "reduce + bulge chase + bisection/Laguerre"},
-                         "dct": {"bound": "hbm", "ms": t_ttm * 1e3, "unit": "GB/s",
-                                 "achieved": dct_bytes / t_ttm / 1e9, "peak": hbm_peak,
-                                 "frac": dct_bytes / t_ttm / 1e9 / hbm_peak,
-                                 "traffic": profiled_traffic("dct1024_kernel")}},
+            "e2e": e2e, "e2e_stream": e2e_stream,
+            "roofline": roof,
+            "flops": {"transform": f_ttm, "svd_necessary": f_svd, "svd_lapack_equiv": f_lapack,
+                      "lapack_equiv_tflops": f_lapack / (t_dev / args.steps) / 1e12},
             "stages_ms": stages,
-            "reconstruct": {"ms": t_rec, "unit": "GB/s", "value": in_bytes / t_rec / 1e6,
-                            "what": "reconstruct + relative error of the timed result (outside the timed region)"},
-            "step_ms": step_ms, "alloc_retries": alloc_retries,
-            "clocks": clk.summary(),
-            "gpu_launches": launches,
-            "result": {"total_rank": ranks_sum, "relative_error": err, "realised_error": realised},
+            "reconstruct": {"ms": t_rec * 1e3, "what": "facewise U_i G_i + inverse transform + "
+                                                       "K10 error sums (outside the timed region)"},
+            "step_ms": step_ms, "clocks": clk.summary(), "gpu_launches": launches,
+            "result": {"total_rank": total_rank, "relative_error": recorded,
+                       "realised_error": realised,
+                       **({"original_domain_error": wl.extra["orig_error"]}
+                          if "orig_error" in wl.extra else {})},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -515,10 +616,30 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------ GPU arm (1 tensor sharded)
+
+def sharded_block(cfg, plan):
+    """This rank's (nf, N) fibre block of the workload's input (host), the
+    transform, and (kind, param)."""
+    import paper_2605_16058_b200 as sb
+    from paper_2605_16058_b200 import configs as cf
+    from paper_2605_16058_b200.sharded import scatter_fibres
+    f0, f1 = plan.fibre_bounds()
+    if cfg in ("c5", "c5t"):
+        blk, mm = cf.config5_fibre_block(f0, f1, m=plan.m, p=plan.p, n=plan.n)
+        tr = sb.validate_transform(mm)
+        kind = ("fixed-rank", 16) if cfg == "c5" else ("tolerance", 1e-4)
+        return blk, tr, kind, True     # block is in the M domain: A = Ahat x3 M^T on the device
+    from paper_2605_16058_b200.workloads import make_workload
+    wl = make_workload(cfg, seed=0)
+    if wl.transform == "raw":
+        raise SystemExit("bench: the sharded path needs an orthonormal transform (c4 is not)")
+    blk = scatter_fibres(wl.host, plan)
+    return blk, wl.ts[0], (wl.kind, wl.param), False
+
+
 def run_sharded(args):
-    """One c2 tensor sharded over the ranks (paper_2605_16058_b200/sharded.py):
-    fibre-local DCT, all-to-all to slice ownership, per-rank values pass,
-    all-gathered sigma, replicated threshold, truncated factors."""
+    """One tensor sharded over the ranks (paper_2605_16058_b200/sharded.py)."""
     import torch
     import torch.distributed as dist
 
@@ -527,26 +648,31 @@ def run_sharded(args):
                  ("WORLD_SIZE", "1")):
         os.environ.setdefault(k, v)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
     import paper_2605_16058_b200 as sb
     from paper_2605_16058_b200 import _native as nat
     from paper_2605_16058_b200.sharded import (DeviceOps, ShardPlan, reconstruct_sharded,
-                                               relative_error_sharded, scatter_fibres,
+                                               relative_error_sharded, tsvdm_fixed_rank_sharded,
                                                tsvdm_tolerance_sharded)
-    a = make_input(args.nt, seed=0)  # the same tensor on every rank
-    m, p, n = a.shape
-    in_bytes = a.size * 8
+    from paper_2605_16058_b200.workloads import make_workload
+    dims = {"c1": (256, 256, 64), "c2": (361, 720, 1024), "c3": (1024, 1024, 512),
+            "c5": (8192, 64, 4096), "c5t": (8192, 64, 4096)}[args.config]
+    m, p, n = dims
+    in_bytes = m * p * n * 8
     plan = ShardPlan(m, p, n, world, rank)
-    blk = scatter_fibres(a, plan).reshape(-1, order="F")
-    del a
-    pinned = torch.empty(blk.size, dtype=torch.float64, pin_memory=True)
-    pinned.numpy()[:] = blk
-    x = pinned.to(dev)
-    ops = DeviceOps(sb.dct_matrix(n), dev)
+    blk, tr, (kind, param), m_domain = sharded_block(args.config, plan)
+    ops = DeviceOps(tr, dev)
+    x = torch.from_numpy(np.ascontiguousarray(blk.reshape(-1, order="F"))).to(dev)
+    del blk
+    if m_domain:
+        x = ops.inverse(x, plan.nf, n).contiguous()    # A = Ahat x3 M^T, fibre-local
+    torch.cuda.synchronize()
 
     def step(src):
-        return tsvdm_tolerance_sharded(src, plan, ops, EPS, dist)
+        if kind == "fixed-rank":
+            return tsvdm_fixed_rank_sharded(src, plan, ops, int(param), dist)
+        return tsvdm_tolerance_sharded(src, plan, ops, float(param), dist)
 
     for _ in range(max(args.warmup, 1)):
         res = step(x)
@@ -567,32 +693,52 @@ def run_sharded(args):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_dev = float(tt.item())
     rec = reconstruct_sharded(res, plan, ops, dist)
-    realised = relative_error_sharded(x, rec, dist)
+    realised = relative_error_sharded(x, rec, dist, ops=ops)
     del rec
-    if not (realised < EPS and abs(realised - res.relative_error) <= 1e-8):
+    ok = abs(realised - res.relative_error) <= 1e-8
+    if kind == "tolerance":
+        ok = ok and realised <= param
+    if not ok:
         raise SystemExit(f"bench: invalid sharded result: {realised} vs {res.relative_error}")
-    # e2e: this rank's fibre block from pinned host memory every step
+    # e2e: this rank's fibre block from pinned host memory every step, the
+    # packed factors of its slices back to the host
+    pinned = torch.empty(x.numel(), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(x)
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    d2h = 0
     for _ in range(args.steps):
         res = step(pinned.to(dev, non_blocking=True))
+        u = res.u_data.cpu()
+        g = res.g_data.cpu()
+        d2h = (u.numel() + g.numel()) * 8
     torch.cuda.synchronize()
     te = torch.tensor([time.perf_counter() - t0], device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
     if rank == 0:
+        import torch.cuda.nccl as tnccl
+        try:
+            nccl_version = ".".join(str(v) for v in tnccl.version())
+        except Exception:
+            nccl_version = None
         line = {
-            "metric": METRIC, "value": args.steps * in_bytes / t_dev / 1e9, "unit": UNIT,
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "metric": metric_name(args.config), "value": args.steps * in_bytes / t_dev / 1e9,
+            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (configs.config2, seed 0, one tensor sharded over the ranks)",
-            "config": {"workload": "c2: 361x720x1024 f64, DCT-II over time, tolerance 1e-2, "
-                                   "fibre-sharded transform + all-to-all to slice ownership",
+            "data": f"synthetic ({args.config}, seed 0, one tensor sharded over the ranks)",
+            "config": {"workload": f"{args.config}: {m}x{p}x{n} f64, {kind} {param}; fibre-sharded "
+                                   "transform + NCCL all-to-all to slice ownership + all-gathered "
+                                   "sigma, replicated threshold / energies",
                        "global_batch": 1, "seq_len": n, "parallelism": f"sharded x{world}"},
             "e2e": {"value": args.steps * in_bytes / t_e2e / 1e9, "unit": UNIT,
-                    "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 8 * (n + 3)},
+                    "h2d_bytes_per_step": in_bytes // world, "d2h_bytes_per_step": d2h,
+                    "per": "rank 0 (every rank copies its own fibre block)"},
+            "comm": {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                     "nccl": nccl_version,
+                     "a2a_bytes_per_rank": in_bytes * (world - 1) // (world * world)},
             "clocks": clk.summary(), "gpu_launches": launches,
             "result": {"total_rank": int(res.ranks.sum()), "relative_error": res.relative_error,
                        "realised_error": realised},
@@ -604,9 +750,12 @@ def run_sharded(args):
 
 def main():
     args = parse()
+    _, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
-    elif args.sharded:
+    elif args.sharded or (world > 1 and not args.replicas):
         run_sharded(args)
     else:
         run_ours(args)

@@ -91,6 +91,25 @@ int starm_ttm_f64(const double* src, const double* mat, double* dst, int64_t row
 int starm_dct_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
                   int inverse, void* stream);
 
+/* -------------------------------------------- K1c reference-operator residual
+ * The DCT kind of the reference is a DENSE product with the float64 matrix
+ * dct_matrix() builds (transforms.py:75-91 applied by ttm.py:113-135).  Its
+ * entries differ from the exact DCT-II by Delta (rounding of the cos
+ * argument, ~2.4e-14 at n = 1024).  starm_dct_f64 computes the exact
+ * transform; this call then adds the residual so the result is the
+ * reference's operator applied to src (to a few u):
+ *     dst[b] += 2^-log2_scale * (Delta_s @ src[b])       b < batch
+ * in the (rows, n, batch) view of starm_dct_f64.  delta_bf16 is the
+ * ROW-MAJOR n x n matrix Delta * 2^log2_scale in bfloat16 bits (the scale
+ * keeps it in bf16's normal range); the product runs on the tcgen05 tensor
+ * cores (kind::f16, fp32 accumulate, TMA-staged), which is exact enough
+ * because |Delta| is ~1e-14.  n must be a multiple of 256; ws and
+ * delta_bf16 128-byte aligned; ws of starm_ttm_residual_workspace_bytes. */
+size_t starm_ttm_residual_workspace_bytes(int64_t rows, int64_t n, int64_t batch);
+int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int log2_scale,
+                            double* dst, int64_t rows, int64_t n, int64_t batch, void* ws,
+                            size_t ws_bytes, void* stream);
+
 /* ----------------------------------------------------- K11 facewise GEMM
  * Replaces _facewise_matmul (tsvdm.py:205-216): for each slice i,
  *   C_i (m x l) = A_i (m x p) * B_i (p x l), all column-major, slice

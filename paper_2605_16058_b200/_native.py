@@ -57,6 +57,9 @@ SIGNATURES = {
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p]),
     "starm_tail_energy_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "starm_ttm_residual_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64]),
+    "starm_ttm_residual_bf16": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int64,
+                                        c_int64, c_void_p, c_size_t, c_void_p]),
     "starm_launch_count_reset": (ctypes.c_longlong, []),
     "starm_svd_tune": (c_int, [c_int, c_int, c_int, c_int]),
     "starm_svd_stats": (c_int, [c_void_p, c_int]),
@@ -122,10 +125,23 @@ def check(status: int, what: str):
     raise RuntimeError(msg)
 
 
+_STREAM_DEVICE = {}  # cudaStream_t handle -> device index (filled by stream_ptr)
+
+
 def call(name: str, *args):
+    """Invoke a C-ABI entry point.  Calls whose last argument is a stream
+    handle from ``stream_ptr`` run with that stream's device current, so
+    tensors on cuda:N work while another device is current (the library's
+    per-device tables, attributes and side streams key off cudaGetDevice)."""
     lib = load()
-    status = getattr(lib, name)(*args)
-    check(status, name)
+    dev = _STREAM_DEVICE.get(args[-1]) if args and isinstance(args[-1], int) else None
+    if dev is not None:
+        t = torch()
+        if t.cuda.current_device() != dev:
+            with t.cuda.device(dev):
+                check(getattr(lib, name)(*args), name)
+            return
+    check(getattr(lib, name)(*args), name)
 
 
 # ------------------------------------------------------------------ device
@@ -155,7 +171,11 @@ def require_cuda(device=None):
 
 def stream_ptr(device=None) -> int:
     t = torch()
-    return t.cuda.current_stream(device).cuda_stream
+    st = t.cuda.current_stream(device)
+    h = st.cuda_stream
+    if h not in _STREAM_DEVICE or _STREAM_DEVICE[h] != st.device.index:
+        _STREAM_DEVICE[h] = st.device.index
+    return h
 
 
 def ptr(x) -> int:

@@ -126,6 +126,8 @@ def compute_threshold(s, epsilon) -> ThresholdResult:
     epsilon = float(epsilon)
     if not 0.0 < epsilon < 1.0:
         raise ValueError(f"tolerance must lie in (0, 1), got {epsilon}")
+    if isinstance(s, torch.Tensor) and not s.is_cuda:
+        s = s.detach().numpy()   # host tensors take the host-array branch
     on_device = isinstance(s, torch.Tensor)
     if on_device:
         if s.dim() != 2:
@@ -418,9 +420,16 @@ def tsvdm_tolerance_stream(tensors, ts: TransformSet, epsilon, strategy=MEMORY_E
             raise TypeError(f"expected DenseTensor inputs, got {type(t).__name__}")
         ts.check_dims(t.dims)
         src = torch.from_numpy(np.ascontiguousarray(t.data))
-        if bufs[b] is None or bufs[b].numel() != src.numel():
-            bufs[b] = torch.empty(src.numel(), dtype=torch.float64, device=dev)
+        compute = torch.cuda.current_stream(dev)
         with torch.cuda.stream(copy_stream):
+            if bufs[b] is None or bufs[b].numel() != src.numel():
+                # allocated on the copy stream (its first writer) and ordered
+                # after everything already queued on the compute stream, so a
+                # block freed by in-flight compute work is never overwritten;
+                # the compute stream's later use is recorded for the allocator
+                copy_stream.wait_stream(compute)
+                bufs[b] = torch.empty(src.numel(), dtype=torch.float64, device=dev)
+                bufs[b].record_stream(compute)
             if free[b] is not None:
                 copy_stream.wait_event(free[b])
             bufs[b].copy_(src, non_blocking=True)

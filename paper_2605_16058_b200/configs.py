@@ -174,6 +174,23 @@ def config5_transform_domain(m=8192, p=64, n=4096, decay=0.8, seed=0):
     return ahat, mmat
 
 
+def config5_fibre_block(f0, f1, m=8192, p=64, n=4096, decay=0.8, seed=0):
+    """Fibres [f0, f1) of config5_transform_domain's Ahat as an (f1 - f0, n)
+    float64 array (row = fibre, column = slice), plus M -- the same draws in
+    the same order, without the full m*p*n tensor (a rank of the sharded
+    bench holds only its fibre block)."""
+    rng = np.random.default_rng(seed)
+    sig = decay ** np.arange(p)
+    out = np.empty((f1 - f0, n), order="F")
+    for i in range(n):
+        u = haar_orthogonal(m, rng, cols=p)
+        v = haar_orthogonal(p, rng)
+        sl = (u * sig) @ v.T
+        out[:, i] = sl.reshape(-1, order="F")[f0:f1]
+    mmat = haar_orthogonal(n, rng)
+    return out, mmat
+
+
 CONFIGS = {
     "c1": dict(kind="fixed-rank", rank=10, dims=(256, 256, 64), transform="dct"),
     "c2": dict(kind="tolerance", epsilon=1e-2, dims=(361, 720, 1024), transform="dct"),

@@ -159,13 +159,10 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 template <int VA, int VB>
 int launch_t(const GemmArgs& g, int64_t batch, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_kernel<VA, VB>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(SMEM_BYTES)));
-    configured = true;
-  }
+  // the attribute is per device: set it on every launch (a cheap host call)
+  STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_kernel<VA, VB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(SMEM_BYTES)));
   const int64_t tiles = g.tiles_n * ceil_div(g.M, BM);
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     GemmArgs gb = g;

@@ -3551,9 +3551,13 @@ namespace starm {
 namespace {
 // Library-owned side stream + events per device for the chunked bulge /
 // sigma overlap (created on first use, never destroyed).
+// The fork ... join enqueue sequence of one call holds `mu`, so host threads
+// running SVDs on different streams of one device cannot interleave their
+// event records / waits on the shared side stream.
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, ev[16] = {};
+  std::mutex mu;
 };
 std::mutex g_side_mu;
 SideStream g_side[64];
@@ -3662,6 +3666,8 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
     const int nch = count >= 4 * int64_t(pl.slots_b) ? 4 : 1;
     SideStream* ss = nch > 1 ? side_stream() : nullptr;
     if (nch > 1 && !ss) return STARM_CUDA;
+    std::unique_lock<std::mutex> side_lock;
+    if (ss) side_lock = std::unique_lock<std::mutex>(ss->mu);
     if (ss) {
       STARM_CUDA_TRY(cudaEventRecord(ss->fork, st));
       STARM_CUDA_TRY(cudaStreamWaitEvent(ss->s, ss->fork, 0));

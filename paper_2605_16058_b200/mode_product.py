@@ -7,14 +7,22 @@ kernel computes dst[b] = M @ src[b] for all b in a single grid.  The
 variant and thread arguments are validated exactly like the reference and
 then have no further effect.
 
-Structured transforms take exact shortcuts of the same linear map: the DCT
-kind (power-of-two extent <= 4096) runs the O(n log n) FFT-based DCT-II /
-DCT-III kernel (starm_dct_f64) instead of the dense product, and the
-identity kind is a device copy (the dense product with I is exact).
+Structured transforms apply the SAME operator as the reference's dense
+product, faster.  The identity kind is a device copy (the product with I is
+exact).  The DCT kind with a power-of-two extent in [256, 4096] whose stored
+matrix is within 1e-9 of the exact DCT-II (always, for dct_matrix) runs the
+O(n log n) FFT DCT-II / DCT-III kernel (starm_dct_f64) for the exact
+transform and then adds the reference matrix's own rounding, Delta =
+M - M_exact, with a tcgen05 bf16 GEMM (starm_ttm_residual_bf16): the result
+is fl(M @ x) of the reference to a few u, not merely the exact DCT.  Shorter
+DCTs (n < 256: the dense DMMA product costs less than FFT + residual) and
+any other matrix take the dense product.  STARM_EXACT_DCT=1 skips the
+residual (diagnostic: the exact DCT-II alone).
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from math import prod
 
@@ -103,25 +111,46 @@ def ttm_device(x: DeviceTensor, mode: int, op, out_cols: int, inner: int) -> Dev
     return out
 
 
+DCT_FFT_MIN = 256   # below this the dense DMMA product is cheaper than FFT + residual
+
+
 def _fast_kind(m, n):
     if isinstance(m, Transform):
-        if m.kind == DCT and 2 <= n <= 4096 and (n & (n - 1)) == 0:
+        if (m.kind == DCT and DCT_FFT_MIN <= n <= 4096 and (n & (n - 1)) == 0
+                and m.residual_host() is not None):
             return DCT
         if m.kind == IDENTITY:
             return IDENTITY
     return None
 
 
-def structured_device(x: DeviceTensor, mode: int, kind: str, inverse: bool) -> DeviceTensor:
+def structured_device(x: DeviceTensor, mode: int, kind: str, inverse: bool,
+                      tr: Transform = None) -> DeviceTensor:
     """Mode-``mode`` product with a DCT (DCT-II, or DCT-III when inverse) or
-    identity transform without the dense matrix."""
+    identity transform without the dense matrix.  For the DCT, ``tr``'s
+    residual Delta = M - M_exact is added on the tensor cores so the result
+    is the reference's dense product with tr.matrix (or its transpose)."""
+    import torch
     plan = TTMPlan.for_dims(x.dims, mode, x.dims[mode])
     out = DeviceTensor.empty(x.dims, x.device)
     if kind == IDENTITY:
         out.data.copy_(x.data)
         return out
+    st = nat.stream_ptr(x.device)
     nat.call("starm_dct_f64", x.data.data_ptr(), out.data.data_ptr(), plan.rows, plan.inner,
-             plan.batch, int(bool(inverse)), nat.stream_ptr(x.device))
+             plan.batch, int(bool(inverse)), st)
+    if tr is not None and os.environ.get("STARM_EXACT_DCT", "0") != "1":
+        op = tr.residual_operand(x.device, transpose=inverse)
+        if op is None:
+            raise ValueError("transform has no DCT residual operand")
+        delta, e = op
+        lib = nat.load()
+        nbytes = lib.starm_ttm_residual_workspace_bytes(plan.rows, plan.inner, plan.batch)
+        ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=x.device)
+        base = ws.data_ptr()
+        base += (-base) % 128
+        nat.call("starm_ttm_residual_bf16", x.data.data_ptr(), delta.data_ptr(), int(e),
+                 out.data.data_ptr(), plan.rows, plan.inner, plan.batch, base, nbytes, st)
     return out
 
 
@@ -156,7 +185,7 @@ def ttm(t, mode, m, variant=BATCHED, threads=1):
     def go(x):
         kind = _fast_kind(m, x.dims[mode])
         if kind is not None:
-            return structured_device(x, mode, kind, inverse=False)
+            return structured_device(x, mode, kind, inverse=False, tr=m)
         op, j, n = _matrix_operand(m, x.device)
         return ttm_device(x, mode, op, j, n)
 
@@ -174,7 +203,7 @@ def ttm_inverse(t, mode, m, variant=BATCHED, threads=1):
     def go(x):
         kind = _fast_kind(m, x.dims[mode])
         if kind is not None:
-            return structured_device(x, mode, kind, inverse=True)
+            return structured_device(x, mode, kind, inverse=True, tr=m)
         op, j, n = _matrix_operand(m, x.device, transpose=True)
         return ttm_device(x, mode, op, j, n)
 
@@ -186,7 +215,7 @@ def forward_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
     for k, tr in enumerate(ts, start=2):
         kind = _fast_kind(tr, out.dims[k])
         if kind is not None:
-            out = structured_device(out, k, kind, inverse=False)
+            out = structured_device(out, k, kind, inverse=False, tr=tr)
             continue
         op, j, n = _matrix_operand(tr, x.device)
         out = ttm_device(out, k, op, j, n)
@@ -198,7 +227,7 @@ def inverse_device(x: DeviceTensor, ts: TransformSet) -> DeviceTensor:
     for k in range(len(ts) + 1, 1, -1):
         kind = _fast_kind(ts[k - 2], out.dims[k])
         if kind is not None:
-            out = structured_device(out, k, kind, inverse=True)
+            out = structured_device(out, k, kind, inverse=True, tr=ts[k - 2])
             continue
         op, j, n = _matrix_operand(ts[k - 2], x.device, transpose=True)
         out = ttm_device(out, k, op, j, n)

@@ -1,4 +1,5 @@
-"""One ⋆M tolerance t-SVDM sharded over ranks (multi-GPU, one process per GPU).
+"""One ⋆M t-SVDM (tolerance or fixed rank) sharded over ranks (multi-GPU,
+one process per GPU).
 
 The reference runs `tsvdm_tolerance` (tsvdm.py:268-321) on one host.  Here
 one tensor A (m, p, N) is split over G ranks:
@@ -33,7 +34,8 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["ShardPlan", "ShardedResult", "DeviceOps", "scatter_fibres", "tsvdm_tolerance_sharded",
-           "reconstruct_sharded", "gather_factors"]
+           "tsvdm_fixed_rank_sharded", "reconstruct_sharded", "relative_error_sharded",
+           "gather_factors"]
 
 
 def _bounds(total: int, world: int, rank: int):
@@ -164,6 +166,33 @@ def tsvdm_tolerance_sharded(local, plan: ShardPlan, ops, epsilon, dist, group=No
     return ShardedResult(ranks, float(tau), float(disc), float(total), local_ranks, u_data, g_data)
 
 
+def tsvdm_fixed_rank_sharded(local, plan: ShardPlan, ops, rank, dist, group=None) -> ShardedResult:
+    """Fixed-rank t-SVDM (tsvdm.py:246-265) over the ranks: transform and
+    all-to-all as in the tolerance path, then the truncated factors of the
+    owned slices WITH their full sigma (keep_values), sigma all-gathered in
+    slice order and the tail / total energies (tsvdm.py:260-262) computed
+    replicated from the gathered (r x N) matrix -- a fixed summation order,
+    so every rank (and every world size) gets the single-GPU numbers."""
+    import torch
+    m, p, n = plan.m, plan.p, plan.n
+    r = min(m, p)
+    rank = int(rank)
+    if not 1 <= rank <= r:
+        raise ValueError(f"rank must lie in [1, {r}], got {rank}")
+    ahat = ops.forward(local, plan.nf, n)
+    recv = torch.empty(sum(plan.recv_counts()), dtype=torch.float64, device=ahat.device)
+    dist.all_to_all_single(recv, ahat, plan.recv_counts(), plan.send_counts(), group=group)
+    del ahat
+    slices = _assemble(recv, plan, torch)
+    del recv
+    local_ranks = np.full(plan.ns, rank, dtype=np.int64)
+    u_data, g_data, s_local = ops.truncated_with_values(slices, m, p, plan.ns, local_ranks)
+    s_all = _all_gather_cols(s_local, r, plan, dist, group, torch)
+    disc, total = ops.tail_energy(s_all, r, n, rank)
+    ranks = np.full(n, rank, dtype=np.int64)
+    return ShardedResult(ranks, 0.0, float(disc), float(total), local_ranks, u_data, g_data)
+
+
 def reconstruct_sharded(res: ShardedResult, plan: ShardPlan, ops, dist, group=None):
     """This rank's fibre block of the reconstruction (flat (nf, N) col-major):
     facewise U_i G_i of the owned slices, all-to-all back to fibres, inverse
@@ -179,9 +208,15 @@ def reconstruct_sharded(res: ShardedResult, plan: ShardPlan, ops, dist, group=No
     return ops.inverse(back, plan.nf, plan.n)
 
 
-def relative_error_sharded(local, rec, dist, group=None) -> float:
+def relative_error_sharded(local, rec, dist, group=None, ops=None) -> float:
+    """||A - rec|| / ||A|| over all ranks: per-rank (sum (a-b)^2, sum a^2)
+    by ``ops.error_sums`` (the K10 kernel on the device) and one all-reduce
+    of the two partials."""
     import torch
-    sums = torch.stack([torch.sum((local - rec) ** 2), torch.sum(local ** 2)]).to(torch.float64)
+    if ops is not None and hasattr(ops, "error_sums"):
+        sums = ops.error_sums(local, rec)
+    else:
+        sums = torch.stack([torch.sum((local - rec) ** 2), torch.sum(local ** 2)]).to(torch.float64)
     dist.all_reduce(sums, group=group)
     num, den = (float(v) for v in sums.cpu())
     return float(np.sqrt(num / den)) if den else 0.0
@@ -248,6 +283,43 @@ class DeviceOps:
         rk = torch.from_numpy(np.ascontiguousarray(local_ranks)).to(self.device)
         f, _ = svd_truncated_device(self._dev(slices, (m, p, ns)), rk, total)
         return f.u_data[:total * m], f.g_data[:total * p]
+
+    def truncated_with_values(self, slices, m, p, ns, local_ranks):
+        """Packed leading factors AND every sigma of the owned slices (the
+        keep_values pass of tsvdm_fixed_rank): (u_data, g_data, s (r*ns))."""
+        import torch
+        from .slice_svd import svd_truncated_device
+        r = min(m, p)
+        total = int(np.sum(local_ranks))
+        if ns == 0:
+            z = torch.empty(0, dtype=torch.float64, device=self.device)
+            return z, z, z
+        rk = torch.from_numpy(np.ascontiguousarray(local_ranks)).to(self.device)
+        f, s = svd_truncated_device(self._dev(slices, (m, p, ns)), rk, total, keep_values=True)
+        return f.u_data[:total * m], f.g_data[:total * p], s[:r * ns]
+
+    def tail_energy(self, s_all, r, n, rank):
+        import torch
+        from . import _native as nat
+        en = torch.empty(2, dtype=torch.float64, device=self.device)
+        nat.call("starm_tail_energy_f64", s_all.data_ptr(), r, n, int(rank), en.data_ptr(),
+                 nat.stream_ptr(self.device))
+        d, t = en.cpu().numpy()
+        return float(d), float(t)
+
+    def error_sums(self, a, b):
+        """(sum (a-b)^2, sum a^2) of two flat device tensors (K10)."""
+        import torch
+        from . import _native as nat
+        lib = nat.load()
+        out = torch.zeros(2, dtype=torch.float64, device=self.device)
+        if a.numel() == 0:
+            return out
+        nbytes = lib.starm_error_sums_workspace_bytes(a.numel())
+        ws = nat.workspace(nbytes, self.device)
+        nat.call("starm_error_sums_f64", a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),
+                 ws.data_ptr(), nbytes, nat.stream_ptr(self.device))
+        return out
 
     def unpack(self, u_data, g_data, local_ranks, m, p, ns):
         import torch

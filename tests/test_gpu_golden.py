@@ -1,0 +1,267 @@
+"""GPU parity on the BASELINE configurations (the driver-run suite).
+
+The goldens in tests/golden/golden_configs.npz are outputs of the reference
+package itself (tests/golden/make_golden.py ran /root/reference/pkg/src in
+the build container): c1 at full size (256x256x64, DCT, rank 10), c2 and c5
+at reduced size.  c3 and c4 (too slow for the reference at any useful size)
+are checked against the oracle restatement, which tests/test_oracle_golden.py
+pins to the same reference outputs.  Every compute call goes through the
+public API into libstarm.so; numpy/LAPACK only check.
+
+Parity bar (BASELINE.json north_star):
+  * sigma elementwise within 1e-10 relative above 64 u sigma_max(slice);
+  * ranks bit-exact; where the reference itself sits on a tie (c5's graded
+    spectrum) a differing slice is accepted only if every sigma^2 between the
+    two ranks lies within 1e-9 of tau (the margin diagnostic);
+  * reconstruction error within 1e-8 relative;
+  * U / V compared by subspace (projector distance), gap-aware.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2605_16058_b200 as sb
+from paper_2605_16058_b200 import configs as cf
+from helpers import projector_distance, rel_error, sigma_close
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GC = np.load(os.path.join(HERE, "golden", "golden_configs.npz"))
+U = np.finfo(float).eps
+
+
+def _sigma_all_close(got, ref):
+    """Number of sigma violating |ds| <= 1e-10 sigma + 64 u sigma_max(slice)."""
+    tol = 1e-10 * ref + 64 * U * ref.max(axis=0, keepdims=True)
+    return int((np.abs(got - ref) > tol).sum())
+
+
+def _margin_explains(got_ranks, ref_ranks, ref_s, tau, margin=1e-9):
+    """Slices whose rank differs must straddle tau only through sigma^2 within
+    ``margin`` (relative) of tau: the reference's own choice there is decided
+    by rounding (SURVEY 8d, c5 at eps = 1e-4)."""
+    bad = np.flatnonzero(got_ranks != ref_ranks)
+    for i in bad:
+        lo, hi = sorted((int(got_ranks[i]), int(ref_ranks[i])))
+        sq = ref_s[lo:hi, i] ** 2
+        if tau <= 0 or np.any(np.abs(sq - tau) > margin * tau):
+            return False, int(i)
+    return True, len(bad)
+
+
+def _gap_subspace_ok(u, uref, s, ks, c=1e-12):
+    """Projector distance of the leading-k columns, bounded by the sigma gap
+    (Wedin: sin(theta) <~ ||E|| / gap with ||E|| ~ eps * sigma_max)."""
+    smax = float(s[0]) if s.size else 0.0
+    worst = 0.0
+    for k in ks:
+        if k <= 0 or k >= len(s):
+            continue
+        gap = float(s[k - 1] - s[k])
+        if gap <= 1e-8 * smax:
+            continue
+        d = projector_distance(u[:, :k], uref[:, :k])
+        bound = c + 512 * U * smax / gap
+        worst = max(worst, d / bound)
+    return worst
+
+
+# ----------------------------------------------------------------- c1 full size
+
+def test_c1_full_size_against_reference_golden():
+    a = cf.config1()
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    c = sb.tsvdm_fixed_rank(t, ts, 10)
+    assert np.array_equal(c.ranks, GC["c1/ranks"])
+    tot = float(GC["c1/total"])
+    assert abs(c.total_energy - tot) <= 1e-12 * tot
+    assert abs(c.discarded_energy - float(GC["c1/disc"])) <= 1e-8 * float(GC["c1/disc"])
+    rec = sb.reconstruct(c)
+    relerr = rel_error(a, rec.array)
+    assert abs(relerr - float(GC["c1/relerr"])) <= 1e-8 * float(GC["c1/relerr"])
+    assert abs(c.relative_error() - relerr) <= 1e-8 * relerr
+    # sigma of every transform-domain slice
+    s = sb.svd_values_only(sb.to_transform_domain(t, ts))
+    assert _sigma_all_close(s, GC["c1/s"]) == 0
+    # slice-0 factors by subspace (signs are arbitrary) and by product
+    u0 = c.factors.u_block(0)
+    g0 = c.factors.g_block(0)
+    assert projector_distance(u0, GC["c1/u0"]) <= 1e-10
+    ref_prod = GC["c1/u0"] @ GC["c1/g0"]
+    assert np.linalg.norm(u0 @ g0 - ref_prod) <= 1e-10 * np.linalg.norm(ref_prod)
+
+
+# ------------------------------------------------------------ c2 / c5 reduced
+
+def test_c2_reduced_against_reference_golden():
+    a = cf.config2(nlat=91, nlon=180, nt=128)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    s = sb.svd_values_only(sb.to_transform_domain(t, ts))
+    assert _sigma_all_close(s, GC["c2r/s"]) == 0
+    th = sb.compute_threshold(s, 1e-2)
+    assert th.j == int(GC["c2r/j"])
+    assert abs(th.tau - float(GC["c2r/tau"])) <= 1e-10 * float(GC["c2r/tau"])
+    c = sb.tsvdm_tolerance(t, ts, 1e-2)
+    assert np.array_equal(c.ranks, GC["c2r/ranks"])
+    tot = float(GC["c2r/total"])
+    assert abs(c.total_energy - tot) <= 1e-12 * tot
+    assert abs(c.discarded_energy - float(GC["c2r/disc"])) <= 1e-10 * tot
+    rec = sb.reconstruct(c)
+    relerr = rel_error(a, rec.array)
+    assert abs(relerr - float(GC["c2r/relerr"])) <= 1e-8 * float(GC["c2r/relerr"])
+
+
+def test_c5_reduced_against_reference_golden():
+    ahat, mmat = cf.config5_transform_domain(m=512, p=64, n=128)
+    a = sb.ttm(sb.DenseTensor(ahat), 2, mmat.T).array
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet((sb.validate_transform(mmat),))
+    s = sb.svd_values_only(sb.to_transform_domain(t, ts))
+    ref_s = GC["c5r/s"]
+    assert _sigma_all_close(s, ref_s) == 0
+    # analytic golden: sigma_j = 0.8^j in every slice
+    sig = 0.8 ** np.arange(64)
+    assert np.max(np.abs(s - sig[:, None]) / sig[:, None]) <= 1e-9
+    c16 = sb.tsvdm_fixed_rank(t, ts, 16)
+    tot = float(GC["c5r/fr_total"])
+    assert abs(c16.total_energy - tot) <= 1e-12 * tot
+    assert abs(c16.discarded_energy - float(GC["c5r/fr_disc"])) <= 1e-10 * tot
+    ct = sb.tsvdm_tolerance(t, ts, 1e-4)
+    th_ref = oracle.compute_threshold(ref_s, 1e-4)   # reference threshold on its own sigma
+    ok, info = _margin_explains(ct.ranks, GC["c5r/tol_ranks"], ref_s, th_ref["tau"])
+    assert ok, f"slice {info} differs in rank outside the tie margin"
+    assert abs(ct.discarded_energy - float(GC["c5r/tol_disc"])) <= 1e-8 * tot
+    rec = sb.reconstruct(ct)
+    err = rel_error(a, rec.array)
+    assert err < 1e-4 and abs(err - ct.relative_error()) <= 1e-8 * err
+
+
+# ------------------------------------------------------ c3 / c4 reduced (oracle)
+
+def test_c3_reduced_against_oracle():
+    a, mmat = cf.config3(nx=128, ny=128, nt=64, modes=16, kmax=8)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet((sb.validate_transform(mmat),))
+    rank = 8
+    c = sb.tsvdm_fixed_rank(t, ts, rank)
+    ref = oracle.tsvdm_fixed_rank(a, [mmat], rank)
+    assert np.array_equal(c.ranks, ref["ranks"])
+    tot = ref["total_energy"]
+    assert abs(c.total_energy - tot) <= 1e-12 * tot
+    assert abs(c.discarded_energy - ref["discarded_energy"]) <= 1e-10 * tot
+    s = sb.svd_values_only(sb.to_transform_domain(t, ts))
+    assert _sigma_all_close(s, ref["s"]) == 0
+    # Traveling modes give cos/sin pairs of (nearly) equal sigma, so a rank-8
+    # cut can fall inside a pair and the truncation is then not unique (the
+    # reference's own choice is rounding).  Where the gap sigma_8 - sigma_9
+    # is real the leading-8 subspace and the slice's rank-8 product must
+    # agree; everywhere the realised error must.
+    uo = oracle.u_offsets(ref["ranks"], a.shape[0])
+    go = oracle.g_offsets(ref["ranks"], a.shape[1])
+    gapped = 0
+    for i in range(a.shape[2]):
+        si = ref["s"][:, i]
+        if si[rank - 1] - si[rank] <= 1e-3 * si[0]:
+            continue
+        gapped += 1
+        uref = ref["u_data"][uo[i]:uo[i + 1]].reshape((a.shape[0], rank), order="F")
+        gref = ref["g_data"][go[i]:go[i + 1]].reshape((rank, a.shape[1]), order="F")
+        assert _gap_subspace_ok(c.factors.u_block(i), uref, si, [rank]) <= 1.0, i
+        prod_ref = uref @ gref
+        assert np.linalg.norm(c.factors.u_block(i) @ c.factors.g_block(i) - prod_ref) <= \
+            1e-8 * np.linalg.norm(prod_ref), i
+    assert gapped >= a.shape[2] // 4
+    rec = sb.reconstruct(c)
+    rec_ref = oracle.reconstruct_packed(a.shape, [mmat], ref["ranks"], ref["u_data"], ref["g_data"])
+    err, err_ref = rel_error(a, rec.array), rel_error(a, rec_ref)
+    assert abs(err - err_ref) <= 1e-8 * err_ref
+
+
+def test_c4_reduced_against_oracle():
+    """SURVEY 8c config-4 restatement: f32 frames upcast to f64, raw
+    non-orthonormal M, values -> threshold -> truncated, reconstruction with
+    the explicit M^-1; both error domains reported."""
+    x32, mmat, minv = cf.config4(nx=64, ny=64, nt=128, peaks=20)
+    a = np.asfortranarray(x32.astype(np.float64))
+    t = sb.DenseTensor(x32)          # the API upcasts like tensor.py:87
+    assert t.array.dtype == np.float64 and np.array_equal(t.array, a)
+    ahat = sb.ttm(t, 2, mmat)
+    ahat_ref = oracle.ttm(a, 2, mmat)
+    assert rel_error(ahat_ref, ahat.array) <= 1e-13
+    s = sb.svd_values_only(ahat)
+    s_ref = oracle.svd_values_only(ahat_ref)
+    assert _sigma_all_close(s, s_ref) == 0
+    th = sb.compute_threshold(s, 1e-3)
+    th_ref = oracle.compute_threshold(s_ref, 1e-3)
+    ok, info = _margin_explains(th.ranks, th_ref["ranks"], s_ref, th_ref["tau"], margin=1e-10)
+    assert ok, info
+    f = sb.svd_truncated_slices(ahat, th.ranks)
+    u_ref, g_ref = oracle.svd_truncated_slices(ahat_ref, th.ranks)
+    chat = oracle.reconstruct_packed(a.shape, [np.eye(128)], th.ranks, f.u_data, f.g_data)
+    chat_ref = oracle.reconstruct_packed(a.shape, [np.eye(128)], th.ranks, u_ref, g_ref)
+    assert rel_error(chat_ref, chat) <= 1e-8
+    err_t = rel_error(ahat_ref, chat)
+    assert abs(err_t - math.sqrt(th.discarded_energy / th.total_energy)) <= 1e-8 * err_t
+    assert err_t <= 1e-3
+    rec = sb.ttm(sb.DenseTensor(chat), 2, minv).array
+    rec_ref = oracle.ttm(chat_ref, 2, minv)
+    assert rel_error(rec_ref, rec) <= 1e-8
+    # original-domain error exceeds eps for a non-orthonormal M
+    err_o = rel_error(a, rec)
+    assert abs(err_o - rel_error(a, rec_ref)) <= 1e-8 * err_o
+
+
+# ------------------------------------------------ c2: SVD parity in isolation
+
+def test_c2_shaped_slices_svd_only():
+    """Feed the ORACLE's transform-domain slices (the reference's dense DCT
+    product) straight to the device SVD: this isolates the SVD from the
+    transform.  361 x 720 slices, noise-dominated high-frequency slices and
+    signal slices; zero violations of the sigma bar."""
+    a = cf.config2(nlat=361, nlon=720, nt=64, seed=3)
+    ahat = oracle.to_transform_domain(a, [oracle.dct_matrix(64)])
+    pick = [0, 1, 2, 5, 17, 40, 55, 63]
+    sub = np.asfortranarray(ahat[:, :, pick])
+    s = sb.svd_values_only(sb.DenseTensor(sub))
+    ref = oracle.svd_values_only(sub)
+    assert _sigma_all_close(s, ref) == 0
+
+
+def test_c2_transform_matches_reference_operator():
+    """The DCT route reproduces the reference's OWN operator (its rounded
+    dct_matrix applied by a dense product), not just the exact DCT-II: on
+    c2-shaped fibres the transform-domain slices agree with the oracle's
+    dense product to the rounding of that product, and the noise-slice sigma
+    that the exact (FFT-only) transform misses by up to 4e-10 agree to 1e-10."""
+    a = cf.config2(nlat=46, nlon=90, nt=1024, seed=0)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    got = sb.to_transform_domain(t, ts).array
+    ref = oracle.to_transform_domain(a, [oracle.dct_matrix(1024)])
+    assert rel_error(ref, got) <= 2e-15
+    pick = [0, 3, 7, 100, 300, 551, 552, 900, 1023]
+    s = sb.svd_values_only(sb.DenseTensor(np.asfortranarray(got[:, :, pick])))
+    s_ref = oracle.svd_values_only(np.asfortranarray(ref[:, :, pick]))
+    assert _sigma_all_close(s, s_ref) == 0
+
+
+# ----------------------------------------------- error kernel (K10) parity
+
+def test_relative_error_device_matches_helpers():
+    from paper_2605_16058_b200.compress import relative_error_device
+    from paper_2605_16058_b200.tensors import as_device
+    import torch
+    rng = np.random.default_rng(8)
+    for dims in [(3, 4, 5), (31, 17, 9), (361, 72, 16)]:
+        a = rng.standard_normal(dims)
+        b = a + 1e-6 * rng.standard_normal(dims)
+        dev = torch.device("cuda", 0)
+        got = relative_error_device(as_device(sb.DenseTensor(a), dev), as_device(sb.DenseTensor(b), dev))
+        assert abs(got - rel_error(a, b)) <= 1e-12 * rel_error(a, b)

@@ -21,7 +21,7 @@ import torch.multiprocessing as mp
 import oracle
 from paper_2605_16058_b200.sharded import (ShardPlan, gather_factors, reconstruct_sharded,
                                            relative_error_sharded, scatter_fibres,
-                                           tsvdm_tolerance_sharded)
+                                           tsvdm_fixed_rank_sharded, tsvdm_tolerance_sharded)
 
 
 class OracleOps:
@@ -55,6 +55,18 @@ class OracleOps:
         a = slices.numpy().reshape((m, p, ns), order="F")
         u, g = oracle.svd_truncated_slices(a, local_ranks)
         return torch.from_numpy(u), torch.from_numpy(g)
+
+    def truncated_with_values(self, slices, m, p, ns, local_ranks):
+        if ns == 0:
+            z = torch.zeros(0, dtype=torch.float64)
+            return z, z, z
+        a = slices.numpy().reshape((m, p, ns), order="F")
+        u, g, s = oracle.svd_truncated_slices(a, local_ranks, keep_values=True)
+        return torch.from_numpy(u), torch.from_numpy(g), torch.from_numpy(s.reshape(-1, order="F").copy())
+
+    def tail_energy(self, s_all, r, n, rank):
+        sq = s_all.numpy().reshape((r, n), order="F") ** 2
+        return float(sq[rank:, :].sum()), float(sq.sum())     # tsvdm.py:260-262
 
     def unpack(self, u_data, g_data, local_ranks, m, p, ns):
         out = np.zeros((m, p, ns), order="F")
@@ -136,6 +148,57 @@ def test_sharded_tolerance_matches_single_process(dims, eps, world):
         np.testing.assert_allclose(u, ref["u_data"], rtol=0, atol=1e-9)
         np.testing.assert_allclose(g, ref["g_data"], rtol=0, atol=1e-9)
         # realised error through the sharded reconstruction
+        assert abs(err - ref_err) <= 1e-10
+        assert abs(err - np.sqrt(disc / total)) <= 1e-10
+
+
+def _worker_fixed(rank, world, port, dims, k, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = _tensor(dims, seed)
+        m, p, n = dims
+        mat = oracle.dct_matrix(n)
+        plan = ShardPlan(m, p, n, world, rank)
+        local = torch.from_numpy(scatter_fibres(a, plan).reshape(-1, order="F").copy())
+        ops = OracleOps(mat)
+        res = tsvdm_fixed_rank_sharded(local, plan, ops, k, dist)
+        u, g = gather_factors(res, plan, dist)
+        rec = reconstruct_sharded(res, plan, ops, dist)
+        err = relative_error_sharded(local, rec, dist)
+        q.put((rank, res.ranks, res.discarded_energy, res.total_energy, u.numpy(), g.numpy(), err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,k,world", [((6, 5, 8), 2, 2), ((7, 3, 5), 1, 2), ((5, 6, 9), 3, 4),
+                                          ((4, 4, 3), 4, 4)])
+def test_sharded_fixed_rank_matches_single_process(dims, k, world):
+    """tsvdm_fixed_rank over 2 / 4 gloo ranks (4 ranks with 3 slices: one rank
+    owns none) equals the single-process oracle of tsvdm.py:246-265."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_fixed, args=(r, world, port, dims, k, 5, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    a = _tensor(dims, 5)
+    mat = oracle.dct_matrix(dims[2])
+    ref = oracle.tsvdm_fixed_rank(a, [mat], k)
+    rec = oracle.reconstruct_packed(dims, [mat], ref["ranks"], ref["u_data"], ref["g_data"])
+    ref_err = float(np.linalg.norm(a - rec) / np.linalg.norm(a))
+    for rank, ranks, disc, total, u, g, err in outs:
+        assert np.array_equal(ranks, ref["ranks"]), rank
+        assert abs(disc - ref["discarded_energy"]) <= 1e-12 * ref["total_energy"]
+        assert abs(total - ref["total_energy"]) <= 1e-12 * ref["total_energy"]
+        np.testing.assert_allclose(u, ref["u_data"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(g, ref["g_data"], rtol=0, atol=1e-9)
         assert abs(err - ref_err) <= 1e-10
         assert abs(err - np.sqrt(disc / total)) <= 1e-10
 
