@@ -134,7 +134,7 @@ def cpu_sample(wl, nslices, threads, a=None):
             ranks = np.full(nslices, int(wl.param), dtype=np.int64)
             oracle.svd_truncated_slices(ahat, ranks, keep_values=True)
     dt = time.perf_counter() - t0
-    return dt, nslices * m * p * 8
+    return dt, nslices * m * p * (wl.in_bytes // (m * p * n))
 
 
 def cpu_info():
@@ -523,15 +523,21 @@ def run_ours(args):
     e2e = None
     e2e_stream = None
     if not args.no_e2e and host_available_bytes() > 3 * in_bytes:
-        pinned = torch.empty(m * p * n, dtype=torch.float64, pin_memory=True)
-        pinned.copy_(x.data, non_blocking=False)
-        host = sb.DenseTensor(pinned.numpy().reshape((m, p, n), order="F"), copy=False)
+        f32 = wl.host is not None and wl.host.dtype == np.float32
+        pinned = torch.empty(m * p * n, dtype=torch.float32 if f32 else torch.float64,
+                             pin_memory=True)
+        if f32:
+            pinned.numpy()[:] = wl.host.reshape(-1, order="F")
+            host = pinned.numpy().reshape((m, p, n), order="F")   # float32 frames
+        else:
+            pinned.copy_(x.data, non_blocking=False)
+            host = sb.DenseTensor(pinned.numpy().reshape((m, p, n), order="F"), copy=False)
         del x
         torch.cuda.empty_cache()
 
         def host_step():
             if wl.transform == "raw":
-                xd = sb.DeviceTensor.from_host(host, dev)
+                xd = sb.DeviceTensor.from_host(host, dev)   # f32 H2D + device upcast
                 r = wl.step(xd)
                 return r.factors.to_host()
             if wl.kind == "fixed-rank":
@@ -575,6 +581,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model, cores = cpu_info()
         a_host = host_for_cpu(wl) if wl.host is not None else None
+        if a_host is not None and a_host.dtype == np.float32:
+            a_host = np.asfortranarray(a_host, dtype=np.float64)   # the reference upcasts
         if a_host is None and e2e is not None:
             a_host = host.array
         if a_host is not None:
@@ -591,6 +599,7 @@ def run_ours(args):
             "metric": metric_name(args.config), "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "input_dtype": "f32" if wl.host is not None and wl.host.dtype == np.float32 else "f64",
             "data": f"synthetic (workloads.{args.config}, seed=rank)",
             "config": {"workload": wl.describe + ("; L2 flushed between steps" if flush is not None
                                                   else "; input > L2 (no flush needed)"),

@@ -81,6 +81,18 @@ size_t starm_last_error(char* buf, size_t len);
 int starm_ttm_f64(const double* src, const double* mat, double* dst, int64_t rows,
                   int64_t inner, int64_t batch, int64_t out_cols, void* stream);
 
+/* float32 twin of starm_ttm_f64 (same view and semantics, f32 in / f32
+ * out): the operands are upcast on the device and contracted in FP64 on the
+ * DMMA path, so the result is the f64 product rounded once to f32 (the
+ * reference itself computes in f64: tensor.py:87 upcasts f32 input).
+ * ws: starm_ttm_f32_workspace_bytes(rows, inner, batch, out_cols) bytes. */
+size_t starm_ttm_f32_workspace_bytes(int64_t rows, int64_t inner, int64_t batch, int64_t out_cols);
+int starm_ttm_f32(const float* src, const float* mat, float* dst, int64_t rows, int64_t inner,
+                  int64_t batch, int64_t out_cols, void* ws, size_t ws_bytes, void* stream);
+/* The DenseTensor upcast (tensor.py:87) on the device: dst[i] = (double)src[i]
+ * (lets a float32 tensor cross PCIe at half the bytes). */
+int starm_upcast_f32_f64(const float* src, double* dst, int64_t count, void* stream);
+
 /* ------------------------------------------------------- K1b fast DCT
  * The DCT transform of the reference (transforms.py dct matrix applied by
  * the mode-k product, ttm.py:87-104) computed in O(n log n) per fiber:
@@ -201,6 +213,28 @@ size_t starm_error_sums_workspace_bytes(int64_t count);
 int starm_error_sums_f64(const double* a, const double* b, int64_t count, double* out2,
                          void* ws, size_t ws_bytes, void* stream);
 
+
+/* ------------------------------ K9 + inverse transform + K10, fused (3-way)
+ * Replaces reconstruct (tsvdm.py:342-357) followed by the relative error of
+ * tests/helpers.py:44-47 / cli.py:185-197, in one stream-ordered call:
+ *     chat_i = U_i G_i                   for the nnz slices in nz_ids (ranks > 0)
+ *     out_(3) = minv @ chat_(3)          (only the nnz columns of minv meet a
+ *                                         nonzero slice: a K = nnz DMMA GEMM)
+ *     err2 = {sum (a - out)^2, sum a^2}  accumulated in that GEMM's epilogue
+ *                                         (deterministic), when a != NULL
+ *  minv   ROW-MAJOR n x n inverse operator: M^T for an orthonormal M (what
+ *         from_transform_domain applies, ttm.py:147-153; for the DCT kind the
+ *         reference's own dense matrix, not the exact DCT-III), or an explicit
+ *         M^-1 (the config-4 restatement).
+ *  nz_ids device int64 list of the nnz slices with ranks > 0 (any order);
+ *         nnz = 0 writes zeros.  out is the (m, p, n) tensor (m*p*n doubles).
+ *  ws     starm_reconstruct_workspace_bytes(m, p, n, nnz) bytes. */
+size_t starm_reconstruct_workspace_bytes(int64_t m, int64_t p, int64_t n, int64_t nnz);
+int starm_reconstruct_f64(const double* u_data, const double* g_data, const int64_t* ranks,
+                          const int64_t* u_off, const int64_t* g_off, int64_t m, int64_t p,
+                          int64_t n, const int64_t* nz_ids, int64_t nnz, const double* minv,
+                          const double* a, double* out, double* err2, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* ------------------------------------------------- K8b pack from full
  * _pack_from_full (tsvdm.py:324-339): from full factors (s (r,N), u

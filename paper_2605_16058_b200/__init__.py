@@ -16,7 +16,8 @@ from .codec import (BadMagicError, BenchRow, CodecError, FormatError, TruncatedP
 from .compress import (COMPUTE_EFFICIENT, MEMORY_EFFICIENT, METHOD_FIXED_RANK, METHOD_TOLERANCE,
                        TOLERANCE_STRATEGIES, TRUNCATE, CompressedTensor, StageClock,
                        ThresholdResult, TSVDMResult, compression_ratio, compute_threshold,
-                       full_tsvdm, reconstruct, relative_error_device, starm_product,
+                       full_tsvdm, reconstruct, reconstruct_fused, relative_error_device,
+                       starm_product,
                        tsvdm_fixed_rank, tsvdm_tolerance, tsvdm_tolerance_stream)
 from .mode_product import (BATCHED, LOOP, PARFOR, TTMPlan, from_transform_domain,
                            to_transform_domain, ttm, ttm_inverse)
@@ -41,7 +42,7 @@ __all__ = [
     "TTMPlan", "ThresholdResult", "Transform", "TransformSet", "VariableRankFactors",
     "compression_ratio", "compute_threshold", "data_driven_transform", "dct_matrix",
     "from_transform_domain", "full_tsvdm", "identity_transform", "linear_index", "multi_index",
-    "orthonormality_residual", "reconstruct", "refold", "relative_error_device", "starm_product",
+    "orthonormality_residual", "reconstruct", "reconstruct_fused", "refold", "relative_error_device", "starm_product",
     "svd_all_slices", "svd_truncated_slices", "svd_values_only", "to_transform_domain",
     "tsvdm_fixed_rank", "tsvdm_tolerance", "tsvdm_tolerance_stream", "ttm", "ttm_inverse", "validate_transform",
 ]

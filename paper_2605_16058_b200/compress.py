@@ -34,7 +34,7 @@ __all__ = [
     "compute_threshold", "TSVDMResult", "CompressedTensor", "starm_product", "full_tsvdm",
     "tsvdm_fixed_rank", "tsvdm_tolerance", "tsvdm_tolerance_stream", "reconstruct",
     "compression_ratio",
-    "threshold_device", "relative_error_device",
+    "threshold_device", "relative_error_device", "reconstruct_fused",
 ]
 
 TRUNCATE = "truncate"
@@ -499,6 +499,64 @@ def _device_factors(c: CompressedTensor, dev):
     return DeviceFactors(f.slice_rows, f.slice_cols, ranks, u_off, g_off, u, g, f.total_rank)
 
 
+def _fused_operator(c: CompressedTensor, nnz, dev):
+    """Row-major inverse operator for starm_reconstruct_f64, or None when the
+    unfused path is cheaper: 3-way tensors only; the identity is a copy; the
+    DCT's FFT route costs ~2 passes over the tensor, so the K = nnz dense
+    product wins only while nnz is small against n."""
+    from .transform_set import DCT, IDENTITY
+    if len(c.dims) != 3 or len(c.transforms) != 1:
+        return None
+    tr = c.transforms[0]
+    n = c.dims[2]
+    if tr.kind == IDENTITY:
+        return None
+    if tr.kind == DCT and nnz > max(16, n // 8):
+        return None
+    return tr.device_operand(dev, transpose=True)   # M^T, row-major (ttm.py:147-153)
+
+
+def reconstruct_fused(c: CompressedTensor, a=None, dev=None, minv=None):
+    """K9 + inverse transform + K10 in one C-ABI call (starm_reconstruct_f64):
+    returns (reconstruction DeviceTensor, relative error or None).  ``minv``
+    overrides the inverse operator (row-major n x n, e.g. an explicit M^-1);
+    raises ValueError when the fused form does not apply (d-way tensors)."""
+    import torch
+    f = c.factors
+    if dev is None:
+        dev = f.u_data.device if isinstance(f, DeviceFactors) else nat.require_cuda()
+    df = _device_factors(c, dev)
+    m, p = c.dims[0], c.dims[1]
+    if len(c.dims) != 3:
+        raise ValueError("the fused reconstruction applies to 3-way tensors")
+    n = c.dims[2]
+    nz = torch.nonzero(df.ranks_dev > 0).reshape(-1).to(torch.int64)
+    nnz = int(nz.numel())
+    op = minv if minv is not None else _fused_operator(c, nnz, dev)
+    if op is None:
+        from .transform_set import IDENTITY
+        if len(c.transforms) == 1 and c.transforms[0].kind != IDENTITY:
+            op = c.transforms[0].device_operand(dev, transpose=True)
+        else:
+            raise ValueError("no dense inverse operator for the fused reconstruction")
+    if not isinstance(op, torch.Tensor):
+        op = torch.from_numpy(np.ascontiguousarray(op, dtype=np.float64)).to(dev)
+    lib = nat.load()
+    nbytes = lib.starm_reconstruct_workspace_bytes(m, p, n, nnz)
+    ws = nat.workspace(nbytes, dev)
+    out = DeviceTensor.empty(c.dims, dev)
+    err2 = torch.empty(2, dtype=torch.float64, device=dev) if a is not None else None
+    nat.call("starm_reconstruct_f64", df.u_data.data_ptr(), df.g_data.data_ptr(),
+             df.ranks_dev.data_ptr(), df.u_off.data_ptr(), df.g_off.data_ptr(), m, p, n,
+             nz.data_ptr() if nnz else 0, nnz, op.data_ptr(),
+             a.data.data_ptr() if a is not None else 0, out.data.data_ptr(), nat.ptr(err2),
+             ws.data_ptr(), nbytes, nat.stream_ptr(dev))
+    if a is None:
+        return out, None
+    d2, a2 = err2.cpu().numpy()
+    return out, (math.sqrt(d2 / a2) if a2 > 0 else 0.0)
+
+
 def reconstruct_device(c: CompressedTensor, dev=None) -> DeviceTensor:
     f = c.factors
     if dev is None:
@@ -506,6 +564,10 @@ def reconstruct_device(c: CompressedTensor, dev=None) -> DeviceTensor:
     df = _device_factors(c, dev)
     m, p = c.dims[0], c.dims[1]
     n = prod(c.dims[2:])
+    if len(c.dims) == 3:
+        nnz = int((df.ranks_dev > 0).sum().item())
+        if _fused_operator(c, nnz, dev) is not None:
+            return reconstruct_fused(c, dev=dev)[0]
     chat = DeviceTensor.empty(c.dims, dev)
     nat.call("starm_unpack_facewise_f64", df.u_data.data_ptr(), df.g_data.data_ptr(),
              df.ranks_dev.data_ptr(), df.u_off.data_ptr(), df.g_off.data_ptr(), m, p, n,

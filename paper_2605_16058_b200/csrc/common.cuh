@@ -45,6 +45,13 @@ void count_launch(int n = 1);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// gemm_f64.cu: C = A * B (batch 1, column-major) with the K10 error partials
+// of E against C fused into the epilogue (epart: 2 doubles per tile).
+int64_t gemm_f64_tiles(int64_t M, int64_t N);
+int gemm_f64_err(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K,
+                 int64_t lda, int64_t ldb, int64_t ldc, const double* E, double* epart,
+                 cudaStream_t st);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -94,7 +94,9 @@ __device__ __forceinline__ void fft_stages(cplx* z, const cplx* tw) {
     // swz(i0 + m h) = swz(i0) ^ swz(m h)
     const int d1 = swz(h), d2 = swz(2 * h), d3 = d1 ^ d2;
     for (int q = threadIdx.x; q < P * Q; q += blockDim.x) {
-      const int p = q >> (LOGN - 2), qq = q & (Q - 1);
+      // the loop never runs for LOGN = 1 (odd LOGN enters it at s = 1); the
+      // guard keeps that instantiation's shift count non-negative
+      const int p = q >> (LOGN >= 2 ? LOGN - 2 : 0), qq = q & (Q - 1);
       const int k = qq & (h - 1);
       const int i0 = ((qq >> s) << (s + 2)) + k;
       cplx* zp = z + p * (N + ZPAD);

@@ -40,6 +40,10 @@ struct GemmArgs {
   double* C;
   int64_t M, N, K, lda, ldb, ldc, sA, sB, sC;
   int64_t tiles_n;
+  // ERR epilogue (K10 fused into the writer of C): reference tensor E with
+  // ld ldc; per CTA {sum (E - C)^2, sum E^2} over the tile -> epart[2 tile]
+  const double* E;
+  double* epart;
 };
 
 template <int VA, int VB>
@@ -82,7 +86,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, const double* A, c
   }
 }
 
-template <int VA, int VB>
+template <int VA, int VB, bool ERR>
 __global__ void __launch_bounds__(THREADS, 2) gemm_f64_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -141,7 +145,18 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_f64_kernel(GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // Epilogue: D[g][2t], D[g][2t+1] -> C(m, n), C(m, n+1).
+  // Epilogue: D[g][2t], D[g][2t+1] -> C(m, n), C(m, n+1); with ERR also the
+  // tile's error partials against E (fixed reduction order: deterministic).
+  double sd = 0.0, sa = 0.0;
+  auto put = [&](int64_t idx, double v) {
+    C[idx] = v;
+    if (ERR) {
+      const double e = g.E[idx];
+      const double d = e - v;
+      sd = fma(d, d, sd);
+      sa = fma(e, e, sa);
+    }
+  };
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t m = m0 + wm * 32 + i * 8 + gq;
@@ -149,18 +164,40 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_f64_kernel(GemmArgs g) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
-      if (n < g.N) C[m + n * g.ldc] = acc[i][j][0];
-      if (n + 1 < g.N) C[m + (n + 1) * g.ldc] = acc[i][j][1];
+      if (n < g.N) put(m + n * g.ldc, acc[i][j][0]);
+      if (n + 1 < g.N) put(m + (n + 1) * g.ldc, acc[i][j][1]);
+    }
+  }
+  if (ERR) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    }
+    __syncthreads();  // the stage buffers are free: reuse them for the warp partials
+    if (lane == 0) {
+      smem[2 * warp] = sd;
+      smem[2 * warp + 1] = sa;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < THREADS / 32; ++w) {
+        s0 += smem[2 * w];
+        s1 += smem[2 * w + 1];
+      }
+      g.epart[2 * tile] = s0;
+      g.epart[2 * tile + 1] = s1;
     }
   }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-template <int VA, int VB>
+template <int VA, int VB, bool ERR = false>
 int launch_t(const GemmArgs& g, int64_t batch, cudaStream_t st) {
   // the attribute is per device: set it on every launch (a cheap host call)
-  STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_kernel<VA, VB>,
+  STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_kernel<VA, VB, ERR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(SMEM_BYTES)));
   const int64_t tiles = g.tiles_n * ceil_div(g.M, BM);
@@ -171,7 +208,7 @@ int launch_t(const GemmArgs& g, int64_t batch, cudaStream_t st) {
     gb.C += b0 * g.sC;
     const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
     dim3 grid(unsigned(tiles), 1, unsigned(nb));
-    gemm_f64_kernel<VA, VB><<<grid, THREADS, SMEM_BYTES, st>>>(gb);
+    gemm_f64_kernel<VA, VB, ERR><<<grid, THREADS, SMEM_BYTES, st>>>(gb);
     STARM_LAUNCH_CHECK();
   }
   return STARM_OK;
@@ -190,13 +227,31 @@ int gemm_f64(const double* A, const double* B, double* C, int64_t M, int64_t N, 
       STARM_CUDA_TRY(cudaMemset2DAsync(C + b * sC, size_t(ldc) * 8, 0, size_t(M) * 8, size_t(N), st));
     return STARM_OK;
   }
-  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, sA, sB, sC, ceil_div(N, BN)};
+  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, sA, sB, sC, ceil_div(N, BN), nullptr, nullptr};
   const bool va = (M % 2 == 0) && (lda % 2 == 0) && (sA % 2 == 0) && aligned16(A);
   const bool vb = (K % 2 == 0) && (ldb % 2 == 0) && (sB % 2 == 0) && aligned16(B);
   if (va && vb) return launch_t<2, 2>(g, batch, st);
   if (va) return launch_t<2, 1>(g, batch, st);
   if (vb) return launch_t<1, 2>(g, batch, st);
   return launch_t<1, 1>(g, batch, st);
+}
+
+// C = A * B (batch 1) with the K10 error partials of E against C fused into
+// the epilogue: epart[2 t], epart[2 t + 1] for tile t < gemm_f64_tiles(M, N).
+int64_t gemm_f64_tiles(int64_t M, int64_t N) { return ceil_div(M, BM) * ceil_div(N, BN); }
+
+int gemm_f64_err(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K,
+                 int64_t lda, int64_t ldb, int64_t ldc, const double* E, double* epart,
+                 cudaStream_t st) {
+  if (M <= 0 || N <= 0) return STARM_OK;
+  STARM_CHECK_ARG(K > 0, "gemm_f64_err: empty contraction");
+  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, ceil_div(N, BN), E, epart};
+  const bool va = (M % 2 == 0) && (lda % 2 == 0) && aligned16(A);
+  const bool vb = (K % 2 == 0) && (ldb % 2 == 0) && aligned16(B);
+  if (va && vb) return launch_t<2, 2, true>(g, 1, st);
+  if (va) return launch_t<2, 1, true>(g, 1, st);
+  if (vb) return launch_t<1, 2, true>(g, 1, st);
+  return launch_t<1, 1, true>(g, 1, st);
 }
 
 }  // namespace starm

@@ -68,21 +68,24 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const int64_t* ranks, int
 // 72 (= 8 mod 32: the (g, t) fragment lanes hit distinct banks).
 constexpr int RT = 64, KC = 16, US = RT + 8;
 
+// ids (optional): slot j of chat holds slice ids[j] (the compacted nonzero
+// slices of the fused reconstruction); NULL: slot j = slice j.
 __global__ void __launch_bounds__(256) unpack_kernel(const double* u_data, const double* g_data,
                                                      const int64_t* ranks, const int64_t* u_off,
                                                      const int64_t* g_off, int64_t m, int64_t p,
                                                      int64_t tiles_m, int64_t tiles_p,
-                                                     double* chat) {
+                                                     double* chat, const int64_t* ids) {
   __shared__ double us[KC][US];  // us[k][row]
   __shared__ double gs[KC][US];  // gs[k][col]
   const int64_t per_slice = tiles_m * tiles_p;
-  const int64_t slice = blockIdx.x / per_slice;
+  const int64_t slot = blockIdx.x / per_slice;
+  const int64_t slice = ids ? ids[slot] : slot;
   const int64_t tile = blockIdx.x % per_slice;
   const int64_t m0 = (tile % tiles_m) * RT, p0 = (tile / tiles_m) * RT;
   const int64_t k = ranks[slice];
   const double* U = u_data + u_off[slice];
   const double* G = g_data + g_off[slice];
-  double* C = chat + slice * m * p;
+  double* C = chat + slot * m * p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;  // rows 32 wm .., cols 16 wn ..
@@ -164,15 +167,42 @@ __global__ void __launch_bounds__(ES_THREADS) err_partial_kernel(const double* a
   }
 }
 
-__global__ void err_final_kernel(const double* part, double* out2) {
-  if (threadIdx.x != 0) return;
+// Fixed-order sum of nparts (d2, a2) partial pairs: each of 256 threads sums a
+// contiguous run, then a fixed tree (deterministic for a given nparts).
+__global__ void __launch_bounds__(256) err_final_kernel(const double* part, int64_t nparts,
+                                                        double* out2) {
+  __shared__ double red[2][256];
+  const int64_t per = (nparts + 255) / 256;
+  const int64_t lo = threadIdx.x * per, hi = lo + per < nparts ? lo + per : nparts;
   double s0 = 0.0, s1 = 0.0;
-  for (int b = 0; b < ES_BLOCKS; ++b) {
+  for (int64_t b = lo; b < hi; ++b) {
     s0 += part[2 * b];
     s1 += part[2 * b + 1];
   }
-  out2[0] = s0;
-  out2[1] = s1;
+  red[0][threadIdx.x] = s0;
+  red[1][threadIdx.x] = s1;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + o];
+      red[1][threadIdx.x] += red[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = red[0][0];
+    out2[1] = red[1][0];
+  }
+}
+
+// B (K x n, column-major) of the fused reconstruction: B[i][t] = minv[t][ids[i]]
+// (minv row-major n x n), i.e. the columns of M^-1 that meet a nonzero slice.
+__global__ void gather_inverse_kernel(const double* minv, const int64_t* ids, int64_t K, int64_t n,
+                                      double* B) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= K * n) return;
+  const int64_t i = e % K, t = e / K;
+  B[e] = minv[t * n + (ids ? ids[i] : i)];
 }
 
 
@@ -284,7 +314,7 @@ extern "C" int starm_unpack_facewise_f64(const double* u_data, const double* g_d
   const int64_t blocks = tm * tp * nslices;
   STARM_CHECK_ARG(blocks < (int64_t(1) << 31), "unpack: grid too large");
   unpack_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(u_data, g_data, ranks, u_off,
-                                                                 g_off, m, p, tm, tp, chat);
+                                                                 g_off, m, p, tm, tp, chat, nullptr);
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }
@@ -303,7 +333,129 @@ extern "C" int starm_error_sums_f64(const double* a, const double* b, int64_t co
   cudaStream_t st = as_stream(stream);
   err_partial_kernel<<<ES_BLOCKS, ES_THREADS, 0, st>>>(a, b, count, part);
   STARM_LAUNCH_CHECK();
-  err_final_kernel<<<1, 32, 0, st>>>(part, out2);
+  err_final_kernel<<<1, 256, 0, st>>>(part, ES_BLOCKS, out2);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+// ------------------------------------------- K9 + inverse transform + K10
+// Workspace: compacted slices (F x nnz), the gathered inverse columns
+// (nnz x n), error partials (2 per GEMM tile, or per error block).
+extern "C" size_t starm_reconstruct_workspace_bytes(int64_t m, int64_t p, int64_t n, int64_t nnz) {
+  if (m < 1 || p < 1 || n < 1 || nnz < 0) return 0;
+  const int64_t F = m * p;
+  const int64_t tiles = gemm_f64_tiles(F, n);
+  const int64_t parts = tiles > ES_BLOCKS ? tiles : ES_BLOCKS;
+  return size_t(F * nnz + nnz * n + 2 * parts) * sizeof(double) + 256;
+}
+
+extern "C" int starm_reconstruct_f64(const double* u_data, const double* g_data,
+                                     const int64_t* ranks, const int64_t* u_off,
+                                     const int64_t* g_off, int64_t m, int64_t p, int64_t n,
+                                     const int64_t* nz_ids, int64_t nnz, const double* minv,
+                                     const double* a, double* out, double* err2, void* ws,
+                                     size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(m >= 1 && p >= 1 && n >= 1 && nnz >= 0 && nnz <= n,
+                  "reconstruct: bad extents (m=%lld p=%lld n=%lld nnz=%lld)", (long long)m,
+                  (long long)p, (long long)n, (long long)nnz);
+  STARM_CHECK_ARG(ranks && u_off && g_off && minv && out && ws, "reconstruct: null pointer");
+  STARM_CHECK_ARG(!a || err2, "reconstruct: err2 is required with a");
+  STARM_CHECK_ARG(ws_bytes >= starm_reconstruct_workspace_bytes(m, p, n, nnz),
+                  "reconstruct: workspace too small");
+  const cudaStream_t st = as_stream(stream);
+  const int64_t F = m * p;
+  double* chat = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  double* B = chat + F * nnz;
+  double* part = B + nnz * n;
+  if (nnz == 0) {  // every rank is zero: the reconstruction is 0
+    STARM_CUDA_TRY(cudaMemsetAsync(out, 0, size_t(F * n) * sizeof(double), st));
+    if (a) {
+      err_partial_kernel<<<ES_BLOCKS, ES_THREADS, 0, st>>>(a, out, F * n, part);
+      STARM_LAUNCH_CHECK();
+      err_final_kernel<<<1, 256, 0, st>>>(part, ES_BLOCKS, err2);
+      STARM_LAUNCH_CHECK();
+    }
+    return STARM_OK;
+  }
+  const int64_t tm = ceil_div(m, RT), tp = ceil_div(p, RT);
+  const int64_t blocks = tm * tp * nnz;
+  STARM_CHECK_ARG(blocks < (int64_t(1) << 31), "reconstruct: grid too large");
+  unpack_kernel<<<unsigned(blocks), 256, 0, st>>>(u_data, g_data, ranks, u_off, g_off, m, p, tm, tp,
+                                                 chat, nz_ids);
+  STARM_LAUNCH_CHECK();
+  gather_inverse_kernel<<<unsigned(ceil_div(nnz * n, 256)), 256, 0, st>>>(minv, nz_ids, nnz, n, B);
+  STARM_LAUNCH_CHECK();
+  // out (F x n, column-major = the (m, p, n) tensor) = chat_nz (F x nnz) * B
+  if (a) {
+    const int rc = gemm_f64_err(chat, B, out, F, n, nnz, F, nnz, F, a, part, st);
+    if (rc) return rc;
+    err_final_kernel<<<1, 256, 0, st>>>(part, gemm_f64_tiles(F, n), err2);
+    STARM_LAUNCH_CHECK();
+  } else {
+    const int rc = starm_ttm_f64(chat, B, out, F, nnz, 1, n, stream);  // out = chat_nz * B
+    if (rc) return rc;
+  }
+  return STARM_OK;
+}
+
+// ---------------------------------------------------------- float32 twins
+// The reference upcasts float32 input to float64 on construction
+// (tensor.py:87); on the device the upcast runs after an f32 H2D (half the
+// PCIe bytes of the f64 tensor).
+namespace starm {
+namespace {
+__global__ void upcast_kernel(const float* __restrict__ src, double* __restrict__ dst, int64_t count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    dst[i] = double(src[i]);
+}
+__global__ void downcast_kernel(const double* __restrict__ src, float* __restrict__ dst, int64_t count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    dst[i] = float(src[i]);
+}
+unsigned stream_grid(int64_t count) {
+  const int64_t b = ceil_div(count, 256);
+  return unsigned(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+}  // namespace
+}  // namespace starm
+
+extern "C" int starm_upcast_f32_f64(const float* src, double* dst, int64_t count, void* stream) {
+  STARM_CHECK_ARG(count >= 0, "upcast: negative count");
+  if (count == 0) return STARM_OK;
+  STARM_CHECK_ARG(src && dst, "upcast: null pointer");
+  upcast_kernel<<<stream_grid(count), 256, 0, as_stream(stream)>>>(src, dst, count);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" size_t starm_ttm_f32_workspace_bytes(int64_t rows, int64_t inner, int64_t batch,
+                                                int64_t out_cols) {
+  if (rows < 1 || inner < 1 || batch < 1 || out_cols < 1) return 0;
+  return size_t(rows * batch * (inner + out_cols) + inner * out_cols) * sizeof(double) + 256;
+}
+
+extern "C" int starm_ttm_f32(const float* src, const float* mat, float* dst, int64_t rows,
+                             int64_t inner, int64_t batch, int64_t out_cols, void* ws,
+                             size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(rows >= 1 && inner >= 1 && batch >= 1 && out_cols >= 1,
+                  "ttm: extents must be positive (rows=%lld inner=%lld batch=%lld out_cols=%lld)",
+                  (long long)rows, (long long)inner, (long long)batch, (long long)out_cols);
+  STARM_CHECK_ARG(src && mat && dst && ws, "ttm: null pointer");
+  STARM_CHECK_ARG(ws_bytes >= starm_ttm_f32_workspace_bytes(rows, inner, batch, out_cols),
+                  "ttm f32: workspace too small");
+  const cudaStream_t st = as_stream(stream);
+  double* s64 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  double* d64 = s64 + rows * batch * inner;
+  double* m64 = d64 + rows * batch * out_cols;
+  upcast_kernel<<<stream_grid(rows * batch * inner), 256, 0, st>>>(src, s64, rows * batch * inner);
+  STARM_LAUNCH_CHECK();
+  upcast_kernel<<<stream_grid(inner * out_cols), 256, 0, st>>>(mat, m64, inner * out_cols);
+  STARM_LAUNCH_CHECK();
+  const int rc = starm_ttm_f64(s64, m64, d64, rows, inner, batch, out_cols, stream);
+  if (rc) return rc;
+  downcast_kernel<<<stream_grid(rows * batch * out_cols), 256, 0, st>>>(d64, dst, rows * batch * out_cols);
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }

@@ -175,7 +175,21 @@ class DeviceTensor:
 
     @classmethod
     def from_host(cls, t, device=None, non_blocking=False):
+        """Upload a DenseTensor or an array.  A float32 array crosses PCIe as
+        float32 and is upcast on the device (starm_upcast_f32_f64): the
+        reference's DenseTensor upcast (tensor.py:87) at half the H2D bytes."""
         import torch
+        if not isinstance(t, DenseTensor):
+            raw = np.asarray(t)
+            if raw.dtype == np.float32:
+                from . import _native as nat
+                dev = torch.device(device or "cuda")
+                h32 = torch.from_numpy(np.ascontiguousarray(raw.reshape(-1, order="F")))
+                d32 = h32.to(dev, non_blocking=non_blocking)
+                out = torch.empty(d32.numel(), dtype=torch.float64, device=dev)
+                nat.call("starm_upcast_f32_f64", d32.data_ptr(), out.data_ptr(), d32.numel(),
+                         nat.stream_ptr(dev))
+                return cls(out, raw.shape)
         arr = t.data if isinstance(t, DenseTensor) else np.asarray(t, dtype=np.float64).reshape(-1, order="F")
         dims = t.dims if isinstance(t, DenseTensor) else np.asarray(t).shape
         host = torch.from_numpy(np.ascontiguousarray(arr))
