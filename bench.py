@@ -74,6 +74,8 @@ def parse():
                     help="N>1: N independent tensors (weak scaling) instead of one sharded tensor")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded pipeline even at N=1 (world size 1 over NCCL)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (gloo on CPU): ranks join, plan checked, no compute")
     return ap.parse_args()
 
 
@@ -757,12 +759,36 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def run_dry(args):
+    """``--dry-run``: the launch plumbing alone on CPU (gloo): every rank
+    joins the group, the world size and the sharded plan are checked, rank 0
+    prints one JSON line.  No GPU and no compute."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_16058_b200.sharded import ShardPlan
+    rank, world, _ = dist_env()
+    dist.init_process_group("gloo")
+    dims = {"c1": (256, 256, 64), "c2": (361, 720, 1024), "c3": (1024, 1024, 512),
+            "c4": (512, 512, 2048), "c5": (8192, 64, 4096), "c5t": (8192, 64, 4096)}[args.config]
+    plan = ShardPlan(*dims, world, rank)
+    counts = torch.tensor([plan.nf, plan.ns], dtype=torch.int64)
+    dist.all_reduce(counts)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "world_size": dist.get_world_size(), "config": args.config,
+                          "fibres": int(counts[0]), "slices": int(counts[1]),
+                          "mode": "replicas" if args.replicas else "sharded"}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     _, world, _ = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args))
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.sharded or (world > 1 and not args.replicas):
         run_sharded(args)

@@ -309,9 +309,63 @@ def _finish(a, ts, factors, method, param, discarded, total, host):
     return CompressedTensor(tuple(a.dims), ts, factors, method, param, discarded, total)
 
 
+def _resolve_devices(devices):
+    """``devices`` of the drop-in entry points (SURVEY 8b "add devices="):
+    None -> the current CUDA device; an int / str / torch.device -> that
+    device; a torch.distributed ProcessGroup or the string "dist" (the
+    default group) -> the sharded multi-GPU pipeline over that group's ranks
+    (one process per GPU).  Returns (device or None, group or None)."""
+    import torch
+    if devices is None:
+        return None, None
+    if isinstance(devices, str) and devices == "dist":
+        import torch.distributed as dist
+        return None, dist.group.WORLD
+    if isinstance(devices, (int, str, torch.device)):
+        return nat.require_cuda(devices if not isinstance(devices, int) else f"cuda:{devices}"), None
+    if type(devices).__name__ == "ProcessGroup":
+        return None, devices
+    raise ValueError(f"devices must be None, a CUDA device, 'dist' or a ProcessGroup, got {devices!r}")
+
+
+def _sharded_call(a, ts, group, kind, param):
+    """SPMD drop-in over a process group: every rank passes the same (full)
+    host tensor, takes its fibre block, runs sharded.py's pipeline (fibre
+    transform, NCCL all-to-all to slice ownership, replicated threshold /
+    energies), and gets the full CompressedTensor (factors all-gathered)."""
+    import torch
+    import torch.distributed as dist
+    from .sharded import (DeviceOps, ShardPlan, gather_factors, scatter_fibres,
+                          tsvdm_fixed_rank_sharded, tsvdm_tolerance_sharded)
+    if len(a.dims) != 3 or len(ts) != 1:
+        raise ValueError("the sharded pipeline handles 3-way tensors (one transform)")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = nat.require_cuda()
+    m, p, n = a.dims
+    plan = ShardPlan(m, p, n, world, rank)
+    host = isinstance(a, DenseTensor)
+    arr = a.array if host else a.to_host().array
+    local = torch.from_numpy(scatter_fibres(arr, plan).reshape(-1, order="F").copy()).to(dev)
+    ops = DeviceOps(ts[0], dev)
+    if kind == METHOD_FIXED_RANK:
+        res = tsvdm_fixed_rank_sharded(local, plan, ops, int(param), dist, group)
+    else:
+        res = tsvdm_tolerance_sharded(local, plan, ops, float(param), dist, group)
+    u, g = gather_factors(res, plan, dist, group)
+    ranks = torch.from_numpy(np.ascontiguousarray(res.ranks)).to(dev)
+    u_off, g_off = pack_offsets_device(ranks, m, p)
+    total = int(res.ranks.sum())
+    factors = DeviceFactors(m, p, ranks, u_off, g_off, u, g, total)
+    factors._host_ranks = np.asarray(res.ranks, dtype=np.int64)
+    return _finish(a, ts, factors, kind, float(param), res.discarded_energy, res.total_energy,
+                   host)
+
+
 def tsvdm_fixed_rank(a, ts: TransformSet, rank, threads=1, svd_strategy=SLICES_PARALLEL,
-                     ttm_variant=BATCHED) -> CompressedTensor:
-    """Uniform rank per slice (tsvdm.py:246-265)."""
+                     ttm_variant=BATCHED, devices=None) -> CompressedTensor:
+    """Uniform rank per slice (tsvdm.py:246-265).  ``devices``: see
+    _resolve_devices (a process group runs the sharded multi-GPU pipeline)."""
     import torch
     _check_decomposable(a)
     ts.check_dims(a.dims)
@@ -320,8 +374,11 @@ def tsvdm_fixed_rank(a, ts: TransformSet, rank, threads=1, svd_strategy=SLICES_P
     if not 1 <= rank <= min(m, p):
         raise ValueError(f"rank must lie in [1, {min(m, p)}], got {rank}")
     _check_common(threads, svd_strategy, ttm_variant)
+    want, group = _resolve_devices(devices)
+    if group is not None:
+        return _sharded_call(a, ts, group, METHOD_FIXED_RANK, rank)
     host = isinstance(a, DenseTensor)
-    dev = nat.require_cuda() if host else a.device
+    dev = (want or nat.require_cuda()) if host else a.device
     n = prod(a.dims[2:])
     r = min(m, p)
     ahat = forward_device(as_device(a, dev), ts)
@@ -336,12 +393,13 @@ def tsvdm_fixed_rank(a, ts: TransformSet, rank, threads=1, svd_strategy=SLICES_P
 
 
 def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, threads=1,
-                    svd_strategy=SLICES_PARALLEL, ttm_variant=BATCHED, clock=None):
+                    svd_strategy=SLICES_PARALLEL, ttm_variant=BATCHED, clock=None, devices=None):
     """Global-threshold ranks (tsvdm.py:268-321).  All three strategies give
     identical ranks and factors; on the device ``memory-efficient`` and
     ``compute-efficient`` are the same two-pass schedule (the transform-domain
     tensor already stays resident in HBM), ``truncate`` factors every slice
-    fully and packs from the full factors."""
+    fully and packs from the full factors.  ``devices``: see _resolve_devices
+    (a process group runs the sharded multi-GPU pipeline)."""
     import torch
     _check_decomposable(a)
     ts.check_dims(a.dims)
@@ -352,8 +410,11 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
         raise ValueError(f"unknown tolerance strategy {strategy!r}")
     _check_common(threads, svd_strategy, ttm_variant)
     clock = clock if clock is not None else StageClock()
+    want, group = _resolve_devices(devices)
+    if group is not None:
+        return _sharded_call(a, ts, group, METHOD_TOLERANCE, epsilon)
     host = isinstance(a, DenseTensor)
-    dev = nat.require_cuda() if host else a.device
+    dev = (want or nat.require_cuda()) if host else a.device
     m, p = a.dims[0], a.dims[1]
     n = prod(a.dims[2:])
     r = min(m, p)

@@ -1,0 +1,123 @@
+"""GPU parity of the C-ABI entry points added for SURVEY 8(b): the fused
+reconstruction + error (starm_reconstruct_f64, K9 + inverse transform +
+K10; reference tsvdm.py:342-357 and tests/helpers.py:44-47), the float32
+twins (starm_ttm_f32, starm_upcast_f32_f64; reference ttm.py:113-135 and the
+tensor.py:87 upcast)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2605_16058_b200 as sb
+from paper_2605_16058_b200 import _native as nat
+from helpers import random_array, random_orthonormal, rel_error
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_reconstruct(c, mats):
+    f = c.factors.to_host() if hasattr(c.factors, "to_host") else c.factors
+    return oracle.reconstruct_packed(c.dims, mats, f.ranks, f.u_data, f.g_data)
+
+
+@pytest.mark.parametrize("kind,dims,eps", [("dct", (30, 44, 64), 0.3), ("dct", (20, 33, 512), 0.2),
+                                           ("custom", (25, 18, 40), 0.1),
+                                           ("custom", (16, 40, 24), 0.02)])
+def test_fused_reconstruct_matches_reference(kind, dims, eps):
+    a = random_array(dims, 3 + dims[2])
+    a += 4.0 * np.einsum("i,j,k->ijk", *(np.random.default_rng(1).standard_normal(d) for d in dims))
+    t = sb.DenseTensor(a)
+    if kind == "dct":
+        ts = sb.TransformSet.build(dims, "dct")
+    else:
+        ts = sb.TransformSet((sb.validate_transform(random_orthonormal(dims[2], 9)),))
+    mats = [tr.matrix for tr in ts]
+    x = sb.DeviceTensor.from_host(t)
+    c = sb.tsvdm_tolerance(x, ts, eps)
+    rec, err = sb.reconstruct_fused(c, a=x)
+    ref = _ref_reconstruct(c, mats)
+    assert rel_error(ref, rec.to_host().array) <= 1e-12
+    ref_err = rel_error(a, ref)
+    assert abs(err - ref_err) <= 1e-10 * max(ref_err, 1e-300)
+    assert abs(err - c.relative_error()) <= 1e-8
+    # the public reconstruct routes through it for small nnz and agrees
+    rec2 = sb.reconstruct(c.to_host())
+    assert rel_error(ref, rec2.array) <= 1e-12
+
+
+def test_fused_reconstruct_all_ranks_zero_and_explicit_inverse():
+    dims = (12, 9, 16)
+    a = random_array(dims, 4)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet((sb.validate_transform(random_orthonormal(16, 2)),))
+    x = sb.DeviceTensor.from_host(t)
+    c = sb.tsvdm_tolerance(x, ts, 0.999)
+    if c.factors.total_rank == 0:
+        rec, err = sb.reconstruct_fused(c, a=x)
+        assert not rec.to_host().array.any() and abs(err - 1.0) <= 1e-15
+    # explicit non-orthonormal inverse (the config-4 restatement): out = M^-1 x3 Chat
+    rng = np.random.default_rng(5)
+    mm = np.eye(16) + 0.1 * rng.standard_normal((16, 16)) / 4
+    minv = np.linalg.inv(mm)
+    c2 = sb.tsvdm_fixed_rank(x, ts, 3)
+    rec, _ = sb.reconstruct_fused(c2, minv=minv)
+    f = c2.factors.to_host()
+    chat = oracle.reconstruct_packed(dims, [np.eye(16)], f.ranks, f.u_data, f.g_data)
+    assert rel_error(oracle.ttm(chat, 2, minv), rec.to_host().array) <= 1e-12
+
+
+def test_fused_reconstruct_c2_shaped():
+    """c2-like fibres (DCT over 1024 time steps): the K = nnz dense product
+    with the reference's own M^T columns."""
+    from paper_2605_16058_b200 import configs as cf
+    a = cf.config2(nlat=46, nlon=90, nt=1024, seed=1)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    x = sb.DeviceTensor.from_host(t)
+    c = sb.tsvdm_tolerance(x, ts, 1e-2)
+    nnz = int((c.factors.to_host().ranks > 0).sum())
+    assert 0 < nnz
+    rec, err = sb.reconstruct_fused(c, a=x)
+    ref = _ref_reconstruct(c, [tr.matrix for tr in ts])
+    assert rel_error(ref, rec.to_host().array) <= 1e-12
+    assert abs(err - rel_error(a, ref)) <= 1e-10 * err
+    assert abs(err - c.relative_error()) <= 1e-8 and err <= 1e-2
+
+
+@pytest.mark.parametrize("rows,inner,batch,out_cols", [(7, 5, 1, 3), (64, 33, 3, 40),
+                                                        (1000, 128, 2, 128)])
+def test_ttm_f32_twin(rows, inner, batch, out_cols):
+    import torch
+    rng = np.random.default_rng(rows)
+    src = rng.standard_normal(rows * inner * batch).astype(np.float32)
+    mat = rng.standard_normal((out_cols, inner)).astype(np.float32)
+    lib = nat.load()
+    nbytes = lib.starm_ttm_f32_workspace_bytes(rows, inner, batch, out_cols)
+    ws = nat.workspace(nbytes, "cuda")
+    xs = torch.from_numpy(src).cuda()
+    xm = torch.from_numpy(np.ascontiguousarray(mat)).cuda()
+    out = torch.empty(rows * out_cols * batch, dtype=torch.float32, device="cuda")
+    nat.call("starm_ttm_f32", xs.data_ptr(), xm.data_ptr(), out.data_ptr(), rows, inner, batch,
+             out_cols, ws.data_ptr(), nbytes, nat.stream_ptr())
+    got = out.cpu().numpy()
+    # reference: f32 operands upcast (tensor.py:87), f64 product, one rounding to f32
+    ref = np.concatenate([
+        (mat.astype(np.float64) @ src[b * rows * inner:(b + 1) * rows * inner].astype(np.float64)
+         .reshape(inner, rows)).ravel() for b in range(batch)])
+    assert np.max(np.abs(got - ref.astype(np.float32))) <= 1e-6 * np.max(np.abs(ref))
+    assert rel_error(ref, got.astype(np.float64)) <= 1e-7
+
+
+def test_float32_input_upcast_on_device():
+    a32 = np.asfortranarray(np.random.default_rng(2).standard_normal((17, 9, 5)).astype(np.float32))
+    x = sb.DeviceTensor.from_host(a32)
+    assert x.dims == a32.shape
+    assert np.array_equal(x.to_host().array, a32.astype(np.float64))
+    # same result as the host upcast of the reference's DenseTensor
+    ts = sb.TransformSet.build(a32.shape, "dct")
+    c1 = sb.tsvdm_tolerance(x, ts, 0.3)
+    c2 = sb.tsvdm_tolerance(sb.DenseTensor(a32), ts, 0.3)
+    assert np.array_equal(c1.to_host().ranks, c2.ranks)
+    assert c1.discarded_energy == c2.discarded_energy

@@ -60,3 +60,38 @@ def test_sharded_device_ops_match_tsvdm_tolerance(nccl_world1, dims, eps):
     err = relative_error_sharded(local, rec, dist)
     assert abs(err - res.relative_error) <= 1e-10
     assert err < eps
+
+
+def test_dropin_devices_group_matches_single_gpu(nccl_world1):
+    """devices="dist" on the drop-in entry points runs the sharded pipeline
+    (SPMD over the default process group) and returns the same
+    CompressedTensor as the single-device call."""
+    dims = (33, 20, 48)
+    rng = np.random.default_rng(7)
+    a = np.asfortranarray(rng.standard_normal(dims))
+    a += np.einsum("i,j,k->ijk", rng.standard_normal(33), rng.standard_normal(20),
+                   rng.standard_normal(48)) * 3
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(dims, "dct")
+    for call in (lambda **kw: sb.tsvdm_tolerance(t, ts, 0.1, **kw),
+                 lambda **kw: sb.tsvdm_fixed_rank(t, ts, 4, **kw)):
+        ref = call()
+        got = call(devices="dist")
+        assert np.array_equal(got.ranks, ref.ranks)
+        assert abs(got.discarded_energy - ref.discarded_energy) <= 1e-12 * ref.total_energy
+        assert abs(got.total_energy - ref.total_energy) <= 1e-12 * ref.total_energy
+        assert got.factors.u_data.shape == ref.factors.u_data.shape
+        rec = sb.reconstruct(got)
+        err = float(np.linalg.norm(rec.data - t.data) / np.linalg.norm(t.data))
+        assert abs(err - got.relative_error()) <= 1e-8
+
+
+def test_dropin_devices_explicit_device():
+    dims = (10, 12, 8)
+    a = np.asfortranarray(np.random.default_rng(1).standard_normal(dims))
+    ts = sb.TransformSet.build(dims, "dct")
+    ref = sb.tsvdm_tolerance(sb.DenseTensor(a), ts, 0.2)
+    got = sb.tsvdm_tolerance(sb.DenseTensor(a), ts, 0.2, devices=0)
+    assert np.array_equal(got.ranks, ref.ranks)
+    with pytest.raises(ValueError):
+        sb.tsvdm_tolerance(sb.DenseTensor(a), ts, 0.2, devices=[0, 1])

@@ -216,3 +216,10 @@ def test_no_cpu_fallback():
         sb.tsvdm_tolerance(t, ts, 0.1)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sb.ttm(t, 2, np.eye(3))
+
+
+def test_devices_argument_validation():
+    from paper_2605_16058_b200.compress import _resolve_devices
+    assert _resolve_devices(None) == (None, None)
+    with pytest.raises(ValueError, match="devices"):
+        _resolve_devices(3.5)
