@@ -118,6 +118,13 @@ int starm_dct_f64(const double* src, double* dst, int64_t rows, int64_t n, int64
  * because |Delta| is ~1e-14.  n must be a multiple of 256; ws and
  * delta_bf16 128-byte aligned; ws of starm_ttm_residual_workspace_bytes. */
 size_t starm_ttm_residual_workspace_bytes(int64_t rows, int64_t n, int64_t batch);
+/* The reference's DCT operator in one call: starm_dct_f64 followed by
+ * starm_ttm_residual_bf16 (inverse = 1 takes Delta^T as delta_bf16).  For
+ * n = 1024 forward the FFT kernel writes the bf16 operand itself, so the
+ * input is read once.  Same workspace as starm_ttm_residual_bf16. */
+int starm_dct_residual_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
+                           int inverse, const uint16_t* delta_bf16, int log2_scale, void* ws,
+                           size_t ws_bytes, void* stream);
 int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int log2_scale,
                             double* dst, int64_t rows, int64_t n, int64_t batch, void* ws,
                             size_t ws_bytes, void* stream);

@@ -68,6 +68,8 @@ SIGNATURES = {
     "starm_ttm_f32": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
                               c_void_p, c_size_t, c_void_p]),
     "starm_upcast_f32_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "starm_dct_residual_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int,
+                                       c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
     "starm_launch_count_reset": (ctypes.c_longlong, []),
     "starm_svd_tune": (c_int, [c_int, c_int, c_int, c_int]),
     "starm_svd_stats": (c_int, [c_void_p, c_int]),

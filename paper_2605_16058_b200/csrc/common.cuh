@@ -45,6 +45,11 @@ void count_launch(int n = 1);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// dct.cu: the fast DCT-II / DCT-III; with xbf the n = 1024 forward kernel
+// also writes the bf16 operand rows of the residual GEMM (*packed = true).
+int dct_launch(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch, bool inv,
+               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st);
+
 // gemm_f64.cu: C = A * B (batch 1, column-major) with the K10 error partials
 // of E against C fused into the epilogue (epart: 2 doubles per tile).
 int64_t gemm_f64_tiles(int64_t M, int64_t N);

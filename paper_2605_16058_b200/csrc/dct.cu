@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace starm {
@@ -326,10 +328,15 @@ __device__ __forceinline__ void fft32_dif(cplx (&z)[32]) {
 // staged tile, and IDFT(z) = conj(DFT(conj z)) / N runs through the same
 // four-step DFT; position pos of the result goes to time 2 pos (pos < N/2)
 // or 2N - 1 - 2 pos.
+// xbf (optional, forward only): also write the tile's input fibres as bf16
+// rows [b * rows_pad + fibre][t] -- the K-major operand of the reference-
+// operator residual GEMM (residual_bf16.cu), so that kernel need not re-read
+// the f64 input.
 template <bool INV>
 __global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
     const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
-    const cplx* __restrict__ gtw, const cplx* __restrict__ gpw, int vec16) {
+    const cplx* __restrict__ gtw, const cplx* __restrict__ gpw, int vec16,
+    uint16_t* __restrict__ xbf, int64_t rows_pad) {
   constexpr int N = D32_N, F = 2 * D32_WARPS, NT = 32 * D32_WARPS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* ch = reinterpret_cast<cplx*>(smem_raw);
@@ -371,6 +378,24 @@ __global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
   }
   cp_async_wait<0>();
   __syncthreads();
+  if (!INV && xbf) {
+    // warp w packs its own pair (fibres 2w, 2w + 1): lane -> time pair
+    // (2 tp, 2 tp + 1), one 4-byte store per fibre (128-byte runs per warp);
+    // ck(2 tp, w) = 9 tp + w keeps the 16-byte reads conflict-free
+    uint32_t* xo = reinterpret_cast<uint32_t*>(xbf);
+    const int64_t rb = b * rows_pad + r0 + 2 * w;
+#pragma unroll 4
+    for (int tp = lane; tp < N / 2; tp += 32) {
+      const cplx u = ch[ck(2 * tp, w)], v = ch[ck(2 * tp + 1, w)];
+      auto pk = [](double lo, double hi) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(float(fmin(fmax(lo, -3.0e38), 3.0e38)),
+                                                       float(fmin(fmax(hi, -3.0e38), 3.0e38)));
+        return *reinterpret_cast<const uint32_t*>(&h);
+      };
+      if (2 * w < nf) xo[(rb * N) / 2 + tp] = pk(u.re, v.re);
+      if (2 * w + 1 < nf) xo[((rb + 1) * N) / 2 + tp] = pk(u.im, v.im);
+    }
+  }
   const double c0 = sqrt(1.0 / N), c1 = sqrt(2.0 / N);
   const cplx pl = gpw[lane];
   // pass 1: lane t1 holds z[t1 + 32 t2]
@@ -499,7 +524,7 @@ int dct_tables(int logn, const cplx** tw, const cplx** pw, cudaStream_t st) {
 
 template <int LOGN>
 int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool inverse,
-               cudaStream_t st) {
+               cudaStream_t st, uint16_t* xbf = nullptr, int64_t rows_pad = 0) {
   constexpr int N = 1 << LOGN;
   constexpr int P = dct_pairs(LOGN);
   const size_t smem = (size_t(P) * (N + ZPAD) + N / 2) * sizeof(cplx);
@@ -522,7 +547,8 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
     // each lane's 32 values straight from global memory (no staging) 2.4 ms
     auto kern = inverse ? dct1024_kernel<true> : dct1024_kernel<false>;
     STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)));
-    kern<<<unsigned(t2), 32 * D32_WARPS, sm2, st>>>(src, dst, rows, tw, pw, vec16);
+    kern<<<unsigned(t2), 32 * D32_WARPS, sm2, st>>>(src, dst, rows, tw, pw, vec16,
+                                                    inverse ? nullptr : xbf, rows_pad);
     STARM_LAUNCH_CHECK();
     return STARM_OK;
   }
@@ -534,6 +560,30 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
 }
 
 }  // namespace
+}  // namespace starm
+
+namespace starm {
+// Internal launcher (also used by starm_dct_residual_f64): when xbf is set
+// and the n = 1024 forward kernel runs, the bf16 operand rows are written
+// too; returns whether that happened through *packed.
+int dct_launch(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch, bool inv,
+               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st) {
+  if (packed) *packed = xbf && n == 1024 && !inv && !g_dct_legacy;
+  switch (n) {
+    case 2: return launch_dct<1>(src, dst, rows, batch, inv, st);
+    case 4: return launch_dct<2>(src, dst, rows, batch, inv, st);
+    case 8: return launch_dct<3>(src, dst, rows, batch, inv, st);
+    case 16: return launch_dct<4>(src, dst, rows, batch, inv, st);
+    case 32: return launch_dct<5>(src, dst, rows, batch, inv, st);
+    case 64: return launch_dct<6>(src, dst, rows, batch, inv, st);
+    case 128: return launch_dct<7>(src, dst, rows, batch, inv, st);
+    case 256: return launch_dct<8>(src, dst, rows, batch, inv, st);
+    case 512: return launch_dct<9>(src, dst, rows, batch, inv, st);
+    case 1024: return launch_dct<10>(src, dst, rows, batch, inv, st, xbf, rows_pad);
+    case 2048: return launch_dct<11>(src, dst, rows, batch, inv, st);
+    default: return launch_dct<12>(src, dst, rows, batch, inv, st);
+  }
+}
 }  // namespace starm
 
 using namespace starm;
@@ -549,18 +599,5 @@ extern "C" int starm_dct_f64(const double* src, double* dst, int64_t rows, int64
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool inv = inverse != 0;
-  switch (n) {
-    case 2: return launch_dct<1>(src, dst, rows, batch, inv, st);
-    case 4: return launch_dct<2>(src, dst, rows, batch, inv, st);
-    case 8: return launch_dct<3>(src, dst, rows, batch, inv, st);
-    case 16: return launch_dct<4>(src, dst, rows, batch, inv, st);
-    case 32: return launch_dct<5>(src, dst, rows, batch, inv, st);
-    case 64: return launch_dct<6>(src, dst, rows, batch, inv, st);
-    case 128: return launch_dct<7>(src, dst, rows, batch, inv, st);
-    case 256: return launch_dct<8>(src, dst, rows, batch, inv, st);
-    case 512: return launch_dct<9>(src, dst, rows, batch, inv, st);
-    case 1024: return launch_dct<10>(src, dst, rows, batch, inv, st);
-    case 2048: return launch_dct<11>(src, dst, rows, batch, inv, st);
-    default: return launch_dct<12>(src, dst, rows, batch, inv, st);
-  }
+  return dct_launch(src, dst, rows, n, batch, inv, nullptr, 0, nullptr, st);
 }

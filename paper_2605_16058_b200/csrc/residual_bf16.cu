@@ -366,34 +366,21 @@ extern "C" size_t starm_ttm_residual_workspace_bytes(int64_t rows, int64_t n, in
   return size_t(rows_padded(rows)) * size_t(n) * size_t(batch) * 2;
 }
 
-extern "C" int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int log2_scale,
-                                       double* dst, int64_t rows, int64_t n, int64_t batch,
-                                       void* ws, size_t ws_bytes, void* stream) {
-  STARM_CHECK_ARG(rows >= 0 && n >= 0 && batch >= 0, "ttm residual: negative extent");
-  if (rows == 0 || batch == 0 || n == 0) return STARM_OK;
-  STARM_CHECK_ARG(src && delta_bf16 && dst && ws, "ttm residual: null pointer");
-  STARM_CHECK_ARG(src != dst, "ttm residual: src and dst alias");
-  if (n % RB_N != 0) {
-    set_error("ttm residual: n = %lld must be a multiple of %d", (long long)n, RB_N);
-    return STARM_UNSUPPORTED;
-  }
-  STARM_CHECK_ARG(ws_bytes >= starm_ttm_residual_workspace_bytes(rows, n, batch),
-                  "ttm residual: workspace too small");
-  STARM_CHECK_ARG((reinterpret_cast<uintptr_t>(ws) & 127) == 0 &&
-                      (reinterpret_cast<uintptr_t>(delta_bf16) & 127) == 0,
-                  "ttm residual: workspace and Delta must be 128-byte aligned");
+namespace starm {
+namespace {
+// Pack (unless the DCT kernel already wrote the bf16 rows) + tcgen05 GEMM.
+int residual_run(const double* pack_src, const uint16_t* delta_bf16, int log2_scale, double* dst,
+                 int64_t rows, int64_t n, int64_t batch, void* ws, cudaStream_t st) {
   const int64_t rows_pad = rows_padded(rows);
   const int64_t total_rows = rows_pad * batch;
-  STARM_CHECK_ARG(total_rows < (int64_t(1) << 31) && n <= 65536,
+  STARM_CHECK_ARG(total_rows < (int64_t(1) << 31) && n <= 65536 && batch <= 65535,
                   "ttm residual: tensor too large for one launch");
-  const cudaStream_t st = as_stream(stream);
   int rc = get_encoder();
   if (rc) return rc;
-
-  {
+  if (pack_src) {
     dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), unsigned(batch));
-    STARM_CHECK_ARG(batch <= 65535, "ttm residual: batch too large");
-    residual_pack_kernel<<<grid, 256, 0, st>>>(src, static_cast<uint16_t*>(ws), rows, n, rows_pad);
+    residual_pack_kernel<<<grid, 256, 0, st>>>(pack_src, static_cast<uint16_t*>(ws), rows, n,
+                                               rows_pad);
     STARM_LAUNCH_CHECK();
   }
   CUtensorMap map_x, map_d;
@@ -401,7 +388,6 @@ extern "C" int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_
   if (rc) return rc;
   rc = make_map(&map_d, delta_bf16, uint64_t(n), uint64_t(n), RB_K, RB_N);
   if (rc) return rc;
-
   int dev = 0, sms = 148;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
   STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -421,4 +407,51 @@ extern "C" int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_
   residual_gemm_kernel<<<unsigned(grid), RB_THREADS, RB_SMEM, st>>>(map_x, map_d, g);
   STARM_LAUNCH_CHECK();
   return STARM_OK;
+}
+
+int residual_args(const double* src, const uint16_t* delta_bf16, double* dst, int64_t n, void* ws,
+                  size_t ws_bytes, int64_t rows, int64_t batch) {
+  STARM_CHECK_ARG(src && delta_bf16 && dst && ws, "ttm residual: null pointer");
+  STARM_CHECK_ARG(src != dst, "ttm residual: src and dst alias");
+  if (n % RB_N != 0) {
+    set_error("ttm residual: n = %lld must be a multiple of %d", (long long)n, RB_N);
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG(ws_bytes >= size_t(rows_padded(rows)) * size_t(n) * size_t(batch) * 2,
+                  "ttm residual: workspace too small");
+  STARM_CHECK_ARG((reinterpret_cast<uintptr_t>(ws) & 127) == 0 &&
+                      (reinterpret_cast<uintptr_t>(delta_bf16) & 127) == 0,
+                  "ttm residual: workspace and Delta must be 128-byte aligned");
+  return STARM_OK;
+}
+}  // namespace
+}  // namespace starm
+
+extern "C" int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int log2_scale,
+                                       double* dst, int64_t rows, int64_t n, int64_t batch,
+                                       void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(rows >= 0 && n >= 0 && batch >= 0, "ttm residual: negative extent");
+  if (rows == 0 || batch == 0 || n == 0) return STARM_OK;
+  const int rc = residual_args(src, delta_bf16, dst, n, ws, ws_bytes, rows, batch);
+  if (rc) return rc;
+  return residual_run(src, delta_bf16, log2_scale, dst, rows, n, batch, ws, as_stream(stream));
+}
+
+extern "C" int starm_dct_residual_f64(const double* src, double* dst, int64_t rows, int64_t n,
+                                      int64_t batch, int inverse, const uint16_t* delta_bf16,
+                                      int log2_scale, void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(rows >= 0 && n >= 0 && batch >= 0, "dct residual: negative extent");
+  if (rows == 0 || batch == 0 || n == 0) return STARM_OK;
+  int rc = residual_args(src, delta_bf16, dst, n, ws, ws_bytes, rows, batch);
+  if (rc) return rc;
+  if ((n & (n - 1)) != 0 || n > 4096) {
+    set_error("dct residual: the fast path needs a power-of-two length in [256, 4096]");
+    return STARM_UNSUPPORTED;
+  }
+  const cudaStream_t st = as_stream(stream);
+  bool packed = false;
+  rc = dct_launch(src, dst, rows, n, batch, inverse != 0, static_cast<uint16_t*>(ws),
+                  rows_padded(rows), &packed, st);
+  if (rc) return rc;
+  return residual_run(packed ? nullptr : src, delta_bf16, log2_scale, dst, rows, n, batch, ws, st);
 }

@@ -3417,6 +3417,10 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
                             : occupancy((const void*)svd_reduce_kernel<256>, 256, g.rsmem, &per);
     if (rc) return rc;
     g.slots_r = clampc(int64_t(sms) * per);
+    if (const char* e = getenv("STARM_REDUCE_SLOTS")) {  // experiment: fewer slices in flight
+      const int v = atoi(e);
+      if (v >= 1 && v < g.slots_r) g.slots_r = v;
+    }
     rc = occupancy(g.hb_gmem ? (const void*)svd_bulge_kernel<true> : (const void*)svd_bulge_kernel<false>,
                    g.hb_threads, g.bsmem, &per);
     if (rc) return rc;

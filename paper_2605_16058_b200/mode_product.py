@@ -137,20 +137,21 @@ def structured_device(x: DeviceTensor, mode: int, kind: str, inverse: bool,
         out.data.copy_(x.data)
         return out
     st = nat.stream_ptr(x.device)
-    nat.call("starm_dct_f64", x.data.data_ptr(), out.data.data_ptr(), plan.rows, plan.inner,
-             plan.batch, int(bool(inverse)), st)
-    if tr is not None and os.environ.get("STARM_EXACT_DCT", "0") != "1":
-        op = tr.residual_operand(x.device, transpose=inverse)
-        if op is None:
-            raise ValueError("transform has no DCT residual operand")
-        delta, e = op
-        lib = nat.load()
-        nbytes = lib.starm_ttm_residual_workspace_bytes(plan.rows, plan.inner, plan.batch)
-        ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=x.device)
-        base = ws.data_ptr()
-        base += (-base) % 128
-        nat.call("starm_ttm_residual_bf16", x.data.data_ptr(), delta.data_ptr(), int(e),
-                 out.data.data_ptr(), plan.rows, plan.inner, plan.batch, base, nbytes, st)
+    if tr is None or os.environ.get("STARM_EXACT_DCT", "0") == "1":
+        nat.call("starm_dct_f64", x.data.data_ptr(), out.data.data_ptr(), plan.rows, plan.inner,
+                 plan.batch, int(bool(inverse)), st)
+        return out
+    op = tr.residual_operand(x.device, transpose=inverse)
+    if op is None:
+        raise ValueError("transform has no DCT residual operand")
+    delta, e = op
+    lib = nat.load()
+    nbytes = lib.starm_ttm_residual_workspace_bytes(plan.rows, plan.inner, plan.batch)
+    ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=x.device)
+    base = ws.data_ptr()
+    base += (-base) % 128
+    nat.call("starm_dct_residual_f64", x.data.data_ptr(), out.data.data_ptr(), plan.rows,
+             plan.inner, plan.batch, int(bool(inverse)), delta.data_ptr(), int(e), base, nbytes, st)
     return out
 
 
