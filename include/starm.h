@@ -7,6 +7,11 @@
  * numpy/LAPACK calls each one names.  The Python package
  * paper_2605_16058_b200 binds them with ctypes.
  *
+ * Collectives: the multi-GPU split (paper_2605_16058_b200/sharded.py) runs
+ * its all-to-all / all-gathers through torch.distributed over NCCL; no entry
+ * point here takes an ncclComm_t.  Every kernel below operates on the
+ * calling rank's buffers only.
+ *
  * Conventions
  *  - All pointers are DEVICE pointers unless stated otherwise; the caller
  *    allocates every buffer (outputs and workspace) and owns it.  Nothing

@@ -19,6 +19,7 @@ c = sb.tsvdm_tolerance(x, ts, 1e-2)
 s = sb.svd_values_only(sb.to_transform_domain(x, ts))
 ranks = np.asarray(c.ranks)
 os.makedirs("gpurun_out", exist_ok=True)
+f = c.factors.to_host()
 np.savez("gpurun_out/c2_gpu.npz", s=s.cpu().numpy(), ranks=np.asarray(ranks),
-         discarded=c.discarded_energy, total=c.total_energy)
+         discarded=c.discarded_energy, total=c.total_energy, u_data=f.u_data, g_data=f.g_data)
 print("dumped", int(np.sum(ranks)), c.relative_error())
