@@ -204,6 +204,26 @@ int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, double epsi
                         double* v_out, double* w_out, int64_t* ranks_out, double* scal_out,
                         int64_t* j_out, void* ws, size_t ws_bytes, void* stream);
 
+/* Pruned form of the same threshold for tsvdm_tolerance: `s` holds the
+ * singular values of a SUBSET of the slices; the left-out slices have total
+ * energy e0 and every one of their sigma^2 is <= tbound (callers use the
+ * slice's Frobenius norm squared, starm_slice_energy_f64).  The running sum
+ * starts at e0, total = e0 + sum of the subset's squares, discarded
+ * includes e0.  cert_out (device int32) = 1 when the crossing value v[j]
+ * exceeds tbound: then every value <= tbound is discarded by the reference's
+ * rule whatever its exact size, so the left-out slices have rank 0 and the
+ * subset's ranks are the reference's.  cert_out = 0: recompute unpruned.
+ * Same workspace as starm_threshold_f64 for (r, nslices). */
+int starm_threshold_pruned_f64(const double* s, int64_t r, int64_t nslices, double epsilon,
+                               double e0, double tbound, int64_t* ranks_out, double* scal_out,
+                               int64_t* j_out, int32_t* cert_out, void* ws, size_t ws_bytes,
+                               void* stream);
+
+/* Per-slice energy f[i] = ||slice i||_F^2 (slice_elems contiguous doubles per
+ * slice), deterministic: the bound sigma_max^2 <= f used for pruning. */
+int starm_slice_energy_f64(const double* a, int64_t slice_elems, int64_t nslices, double* f_out,
+                           void* stream);
+
 /* ---------------------------------------------------------- K8 offsets
  * slicesvd.py:208-211: u_off[0]=g_off[0]=0, u_off[i+1] = u_off[i] +
  * ranks[i]*m, g_off likewise with p.  Arrays hold nslices+1 int64. */

@@ -70,6 +70,10 @@ SIGNATURES = {
     "starm_upcast_f32_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "starm_dct_residual_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int,
                                        c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
+    "starm_threshold_pruned_f64": (c_int, [c_void_p, c_int64, c_int64, c_double, c_double,
+                                           c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                                           c_void_p, c_size_t, c_void_p]),
+    "starm_slice_energy_f64": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "starm_launch_count_reset": (ctypes.c_longlong, []),
     "starm_svd_tune": (c_int, [c_int, c_int, c_int, c_int]),
     "starm_svd_stats": (c_int, [c_void_p, c_int]),

@@ -13,6 +13,7 @@ copied back once.
 from __future__ import annotations
 
 import math
+import os
 import time
 from contextlib import contextmanager
 from dataclasses import dataclass
@@ -53,6 +54,7 @@ class StageClock:
     def __init__(self):
         self._host = {}
         self._events = {}
+        self.info = {}   # non-timing facts of the call (e.g. pruned slice count)
 
     @contextmanager
     def stage(self, name):
@@ -438,6 +440,10 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
             factors = DeviceFactors(m, p, ranks, u_off, g_off, u_data[: total_rank * m],
                                     g_data[: total_rank * p], total_rank)
     else:
+        pruned = _tolerance_pruned(ahat3, epsilon, strategy, clock) if PRUNE else None
+        if pruned is not None:
+            factors, discarded, total = pruned
+            return _finish(a, ts, factors, METHOD_TOLERANCE, epsilon, discarded, total, host)
         # Keep every slice's factorisation in HBM between the passes when it
         # fits comfortably (always for compute-efficient); otherwise refactor
         # the rank>0 slices (memory-efficient in the reference's sense).
@@ -515,6 +521,109 @@ def tsvdm_tolerance_stream(tensors, ts: TransformSet, epsilon, strategy=MEMORY_E
         free[b] = ev
         yield c.to_host()
         cur, b = nxt, 1 - b
+
+
+PRUNE = os.environ.get("STARM_PRUNE", "1") != "0"   # STARM_PRUNE=0: diagnostic, unpruned
+PRUNE_GAMMA = 0.3      # left-out energy target as a fraction of the budget
+PRUNE_MIN = 0.25       # prune only when at least this fraction of the slices drops out
+
+
+def prune_select(ahat3, epsilon):
+    """The slice selection of the pruned tolerance path: per-slice energies f
+    (starm_slice_energy_f64, one 8N-byte D2H), the slices of smallest f whose
+    total stays below PRUNE_GAMMA * eps^2 * sum(f) are left out.  Returns
+    (kept slice ids ascending, e0 = left-out energy, tbound = largest left-out
+    f) or None when too few slices would drop out or f is not finite."""
+    import torch
+    m, p, n = ahat3.dims
+    dev = ahat3.device
+    f_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    nat.call("starm_slice_energy_f64", ahat3.data.data_ptr(), m * p, n, f_dev.data_ptr(),
+             nat.stream_ptr(dev))
+    f = f_dev.cpu().numpy()
+    if not np.isfinite(f).all():
+        return None                      # the SVD names the non-finite slice
+    budget = epsilon * epsilon * math.fsum(f.tolist())
+    order = np.argsort(f, kind="stable")
+    k = int(np.searchsorted(np.cumsum(f[order]), PRUNE_GAMMA * budget, side="right"))
+    if k < PRUNE_MIN * n or k >= n:
+        return None
+    keep_ids = np.sort(order[k:])
+    return keep_ids, math.fsum(f[np.sort(order[:k])].tolist()), float(f[order[k - 1]])
+
+
+def _tolerance_pruned(ahat3, epsilon, strategy, clock):
+    """Certified slice pruning for tsvdm_tolerance (same ranks, factors and
+    energies as the unpruned path, which the reference computes).
+
+    Every sigma^2 of slice i is at most f_i = ||Ahat_i||_F^2.  Leave out the
+    slices of smallest f whose total energy e0 stays below PRUNE_GAMMA of the
+    budget eps^2 * sum(f); t = their largest f.  The values pass, threshold
+    and truncated pass then run on the remaining slices only, with the
+    threshold's running sum started at e0 (starm_threshold_pruned_f64).  If
+    the crossing value lies above t, every value <= t -- in particular every
+    left-out sigma^2 -- is discarded by compute_threshold's rule
+    (tsvdm.py:85-115) whatever its exact size: the left-out slices have rank
+    0, the others get the reference's ranks, the discarded energy is e0 plus
+    their dropped squares.  Otherwise (certificate fails) return None and the
+    caller runs the unpruned path.  Returns (factors, discarded, total)."""
+    import torch
+    m, p, n = ahat3.dims
+    r = min(m, p)
+    dev = ahat3.device
+    if n < 8 or strategy not in (MEMORY_EFFICIENT, COMPUTE_EFFICIENT):
+        return None
+    with clock.stage("prune-energy"):
+        sel = prune_select(ahat3, epsilon)
+    if sel is None:
+        return None
+    keep_ids, e0, tbound = sel
+    k = n - int(keep_ids.size)
+    ns = int(keep_ids.size)
+    ids_dev = torch.from_numpy(keep_ids.astype(np.int64)).to(dev)
+    sub = DeviceTensor(ahat3.data.view(n, m * p).index_select(0, ids_dev).reshape(-1), (m, p, ns))
+    pending = []
+    with clock.stage("stage1-svd"):
+        keep = strategy == COMPUTE_EFFICIENT or _state_fits(sub)
+        if keep:
+            s, state = svd_values_device(sub, keep_state=True, defer=pending)
+        else:
+            s, state = svd_values_device(sub, defer=pending), None
+    with clock.stage("threshold"):
+        lib = nat.load()
+        nbytes = lib.starm_threshold_workspace_bytes(r, ns)
+        ws = nat.workspace(nbytes, dev)
+        ranks_s = torch.empty(ns, dtype=torch.int64, device=dev)
+        scal = torch.empty(3, dtype=torch.float64, device=dev)
+        j = torch.empty(1, dtype=torch.int64, device=dev)
+        cert = torch.empty(1, dtype=torch.int32, device=dev)
+        nat.call("starm_threshold_pruned_f64", s.data_ptr(), r, ns, float(epsilon), e0, tbound,
+                 ranks_s.data_ptr(), scal.data_ptr(), j.data_ptr(), cert.data_ptr(), ws.data_ptr(),
+                 nbytes, nat.stream_ptr(dev))
+        h = torch.cat([scal, ranks_s.sum().reshape(1).to(torch.float64),
+                       cert.to(torch.float64)] + [st.to(torch.float64) for st in pending])
+        h = h.cpu().numpy()
+        if pending:
+            check_status(h[5:].astype(np.int64))
+    clock.info["pruned_slices"] = k
+    if h[4] != 1.0:
+        clock.info["prune_certificate"] = "failed"
+        return None
+    clock.info["prune_certificate"] = "ok"
+    _, discarded, total, total_rank = float(h[0]), float(h[1]), float(h[2]), int(h[3])
+    with clock.stage("stage2-svd"):
+        pending = []
+        fs, _ = svd_truncated_device(sub, ranks_s, total_rank, state=state, defer=pending)
+        if pending:
+            check_status(torch.cat(pending).cpu().numpy())
+        del state
+        ranks = torch.zeros(n, dtype=torch.int64, device=dev)
+        ranks.index_copy_(0, ids_dev, ranks_s)
+        u_off, g_off = pack_offsets_device(ranks, m, p)
+        # the kept slices are in ascending slice order and the left-out ones
+        # have rank 0, so the subset's packed payload IS the global layout
+        factors = DeviceFactors(m, p, ranks, u_off, g_off, fs.u_data, fs.g_data, total_rank)
+    return factors, discarded, total
 
 
 _HBM_BUDGET = {}  # device index -> bytes this process can hold (free + own reserved), read once

@@ -459,3 +459,45 @@ extern "C" int starm_ttm_f32(const float* src, const float* mat, float* dst, int
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }
+
+// ------------------------------------------------------ per-slice energy
+// f[i] = sum of squares of slice i (slice_elems contiguous doubles), one CTA
+// per slice, fixed reduction order (deterministic).  sigma_max(slice)^2 <=
+// f[i]: the bound the pruned tolerance path uses.
+namespace starm {
+namespace {
+__global__ void __launch_bounds__(256) slice_energy_kernel(const double* __restrict__ a,
+                                                           int64_t elems, double* __restrict__ f) {
+  __shared__ double red[256];
+  const double* x = a + int64_t(blockIdx.x) * elems;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t i = threadIdx.x;
+  for (; i + 768 < elems; i += 1024) {
+    const double x0 = x[i], x1 = x[i + 256], x2 = x[i + 512], x3 = x[i + 768];
+    acc[0] = fma(x0, x0, acc[0]);
+    acc[1] = fma(x1, x1, acc[1]);
+    acc[2] = fma(x2, x2, acc[2]);
+    acc[3] = fma(x3, x3, acc[3]);
+  }
+  for (; i < elems; i += 256) acc[0] = fma(x[i], x[i], acc[0]);
+  red[threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) f[blockIdx.x] = red[0];
+}
+}  // namespace
+}  // namespace starm
+
+extern "C" int starm_slice_energy_f64(const double* a, int64_t slice_elems, int64_t nslices,
+                                      double* f_out, void* stream) {
+  STARM_CHECK_ARG(slice_elems >= 1 && nslices >= 0, "slice energy: bad extents");
+  if (nslices == 0) return STARM_OK;
+  STARM_CHECK_ARG(a && f_out, "slice energy: null pointer");
+  STARM_CHECK_ARG(nslices < (int64_t(1) << 31), "slice energy: too many slices");
+  slice_energy_kernel<<<unsigned(nslices), 256, 0, as_stream(stream)>>>(a, slice_elems, f_out);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}

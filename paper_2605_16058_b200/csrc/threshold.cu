@@ -39,6 +39,13 @@ struct ThState {
   int64_t j;
   int64_t cnt[2];
   int mode;        // -1: all-zero total, 0: keep sq > tau, 1: keep sq >= tau
+  // pruned form (starm_threshold_pruned_f64): e0 = energy of the slices left
+  // out (every one of their sigma^2 <= tbound); cert = the crossing value
+  // v[j] exceeds tbound, i.e. all values <= tbound are discarded whatever
+  // they are.  e0 = 0, tbound = -1 for the plain call (bitwise unchanged).
+  double e0;
+  double tbound;
+  int cert;
 };
 
 __global__ void square_keys_kernel(const double* s, int64_t count, unsigned long long* keys) {
@@ -59,7 +66,8 @@ constexpr int CS_TILE = 1024;
 
 __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long long* vbits,
                                                            int64_t count, double eps, double* w,
-                                                           double* v_out, ThState* st) {
+                                                           double* v_out, ThState* st, double e0,
+                                                           double tbound) {
   __shared__ __align__(16) double tile[2][CS_TILE];
   __shared__ __align__(16) double wt[2][CS_TILE];
   __shared__ double acc_sh;
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
         const int len = tlen(t);
         int k = 0;
         if (t == 0) {
-          acc = tl[0];
+          acc = e0 == 0.0 ? tl[0] : __dadd_rn(e0, tl[0]);  // pruned form: the left-out energy first
           wl[0] = acc;
           for (k = 1; k < 8 && k < len; ++k) {
             acc = __dadd_rn(acc, tl[k]);
@@ -177,13 +185,17 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
   __syncthreads();
   acc = acc_sh;
   if (threadIdx.x != 0) return;
-  const double total = count ? acc : 0.0;
+  const double total = count ? acc : e0;
   st->total = total;
+  st->e0 = e0;
+  st->tbound = tbound;
+  st->cert = 0;
   if (total == 0.0) {
     st->mode = -1;
     st->j = 0;
     st->tau = 0.0;
     st->budget = 0.0;
+    st->cert = 1;
     return;
   }
   const double budget = __dmul_rn(__dmul_rn(eps, eps), total);
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(64) cumsum_search_kernel(const unsigned long l
   st->j = lo;
   st->tau = lo > 0 ? v[lo - 1] : 0.0;
   st->mode = 0;
+  st->cert = lo < count && v[lo] > tbound;
 }
 
 // Masks in C (row-major) order of the (r, N) matrix: c = row*N + slice.
@@ -348,11 +361,14 @@ __global__ void __launch_bounds__(PW_THREADS) pairwise_kernel(const int* fa, con
   __syncthreads();
   const double sb = pw_combine_levels(nb, part);
   if (threadIdx.x == 0) {
-    st->disc[0] = sa;
-    st->disc[1] = sb;
+    // pruned form: the left-out slices' energy is discarded too (e0 = 0 otherwise)
+    const double da = st->e0 == 0.0 ? sa : __dadd_rn(st->e0, sa);
+    const double dbb = st->e0 == 0.0 ? sb : __dadd_rn(st->e0, sb);
+    st->disc[0] = da;
+    st->disc[1] = dbb;
     st->cnt[0] = na;
     st->cnt[1] = nb;
-    st->mode = (sa >= st->budget && st->tau > 0.0) ? 1 : 0;
+    st->mode = (da >= st->budget && st->tau > 0.0) ? 1 : 0;
   }
 }
 
@@ -439,10 +455,39 @@ extern "C" size_t starm_threshold_workspace_bytes(int64_t r, int64_t nslices) {
   return layout(r * nslices).total;
 }
 
+namespace starm {
+namespace {
+int threshold_run(const double* s, int64_t r, int64_t nslices, double epsilon, double* v_out,
+                  double* w_out, int64_t* ranks_out, double* scal_out, int64_t* j_out, void* ws,
+                  size_t ws_bytes, void* stream, double e0, double tbound, int32_t* cert_out);
+}  // namespace
+}  // namespace starm
+
 extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, double epsilon,
                                    double* v_out, double* w_out, int64_t* ranks_out,
                                    double* scal_out, int64_t* j_out, void* ws, size_t ws_bytes,
                                    void* stream) {
+  return threshold_run(s, r, nslices, epsilon, v_out, w_out, ranks_out, scal_out, j_out, ws,
+                       ws_bytes, stream, 0.0, -1.0, nullptr);
+}
+
+extern "C" int starm_threshold_pruned_f64(const double* s, int64_t r, int64_t nslices,
+                                          double epsilon, double e0, double tbound,
+                                          int64_t* ranks_out, double* scal_out, int64_t* j_out,
+                                          int32_t* cert_out, void* ws, size_t ws_bytes,
+                                          void* stream) {
+  STARM_CHECK_ARG(e0 >= 0.0 && tbound >= 0.0 && cert_out, "threshold pruned: bad e0 / tbound");
+  return threshold_run(s, r, nslices, epsilon, nullptr, nullptr, ranks_out, scal_out, j_out, ws,
+                       ws_bytes, stream, e0, tbound, cert_out);
+}
+
+__global__ void cert_kernel(const starm::ThState* st, int32_t* cert) { *cert = st->cert; }
+
+namespace starm {
+namespace {
+int threshold_run(const double* s, int64_t r, int64_t nslices, double epsilon, double* v_out,
+                  double* w_out, int64_t* ranks_out, double* scal_out, int64_t* j_out, void* ws,
+                  size_t ws_bytes, void* stream, double e0, double tbound, int32_t* cert_out) {
   STARM_CHECK_ARG(r >= 1 && nslices >= 1, "threshold: extents must be positive");
   STARM_CHECK_ARG(epsilon > 0.0 && epsilon < 1.0, "tolerance must lie in (0, 1), got %g", epsilon);
   const int64_t count = r * nslices;
@@ -470,7 +515,7 @@ extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, 
   STARM_LAUNCH_CHECK();
   STARM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(cubtmp, cub_bytes, keys, sorted, int(count), 0, 64, st));
   count_launch(3);  // the three CUB device-wide calls of this function
-  cumsum_search_kernel<<<1, 64, 0, st>>>(sorted, count, epsilon, w, v_out, stt);
+  cumsum_search_kernel<<<1, 64, 0, st>>>(sorted, count, epsilon, w, v_out, stt, e0, tbound);
   STARM_LAUNCH_CHECK();
   mask_kernel<<<grid, 256, 0, st>>>(s, r, nslices, stt, fa, fb);
   STARM_LAUNCH_CHECK();
@@ -488,5 +533,11 @@ extern "C" int starm_threshold_f64(const double* s, int64_t r, int64_t nslices, 
   STARM_LAUNCH_CHECK();
   ranks_kernel<<<grid_for(nslices), 256, 0, st>>>(s, r, nslices, stt, ranks_out, scal_out, j_out);
   STARM_LAUNCH_CHECK();
+  if (cert_out) {
+    cert_kernel<<<1, 1, 0, st>>>(stt, cert_out);
+    STARM_LAUNCH_CHECK();
+  }
   return STARM_OK;
 }
+}  // namespace
+}  // namespace starm

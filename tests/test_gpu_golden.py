@@ -265,3 +265,51 @@ def test_relative_error_device_matches_helpers():
         dev = torch.device("cuda", 0)
         got = relative_error_device(as_device(sb.DenseTensor(a), dev), as_device(sb.DenseTensor(b), dev))
         assert abs(got - rel_error(a, b)) <= 1e-12 * rel_error(a, b)
+
+
+# ----------------------------------------- certified slice pruning (tolerance)
+
+def test_tolerance_pruning_certified_equals_unpruned():
+    """tsvdm_tolerance leaves out low-energy slices only when the threshold
+    certifies that all their sigma^2 are discarded; the result must equal the
+    unpruned path (ranks and factors bitwise, energies to rounding) and the
+    oracle's ranks."""
+    from paper_2605_16058_b200 import compress
+    a = cf.config2(nlat=46, nlon=90, nt=512, seed=2)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    x = sb.DeviceTensor.from_host(t)
+    clock = sb.StageClock()
+    got = sb.tsvdm_tolerance(x, ts, 1e-2, clock=clock)
+    assert clock.info.get("pruned_slices", 0) > 0 and clock.info["prune_certificate"] == "ok"
+    compress.PRUNE = False
+    try:
+        ref = sb.tsvdm_tolerance(x, ts, 1e-2)
+    finally:
+        compress.PRUNE = True
+    assert np.array_equal(got.ranks, ref.ranks)
+    gf, rf = got.factors.to_host(), ref.factors.to_host()
+    assert np.array_equal(gf.u_data, rf.u_data) and np.array_equal(gf.g_data, rf.g_data)
+    assert abs(got.total_energy - ref.total_energy) <= 1e-13 * ref.total_energy
+    assert abs(got.discarded_energy - ref.discarded_energy) <= 1e-12 * ref.total_energy
+    oref = oracle.tsvdm_tolerance(a, [oracle.dct_matrix(512)], 1e-2)
+    assert np.array_equal(got.ranks, oref["ranks"])
+    _, err = sb.reconstruct_fused(got, a=x)
+    assert abs(err - got.relative_error()) <= 1e-8 and err <= 1e-2
+
+
+def test_tolerance_pruning_certificate_failure_falls_back():
+    from paper_2605_16058_b200 import compress
+    a = cf.config2(nlat=46, nlon=90, nt=512, seed=2)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    old = compress.PRUNE_GAMMA
+    compress.PRUNE_GAMMA = 0.999          # leaves out too much: the certificate must fail
+    try:
+        clock = sb.StageClock()
+        got = sb.tsvdm_tolerance(t, ts, 1e-2, clock=clock)
+    finally:
+        compress.PRUNE_GAMMA = old
+    assert clock.info.get("prune_certificate") in ("failed", None)
+    oref = oracle.tsvdm_tolerance(a, [oracle.dct_matrix(512)], 1e-2)
+    assert np.array_equal(got.ranks, oref["ranks"])
