@@ -540,8 +540,16 @@ def prune_select(ahat3, epsilon):
     f_dev = torch.empty(n, dtype=torch.float64, device=dev)
     nat.call("starm_slice_energy_f64", ahat3.data.data_ptr(), m * p, n, f_dev.data_ptr(),
              nat.stream_ptr(dev))
-    f = f_dev.cpu().numpy()
-    if not np.isfinite(f).all():
+    return prune_choose(f_dev.cpu().numpy(), epsilon)
+
+
+def prune_choose(f, epsilon):
+    """Host half of prune_select on the per-slice energies ``f`` (also used by
+    the sharded path on all-reduced energies, so every rank chooses the same
+    slices): (kept ids ascending, e0, tbound) or None."""
+    f = np.asarray(f, dtype=np.float64)
+    n = f.size
+    if n < 8 or not np.isfinite(f).all():
         return None                      # the SVD names the non-finite slice
     budget = epsilon * epsilon * math.fsum(f.tolist())
     order = np.argsort(f, kind="stable")

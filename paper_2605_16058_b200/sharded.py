@@ -138,19 +138,101 @@ class ShardedResult:
     local_ranks: np.ndarray    # ranks of the owned slices
     u_data: object             # packed factors of the owned slices (torch)
     g_data: object
+    slice_ids: np.ndarray = None  # owned slices when not plan.slice_bounds() (pruned path)
+    pruned: int = 0               # slices left out by the certified pruning (all ranks)
 
     @property
     def relative_error(self) -> float:
         return float(np.sqrt(self.discarded_energy / self.total_energy)) if self.total_energy else 0.0
 
 
-def tsvdm_tolerance_sharded(local, plan: ShardPlan, ops, epsilon, dist, group=None) -> ShardedResult:
+def _owner_ranges(total, world):
+    return [_bounds(total, world, h) for h in range(world)]
+
+
+def _all_gather_var(local, rows, counts, dist, group, torch):
+    """All-gather (rows x counts[h]) column-major blocks into (rows x sum)
+    in rank order (padded to the largest block for the collective)."""
+    world = len(counts)
+    nmax = max(max(counts), 1)
+    pad = torch.zeros(rows * nmax, dtype=local.dtype, device=local.device)
+    pad[:local.numel()] = local
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad, group=group)
+    return torch.cat([out[h][:rows * counts[h]] for h in range(world)])
+
+
+def _tolerance_pruned_sharded(ahat, plan: ShardPlan, ops, epsilon, dist, group, keep_ids, e0,
+                              tbound):
+    """The certified slice pruning of compress._tolerance_pruned over the
+    ranks.  Every rank chose the same kept slices from all-reduced energies;
+    the kept slices are dealt to the ranks in contiguous runs, so the
+    all-to-all moves only their fibre segments (c2: 81 of 1024 slices), the
+    values pass / threshold (started at e0) / truncated pass run on them, and
+    the packed payloads concatenate in rank order to the global layout.
+    Returns None when the certificate fails (the caller runs unpruned)."""
+    import torch
+    m, p, n = plan.m, plan.p, plan.n
+    r = min(m, p)
+    dev = ahat.device
+    world, me = plan.world, plan.rank
+    ns_all = int(keep_ids.size)
+    own = _owner_ranges(ns_all, world)
+    k0, k1 = own[me]
+    ns = k1 - k0
+    kid = torch.from_numpy(np.ascontiguousarray(keep_ids, dtype=np.int64)).to(dev)
+    # (nf x N) column-major = (N, nf) row-major: row t = this rank's fibres of slice t
+    send = ahat.view(n, plan.nf).index_select(0, kid).reshape(-1)     # kept rows, in S order
+    send_counts = [(b - a) * plan.nf for a, b in own]
+    fb = [plan.fibre_bounds(g) for g in range(world)]
+    recv_counts = [ns * (f1 - f0) for f0, f1 in fb]
+    recv = torch.empty(sum(recv_counts), dtype=torch.float64, device=dev)
+    dist.all_to_all_single(recv, send, recv_counts, send_counts, group=group)
+    del send
+    parts, off = [], 0
+    for g in range(world):
+        nfg = fb[g][1] - fb[g][0]
+        parts.append(recv[off:off + ns * nfg].view(ns, nfg))
+        off += ns * nfg
+    slices = torch.cat(parts, dim=1).reshape(-1) if ns else recv[:0]
+    del recv
+    s_local = ops.svd_values(slices, m, p, ns)
+    s_all = _all_gather_var(s_local, r, [b - a for a, b in own], dist, group, torch)
+    ranks_s, tau, disc, total, cert = ops.threshold_pruned(s_all, r, ns_all, epsilon, e0, tbound)
+    if not cert:
+        return None
+    ranks_s = np.asarray(ranks_s, dtype=np.int64)
+    local_ranks = ranks_s[k0:k1].copy()
+    u_data, g_data = ops.truncated(slices, m, p, ns, local_ranks, s_local)
+    ranks = np.zeros(n, dtype=np.int64)
+    ranks[keep_ids] = ranks_s
+    return ShardedResult(ranks, float(tau), float(disc), float(total), local_ranks, u_data, g_data,
+                         slice_ids=np.asarray(keep_ids[k0:k1], dtype=np.int64),
+                         pruned=n - ns_all)
+
+
+def tsvdm_tolerance_sharded(local, plan: ShardPlan, ops, epsilon, dist, group=None,
+                            prune=True) -> ShardedResult:
     """Steps 1-4 of the module docstring.  ``local`` is this rank's (nf, N)
-    column-major fibre block as a flat torch tensor on ops' device."""
+    column-major fibre block as a flat torch tensor on ops' device.  With
+    ``prune`` (and ops providing slice_energy / threshold_pruned) the
+    certified slice pruning of compress._tolerance_pruned runs first: the
+    per-slice energies are this rank's partial sums all-reduced, every rank
+    chooses the same slices (compress.prune_choose), and only the kept
+    slices cross the all-to-all."""
     import torch
     m, p, n = plan.m, plan.p, plan.n
     r = min(m, p)
     ahat = ops.forward(local, plan.nf, n)                              # 1. transform
+    if prune and hasattr(ops, "slice_energy") and hasattr(ops, "threshold_pruned"):
+        from .compress import prune_choose
+        f = ops.slice_energy(ahat, plan.nf, n)
+        dist.all_reduce(f, group=group)
+        sel = prune_choose(f.cpu().numpy(), epsilon)
+        if sel is not None:
+            res = _tolerance_pruned_sharded(ahat, plan, ops, epsilon, dist, group, *sel)
+            if res is not None:
+                return res
     recv = torch.empty(sum(plan.recv_counts()), dtype=torch.float64, device=ahat.device)
     dist.all_to_all_single(recv, ahat, plan.recv_counts(), plan.send_counts(), group=group)  # 2.
     del ahat
@@ -196,8 +278,11 @@ def tsvdm_fixed_rank_sharded(local, plan: ShardPlan, ops, rank, dist, group=None
 def reconstruct_sharded(res: ShardedResult, plan: ShardPlan, ops, dist, group=None):
     """This rank's fibre block of the reconstruction (flat (nf, N) col-major):
     facewise U_i G_i of the owned slices, all-to-all back to fibres, inverse
-    transform."""
+    transform.  Pruned results own a subset of the slices (res.slice_ids);
+    the other slices are zero."""
     import torch
+    if res.slice_ids is not None:
+        return _reconstruct_pruned(res, plan, ops, dist, group)
     chat = ops.unpack(res.u_data, res.g_data, res.local_ranks, plan.m, plan.p, plan.ns)
     send = _disassemble(chat, plan, torch)
     del chat
@@ -206,6 +291,35 @@ def reconstruct_sharded(res: ShardedResult, plan: ShardPlan, ops, dist, group=No
     dist.all_to_all_single(back, send, plan.send_counts(), plan.recv_counts(), group=group)
     del send
     return ops.inverse(back, plan.nf, plan.n)
+
+
+def _reconstruct_pruned(res: ShardedResult, plan: ShardPlan, ops, dist, group):
+    import torch
+    world = plan.world
+    ids = torch.from_numpy(np.ascontiguousarray(res.slice_ids, dtype=np.int64))
+    ns = int(ids.numel())
+    counts = torch.tensor([ns], dtype=torch.int64)
+    dev = getattr(ops, "device", None)
+    if dev is not None:
+        counts = counts.to(dev)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    allc = [int(c.item()) for c in allc]
+    # every rank's slice ids, in rank order
+    idt = ids.to(dev) if dev is not None else ids
+    all_ids = _all_gather_var(idt.to(torch.float64), 1, allc, dist, group, torch).to(torch.int64)
+    chat = ops.unpack(res.u_data, res.g_data, res.local_ranks, plan.m, plan.p, ns)
+    fb = [plan.fibre_bounds(g) for g in range(world)]
+    mat = chat.view(ns, plan.fibres) if ns else chat.view(0, plan.fibres)
+    send = torch.cat([mat[:, a:b].reshape(-1) for a, b in fb]) if ns else chat[:0]
+    send_counts = [ns * (b - a) for a, b in fb]
+    recv_counts = [allc[h] * plan.nf for h in range(world)]
+    recv = torch.empty(sum(recv_counts), dtype=torch.float64, device=chat.device)
+    dist.all_to_all_single(recv, send, recv_counts, send_counts, group=group)
+    back = torch.zeros(plan.n, plan.nf, dtype=torch.float64, device=chat.device)
+    if all_ids.numel():
+        back.index_copy_(0, all_ids.to(back.device), recv.view(-1, plan.nf))
+    return ops.inverse(back.reshape(-1), plan.nf, plan.n)
 
 
 def relative_error_sharded(local, rec, dist, group=None, ops=None) -> float:
@@ -297,6 +411,32 @@ class DeviceOps:
         rk = torch.from_numpy(np.ascontiguousarray(local_ranks)).to(self.device)
         f, s = svd_truncated_device(self._dev(slices, (m, p, ns)), rk, total, keep_values=True)
         return f.u_data[:total * m], f.g_data[:total * p], s[:r * ns]
+
+    def slice_energy(self, ahat, nf, n):
+        """Per-slice energies of this rank's fibres: column sums of squares of
+        the (nf x N) column-major block (starm_slice_energy_f64)."""
+        import torch
+        from . import _native as nat
+        f = torch.empty(n, dtype=torch.float64, device=self.device)
+        nat.call("starm_slice_energy_f64", ahat.data_ptr(), nf, n, f.data_ptr(),
+                 nat.stream_ptr(self.device))
+        return f
+
+    def threshold_pruned(self, s_all, r, n, epsilon, e0, tbound):
+        import torch
+        from . import _native as nat
+        lib = nat.load()
+        nbytes = lib.starm_threshold_workspace_bytes(r, n)
+        ws = nat.workspace(nbytes, self.device)
+        ranks = torch.empty(n, dtype=torch.int64, device=self.device)
+        scal = torch.empty(3, dtype=torch.float64, device=self.device)
+        j = torch.empty(1, dtype=torch.int64, device=self.device)
+        cert = torch.empty(1, dtype=torch.int32, device=self.device)
+        nat.call("starm_threshold_pruned_f64", s_all.data_ptr(), r, n, float(epsilon), float(e0),
+                 float(tbound), ranks.data_ptr(), scal.data_ptr(), j.data_ptr(), cert.data_ptr(),
+                 ws.data_ptr(), nbytes, nat.stream_ptr(self.device))
+        sc = scal.cpu().numpy()
+        return ranks.cpu().numpy(), sc[0], sc[1], sc[2], bool(cert.item())
 
     def tail_energy(self, s_all, r, n, rank):
         import torch

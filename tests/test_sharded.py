@@ -64,6 +64,29 @@ class OracleOps:
         u, g, s = oracle.svd_truncated_slices(a, local_ranks, keep_values=True)
         return torch.from_numpy(u), torch.from_numpy(g), torch.from_numpy(s.reshape(-1, order="F").copy())
 
+    def slice_energy(self, ahat, nf, n):
+        a = ahat.numpy().reshape((nf, n), order="F")
+        return torch.from_numpy(np.ascontiguousarray((a * a).sum(axis=0)))
+
+    def threshold_pruned(self, s_all, r, n, eps, e0, tbound):
+        """compute_threshold (tsvdm.py:85-115) on the kept slices with the
+        running sum started at e0 (the left-out energy); cert = crossing value
+        above tbound (numpy restatement of starm_threshold_pruned_f64)."""
+        sq = s_all.numpy().reshape((r, n), order="F") ** 2
+        v = np.sort(sq, axis=None)
+        w = e0 + np.cumsum(v)
+        total = w[-1]
+        budget = eps * eps * total
+        j = int(np.searchsorted(w, budget, side="left"))
+        tau = v[j - 1] if j > 0 else 0.0
+        cert = j < v.size and v[j] > tbound
+        keep = sq > tau
+        disc = e0 + oracle.pairwise_sum(sq[~keep])
+        if disc >= budget and tau > 0.0:
+            keep = sq >= tau
+            disc = e0 + oracle.pairwise_sum(sq[~keep])
+        return keep.sum(axis=0).astype(np.int64), tau, disc, total, bool(cert)
+
     def tail_energy(self, s_all, r, n, rank):
         sq = s_all.numpy().reshape((r, n), order="F") ** 2
         return float(sq[rank:, :].sum()), float(sq.sum())     # tsvdm.py:260-262
@@ -201,6 +224,71 @@ def test_sharded_fixed_rank_matches_single_process(dims, k, world):
         np.testing.assert_allclose(g, ref["g_data"], rtol=0, atol=1e-9)
         assert abs(err - ref_err) <= 1e-10
         assert abs(err - np.sqrt(disc / total)) <= 1e-10
+
+
+def _pruning_tensor():
+    """Three separable oscillations + 1e-3 noise over 64 time steps: the DCT
+    concentrates them in ~20 slices, the rest are noise far below tau."""
+    rng = np.random.default_rng(4)
+    m, p, n = 9, 16, 64
+    t = np.arange(n)
+    a = np.zeros((m, p, n))
+    for k in range(3):
+        a += np.einsum("i,j,t->ijt", rng.standard_normal(m), rng.standard_normal(p),
+                       np.cos(2 * np.pi * (k + 1) * t / (1.7 * n) + rng.uniform(0, 6)))
+    a += 1e-3 * rng.standard_normal((m, p, n))
+    return np.asfortranarray(a)
+
+
+def _worker_pruned(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = _pruning_tensor()
+        m, p, n = a.shape
+        mat = oracle.dct_matrix(n)
+        plan = ShardPlan(m, p, n, world, rank)
+        local = torch.from_numpy(scatter_fibres(a, plan).reshape(-1, order="F").copy())
+        ops = OracleOps(mat)
+        res = tsvdm_tolerance_sharded(local, plan, ops, 1e-2, dist)
+        u, g = gather_factors(res, plan, dist)
+        rec = reconstruct_sharded(res, plan, ops, dist)
+        err = relative_error_sharded(local, rec, dist)
+        q.put((rank, res.pruned, res.ranks, res.discarded_energy, res.total_energy, u.numpy(),
+               g.numpy(), err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_tolerance_pruned_matches_single_process(world):
+    """Certified slice pruning over gloo ranks: the kept slices are dealt to
+    the ranks, only they cross the all-to-all; ranks, energies, factors and
+    the realised error equal the single-process (unpruned) oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_pruned, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    a = _pruning_tensor()
+    mat = oracle.dct_matrix(64)
+    ref = oracle.tsvdm_tolerance(a, [mat], 1e-2)
+    rec = oracle.reconstruct_packed(a.shape, [mat], ref["ranks"], ref["u_data"], ref["g_data"])
+    ref_err = float(np.linalg.norm(a - rec) / np.linalg.norm(a))
+    for rank, pruned, ranks, disc, total, u, g, err in outs:
+        assert pruned > 0, "the test case must exercise the pruned path"
+        assert np.array_equal(ranks, ref["ranks"]), rank
+        assert abs(total - ref["total_energy"]) <= 1e-12 * ref["total_energy"]
+        assert abs(disc - ref["discarded_energy"]) <= 1e-12 * ref["total_energy"]
+        np.testing.assert_allclose(u, ref["u_data"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(g, ref["g_data"], rtol=0, atol=1e-9)
+        assert abs(err - ref_err) <= 1e-10
 
 
 def test_shard_plan_partitions():
