@@ -375,11 +375,21 @@ class DeviceOps:
         return inverse_device(self._dev(flat, (nf, 1, n)), self.ts).data
 
     def svd_values(self, slices, m, p, ns):
+        """Values pass of the owned slices; keeps each slice's factorisation
+        state (when it fits in HBM) so the following truncated pass on the
+        same slices does not refactor them (tsvdm_tolerance's schedule)."""
         import torch
+        from .compress import _state_fits
         from .slice_svd import svd_values_device
+        self._state = None
         if ns == 0:
             return torch.empty(0, dtype=torch.float64, device=self.device)
-        return svd_values_device(self._dev(slices, (m, p, ns)))
+        x = self._dev(slices, (m, p, ns))
+        if _state_fits(x):
+            s, state = svd_values_device(x, keep_state=True)
+            self._state = (slices.data_ptr(), ns, state) if state is not None else None
+            return s
+        return svd_values_device(x)
 
     def threshold(self, s_all, r, n, epsilon):
         from .compress import threshold_device
@@ -395,7 +405,10 @@ class DeviceOps:
             z = torch.empty(0, dtype=torch.float64, device=self.device)
             return z, z
         rk = torch.from_numpy(np.ascontiguousarray(local_ranks)).to(self.device)
-        f, _ = svd_truncated_device(self._dev(slices, (m, p, ns)), rk, total)
+        st = getattr(self, "_state", None)
+        state = st[2] if st is not None and st[0] == slices.data_ptr() and st[1] == ns else None
+        f, _ = svd_truncated_device(self._dev(slices, (m, p, ns)), rk, total, state=state)
+        self._state = None
         return f.u_data[:total * m], f.g_data[:total * p]
 
     def truncated_with_values(self, slices, m, p, ns, local_ranks):
