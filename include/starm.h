@@ -130,6 +130,18 @@ size_t starm_ttm_residual_workspace_bytes(int64_t rows, int64_t n, int64_t batch
 int starm_dct_residual_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
                            int inverse, const uint16_t* delta_bf16, int log2_scale, void* ws,
                            size_t ws_bytes, void* stream);
+/* The same two halves separately, so a caller can correct only some output
+ * columns (the pruned tolerance path corrects only the slices it keeps):
+ * starm_dct_pack_f64 = the exact FFT DCT into dst and the bf16 operand into
+ * ws; starm_residual_apply_f64 then adds 2^-e Dsel @ x to dst, where Dsel is
+ * an nout x n row-major bf16 matrix (rows of Delta * 2^e, padded with zero
+ * rows to a multiple of 256 and 128-byte aligned) and dst holds nout output
+ * columns per batch block (dst[b * rows * nout + f + j * rows]). */
+int starm_dct_pack_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
+                       int inverse, void* ws, size_t ws_bytes, void* stream);
+int starm_residual_apply_f64(const void* ws, const uint16_t* delta_bf16, int log2_scale,
+                             double* dst, int64_t rows, int64_t n, int64_t nout, int64_t batch,
+                             void* stream);
 int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int log2_scale,
                             double* dst, int64_t rows, int64_t n, int64_t batch, void* ws,
                             size_t ws_bytes, void* stream);

@@ -22,7 +22,8 @@ from math import prod
 import numpy as np
 
 from . import _native as nat
-from .mode_product import BATCHED, VARIANTS, forward_device, inverse_device
+from .mode_product import (BATCHED, VARIANTS, DeferredResidual, deferrable, forward_device,
+                           inverse_device)
 from .slice_svd import (check_status, SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
                         VariableRankFactors, pack_offsets_device, svd_full_device,
                         svd_truncated_device, svd_values_device)
@@ -420,7 +421,14 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
     m, p = a.dims[0], a.dims[1]
     n = prod(a.dims[2:])
     r = min(m, p)
-    ahat = forward_device(as_device(a, dev), ts)
+    deferred = None
+    if PRUNE and strategy != TRUNCATE and deferrable(ts, a.dims):
+        # exact FFT DCT now; the reference operator's residual is added to the
+        # slices the pruning keeps (or to all of them if it does not prune)
+        deferred = DeferredResidual(as_device(a, dev), ts[0])
+        ahat = deferred.out
+    else:
+        ahat = forward_device(as_device(a, dev), ts)
     ahat3 = DeviceTensor(ahat.data, (m, p, n))
     if strategy == TRUNCATE:
         with clock.stage("stage1-svd"):
@@ -440,10 +448,12 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
             factors = DeviceFactors(m, p, ranks, u_off, g_off, u_data[: total_rank * m],
                                     g_data[: total_rank * p], total_rank)
     else:
-        pruned = _tolerance_pruned(ahat3, epsilon, strategy, clock) if PRUNE else None
+        pruned = _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred) if PRUNE else None
         if pruned is not None:
             factors, discarded, total = pruned
             return _finish(a, ts, factors, METHOD_TOLERANCE, epsilon, discarded, total, host)
+        if deferred is not None:
+            deferred.apply_all()     # unpruned: every slice gets the reference operator
         # Keep every slice's factorisation in HBM between the passes when it
         # fits comfortably (always for compute-efficient); otherwise refactor
         # the rank>0 slices (memory-efficient in the reference's sense).
@@ -560,7 +570,7 @@ def prune_choose(f, epsilon):
     return keep_ids, math.fsum(f[np.sort(order[:k])].tolist()), float(f[order[k - 1]])
 
 
-def _tolerance_pruned(ahat3, epsilon, strategy, clock):
+def _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred=None):
     """Certified slice pruning for tsvdm_tolerance (same ranks, factors and
     energies as the unpruned path, which the reference computes).
 
@@ -586,10 +596,16 @@ def _tolerance_pruned(ahat3, epsilon, strategy, clock):
     if sel is None:
         return None
     keep_ids, e0, tbound = sel
+    if deferred is not None:
+        # energies of the exact-DCT slices: the reference operator differs by
+        # |Delta x| ~ 1e-13 |x|, so widen the bound well past that
+        tbound *= 1.0 + 1e-9
     k = n - int(keep_ids.size)
     ns = int(keep_ids.size)
     ids_dev = torch.from_numpy(keep_ids.astype(np.int64)).to(dev)
     sub = DeviceTensor(ahat3.data.view(n, m * p).index_select(0, ids_dev).reshape(-1), (m, p, ns))
+    if deferred is not None:
+        deferred.apply_cols(sub.data, ids_dev)   # reference operator on the kept slices only
     pending = []
     with clock.stage("stage1-svd"):
         keep = strategy == COMPUTE_EFFICIENT or _state_fits(sub)

@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(256) residual_pack_kernel(const double* __rest
 struct ResidualArgs {
   double* dst;
   int64_t rows, n, rows_pad, batch;
-  int64_t tiles, nblk;     // total tiles, output blocks per fibre block (n / RB_N)
+  int64_t nout;            // output columns (n, or the selected rows of Delta)
+  int64_t tiles, nblk;     // total tiles, output blocks per fibre block (nout padded / RB_N)
   double scale;            // 2^-e
 };
 
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(RB_THREADS, 1)
       const int64_t b = grow / g.rows_pad;
       const int64_t f = grow - b * g.rows_pad + 32 * q + lane;
       const bool live = f < g.rows;
-      double* out = g.dst + b * g.rows * g.n + f;
+      double* out = g.dst + b * g.rows * g.nout + f;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
 #pragma unroll 1
@@ -292,13 +293,20 @@ __global__ void __launch_bounds__(RB_THREADS, 1)
         const int col = half * (RB_N / 2) + c;
         float v[32];
         tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * RB_N + col), v);
-        if (live) {
-          double* p = out + (nb * RB_N + col) * g.rows;
+        const int64_t col0 = nb * RB_N + col;
+        if (live && col0 + 32 <= g.nout) {
+          double* p = out + col0 * g.rows;
           double x[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) x[j] = p[int64_t(j) * g.rows];
 #pragma unroll
           for (int j = 0; j < 32; ++j) p[int64_t(j) * g.rows] = fma(double(v[j]), g.scale, x[j]);
+        } else if (live && col0 < g.nout) {   // last, partial block of selected columns
+          double* p = out + col0 * g.rows;
+          const int lim = int(g.nout - col0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) p[int64_t(j) * g.rows] = fma(double(v[j]), g.scale, p[int64_t(j) * g.rows]);
         }
       }
       tc_fence_before();
@@ -370,7 +378,10 @@ namespace starm {
 namespace {
 // Pack (unless the DCT kernel already wrote the bf16 rows) + tcgen05 GEMM.
 int residual_run(const double* pack_src, const uint16_t* delta_bf16, int log2_scale, double* dst,
-                 int64_t rows, int64_t n, int64_t batch, void* ws, cudaStream_t st) {
+                 int64_t rows, int64_t n, int64_t batch, const void* ws, cudaStream_t st,
+                 int64_t nout = -1) {
+  if (nout < 0) nout = n;
+  const int64_t nout_pad = round_up(nout, RB_N);
   const int64_t rows_pad = rows_padded(rows);
   const int64_t total_rows = rows_pad * batch;
   STARM_CHECK_ARG(total_rows < (int64_t(1) << 31) && n <= 65536 && batch <= 65535,
@@ -379,14 +390,14 @@ int residual_run(const double* pack_src, const uint16_t* delta_bf16, int log2_sc
   if (rc) return rc;
   if (pack_src) {
     dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), unsigned(batch));
-    residual_pack_kernel<<<grid, 256, 0, st>>>(pack_src, static_cast<uint16_t*>(ws), rows, n,
-                                               rows_pad);
+    residual_pack_kernel<<<grid, 256, 0, st>>>(pack_src, static_cast<uint16_t*>(const_cast<void*>(ws)),
+                                               rows, n, rows_pad);
     STARM_LAUNCH_CHECK();
   }
   CUtensorMap map_x, map_d;
   rc = make_map(&map_x, ws, uint64_t(n), uint64_t(total_rows), RB_K, RB_M);
   if (rc) return rc;
-  rc = make_map(&map_d, delta_bf16, uint64_t(n), uint64_t(n), RB_K, RB_N);
+  rc = make_map(&map_d, delta_bf16, uint64_t(n), uint64_t(nout_pad), RB_K, RB_N);
   if (rc) return rc;
   int dev = 0, sms = 148;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
@@ -400,7 +411,8 @@ int residual_run(const double* pack_src, const uint16_t* delta_bf16, int log2_sc
   g.n = n;
   g.rows_pad = rows_pad;
   g.batch = batch;
-  g.nblk = n / RB_N;
+  g.nout = nout;
+  g.nblk = nout_pad / RB_N;
   g.tiles = (total_rows / RB_M) * g.nblk;
   g.scale = ldexp(1.0, -log2_scale);
   const int64_t grid = g.tiles < sms ? g.tiles : sms;
@@ -454,4 +466,46 @@ extern "C" int starm_dct_residual_f64(const double* src, double* dst, int64_t ro
                   rows_padded(rows), &packed, st);
   if (rc) return rc;
   return residual_run(packed ? nullptr : src, delta_bf16, log2_scale, dst, rows, n, batch, ws, st);
+}
+
+extern "C" int starm_dct_pack_f64(const double* src, double* dst, int64_t rows, int64_t n,
+                                  int64_t batch, int inverse, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  STARM_CHECK_ARG(rows >= 0 && n >= 0 && batch >= 0, "dct pack: negative extent");
+  if (rows == 0 || batch == 0 || n == 0) return STARM_OK;
+  STARM_CHECK_ARG(src && dst && ws && src != dst, "dct pack: null or aliased pointer");
+  if ((n & (n - 1)) != 0 || n < RB_N || n > 4096) {
+    set_error("dct pack: the fast path needs a power-of-two length in [256, 4096]");
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG(ws_bytes >= starm_ttm_residual_workspace_bytes(rows, n, batch) &&
+                      (reinterpret_cast<uintptr_t>(ws) & 127) == 0,
+                  "dct pack: workspace too small or not 128-byte aligned");
+  const cudaStream_t st = as_stream(stream);
+  bool packed = false;
+  int rc = dct_launch(src, dst, rows, n, batch, inverse != 0, static_cast<uint16_t*>(ws),
+                      rows_padded(rows), &packed, st);
+  if (rc || packed) return rc;
+  const int64_t rows_pad = rows_padded(rows);
+  dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), unsigned(batch));
+  residual_pack_kernel<<<grid, 256, 0, st>>>(src, static_cast<uint16_t*>(ws), rows, n, rows_pad);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+extern "C" int starm_residual_apply_f64(const void* ws, const uint16_t* delta_bf16, int log2_scale,
+                                        double* dst, int64_t rows, int64_t n, int64_t nout,
+                                        int64_t batch, void* stream) {
+  STARM_CHECK_ARG(rows >= 0 && n >= 0 && nout >= 0 && batch >= 0, "residual apply: negative extent");
+  if (rows == 0 || batch == 0 || n == 0 || nout == 0) return STARM_OK;
+  STARM_CHECK_ARG(ws && delta_bf16 && dst, "residual apply: null pointer");
+  if (n % RB_N != 0) {
+    set_error("residual apply: n = %lld must be a multiple of %d", (long long)n, RB_N);
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG((reinterpret_cast<uintptr_t>(ws) & 127) == 0 &&
+                      (reinterpret_cast<uintptr_t>(delta_bf16) & 127) == 0,
+                  "residual apply: operands must be 128-byte aligned");
+  return residual_run(nullptr, delta_bf16, log2_scale, dst, rows, n, batch, ws, as_stream(stream),
+                      nout);
 }

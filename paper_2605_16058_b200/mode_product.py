@@ -251,3 +251,55 @@ def from_transform_domain(t, ts: TransformSet, variant=BATCHED, threads=1):
         raise ValueError(f"unknown ttm variant {variant!r}")
     ts.check_dims(t.dims)
     return _run(t, lambda x: inverse_device(x, ts))
+
+
+class DeferredResidual:
+    """The exact FFT DCT of a tensor whose reference-operator residual
+    (starm_ttm_residual_bf16) has NOT been added yet: the bf16 operand is
+    kept in ``ws`` so the residual can be applied later to all output slices
+    (``apply_all``) or only to a selection of them (``apply_cols`` on a
+    gathered copy): the pruned tolerance path corrects only the slices it
+    keeps.  3-way tensors, forward DCT-II, n in [256, 4096]."""
+
+    def __init__(self, x: DeviceTensor, tr: Transform):
+        import torch
+        m, p, n = x.dims
+        self.tr, self.rows, self.n, self.device = tr, m * p, n, x.device
+        lib = nat.load()
+        nbytes = lib.starm_ttm_residual_workspace_bytes(self.rows, n, 1)
+        self._ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=x.device)
+        self.base = self._ws.data_ptr() + (-self._ws.data_ptr()) % 128
+        self.out = DeviceTensor.empty(x.dims, x.device)
+        nat.call("starm_dct_pack_f64", x.data.data_ptr(), self.out.data.data_ptr(), self.rows, n, 1,
+                 0, self.base, nbytes, nat.stream_ptr(x.device))
+
+    def _apply(self, dst, delta_rows, nout):
+        op = self.tr.residual_operand(self.device)
+        delta, e = op
+        nat.call("starm_residual_apply_f64", self.base, delta_rows.data_ptr(), int(e),
+                 dst.data_ptr(), self.rows, self.n, nout, 1, nat.stream_ptr(self.device))
+
+    def apply_all(self, dst=None):
+        """Complete the reference operator on every slice of ``self.out``."""
+        delta, _ = self.tr.residual_operand(self.device)
+        self._apply((dst if dst is not None else self.out.data), delta, self.n)
+
+    def apply_cols(self, sub, ids_dev):
+        """``sub`` (rows x len(ids)) holds FFT-only slices ``ids`` of out: add
+        their residual columns (Delta rows ids, zero-padded to 256)."""
+        import torch
+        delta, _ = self.tr.residual_operand(self.device)
+        ns = int(ids_dev.numel())
+        pad = ((ns + 255) // 256) * 256
+        sel = torch.zeros((pad, self.n), dtype=delta.dtype, device=self.device)
+        sel[:ns] = delta.view(self.n, self.n).index_select(0, ids_dev)
+        self._apply(sub, sel, ns)
+
+
+def deferrable(ts: TransformSet, dims) -> bool:
+    """True when the forward transform is one DCT-kind mode with the FFT +
+    residual route (so the residual can be deferred)."""
+    if len(dims) != 3 or len(ts) != 1 or os.environ.get("STARM_EXACT_DCT", "0") == "1":
+        return False
+    return _fast_kind(ts[0], dims[2]) == DCT
+
