@@ -1,11 +1,18 @@
 """t-SVDM compression entry points on the B200 (reference tsvdm.py).
 
 Pipeline of ``tsvdm_tolerance`` for a tensor A (m x p x N slices):
-  K1 forward TTM (DMMA)  ->  K3-K6 values-only Jacobi over every slice
-  ->  K7 device threshold (exact compute_threshold semantics)
-  ->  one 40-byte D2H (ranks total, j, tau, energies)
-  ->  K3-K6 truncated Jacobi on the slices with rank > 0, writing the
-      packed factors directly (the pack is fused into the SVD epilogue).
+  K1 forward transform (DCT: exact FFT + the reference operator's residual
+     on tcgen05; other M: DMMA GEMM)
+  ->  per-slice energies and the certified pruning (_tolerance_pruned):
+      slices whose energy bounds every sigma^2 below the crossing value are
+      left out of the SVD when the threshold certifies it
+  ->  K3-K6 values pass (QR + band reduction, bulge chase, bisection) over
+      the kept slices, keeping each slice's factorisation state
+  ->  K7 device threshold (compute_threshold semantics; started at the
+      left-out energy when pruned)
+  ->  one small D2H (tau, energies, ranks total, certificate, SVD status)
+  ->  K3-K6 truncated pass on the slices with rank > 0 from the kept state,
+      writing the packed factors directly.
 Everything stays in HBM; host inputs are uploaded once and outputs are
 copied back once.
 """
