@@ -3067,6 +3067,239 @@ __global__ void __launch_bounds__(256) svd_lqapply_kernel(SvdParams P) {
   }
 }
 
+// ----------------------------------------------------------------------
+// Blocked back-transformation of the bulge-chase reflectors on DMMA
+// (n > 400: c3, c4).  The right reflectors H_{i,k} (sweep i, task k) act on
+// coordinates c0 = i + 16k + 1 .. c0 + 15 and must be applied to every
+// vector x in the reverse of the chase order.  Grouping 16 consecutive
+// sweeps with the same task index, B(g, k) = H_{16g,k} ... H_{16g+15,k},
+// gives a compact-WY block I - V T V^T on the 32-row window
+// [16 (g + k), 16 (g + k) + 32) (V lower trapezoidal: column j holds
+// v_{16g+j,k} at window rows j + 1 .. j + 16).  Reflectors of different
+// blocks overlap only as follows: B(g, k) meets B(g, k - 1) and
+// B(g + 1, k - 2 .. k), and in every overlapping pair the reverse chase
+// order applies the larger sweep first -- i.e. B(g + 1, .) before B(g, .),
+// and within a group B(g, k - 1) before B(g, k) (H_{i',k-1} with i' > i
+// overlaps H_{i,k}; H_{i,k-1} with i' < i does not).  So the schedule
+// g = G - 1 .. 0, k = 0 .. K_g - 1 is the sequential product exactly.
+// T (16 x 16, dlarft forward) of every block is built once per slice by
+// svd_bt_tlog_kernel; svd_bt_blocked_kernel keeps KB vectors resident in
+// shared memory and applies each block with three DMMA phases per warp
+// (warp = 8 vectors): Y^T = X_R^T V, Z^T = Y^T T^T, X_R^T -= Z^T V^T, the
+// K index of the last two permuted to (2t, 2t+1, 8+2t, 9+2t) so the
+// accumulators of one phase are the A fragments of the next (no shuffle, no
+// shared-memory round trip).  Every vector depends only on itself: the
+// truncated factors stay the leading full factors bit for bit.
+// ----------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t bt_groups(int64_t n) { return n >= 3 ? (n - 3) / BW + 1 : 0; }
+__host__ __device__ __forceinline__ int64_t bt_gtasks(int64_t n, int64_t g) { return hb_tasks(n, g * BW); }
+__host__ __device__ __forceinline__ int64_t bt_nblocks(int64_t n) {
+  int64_t t = 0;
+  for (int64_t g = 0; g < bt_groups(n); ++g) t += bt_gtasks(n, g);
+  return t;
+}
+constexpr int BTV_S = 20;  // V window row stride (doubles, = 4 mod 16: conflict-free B fragments)
+constexpr int BTT_S = 20;  // T row stride
+constexpr int BT_NST = 8;  // blocks in flight (records + T): covers the L2/HBM latency of a block
+
+// T of every block of every slice: one warp per (list position, block).
+__global__ void __launch_bounds__(128) svd_bt_tlog_kernel(SvdParams P, double* tlog, int64_t nblk) {
+  __shared__ double vbuf[4][32 * 17];
+  __shared__ double gbuf[4][16 * 17];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = int(P.n);
+  const int64_t kmax = hb_kmax(n), G = bt_groups(n);
+  double* V = vbuf[warp];
+  double* Gm = gbuf[warp];
+  const int64_t total = P.count * nblk;
+  for (int64_t w = int64_t(blockIdx.x) * 4 + warp; w < total; w += int64_t(gridDim.x) * 4) {
+    const int64_t it = w / nblk, b = w % nblk;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
+    // block index b -> (g, k): groups from the last one down
+    int64_t g = G - 1, rem = b;
+    while (rem >= bt_gtasks(n, g)) rem -= bt_gtasks(n, g--);
+    const int64_t k = rem;
+    const double* lg = P.hhlog + si * P.hhcap;
+    for (int e = lane; e < 32 * 17; e += 32) V[e] = 0.0;
+    __syncwarp();
+    double tau = 0.0;
+    if (lane < BW) {  // lane j: reflector of sweep 16 g + j (identity if the task does not exist)
+      const int64_t i = g * BW + lane;
+      if (i <= n - 3 && k < hb_tasks(n, i)) {
+        const double* rec = lg + (i * kmax + k) * HLOG;
+        tau = rec[0];
+        if (tau != 0.0) {
+          V[(lane + 1) * 17 + lane] = 1.0;
+          for (int l = 1; l < BW; ++l) V[(lane + 1 + l) * 17 + lane] = rec[l];
+        }
+      }
+    }
+    __syncwarp();
+    // Gram G[a][c] = sum_l V[l][a] V[l][c] (8 entries per lane)
+    for (int e = lane; e < BW * BW; e += 32) {
+      const int a = e >> 4, c = e & 15;
+      double acc = 0.0;
+      for (int l = 0; l < 32; ++l) acc = fma(V[l * 17 + a], V[l * 17 + c], acc);
+      Gm[a * 17 + c] = acc;
+    }
+    __syncwarp();
+    // dlarft (forward, columnwise): lane i owns row i of T
+    double* T = tlog + (si * nblk + b) * (BW * BW);
+    const double taui = __shfl_sync(0xffffffffu, tau, lane & 15);
+    if (lane < BW) {
+      double row[BW];
+#pragma unroll
+      for (int j = 0; j < BW; ++j) row[j] = 0.0;
+#pragma unroll
+      for (int j = 0; j < BW; ++j) {
+        const double tj = __shfl_sync(0x0000ffffu, tau, j);
+        if (j == lane) row[j] = taui;
+        if (j > lane) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < BW; ++l)
+            if (l >= lane && l < j) acc = fma(row[l], Gm[l * 17 + j], acc);
+          row[j] = -tj * acc;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BW; ++j) T[lane * BW + j] = row[j];
+    }
+    __syncwarp();
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(KB * 4) svd_bt_blocked_kernel(SvdParams P, const double* tlog,
+                                                               int64_t nblk) {
+  constexpr int NW = KB / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int n = int(P.n), xs = lq_xs(P.n);
+  const int64_t NP = P.NP, RP = P.RP, kmax = hb_kmax(n), G = bt_groups(n);
+  double* X = reinterpret_cast<double*>(smem_raw);   // [KB][xs]
+  double* Vb = X + KB * xs;                          // [2][32 * BTV_S]
+  double* Tb = Vb + 2 * 32 * BTV_S;                  // [BT_NST][16 * BTT_S]
+  double* Rb = Tb + BT_NST * BW * BTT_S;             // [BT_NST][16 records * 16] raw log records
+  const int ngroups = (n + KB - 1) / KB;
+  for (int64_t cta = blockIdx.x; cta < P.count * ngroups; cta += gridDim.x) {
+    const int64_t it = cta / ngroups;
+    const int j0 = int(cta % ngroups) * KB;
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;
+    const int64_t slice = P.ids ? P.ids[it] : it;
+    const int kv = int(kout_of(P, slice));
+    if (j0 >= kv) continue;
+    double* vb = P.vsel + si * RP * NP;
+    for (int e = tid; e < KB * xs; e += KB * 4) {
+      const int v = e / xs, q = e - v * xs;
+      X[e] = (j0 + v < kv && q < n) ? vb[int64_t(j0 + v) * RP + q] : 0.0;
+    }
+    const double* lg = P.hhlog + si * P.hhcap;
+    const double* tl = tlog + si * nblk * (BW * BW);
+    // stage block b (records + T) into buffer slot: records of sweeps 16 g + j, task k
+    auto stage = [&](int64_t b, int64_t g, int64_t k, int slot) {
+      double* rb = Rb + slot * (BW * BW);
+      double* tb = Tb + slot * (BW * BTT_S);
+      for (int e = tid; e < BW * (BW / 2); e += KB * 4) {
+        const int j = e / (BW / 2), h = (e % (BW / 2)) * 2;
+        const int64_t i = g * BW + j;
+        const bool live = i <= n - 3 && k < hb_tasks(n, i);
+        cp_async16(rb + j * BW + h, live ? lg + (i * kmax + k) * HLOG + h : lg, live ? 16 : 0);
+        const int a = e / (BW / 2), c = (e % (BW / 2)) * 2;
+        cp_async16(tb + a * BTT_S + c, tl + b * (BW * BW) + a * BW + c, 16);
+      }
+      cp_async_commit();
+    };
+    int64_t gcur = G - 1, kcur = 0;
+    auto advance = [&](int64_t& g, int64_t& k) {
+      if (++k >= bt_gtasks(n, g)) {
+        --g;
+        k = 0;
+      }
+    };
+    // ring of BT_NST blocks: blocks b .. b + BT_NST - 2 in flight
+    int64_t gs = gcur, ks = kcur;
+    for (int q = 0; q < BT_NST - 1; ++q) {
+      if (q < nblk) {
+        stage(q, gs, ks, q);
+        advance(gs, ks);
+      } else {
+        cp_async_commit();
+      }
+    }
+    const double* xw = X + (8 * warp + g8) * xs;   // this lane's vector (row = vector g8 of the warp)
+    double* xwm = X + (8 * warp + g8) * xs;
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int slot = int(b % BT_NST), vslot = int(b & 1);
+      cp_async_wait<BT_NST - 2>();
+      __syncthreads();
+      {  // V window of block b from its staged records
+        double* Vw = Vb + vslot * (32 * BTV_S);
+        const double* rb = Rb + slot * (BW * BW);
+        for (int e = tid; e < 32 * BW; e += KB * 4) {
+          const int l = e / BW, j = e % BW;
+          const int d = l - 1 - j;
+          double v = 0.0;
+          if (d >= 0 && d < BW && rb[j * BW] != 0.0) v = d == 0 ? 1.0 : rb[j * BW + d];
+          Vw[l * BTV_S + j] = v;
+        }
+      }
+      if (b + BT_NST - 1 < nblk) {  // refill the slot block b - 1 used
+        stage(b + BT_NST - 1, gs, ks, int((b + BT_NST - 1) % BT_NST));
+        advance(gs, ks);
+      } else {
+        cp_async_commit();
+      }
+      __syncthreads();
+      const int rb0 = int(BW * (gcur + kcur));          // window rows rb0 .. rb0 + 31
+      const double* V = Vb + vslot * (32 * BTV_S);
+      const double* T = Tb + slot * (BW * BTT_S);
+      // Y^T (8 vectors x 16) = X_R^T V: K = 32 window rows
+      double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int s4 = 0; s4 < 8; ++s4) {
+        const int rr = 4 * s4 + t4;
+        const double a = rb0 + rr < xs ? xw[rb0 + rr] : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma884n(y[ni][0], y[ni][1], a, V[rr * BTV_S + 8 * ni + g8]);
+      }
+      // Z^T = Y^T T^T: K order (2t, 2t+1, 8+2t, 9+2t) = (y[0][0], y[0][1], y[1][0], y[1][1])
+      double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const int cs[4] = {2 * t4, 2 * t4 + 1, 8 + 2 * t4, 9 + 2 * t4};
+      const double ya[4] = {y[0][0], y[0][1], y[1][0], y[1][1]};
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+          dmma884n(z[ni][0], z[ni][1], ya[s4], T[(8 * ni + g8) * BTT_S + cs[s4]]);
+      // X_R^T -= Z^T V^T: 4 row tiles of 8, same K order
+      const double za[4] = {-z[0][0], -z[0][1], -z[1][0], -z[1][1]};
+      __syncwarp();
+#pragma unroll
+      for (int ri = 0; ri < 4; ++ri) {
+        const int r = rb0 + 8 * ri + 2 * t4;
+        double d0 = r < xs ? xwm[r] : 0.0, d1 = r + 1 < xs ? xwm[r + 1] : 0.0;
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) dmma884n(d0, d1, za[s4], V[(8 * ri + g8) * BTV_S + cs[s4]]);
+        __syncwarp();
+        if (r < xs) xwm[r] = d0;
+        if (r + 1 < xs) xwm[r + 1] = d1;
+      }
+      advance(gcur, kcur);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int e = tid; e < KB * int(RP); e += KB * 4) {
+      const int v = e / int(RP), q = e - v * int(RP);
+      if (j0 + v < kv) vb[int64_t(j0 + v) * RP + q] = q < n ? X[v * xs + q] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
 // Output kernel of the bidiagonal vector path: sigma are in P.s (bisection),
 // right singular vectors of X in vsel (sorted order); emit U / V / packed
 // factors through the shared emit_vectors (other side = X V / ||X V||).
@@ -3286,10 +3519,21 @@ struct Plan {
   int hb_threads;
   size_t vsmem, tsmem;
   size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
-      off_vsel, off_ii, total;
+      off_vsel, off_ii, off_tlog, total;
+  int bt_kb;                // blocked back-transformation: vectors per CTA (0 = per-warp kernel)
+  int64_t bt_nblk;
 };
 
 int g_tune_inner = 1;
+// STARM_BT_BLOCKED=0: the per-warp back-transformation for n > 400 too (A/B runs)
+const bool g_bt_blocked = [] {
+  const char* e = getenv("STARM_BT_BLOCKED");
+  return !(e && e[0] == '0');
+}();
+size_t bt_blocked_smem(int64_t n, int kb) {
+  return (size_t(kb) * lq_xs(n) + 2 * 32 * BTV_S + size_t(BT_NST) * (BW * BTT_S + BW * BW)) *
+         sizeof(double);
+}
 // reduce-kernel CTA size: 0 = automatic, else 256 or 512 (env STARM_REDUCE_THREADS)
 int g_reduce_threads = [] {
   const char* e = getenv("STARM_REDUCE_THREADS");
@@ -3450,6 +3694,19 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.off_rcnt = take(0);
   g.off_vsel = take(g.logs ? size_t(count) * g.RP * g.NP * sizeof(double) : 0);
   g.off_ii = take(g.logs ? size_t(g.ii_threads) * 6 * 2 * g.NP * sizeof(double) : 0);
+  // blocked back-transformation (n > 400, the DMMA LQ-panel range): T of
+  // every 16-sweep block per slice, 32 or 16 resident vectors per CTA
+  g.bt_kb = 0;
+  g.bt_nblk = 0;
+  if (g.logs && g.n > 400 && g_bt_blocked) {
+    auto btsm = [&](int kb) { return bt_blocked_smem(g.n, kb); };
+    // measured: c4 (n = 512, 32 vectors / 4 warps per CTA) 238 -> 172 ms against the
+    // per-warp kernel; c3 (n = 1024: only 16 vectors / 2 warps fit) 26 -> 55 ms,
+    // so the 16-vector form is not used
+    g.bt_kb = btsm(32) <= size_t(200 * 1024) ? 32 : 0;
+    if (g.bt_kb) g.bt_nblk = bt_nblocks(g.n);
+  }
+  g.off_tlog = take(g.bt_kb ? size_t(count) * g.bt_nblk * BW * BW * sizeof(double) : 0);
   g.total = off;
   *pl = g;
   return STARM_OK;
@@ -3742,7 +3999,24 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       const int lkb = (g_lq_warp || pl.n <= 400) ? 0
                       : (lq_smem(pl.n, 32) <= size_t(200 * 1024) ? 32
                          : (lq_smem(pl.n, 16) <= size_t(200 * 1024) ? 16 : 0));
-      svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0);
+      if (lkb && pl.bt_kb) {
+        double* tlog = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + pl.off_tlog);
+        const int64_t warps = count * pl.bt_nblk;
+        int64_t tb = (warps + 3) / 4;
+        if (tb > int64_t(sms) * 16) tb = int64_t(sms) * 16;
+        svd_bt_tlog_kernel<<<unsigned(tb), 128, 0, st>>>(P, tlog, pl.bt_nblk);
+        STARM_LAUNCH_CHECK();
+        const size_t bsm = bt_blocked_smem(pl.n, pl.bt_kb);
+        auto bk = pl.bt_kb == 32 ? svd_bt_blocked_kernel<32> : svd_bt_blocked_kernel<16>;
+        STARM_CUDA_TRY(cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bsm)));
+        int per = int((227 * 1024) / (bsm + 1024));
+        per = per < 1 ? 1 : (per > 4 ? 4 : per);
+        int64_t bb = count * ((pl.n + pl.bt_kb - 1) / pl.bt_kb);
+        if (bb > int64_t(sms) * per) bb = int64_t(sms) * per;
+        bk<<<unsigned(bb), pl.bt_kb * 4, bsm, st>>>(P, tlog, pl.bt_nblk);
+      } else {
+        svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0);
+      }
       STARM_LAUNCH_CHECK();
       if (lkb) {
         const size_t lsm = lq_smem(pl.n, lkb);
