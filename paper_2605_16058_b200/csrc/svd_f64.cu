@@ -3525,6 +3525,13 @@ struct Plan {
 };
 
 int g_tune_inner = 1;
+// inverse-iteration threads per SM (env STARM_II_PER_SM; each owns 12 n doubles of scratch)
+const int g_ii_per_sm = [] {
+  // measured on c4 (895 K vectors): 128 -> 173 ms, 512 -> 111 ms, 1024 -> 110 ms
+  const char* e = getenv("STARM_II_PER_SM");
+  const int v = e ? atoi(e) : 512;
+  return (v >= 32 && v <= 2048) ? (v / 32) * 32 : 512;
+}();
 // STARM_BT_BLOCKED=0: the per-warp back-transformation for n > 400 too (A/B runs)
 const bool g_bt_blocked = [] {
   const char* e = getenv("STARM_BT_BLOCKED");
@@ -3652,7 +3659,8 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     if (rc) return rc;
     g.btw = per;  // back-transform CTAs per SM
     const int64_t work = count * g.n;
-    g.ii_threads = int(work < int64_t(sms) * 128 ? work : int64_t(sms) * 128);
+    const int64_t iicap = int64_t(sms) * g_ii_per_sm;
+    g.ii_threads = int(work < iicap ? work : iicap);
     g.ii_threads = int(round_up(g.ii_threads < 1 ? 1 : g.ii_threads, 128));  // whole blocks
     g.hhcap = (g.n >= 3 ? (g.n - 2) : 1) * hb_kmax(g.n) * HLOG;
   }
