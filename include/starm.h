@@ -146,6 +146,16 @@ int starm_ttm_residual_bf16(const double* src, const uint16_t* delta_bf16, int l
                             double* dst, int64_t rows, int64_t n, int64_t batch, void* ws,
                             size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------ data-driven transform
+ * G = unfold(k) unfold(k)^T (inner x inner, column-major, exactly
+ * symmetric) over the (rows, inner, batch) view of the mode-k product: the
+ * Gram matrix whose eigenvectors (starm_svd_f64 on G) are the left singular
+ * vectors data_driven_transform takes (transforms.py:94-110).  FP64 DMMA,
+ * deterministic split-K.  ws: starm_gram_workspace_bytes bytes. */
+size_t starm_gram_workspace_bytes(int64_t rows, int64_t inner, int64_t batch);
+int starm_gram_f64(const double* a, int64_t rows, int64_t inner, int64_t batch, double* g, void* ws,
+                   size_t ws_bytes, void* stream);
+
 /* ----------------------------------------------------- K11 facewise GEMM
  * Replaces _facewise_matmul (tsvdm.py:205-216): for each slice i,
  *   C_i (m x l) = A_i (m x p) * B_i (p x l), all column-major, slice

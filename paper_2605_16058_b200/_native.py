@@ -78,6 +78,9 @@ SIGNATURES = {
                                    c_void_p, c_size_t, c_void_p]),
     "starm_residual_apply_f64": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p]),
+    "starm_gram_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64]),
+    "starm_gram_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_size_t,
+                               c_void_p]),
     "starm_launch_count_reset": (ctypes.c_longlong, []),
     "starm_svd_tune": (c_int, [c_int, c_int, c_int, c_int]),
     "starm_svd_stats": (c_int, [c_void_p, c_int]),

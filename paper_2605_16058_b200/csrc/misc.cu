@@ -501,3 +501,116 @@ extern "C" int starm_slice_energy_f64(const double* a, int64_t slice_elems, int6
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }
+
+// ------------------------------------------------------------- mode Gram
+// G = sum_b A_b^T A_b for the `batch` column-major (rows x inner) blocks of
+// the mode-k view (TTMPlan): G = unfold(k) unfold(k)^T, the Gram matrix of
+// the data-driven transform (transforms.py:94-110).  64 x 64 output tiles on
+// DMMA (8 warps of 32 x 16), K = rows x batch split over `ks` CTA slices
+// whose partial tiles are summed in a fixed order (deterministic), then
+// symmetrised.
+namespace starm {
+namespace {
+constexpr int GR_T = 64, GR_KC = 16, GR_S = GR_T + 8;
+
+__global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restrict__ a, int64_t rows,
+                                                           int64_t inner, int64_t batch, int64_t kchunk,
+                                                           int64_t tiles1, double* __restrict__ part) {
+  __shared__ double us[GR_KC][GR_S];
+  __shared__ double gs[GR_KC][GR_S];
+  const int64_t tile = blockIdx.x, ks = blockIdx.y;
+  const int64_t i0 = (tile % tiles1) * GR_T, j0 = (tile / tiles1) * GR_T;
+  const int64_t K = rows * batch;
+  const int64_t k_lo = ks * kchunk, k_hi = k_lo + kchunk < K ? k_lo + kchunk : K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[4][2][2] = {};
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += GR_KC) {
+    for (int e = threadIdx.x; e < GR_KC * GR_T; e += 256) {
+      const int kk = e % GR_KC, c = e / GR_KC;
+      const int64_t k = k0 + kk;
+      const bool in = k < k_hi;
+      const int64_t b = in ? k / rows : 0, r = in ? k - b * rows : 0;
+      const double* blk = a + b * rows * inner + r;
+      us[kk][c] = (in && i0 + c < inner) ? blk[(i0 + c) * rows] : 0.0;
+      gs[kk][c] = (in && j0 + c < inner) ? blk[(j0 + c) * rows] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < GR_KC; k4 += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = us[k4 + tq][32 * wm + 8 * i + gq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = gs[k4 + tq][16 * wn + 8 * j + gq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884n(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (ks * gridDim.x + tile) * (GR_T * GR_T);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = 32 * wm + 8 * i + gq, c = 16 * wn + 8 * j + 2 * tq;
+      out[r + c * GR_T] = acc[i][j][0];
+      out[r + (c + 1) * GR_T] = acc[i][j][1];
+    }
+}
+
+__global__ void gram_final_kernel(const double* __restrict__ part, int64_t inner, int64_t tiles1,
+                                  int64_t ntiles, int64_t nks, double* __restrict__ g) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= inner * inner) return;
+  const int64_t i = e % inner, j = e / inner;
+  auto at = [&](int64_t r, int64_t c) {
+    const int64_t tile = (r / GR_T) + (c / GR_T) * tiles1;
+    const int64_t off = (r % GR_T) + (c % GR_T) * GR_T;
+    double s = 0.0;
+    for (int64_t ks = 0; ks < nks; ++ks) s += part[(ks * ntiles + tile) * (GR_T * GR_T) + off];
+    return s;
+  };
+  g[e] = 0.5 * (at(i, j) + at(j, i));   // exact symmetry
+}
+
+int64_t gram_ksplit(int64_t rows, int64_t inner, int64_t batch) {
+  const int64_t tiles1 = (inner + GR_T - 1) / GR_T;
+  const int64_t K = rows * batch;
+  int64_t ks = (4 * 148 + tiles1 * tiles1 - 1) / (tiles1 * tiles1);   // ~4 CTAs per SM
+  const int64_t maxks = (K + 4 * GR_KC - 1) / (4 * GR_KC);
+  if (ks > maxks) ks = maxks;
+  return ks < 1 ? 1 : ks;
+}
+}  // namespace
+}  // namespace starm
+
+extern "C" size_t starm_gram_workspace_bytes(int64_t rows, int64_t inner, int64_t batch) {
+  if (rows < 1 || inner < 1 || batch < 1) return 0;
+  const int64_t tiles1 = (inner + GR_T - 1) / GR_T;
+  return size_t(gram_ksplit(rows, inner, batch) * tiles1 * tiles1 * GR_T * GR_T) * sizeof(double);
+}
+
+extern "C" int starm_gram_f64(const double* a, int64_t rows, int64_t inner, int64_t batch, double* g,
+                              void* ws, size_t ws_bytes, void* stream) {
+  STARM_CHECK_ARG(rows >= 1 && inner >= 1 && batch >= 1, "gram: extents must be positive");
+  STARM_CHECK_ARG(a && g && ws, "gram: null pointer");
+  STARM_CHECK_ARG(ws_bytes >= starm_gram_workspace_bytes(rows, inner, batch), "gram: workspace too small");
+  const cudaStream_t st = as_stream(stream);
+  const int64_t tiles1 = (inner + GR_T - 1) / GR_T, ntiles = tiles1 * tiles1;
+  const int64_t ks = gram_ksplit(rows, inner, batch);
+  const int64_t K = rows * batch;
+  const int64_t kchunk = round_up(ceil_div(K, ks), GR_KC);
+  STARM_CHECK_ARG(ntiles < (int64_t(1) << 31) && ks < 65536, "gram: too large");
+  const dim3 grid{unsigned(ntiles), unsigned(ks), 1u};
+  gram_partial_kernel<<<grid, 256, 0, st>>>(a, rows, inner, batch, kchunk, tiles1,
+                                           static_cast<double*>(ws));
+  STARM_LAUNCH_CHECK();
+  gram_final_kernel<<<unsigned(ceil_div(inner * inner, 256)), 256, 0, st>>>(
+      static_cast<const double*>(ws), inner, tiles1, ntiles, ks, g);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}

@@ -135,3 +135,28 @@ def configs():
 
 if __name__ == "__main__":
     main()
+
+
+def datadriven():
+    """Reference data_driven_transform (transforms.py:94-110) on seeded tensors,
+    and a tolerance t-SVDM over it -> tests/golden/golden_datadriven.npz."""
+    out = {}
+    cases = {"3way": ((12, 9, 16), 2, 21), "wide_rest": ((3, 2, 12), 2, 22), "4way_m3": ((4, 5, 3, 10), 3, 23)}
+    for name, (dims, mode, seed) in cases.items():
+        rng = np.random.default_rng(seed)
+        a = np.asfortranarray(rng.standard_normal(dims) * np.logspace(0, -1, dims[mode]).reshape(
+            [dims[mode] if k == mode else 1 for k in range(len(dims))]))
+        tr = starm.data_driven_transform(starm.DenseTensor(a), mode)
+        out[f"{name}/m"] = tr.matrix
+    rng = np.random.default_rng(30)
+    a = np.asfortranarray(rng.standard_normal((10, 12, 24)) + np.einsum(
+        "i,j,k->ijk", rng.standard_normal(10), rng.standard_normal(12), rng.standard_normal(24)) * 3)
+    t = starm.DenseTensor(a)
+    ts = starm.TransformSet.build(a.shape, "data-driven", tensor=t)
+    c = starm.tsvdm_tolerance(t, ts, 0.2)
+    out["tol/ranks"] = c.ranks
+    out["tol/disc"] = np.array(c.discarded_energy)
+    out["tol/total"] = np.array(c.total_energy)
+    out["tol/s"] = starm.svd_values_only(starm.to_transform_domain(t, ts))
+    np.savez_compressed(os.path.join(HERE, "golden_datadriven.npz"), **out)
+    print(f"wrote {len(out)} arrays to tests/golden/golden_datadriven.npz")

@@ -313,3 +313,66 @@ def test_tolerance_pruning_certificate_failure_falls_back():
     assert clock.info.get("prune_certificate") in ("failed", None)
     oref = oracle.tsvdm_tolerance(a, [oracle.dct_matrix(512)], 1e-2)
     assert np.array_equal(got.ranks, oref["ranks"])
+
+
+# ------------------------------------------ data-driven transform
+
+DD = np.load(os.path.join(HERE, "golden", "golden_datadriven.npz"))
+
+
+@pytest.mark.parametrize("name,dims,mode,seed", [("3way", (12, 9, 16), 2, 21),
+                                                  ("wide_rest", (3, 2, 12), 2, 22),
+                                                  ("4way_m3", (4, 5, 3, 10), 3, 23)])
+def test_data_driven_transform_matches_reference(name, dims, mode, seed):
+    """Device Gram (starm_gram_f64) + device SVD of G against the reference's
+    gesvd of the unfolding (transforms.py:94-110): rows equal up to sign for
+    the nonzero singular values; the null-space completion spans the same
+    subspace."""
+    rng = np.random.default_rng(seed)
+    a = np.asfortranarray(rng.standard_normal(dims) * np.logspace(0, -1, dims[mode]).reshape(
+        [dims[mode] if k == mode else 1 for k in range(len(dims))]))
+    tr = sb.data_driven_transform(sb.DenseTensor(a), mode)
+    assert tr.kind == sb.DATA_DRIVEN
+    m, ref = tr.matrix, DD[f"{name}/m"]
+    n = m.shape[0]
+    assert np.linalg.norm(m @ m.T - np.eye(n)) <= 1e-12 * n
+    unf = sb.DenseTensor(a).unfold(mode)
+    rank = min(unf.shape)
+    for j in range(rank):
+        assert abs(abs(float(m[j] @ ref[j])) - 1.0) <= 1e-9, (j, float(m[j] @ ref[j]))
+    if rank < n:
+        p_got = m[rank:].T @ m[rank:]
+        p_ref = ref[rank:].T @ ref[rank:]
+        assert np.linalg.norm(p_got - p_ref) <= 1e-9
+
+
+def test_data_driven_tolerance_matches_reference():
+    rng = np.random.default_rng(30)
+    a = np.asfortranarray(rng.standard_normal((10, 12, 24)) + np.einsum(
+        "i,j,k->ijk", rng.standard_normal(10), rng.standard_normal(12), rng.standard_normal(24)) * 3)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "data-driven", tensor=t)
+    c = sb.tsvdm_tolerance(t, ts, 0.2)
+    assert np.array_equal(c.ranks, DD["tol/ranks"])
+    tot = float(DD["tol/total"])
+    assert abs(c.total_energy - tot) <= 1e-12 * tot
+    assert abs(c.discarded_energy - float(DD["tol/disc"])) <= 1e-10 * tot
+    s = sb.svd_values_only(sb.to_transform_domain(t, ts))
+    assert _sigma_all_close(s, DD["tol/s"]) == 0
+
+
+def test_data_driven_transform_at_scale():
+    """c2-shaped fibres (the paper's time mode, n = 1024): the Gram route
+    never forms the 1024 x 259920 unfolding's SVD; the basis is orthonormal
+    and diagonalises G to its eigenvalues."""
+    import torch
+    a = cf.config2(nlat=91, nlon=180, nt=1024, seed=5)
+    tr = sb.data_driven_transform(sb.DenseTensor(a), 2)
+    m = tr.matrix
+    assert np.linalg.norm(m @ m.T - np.eye(1024)) <= 1e-10 * 1024
+    unf = sb.DenseTensor(a).unfold(2)
+    g = unf @ unf.T
+    d = m @ g @ m.T
+    off = d - np.diag(np.diag(d))
+    assert np.linalg.norm(off) <= 1e-10 * np.linalg.norm(g)
+    assert np.all(np.diff(np.diag(d)) <= 1e-9 * d[0, 0])   # descending
