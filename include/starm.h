@@ -139,6 +139,16 @@ int starm_dct_residual_f64(const double* src, double* dst, int64_t rows, int64_t
  * columns per batch block (dst[b * rows * nout + f + j * rows]). */
 int starm_dct_pack_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch,
                        int inverse, void* ws, size_t ws_bytes, void* stream);
+/* starm_dct_pack_f64 restricted to the fibre block [f0, f0 + nf) of a
+ * (rows x n) tensor (batch 1, forward), transformed where it lies: src, dst
+ * and ws are the FULL tensor's buffers.  Blocks start on multiples of 128
+ * fibres and end on one or at `rows`; after every block has run the three
+ * buffers are exactly those starm_dct_pack_f64 leaves.  The drop-in
+ * tsvdm_tolerance(DenseTensor) uses it to transform each block behind the
+ * host-to-device copy of the next (the reference's np.matmul in
+ * ttm.py:113-135 has the whole tensor in memory at once). */
+int starm_dct_pack_block_f64(const double* src, double* dst, int64_t rows, int64_t n, int64_t f0,
+                             int64_t nf, void* ws, size_t ws_bytes, void* stream);
 int starm_residual_apply_f64(const void* ws, const uint16_t* delta_bf16, int log2_scale,
                              double* dst, int64_t rows, int64_t n, int64_t nout, int64_t batch,
                              void* stream);
@@ -245,6 +255,18 @@ int starm_threshold_pruned_f64(const double* s, int64_t r, int64_t nslices, doub
  * slice), deterministic: the bound sigma_max^2 <= f used for pruning. */
 int starm_slice_energy_f64(const double* a, int64_t slice_elems, int64_t nslices, double* f_out,
                            void* stream);
+
+/* Partial energies over the fibre block [f0, f0 + nf) of every slice
+ * (f_out[i] = sum_{f0 <= q < f0 + nf} a[i * slice_elems + q]^2). */
+int starm_slice_energy_block_f64(const double* a, int64_t slice_elems, int64_t nslices, int64_t f0,
+                                 int64_t nf, double* f_out, void* stream);
+
+/* Strided host-to-device copy (cudaMemcpy2DAsync, pitches and width in
+ * bytes): one fibre block of a host DenseTensor (tensor.py:76-98 layout)
+ * into the same place of its device copy; asynchronous for page-locked
+ * host memory. */
+int starm_copy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                     size_t height, void* stream);
 
 /* ---------------------------------------------------------- K8 offsets
  * slicesvd.py:208-211: u_off[0]=g_off[0]=0, u_off[i+1] = u_off[i] +

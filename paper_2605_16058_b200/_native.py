@@ -76,6 +76,12 @@ SIGNATURES = {
     "starm_slice_energy_f64": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "starm_dct_pack_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int,
                                    c_void_p, c_size_t, c_void_p]),
+    "starm_dct_pack_block_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                         c_void_p, c_size_t, c_void_p]),
+    "starm_slice_energy_block_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                             c_void_p, c_void_p]),
+    "starm_copy2d_h2d": (c_int, [c_void_p, c_size_t, c_void_p, c_size_t, c_size_t, c_size_t,
+                                 c_void_p]),
     "starm_residual_apply_f64": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int64,
                                          c_int64, c_int64, c_void_p]),
     "starm_gram_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64]),
@@ -196,6 +202,14 @@ def stream_ptr(device=None) -> int:
     h = st.cuda_stream
     if h not in _STREAM_DEVICE or _STREAM_DEVICE[h] != st.device.index:
         _STREAM_DEVICE[h] = st.device.index
+    return h
+
+
+def register_stream(stream) -> int:
+    """Handle of an explicit torch stream, registered so ``call`` runs its
+    launches with the stream's device current."""
+    h = stream.cuda_stream
+    _STREAM_DEVICE[h] = stream.device.index
     return h
 
 

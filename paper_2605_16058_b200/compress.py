@@ -30,6 +30,7 @@ import numpy as np
 
 from . import _native as nat
 from .mode_product import (BATCHED, VARIANTS, DeferredResidual, deferrable, forward_device,
+                           pipelined_upload_applies,
                            inverse_device)
 from .slice_svd import (check_status, SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
                         VariableRankFactors, pack_offsets_device, svd_full_device,
@@ -432,7 +433,12 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
     if PRUNE and strategy != TRUNCATE and deferrable(ts, a.dims):
         # exact FFT DCT now; the reference operator's residual is added to the
         # slices the pruning keeps (or to all of them if it does not prune)
-        deferred = DeferredResidual(as_device(a, dev), ts[0])
+        if pipelined_upload_applies(a, ts):
+            # host input: block-wise H2D with the DCT, operand rows and slice
+            # energies of each block running behind the next block's copy
+            deferred = DeferredResidual.from_host(a, ts[0], dev)
+        else:
+            deferred = DeferredResidual(as_device(a, dev), ts[0])
         ahat = deferred.out
     else:
         ahat = forward_device(as_device(a, dev), ts)
@@ -599,7 +605,10 @@ def _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred=None):
     if n < 8 or strategy not in (MEMORY_EFFICIENT, COMPUTE_EFFICIENT):
         return None
     with clock.stage("prune-energy"):
-        sel = prune_select(ahat3, epsilon)
+        if deferred is not None and deferred.energies is not None:
+            sel = prune_choose(deferred.energies.cpu().numpy(), epsilon)
+        else:
+            sel = prune_select(ahat3, epsilon)
     if sel is None:
         return None
     keep_ids, e0, tbound = sel

@@ -47,8 +47,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // dct.cu: the fast DCT-II / DCT-III; with xbf the n = 1024 forward kernel
 // also writes the bf16 operand rows of the residual GEMM (*packed = true).
+// pitch: doubles between consecutive mode indices of a fibre (0 = rows).
 int dct_launch(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch, bool inv,
-               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st);
+               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st, int64_t pitch = 0);
 
 // gemm_f64.cu: C = A * B (batch 1, column-major) with the K10 error partials
 // of E against C fused into the epilogue (epart: 2 doubles per tile).

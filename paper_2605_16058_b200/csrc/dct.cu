@@ -128,7 +128,7 @@ __device__ __forceinline__ void fft_stages(cplx* z, const cplx* tw) {
 template <int LOGN, bool INVERSE>
 __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restrict__ src,
                                                           double* __restrict__ dst, int64_t rows,
-                                                          int64_t batch,
+                                                          int64_t pitch, int64_t batch,
                                                           const cplx* __restrict__ gtw,
                                                           const cplx* __restrict__ gpw) {
   constexpr int N = 1 << LOGN;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
         const int e = e0 + u * DCT_THREADS + threadIdx.x;
         const int f = e % F, t = e / F;
         const int64_t r = r0 + f;
-        v[u] = (e < total && r < rows) ? src[base + r + int64_t(t) * rows] : 0.0;
+        v[u] = (e < total && r < rows) ? src[base + r + int64_t(t) * pitch] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
       }
       const cplx w = gpw[j];
       const double xr = fma(w.re, v.re, w.im * v.im);  // Re(e^{-i theta} v)
-      dst[base + r + int64_t(j) * rows] = (j ? c1 : c0) * xr;
+      dst[base + r + int64_t(j) * pitch] = (j ? c1 : c0) * xr;
     }
   } else {
     // V^f_j = e^{i theta_j} (Y_j / c_j - i Y_{n-j} / c_{n-j}); z = V^a + i V^b
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
       const int p = e % P, j = e / P;  // consecutive threads: consecutive fibers
       double ya = 0.0, yb = 0.0, yna = 0.0, ynb = 0.0;
       const int64_t ra = r0 + 2 * p, rb = ra + 1;
-      const int64_t oj = base + int64_t(j) * rows, on = base + int64_t(N - j) * rows;
+      const int64_t oj = base + int64_t(j) * pitch, on = base + int64_t(N - j) * pitch;
       const double sj = j ? ic1 : ic0;
       if (ra < rows) {
         ya = src[oj + ra] * sj;
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(DCT_THREADS) dct_kernel(const double* __restri
       if (r >= rows) continue;
       const int pos = (t & 1) ? N - 1 - (t >> 1) : (t >> 1);
       const cplx zz = z[(f >> 1) * (N + ZPAD) + swz(pos)];
-      dst[base + r + int64_t(t) * rows] = ((f & 1) ? zz.im : zz.re) * inv;
+      dst[base + r + int64_t(t) * pitch] = ((f & 1) ? zz.im : zz.re) * inv;
     }
   }
 }
@@ -334,7 +334,7 @@ __device__ __forceinline__ void fft32_dif(cplx (&z)[32]) {
 // the f64 input.
 template <bool INV>
 __global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
-    const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
+    const double* __restrict__ src, double* __restrict__ dst, int64_t rows, int64_t pitch,
     const cplx* __restrict__ gtw, const cplx* __restrict__ gpw, int vec16,
     uint16_t* __restrict__ xbf, int64_t rows_pad) {
   constexpr int N = D32_N, F = 2 * D32_WARPS, NT = 32 * D32_WARPS;
@@ -352,14 +352,14 @@ __global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
 #pragma unroll 4
     for (int q = tid; q < 4 * N; q += NT) {
       const int t = q >> 2, s = q & 3;
-      cp_async16(&ch[ck(t, s)], sb + 2 * s + int64_t(t) * rows, 2 * s < nf ? 16 : 0);
+      cp_async16(&ch[ck(t, s)], sb + 2 * s + int64_t(t) * pitch, 2 * s < nf ? 16 : 0);
     }
   } else {
 #pragma unroll 4
     for (int q = tid; q < 4 * N; q += NT) {
       const int t = q >> 2, s = q & 3;
       double* d = reinterpret_cast<double*>(&ch[ck(t, s)]);
-      const double* g = sb + 2 * s + int64_t(t) * rows;
+      const double* g = sb + 2 * s + int64_t(t) * pitch;
       cp_async8(d, g, 2 * s < nf ? 8 : 0);
       cp_async8(d + 1, g + 1, 2 * s + 1 < nf ? 8 : 0);
     }
@@ -471,13 +471,13 @@ __global__ void __launch_bounds__(32 * D32_WARPS, 2) dct1024_kernel(
     for (int q = tid; q < 4 * N; q += NT) {
       const int t = q >> 2, s = q & 3;
       const cplx v = ch[ck(t, s)];
-      *reinterpret_cast<double2*>(db + 2 * s + int64_t(t) * rows) = make_double2(v.re, v.im);
+      *reinterpret_cast<double2*>(db + 2 * s + int64_t(t) * pitch) = make_double2(v.re, v.im);
     }
   } else {
     for (int q = tid; q < 4 * N; q += NT) {
       const int t = q >> 2, s = q & 3;
       const cplx v = ch[ck(t, s)];
-      double* g = db + 2 * s + int64_t(t) * rows;
+      double* g = db + 2 * s + int64_t(t) * pitch;
       if (2 * s < nf) g[0] = v.re;
       if (2 * s + 1 < nf) g[1] = v.im;
     }
@@ -523,8 +523,8 @@ int dct_tables(int logn, const cplx** tw, const cplx** pw, cudaStream_t st) {
 }
 
 template <int LOGN>
-int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool inverse,
-               cudaStream_t st, uint16_t* xbf = nullptr, int64_t rows_pad = 0) {
+int launch_dct(const double* src, double* dst, int64_t rows, int64_t pitch, int64_t batch,
+               bool inverse, cudaStream_t st, uint16_t* xbf = nullptr, int64_t rows_pad = 0) {
   constexpr int N = 1 << LOGN;
   constexpr int P = dct_pairs(LOGN);
   const size_t smem = (size_t(P) * (N + ZPAD) + N / 2) * sizeof(cplx);
@@ -539,7 +539,8 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
   if (LOGN == 10 && !g_dct_legacy) {
     const size_t sm2 = size_t(D32_CHUNKS) * sizeof(cplx);
     const int64_t t2 = (rows + 2 * D32_WARPS - 1) / (2 * D32_WARPS) * batch;
-    const int vec16 = (rows % 2 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
+    const int vec16 = (rows % 2 == 0) && (pitch % 2 == 0) &&
+                      (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
     // hoisted twiddle products at 2 CTAs / SM: 1.33 ms on c2, against 1.44 ms
     // for per-k1 table loads at 3 CTAs / SM and 1.36 ms for the hoisted
@@ -547,14 +548,14 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
     // each lane's 32 values straight from global memory (no staging) 2.4 ms
     auto kern = inverse ? dct1024_kernel<true> : dct1024_kernel<false>;
     STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)));
-    kern<<<unsigned(t2), 32 * D32_WARPS, sm2, st>>>(src, dst, rows, tw, pw, vec16,
+    kern<<<unsigned(t2), 32 * D32_WARPS, sm2, st>>>(src, dst, rows, pitch, tw, pw, vec16,
                                                     inverse ? nullptr : xbf, rows_pad);
     STARM_LAUNCH_CHECK();
     return STARM_OK;
   }
   auto kern = inverse ? dct_kernel<LOGN, true> : dct_kernel<LOGN, false>;
   STARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, batch, tw, pw);
+  kern<<<unsigned(tiles), DCT_THREADS, smem, st>>>(src, dst, rows, pitch, batch, tw, pw);
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }
@@ -565,23 +566,27 @@ int launch_dct(const double* src, double* dst, int64_t rows, int64_t batch, bool
 namespace starm {
 // Internal launcher (also used by starm_dct_residual_f64): when xbf is set
 // and the n = 1024 forward kernel runs, the bf16 operand rows are written
-// too; returns whether that happened through *packed.
+// too; returns whether that happened through *packed.  pitch (0: rows) is
+// the distance in doubles between consecutive mode indices of one fibre, so
+// a block of `rows` fibres of a wider tensor can be transformed where it
+// lies (batch must be 1 when pitch != rows).
 int dct_launch(const double* src, double* dst, int64_t rows, int64_t n, int64_t batch, bool inv,
-               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st) {
+               uint16_t* xbf, int64_t rows_pad, bool* packed, cudaStream_t st, int64_t pitch) {
+  if (pitch == 0) pitch = rows;
   if (packed) *packed = xbf && n == 1024 && !inv && !g_dct_legacy;
   switch (n) {
-    case 2: return launch_dct<1>(src, dst, rows, batch, inv, st);
-    case 4: return launch_dct<2>(src, dst, rows, batch, inv, st);
-    case 8: return launch_dct<3>(src, dst, rows, batch, inv, st);
-    case 16: return launch_dct<4>(src, dst, rows, batch, inv, st);
-    case 32: return launch_dct<5>(src, dst, rows, batch, inv, st);
-    case 64: return launch_dct<6>(src, dst, rows, batch, inv, st);
-    case 128: return launch_dct<7>(src, dst, rows, batch, inv, st);
-    case 256: return launch_dct<8>(src, dst, rows, batch, inv, st);
-    case 512: return launch_dct<9>(src, dst, rows, batch, inv, st);
-    case 1024: return launch_dct<10>(src, dst, rows, batch, inv, st, xbf, rows_pad);
-    case 2048: return launch_dct<11>(src, dst, rows, batch, inv, st);
-    default: return launch_dct<12>(src, dst, rows, batch, inv, st);
+    case 2: return launch_dct<1>(src, dst, rows, pitch, batch, inv, st);
+    case 4: return launch_dct<2>(src, dst, rows, pitch, batch, inv, st);
+    case 8: return launch_dct<3>(src, dst, rows, pitch, batch, inv, st);
+    case 16: return launch_dct<4>(src, dst, rows, pitch, batch, inv, st);
+    case 32: return launch_dct<5>(src, dst, rows, pitch, batch, inv, st);
+    case 64: return launch_dct<6>(src, dst, rows, pitch, batch, inv, st);
+    case 128: return launch_dct<7>(src, dst, rows, pitch, batch, inv, st);
+    case 256: return launch_dct<8>(src, dst, rows, pitch, batch, inv, st);
+    case 512: return launch_dct<9>(src, dst, rows, pitch, batch, inv, st);
+    case 1024: return launch_dct<10>(src, dst, rows, pitch, batch, inv, st, xbf, rows_pad);
+    case 2048: return launch_dct<11>(src, dst, rows, pitch, batch, inv, st);
+    default: return launch_dct<12>(src, dst, rows, pitch, batch, inv, st);
   }
 }
 }  // namespace starm
@@ -599,5 +604,5 @@ extern "C" int starm_dct_f64(const double* src, double* dst, int64_t rows, int64
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool inv = inverse != 0;
-  return dct_launch(src, dst, rows, n, batch, inv, nullptr, 0, nullptr, st);
+  return dct_launch(src, dst, rows, n, batch, inv, nullptr, 0, nullptr, st, 0);
 }

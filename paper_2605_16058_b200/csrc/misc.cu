@@ -467,9 +467,10 @@ extern "C" int starm_ttm_f32(const float* src, const float* mat, float* dst, int
 namespace starm {
 namespace {
 __global__ void __launch_bounds__(256) slice_energy_kernel(const double* __restrict__ a,
-                                                           int64_t elems, double* __restrict__ f) {
+                                                           int64_t elems, int64_t pitch,
+                                                           double* __restrict__ f) {
   __shared__ double red[256];
-  const double* x = a + int64_t(blockIdx.x) * elems;
+  const double* x = a + int64_t(blockIdx.x) * pitch;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t i = threadIdx.x;
   for (; i + 768 < elems; i += 1024) {
@@ -497,8 +498,36 @@ extern "C" int starm_slice_energy_f64(const double* a, int64_t slice_elems, int6
   if (nslices == 0) return STARM_OK;
   STARM_CHECK_ARG(a && f_out, "slice energy: null pointer");
   STARM_CHECK_ARG(nslices < (int64_t(1) << 31), "slice energy: too many slices");
-  slice_energy_kernel<<<unsigned(nslices), 256, 0, as_stream(stream)>>>(a, slice_elems, f_out);
+  slice_energy_kernel<<<unsigned(nslices), 256, 0, as_stream(stream)>>>(a, slice_elems, slice_elems,
+                                                                        f_out);
   STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+// The same sums over the fibre block [f0, f0 + nf) of every slice
+// (f_out[i] = sum of squares of a[i * slice_elems + f0 .. + nf)): partial
+// energies of a tensor whose fibre blocks become available one at a time.
+extern "C" int starm_slice_energy_block_f64(const double* a, int64_t slice_elems, int64_t nslices,
+                                            int64_t f0, int64_t nf, double* f_out, void* stream) {
+  STARM_CHECK_ARG(slice_elems >= 1 && nslices >= 0 && f0 >= 0 && nf >= 1 && f0 + nf <= slice_elems,
+                  "slice energy block: bad extents");
+  if (nslices == 0) return STARM_OK;
+  STARM_CHECK_ARG(a && f_out, "slice energy block: null pointer");
+  STARM_CHECK_ARG(nslices < (int64_t(1) << 31), "slice energy block: too many slices");
+  slice_energy_kernel<<<unsigned(nslices), 256, 0, as_stream(stream)>>>(a + f0, nf, slice_elems, f_out);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+// Strided host-to-device copy (cudaMemcpy2DAsync): `height` runs of `width`
+// bytes, pitches in bytes -- one fibre block of a host tensor into the same
+// place of its device copy.  Asynchronous for page-locked host memory.
+extern "C" int starm_copy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch,
+                                size_t width, size_t height, void* stream) {
+  if (width == 0 || height == 0) return STARM_OK;
+  STARM_CHECK_ARG(dst && src && dpitch >= width && spitch >= width, "copy2d: bad arguments");
+  STARM_CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice,
+                                   as_stream(stream)));
   return STARM_OK;
 }
 

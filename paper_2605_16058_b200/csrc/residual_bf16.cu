@@ -142,7 +142,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 __global__ void __launch_bounds__(256) residual_pack_kernel(const double* __restrict__ src,
                                                             uint16_t* __restrict__ ws,
                                                             int64_t rows, int64_t n,
-                                                            int64_t rows_pad) {
+                                                            int64_t rows_pad, int64_t pitch) {
   __shared__ float tile[64][65];
   const int tid = threadIdx.x;
   const int64_t f0 = int64_t(blockIdx.x) * 64;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) residual_pack_kernel(const double* __rest
   for (int i = tid; i < 64 * 64; i += 256) {
     const int kk = i >> 6, ff = i & 63;
     const int64_t f = f0 + ff;
-    double x = f < rows ? __ldg(s + (k0 + kk) * rows + f) : 0.0;
+    double x = f < rows ? __ldg(s + (k0 + kk) * pitch + f) : 0.0;
     // bf16 saturates instead of overflowing: a fibre beyond 3.4e38 keeps the
     // FFT result's accuracy (its residual term is then inexact, not inf)
     x = fmin(fmax(x, -3.0e38), 3.0e38);
@@ -391,7 +391,7 @@ int residual_run(const double* pack_src, const uint16_t* delta_bf16, int log2_sc
   if (pack_src) {
     dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), unsigned(batch));
     residual_pack_kernel<<<grid, 256, 0, st>>>(pack_src, static_cast<uint16_t*>(const_cast<void*>(ws)),
-                                               rows, n, rows_pad);
+                                               rows, n, rows_pad, rows);
     STARM_LAUNCH_CHECK();
   }
   CUtensorMap map_x, map_d;
@@ -488,7 +488,39 @@ extern "C" int starm_dct_pack_f64(const double* src, double* dst, int64_t rows, 
   if (rc || packed) return rc;
   const int64_t rows_pad = rows_padded(rows);
   dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), unsigned(batch));
-  residual_pack_kernel<<<grid, 256, 0, st>>>(src, static_cast<uint16_t*>(ws), rows, n, rows_pad);
+  residual_pack_kernel<<<grid, 256, 0, st>>>(src, static_cast<uint16_t*>(ws), rows, n, rows_pad, rows);
+  STARM_LAUNCH_CHECK();
+  return STARM_OK;
+}
+
+// Fibre block [f0, f0 + nf) of a (rows x n) tensor, transformed where it
+// lies: src/dst/ws are the FULL tensor's buffers, so a caller can run the
+// forward DCT block by block (e.g. behind the host-to-device copy of each
+// block) and end with exactly the buffers starm_dct_pack_f64 leaves.
+extern "C" int starm_dct_pack_block_f64(const double* src, double* dst, int64_t rows, int64_t n,
+                                        int64_t f0, int64_t nf, void* ws, size_t ws_bytes,
+                                        void* stream) {
+  STARM_CHECK_ARG(rows >= 0 && n >= 0 && f0 >= 0 && nf >= 0 && f0 + nf <= rows,
+                  "dct pack block: bad extents");
+  if (nf == 0 || n == 0) return STARM_OK;
+  STARM_CHECK_ARG(src && dst && ws && src != dst, "dct pack block: null or aliased pointer");
+  if ((n & (n - 1)) != 0 || n < RB_N || n > 4096) {
+    set_error("dct pack block: the fast path needs a power-of-two length in [256, 4096]");
+    return STARM_UNSUPPORTED;
+  }
+  STARM_CHECK_ARG(f0 % RB_M == 0 && (f0 + nf == rows || nf % RB_M == 0),
+                  "dct pack block: blocks must start and end on multiples of 128 fibres");
+  STARM_CHECK_ARG(ws_bytes >= starm_ttm_residual_workspace_bytes(rows, n, 1) &&
+                      (reinterpret_cast<uintptr_t>(ws) & 127) == 0,
+                  "dct pack block: workspace too small or not 128-byte aligned");
+  const cudaStream_t st = as_stream(stream);
+  uint16_t* wsb = static_cast<uint16_t*>(ws) + f0 * n;
+  bool packed = false;
+  int rc = dct_launch(src + f0, dst + f0, nf, n, 1, false, wsb, rows_padded(nf), &packed, st, rows);
+  if (rc || packed) return rc;
+  const int64_t rows_pad = rows_padded(nf);
+  dim3 grid(unsigned(rows_pad / 64), unsigned(n / 64), 1);
+  residual_pack_kernel<<<grid, 256, 0, st>>>(src + f0, wsb, nf, n, rows_pad, rows);
   STARM_LAUNCH_CHECK();
   return STARM_OK;
 }

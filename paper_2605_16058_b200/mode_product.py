@@ -253,6 +253,26 @@ def from_transform_domain(t, ts: TransformSet, variant=BATCHED, threads=1):
     return _run(t, lambda x: inverse_device(x, ts))
 
 
+PIPELINE_BLOCKS = 16            # fibre runs of the pipelined host upload
+PIPELINE_MIN_BYTES = 64 << 20   # smaller tensors upload in one piece
+_COPY_STREAMS = {}
+
+
+def _copy_stream(dev):
+    import torch
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _COPY_STREAMS:
+        _COPY_STREAMS[idx] = torch.cuda.Stream(torch.device("cuda", idx))
+    return _COPY_STREAMS[idx]
+
+
+def pipelined_upload_applies(a, ts: TransformSet) -> bool:
+    """True for a host tensor whose forward transform is the deferrable DCT
+    and which is large enough for the block-wise upload to pay."""
+    return (isinstance(a, DenseTensor) and os.environ.get("STARM_PIPELINE", "1") != "0"
+            and deferrable(ts, a.dims) and a.data.nbytes >= PIPELINE_MIN_BYTES)
+
+
 class DeferredResidual:
     """The exact FFT DCT of a tensor whose reference-operator residual
     (starm_ttm_residual_bf16) has NOT been added yet: the bf16 operand is
@@ -270,8 +290,60 @@ class DeferredResidual:
         self._ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=x.device)
         self.base = self._ws.data_ptr() + (-self._ws.data_ptr()) % 128
         self.out = DeviceTensor.empty(x.dims, x.device)
+        self.energies = None
         nat.call("starm_dct_pack_f64", x.data.data_ptr(), self.out.data.data_ptr(), self.rows, n, 1,
                  0, self.base, nbytes, nat.stream_ptr(x.device))
+
+    @classmethod
+    def from_host(cls, a: DenseTensor, tr: Transform, dev, blocks=None):
+        """The same state for a HOST tensor, built block by block: the m*p
+        fibres are cut into ``blocks`` runs (multiples of 128 fibres); the
+        strided host-to-device copy of run g+1 (starm_copy2d_h2d on a copy
+        stream) overlaps the FFT DCT, the bf16 operand rows and the partial
+        slice energies of run g (starm_dct_pack_block_f64,
+        starm_slice_energy_block_f64), so that when the last bytes have
+        crossed PCIe the transform-domain tensor and its slice energies
+        (``self.energies``, device, summed over the runs in order) are nearly
+        complete.  Every fibre goes through the same kernel as in __init__, so
+        ``out`` and the operand are bit-identical to the one-shot path."""
+        import torch
+        m, p, n = a.dims
+        rows = m * p
+        self = cls.__new__(cls)
+        self.tr, self.rows, self.n, self.device = tr, rows, n, dev
+        lib = nat.load()
+        nbytes = lib.starm_ttm_residual_workspace_bytes(rows, n, 1)
+        self._ws = torch.empty(nbytes + 128, dtype=torch.uint8, device=dev)
+        self.base = self._ws.data_ptr() + (-self._ws.data_ptr()) % 128
+        self.out = DeviceTensor.empty(a.dims, dev)
+        host = a.data
+        if not (host.flags.f_contiguous or host.flags.c_contiguous) or host.dtype != np.float64:
+            host = np.ascontiguousarray(host.reshape(-1, order="F"))
+        nb = int(blocks or PIPELINE_BLOCKS)
+        step = max(128, -(-rows // nb + 127) // 128 * 128)
+        starts = list(range(0, rows, step))
+        x = torch.empty(rows * n, dtype=torch.float64, device=dev)
+        parts = torch.empty((len(starts), n), dtype=torch.float64, device=dev)
+        compute = torch.cuda.current_stream(dev)
+        copy = _copy_stream(dev)
+        copy.wait_stream(compute)       # x may reuse a block with compute work pending
+        x.record_stream(copy)
+        hc, hs = nat.register_stream(copy), nat.stream_ptr(dev)
+        src0 = host.ctypes.data
+        for g, f0 in enumerate(starts):
+            nf = min(step, rows - f0)
+            nat.call("starm_copy2d_h2d", x.data_ptr() + 8 * f0, 8 * rows, src0 + 8 * f0, 8 * rows,
+                     8 * nf, n, hc)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            compute.wait_event(ev)
+            nat.call("starm_dct_pack_block_f64", x.data_ptr(), self.out.data.data_ptr(), rows, n,
+                     f0, nf, self.base, nbytes, hs)
+            nat.call("starm_slice_energy_block_f64", self.out.data.data_ptr(), rows, n, f0, nf,
+                     parts[g].data_ptr(), hs)
+        self.energies = parts.sum(dim=0) if len(starts) > 1 else parts[0]
+        self._keep = (host, x)          # alive until the queued work has consumed them
+        return self
 
     def _apply(self, dst, delta_rows, nout):
         op = self.tr.residual_operand(self.device)

@@ -121,3 +121,69 @@ def test_float32_input_upcast_on_device():
     c2 = sb.tsvdm_tolerance(sb.DenseTensor(a32), ts, 0.3)
     assert np.array_equal(c1.to_host().ranks, c2.ranks)
     assert c1.discarded_energy == c2.discarded_energy
+
+
+# ------------------------------------------------------------------ block-wise host upload
+# tsvdm_tolerance(DenseTensor) cuts the fibres into runs and transforms run g
+# behind the host-to-device copy of run g+1 (starm_copy2d_h2d,
+# starm_dct_pack_block_f64, starm_slice_energy_block_f64).  Every fibre goes
+# through the same kernel as in the one-shot path, so the transform-domain
+# tensor and the bf16 operand must be BITWISE those of starm_dct_pack_f64 and
+# the compression result identical to the device-resident call
+# (reference: to_transform_domain, ttm.py:138-144, then tsvdm.py:268-321).
+
+@pytest.mark.parametrize("dims,blocks", [((40, 52, 1024), 5), ((37, 21, 1024), 3), ((16, 24, 256), 2),
+                                         ((9, 31, 512), 16)])
+def test_blockwise_upload_is_bitwise_the_one_shot_transform(dims, blocks):
+    import torch
+    from paper_2605_16058_b200.mode_product import DeferredResidual
+    a = random_array(dims, 11 + dims[0])
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(dims, "dct")
+    dev = nat.require_cuda()
+    one = DeferredResidual(sb.DeviceTensor.from_host(t), ts[0])
+    blk = DeferredResidual.from_host(t, ts[0], dev, blocks=blocks)
+    torch.cuda.synchronize()
+    assert torch.equal(one.out.data, blk.out.data)
+    nb = nat.load().starm_ttm_residual_workspace_bytes(dims[0] * dims[1], dims[2], 1)
+    off1 = one.base - one._ws.data_ptr()
+    off2 = blk.base - blk._ws.data_ptr()
+    rows = dims[0] * dims[1]
+    live = rows * dims[2] * 2          # the live operand rows (pad rows are never read past TMA bounds)
+    assert torch.equal(one._ws[off1:off1 + live], blk._ws[off2:off2 + live])
+    assert nb >= live
+    # partial energies summed over the runs = the per-slice energies
+    f = torch.empty(dims[2], dtype=torch.float64, device=dev)
+    nat.call("starm_slice_energy_f64", one.out.data.data_ptr(), rows, dims[2], f.data_ptr(),
+             nat.stream_ptr(dev))
+    ref = (np.asarray(one.out.data.cpu()).reshape(dims[2], rows) ** 2).sum(axis=1)
+    assert np.allclose(blk.energies.cpu().numpy(), ref, rtol=1e-13)
+    assert np.allclose(f.cpu().numpy(), ref, rtol=1e-13)
+
+
+def test_blockwise_upload_compression_equals_device_resident_call(monkeypatch):
+    import torch
+    from paper_2605_16058_b200 import mode_product as mp_
+    dims = (48, 40, 1024)
+    rng = np.random.default_rng(5)
+    tt = np.arange(dims[2])
+    a = sum(np.einsum("i,j,k->ijk", rng.standard_normal(dims[0]), rng.standard_normal(dims[1]),
+                      np.cos(2 * np.pi * (q + 1) * tt / dims[2] + rng.uniform(0, 6.28)))
+            for q in range(5))
+    a = np.asfortranarray(a + 1e-2 * rng.standard_normal(dims))
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(dims, "dct")
+    ref = sb.tsvdm_tolerance(sb.DeviceTensor.from_host(t), ts, 2e-2)
+    monkeypatch.setattr(mp_, "PIPELINE_MIN_BYTES", 0)
+    monkeypatch.setattr(mp_, "PIPELINE_BLOCKS", 4)
+    assert mp_.pipelined_upload_applies(t, ts)
+    got = sb.tsvdm_tolerance(t, ts, 2e-2)          # host in -> host out, block-wise upload
+    rf = ref.factors.to_host()
+    assert np.array_equal(got.ranks, ref.ranks)
+    assert np.array_equal(got.factors.u_data, rf.u_data)
+    assert np.array_equal(got.factors.g_data, rf.g_data)
+    assert abs(got.total_energy - ref.total_energy) <= 1e-13 * ref.total_energy
+    assert abs(got.discarded_energy - ref.discarded_energy) <= 1e-12 * ref.total_energy
+    mats = [tr.matrix for tr in ts]
+    o = oracle.tsvdm_tolerance(a, mats, 2e-2)
+    assert np.array_equal(got.ranks, o["ranks"])
