@@ -40,6 +40,7 @@ struct GemmArgs {
   double* C;
   int64_t M, N, K, lda, ldb, ldc, sA, sB, sC;
   int64_t tiles_n;
+  int64_t tiles;           // tiles per batch block
   // ERR epilogue (K10 fused into the writer of C): reference tensor E with
   // ld ldc; per CTA {sum (E - C)^2, sum E^2} over the tile -> epart[2 tile]
   const double* E;
@@ -148,24 +149,46 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_f64_kernel(GemmArgs g) {
   // Epilogue: D[g][2t], D[g][2t+1] -> C(m, n), C(m, n+1); with ERR also the
   // tile's error partials against E (fixed reduction order: deterministic).
   double sd = 0.0, sa = 0.0;
-  auto put = [&](int64_t idx, double v) {
-    C[idx] = v;
+  // ERR: the E values of a half are loaded before its first store to C (C
+  // and E may alias as far as the compiler knows, so loads interleaved
+  // with the stores would each wait out a full memory latency); two halves
+  // of 16 values: 32 at once would spill at 128 registers.
+#pragma unroll
+  for (int ih = 0; ih < 4; ih += 2) {
+    double ev[ERR ? 2 : 1][4][2];
     if (ERR) {
-      const double e = g.E[idx];
-      const double d = e - v;
-      sd = fma(d, d, sd);
-      sa = fma(e, e, sa);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int64_t m = m0 + wm * 32 + (ih + i) * 8 + gq;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
+          ev[i][j][0] = (m < g.M && n < g.N) ? __ldg(g.E + m + n * g.ldc) : 0.0;
+          ev[i][j][1] = (m < g.M && n + 1 < g.N) ? __ldg(g.E + m + (n + 1) * g.ldc) : 0.0;
+        }
+      }
     }
-  };
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t m = m0 + wm * 32 + i * 8 + gq;
-    if (m >= g.M) continue;
+    for (int i = 0; i < 2; ++i) {
+      const int64_t m = m0 + wm * 32 + (ih + i) * 8 + gq;
+      if (m >= g.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
-      if (n < g.N) put(m + n * g.ldc, acc[i][j][0]);
-      if (n + 1 < g.N) put(m + (n + 1) * g.ldc, acc[i][j][1]);
+      for (int j = 0; j < 4; ++j) {
+        const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          if (n + e2 < g.N) {
+            const double v = acc[ih + i][j][e2];
+            C[m + (n + e2) * g.ldc] = v;
+            if (ERR) {
+              const double e = ev[i][j][e2];
+              const double d = e - v;
+              sd = fma(d, d, sd);
+              sa = fma(e, e, sa);
+            }
+          }
+        }
+      }
     }
   }
   if (ERR) {
@@ -192,6 +215,175 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_f64_kernel(GemmArgs g) {
   }
 }
 
+// Persistent over the tiles of one batch block: CTA c runs tiles c, c + grid,
+// ... and the cp.async ring runs straight across tile boundaries (k-tile
+// stream s = (tile index, kt)), so the loads of the next tile are in flight
+// while the epilogue of the current one stores C (and, with ERR, reads E).
+// With a short K (the fused reconstruction has K = nnz = 64: four k-tiles)
+// a per-tile prologue would otherwise expose a full memory latency per tile.
+template <int VA, int VB, bool ERR>
+__global__ void __launch_bounds__(THREADS, 2) gemm_f64_pers_kernel(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double wred[2 * THREADS / 32];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_TILE;
+
+  const int64_t b = blockIdx.z;
+  const double* A = g.A + b * g.sA;
+  const double* B = g.B + b * g.sB;
+  double* C = g.C + b * g.sC;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  const int64_t KT = (g.K + BK - 1) / BK;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t mine = first < g.tiles ? (g.tiles - first + stride - 1) / stride : 0;
+  const int64_t total = mine * KT;  // k-tile steps of this CTA
+
+  // prefetch cursor (k-tile step ps of the stream): tile origin and kt kept
+  // incrementally (no divisions in the loop)
+  int64_t ps = 0, pkt = 0, ptile = first;
+  int64_t pm0 = (ptile / g.tiles_n) * BM, pn0 = (ptile % g.tiles_n) * BN;
+  auto issue = [&]() {
+    if (ps < total) {
+      const int slot = int(ps % STAGES);
+      load_stage<VA, VB>(g, A, B, As + slot * A_TILE, Bs + slot * B_TILE, pm0, pn0, pkt * BK);
+      ++ps;
+      if (++pkt == KT) {
+        pkt = 0;
+        ptile += stride;
+        pm0 = (ptile / g.tiles_n) * BM;
+        pn0 = (ptile % g.tiles_n) * BN;
+      }
+    }
+    cp_async_commit();
+  };
+  // L2 prefetch of the E values of a tile (read by its epilogue).
+  auto prefetch_e = [&](int64_t tile) {
+    const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+#pragma unroll
+    for (int q = 0; q < BM * BN / 16 / THREADS; ++q) {  // one prefetch per 128-byte line
+      const int e = threadIdx.x + q * THREADS;
+      const int64_t m = m0 + (e % (BM / 16)) * 16, n = n0 + e / (BM / 16);
+      if (m < g.M && n < g.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.E + m + n * g.ldc));
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue();
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  int64_t kt = 0, ti = 0;
+  if (ERR && mine > 0) prefetch_e(first);
+  for (int64_t s = 0; s < total; ++s) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue();
+    const int slot = int(s % STAGES);
+    const double* as = As + slot * A_TILE + wm * 32 + gq;
+    const double* bs = Bs + slot * B_TILE + (wn * 32 + gq) * BPAD + tq;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(k4 * 4 + tq) * APAD + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[j * 8 * BPAD + k4 * 4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (++kt < KT) continue;
+    kt = 0;
+
+    // Epilogue of tile ti: D[g][2t], D[g][2t+1] -> C(m, n), C(m, n+1); with
+    // ERR also the tile's error partials against E (fixed reduction order:
+    // deterministic).
+    const int64_t tile = first + ti * stride;
+    ++ti;
+    const int64_t m0 = (tile / g.tiles_n) * BM, n0 = (tile % g.tiles_n) * BN;
+    if (ERR && ti < mine) prefetch_e(first + ti * stride);
+    double sd = 0.0, sa = 0.0;
+    // ERR: the E values of a half are loaded before its first store to C (C
+    // and E may alias as far as the compiler knows, so loads interleaved
+    // with the stores would each wait out a full memory latency); two halves
+    // of 16 values: 32 at once would spill at 128 registers.
+#pragma unroll
+    for (int ih = 0; ih < 4; ih += 2) {
+      double ev[ERR ? 2 : 1][4][2];
+      if (ERR) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int64_t m = m0 + wm * 32 + (ih + i) * 8 + gq;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
+            ev[i][j][0] = (m < g.M && n < g.N) ? __ldg(g.E + m + n * g.ldc) : 0.0;
+            ev[i][j][1] = (m < g.M && n + 1 < g.N) ? __ldg(g.E + m + (n + 1) * g.ldc) : 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int64_t m = m0 + wm * 32 + (ih + i) * 8 + gq;
+        if (m >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t n = n0 + wn * 32 + j * 8 + 2 * tq;
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            if (n + e2 < g.N) {
+              const double v = acc[ih + i][j][e2];
+              C[m + (n + e2) * g.ldc] = v;
+              if (ERR) {
+                const double e = ev[i][j][e2];
+                const double d = e - v;
+                sd = fma(d, d, sd);
+                sa = fma(e, e, sa);
+              }
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (ERR) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      }
+      if (lane == 0) {
+        wred[2 * warp] = sd;
+        wred[2 * warp + 1] = sa;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < THREADS / 32; ++w) {
+          s0 += wred[2 * w];
+          s1 += wred[2 * w + 1];
+        }
+        g.epart[2 * tile] = s0;
+        g.epart[2 * tile + 1] = s1;
+      }
+      // (the next write of wred is behind the next step's CTA barrier)
+    }
+  }
+  cp_async_wait<0>();
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <int VA, int VB, bool ERR = false>
@@ -200,15 +392,30 @@ int launch_t(const GemmArgs& g, int64_t batch, cudaStream_t st) {
   STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_kernel<VA, VB, ERR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(SMEM_BYTES)));
+  STARM_CUDA_TRY(cudaFuncSetAttribute(gemm_f64_pers_kernel<VA, VB, ERR>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(SMEM_BYTES)));
   const int64_t tiles = g.tiles_n * ceil_div(g.M, BM);
+  // persistent: at most 2 CTAs per SM per batch block when there is a single
+  // block (batched launches keep one tile per CTA: the blocks fill the GPU)
+  int dev = 0, sms = 148;
+  STARM_CUDA_TRY(cudaGetDevice(&dev));
+  STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // ... and only for a short K, where the per-tile prologue is what costs: a
+  // long K loop hides it, and one tile per CTA lets the hardware stagger the
+  // CTAs (c3's K = 512 transform: 17.0 ms against 19.4 ms persistent)
+  const bool persistent = batch == 1 && g.K <= 8 * BK && tiles > 2 * int64_t(sms);
+  const int64_t gx = persistent ? 2 * int64_t(sms) : tiles;
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     GemmArgs gb = g;
+    gb.tiles = tiles;
     gb.A += b0 * g.sA;
     gb.B += b0 * g.sB;
     gb.C += b0 * g.sC;
     const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
-    dim3 grid(unsigned(tiles), 1, unsigned(nb));
-    gemm_f64_kernel<VA, VB, ERR><<<grid, THREADS, SMEM_BYTES, st>>>(gb);
+    dim3 grid(unsigned(gx), 1, unsigned(nb));
+    if (persistent) gemm_f64_pers_kernel<VA, VB, ERR><<<grid, THREADS, SMEM_BYTES, st>>>(gb);
+    else gemm_f64_kernel<VA, VB, ERR><<<grid, THREADS, SMEM_BYTES, st>>>(gb);
     STARM_LAUNCH_CHECK();
   }
   return STARM_OK;
@@ -227,7 +434,7 @@ int gemm_f64(const double* A, const double* B, double* C, int64_t M, int64_t N, 
       STARM_CUDA_TRY(cudaMemset2DAsync(C + b * sC, size_t(ldc) * 8, 0, size_t(M) * 8, size_t(N), st));
     return STARM_OK;
   }
-  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, sA, sB, sC, ceil_div(N, BN), nullptr, nullptr};
+  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, sA, sB, sC, ceil_div(N, BN), 0, nullptr, nullptr};
   const bool va = (M % 2 == 0) && (lda % 2 == 0) && (sA % 2 == 0) && aligned16(A);
   const bool vb = (K % 2 == 0) && (ldb % 2 == 0) && (sB % 2 == 0) && aligned16(B);
   if (va && vb) return launch_t<2, 2>(g, batch, st);
@@ -245,7 +452,7 @@ int gemm_f64_err(const double* A, const double* B, double* C, int64_t M, int64_t
                  cudaStream_t st) {
   if (M <= 0 || N <= 0) return STARM_OK;
   STARM_CHECK_ARG(K > 0, "gemm_f64_err: empty contraction");
-  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, ceil_div(N, BN), E, epart};
+  GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, ceil_div(N, BN), 0, E, epart};
   const bool va = (M % 2 == 0) && (lda % 2 == 0) && aligned16(A);
   const bool vb = (K % 2 == 0) && (ldb % 2 == 0) && aligned16(B);
   if (va && vb) return launch_t<2, 2, true>(g, 1, st);
