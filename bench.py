@@ -499,6 +499,29 @@ def run_ours(args):
             t_red, _ = timed(torch, lambda: svd_values_device(ahat3), reps=2)
         finally:
             lib.starm_svd_tune(-1, -1, 1, -1)
+    # ---- the same step and reduce launch WITHOUT the certified pruning (what
+    # the reference's schedule does: every slice factored), for the record
+    unpruned = None
+    if n_svd < n:
+        from paper_2605_16058_b200 import compress
+        full3 = sb.DeviceTensor(ahat.data, (m, p, n))
+        lib.starm_svd_tune(-1, -1, 3, -1)
+        try:
+            svd_values_device(full3)
+            t_red_full, _ = timed(torch, lambda: svd_values_device(full3), reps=2)
+        finally:
+            lib.starm_svd_tune(-1, -1, 1, -1)
+        del full3
+        compress.PRUNE = False
+        try:
+            wl.step(x)
+            t_full, _ = timed(torch, lambda: wl.step(x), reps=3)
+        finally:
+            compress.PRUNE = True
+        unpruned = {"ms_per_step": t_full * 1e3, "value": in_bytes / t_full / 1e9, "unit": UNIT,
+                    "reduce_ms": t_red_full * 1e3, "slices": n,
+                    "what": "STARM_PRUNE=0: all slices through the values pass, as the "
+                            "reference's schedule (tsvdm.py:268-321); same ranks and factors"}
     del ahat, ahat3
     f_ttm, f_svd, f_lapack = wl.flops(total_rank)
     a_, b_ = max(m, p), min(m, p)
@@ -530,6 +553,11 @@ def run_ours(args):
                    "traffic": profiled_traffic("svd_reduce_kernel", args.config),
                    "algorithmic_flops": f_red, "ms": t_red * 1e3, "slices": n_svd,
                    "wave": f"{n_svd} slices on {torch.cuda.get_device_properties(dev).multi_processor_count} SMs (one CTA per slice)"}
+    if unpruned is not None:
+        f_full = n * (2 * a_ * b_ ** 2 + 2 * b_ ** 3)
+        unpruned["reduce_achieved_tflops"] = f_full / (unpruned["reduce_ms"] / 1e3) / 1e12
+        unpruned["reduce_frac"] = unpruned["reduce_achieved_tflops"] / peak
+        unpruned["reduce_traffic"] = profiled_traffic("svd_reduce_kernel_unpruned", args.config)
     dominant = fwd_obj if (red_obj is None or (dense and t_fwd > t_red)) else red_obj
     roof = dict(dominant)
     roof["peak_source"] = ("cuBLAS DGEMM 4096^3 measured in this run (FP64 not in "
@@ -635,7 +663,7 @@ def run_ours(args):
             "flops": {"transform": f_ttm, "svd_necessary": f_svd, "svd_lapack_equiv": f_lapack,
                       "svd_slices_factored": n_svd, "svd_in_step": f_svd_step,
                       "lapack_equiv_tflops": f_lapack / (t_dev / args.steps) / 1e12},
-            "stages_ms": stages,
+            "stages_ms": stages, "unpruned": unpruned,
             "reconstruct": {"ms": t_rec * 1e3, "what": "facewise U_i G_i + inverse transform + "
                                                        "K10 error sums (outside the timed region)"},
             "step_ms": step_ms, "clocks": clk.summary(), "gpu_launches": launches,

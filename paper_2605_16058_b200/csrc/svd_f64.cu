@@ -1751,6 +1751,24 @@ __host__ __device__ __forceinline__ int hb_warps(int64_t n, int cap) {  // ceil(
 }
 __device__ __forceinline__ double& HEL(double* W, int r, int c) { return W[r * (HB - 1) + c + HOFF]; }
 
+// Window accessors of the chase: one flat window (shared or global memory),
+// or the rows split over the two CTAs of a cluster (rows < H in rank 0's
+// shared memory, the rest in rank 1's; both pointers are generic addresses
+// from cluster.map_shared_rank, so either CTA reaches either half).
+struct WinFlat {
+  double* W;
+  __device__ __forceinline__ double* at(int r, int c) const { return W + r * (HB - 1) + c + HOFF; }
+};
+struct WinSplit {
+  double* W0;
+  double* W1;
+  int H;
+  __device__ __forceinline__ double* at(int r, int c) const {
+    // (element (r, c) sits at row * HB + (c - r) + HOFF of its half)
+    return r < H ? W0 + r * (HB - 1) + c + HOFF : W1 + (r - H) * (HB - 1) + (c - H) + HOFF;
+  }
+};
+
 
 // Warp-wide dlarfg: lanes 0..L-1 hold x (0 beyond); on return x holds v
 // (lane 0: 1, 0 beyond L), beta the new leading entry; returns tau (0: H = I).
@@ -1787,7 +1805,8 @@ __device__ __forceinline__ double warp_house(double& x, int lane, double& beta) 
 // with v_l = 0 beyond L and constant offsets from one base pointer.
 // Inactive warps (act false) run the shuffles on zeros and touch nothing, so
 // every warp reaches each shuffle converged.
-__device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act, int lane,
+template <class Win>
+__device__ __forceinline__ void hb_task(const Win& W, int n, int i, int k, bool act, int lane,
                                         double* vs, double* lg) {
   const int c0 = i + k * BW + 1;
   const int c1 = min(c0 + BW - 1, n - 1);
@@ -1795,17 +1814,17 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
   const int rho = k ? c0 - BW : i;
   double beta;
   // ---- right reflector from row rho, applied to rows (rho, c1]
-  double x = (lane & 15) < L ? HEL(W, rho, c0 + (lane & 15)) : 0.0;  // mirrored halves
+  double x = (lane & 15) < L ? *W.at(rho, c0 + (lane & 15)) : 0.0;  // mirrored halves
   const double tau = warp_house(x, lane, beta);
   if (act && lg && lane < BW) lg[lane] = lane ? x : tau;
   double col0 = 0.0;  // this lane's updated A(rho + 1 + lane, c0)
   if (tau != 0.0) {
-    if (lane < L) HEL(W, rho, c0 + lane) = lane ? 0.0 : beta;
+    if (lane < L) *W.at(rho, c0 + lane) = lane ? 0.0 : beta;
     vs[lane] = x;
     __syncwarp();
     const int r = rho + 1 + lane;
     if (r <= c1) {
-      double* row = &HEL(W, r, c0);  // row[l] = A(r, c0 + l)
+      double* row = W.at(r, c0);  // row[l] = A(r, c0 + l)
       double a[BW];
 #pragma unroll
       for (int l = 0; l < BW; ++l) a[l] = row[l];
@@ -1824,24 +1843,23 @@ __device__ __forceinline__ void hb_task(double* W, int n, int i, int k, bool act
   // Its column c0 entries were just produced in registers by lanes
   // c0 + l - rho - 1 (when the right reflector was applied): shuffle them.
   const double ysh = __shfl_sync(0xffffffffu, col0, (c0 + (lane & 15) - rho - 1) & 31);
-  double y = (lane & 15) < L ? (tau != 0.0 ? ysh : HEL(W, c0 + (lane & 15), c0)) : 0.0;
+  double y = (lane & 15) < L ? (tau != 0.0 ? ysh : *W.at(c0 + (lane & 15), c0)) : 0.0;
   const double tl = warp_house(y, lane, beta);
   if (tl != 0.0) {
-    if (lane < L) HEL(W, c0 + lane, c0) = lane ? 0.0 : beta;
+    if (lane < L) *W.at(c0 + lane, c0) = lane ? 0.0 : beta;
     vs[lane] = y;
     __syncwarp();
     const int c = c0 + 1 + lane;
     if (c < n) {
-      double* col = &HEL(W, c0, c);  // col[l * (HB - 1)] = A(c0 + l, c)
       double a[BW];
 #pragma unroll
-      for (int l = 0; l < BW; ++l) a[l] = col[l * (HB - 1)];
+      for (int l = 0; l < BW; ++l) a[l] = *W.at(c0 + l, c);  // A(c0 + l, c)
       double w4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < BW; ++l) w4[l & 3] = fma(vs[l], a[l], w4[l & 3]);
       const double w = ((w4[0] + w4[1]) + (w4[2] + w4[3])) * tl;
 #pragma unroll
-      for (int l = 0; l < BW; ++l) col[l * (HB - 1)] = fma(-w, vs[l], a[l]);
+      for (int l = 0; l < BW; ++l) *W.at(c0 + l, c) = fma(-w, vs[l], a[l]);
     }
     __syncwarp();
   }
@@ -1856,6 +1874,7 @@ __global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams 
   const int n = int(P.n);
   const int64_t NP = P.NP;
   double* W = GMEM ? P.hbbuf + int64_t(blockIdx.x) * (n + BW) * HB : reinterpret_cast<double*>(smem_raw);
+  const WinFlat Wf{W};
   const int64_t kmax = hb_kmax(n), T = hb_steps(n);
   for (;;) {
     if (threadIdx.x == 0) cur = P.lo + int64_t(atomicAdd(&P.counter[P.cctr], 1ull));
@@ -1886,12 +1905,12 @@ __global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams 
         const int k = int(t - 3 * int64_t(cur));
         const bool act = cur >= 0 && k < hb_tasks(n, cur);
         if (act)  // (warp-uniform: idle warps go straight to the step barrier)
-          hb_task(W, n, cur, k, true, lane, vsh[warp], lg ? lg + (int64_t(cur) * kmax + k) * HLOG : nullptr);
+          hb_task(Wf, n, cur, k, true, lane, vsh[warp], lg ? lg + (int64_t(cur) * kmax + k) * HLOG : nullptr);
       } else {
         for (int i = cur; i >= 0 && t - 3 * int64_t(i) < kmax; i -= nw) {
           const int k = int(t - 3 * int64_t(i));
           const bool act = k < hb_tasks(n, i);
-          hb_task(W, n, act ? i : 0, act ? k : 0, act, lane, vsh[warp],
+          hb_task(Wf, n, act ? i : 0, act ? k : 0, act, lane, vsh[warp],
                   lg ? lg + (int64_t(i) * kmax + k) * HLOG : nullptr);
         }
       }
@@ -1905,6 +1924,84 @@ __global__ void __launch_bounds__(GMEM ? 1024 : 512) svd_bulge_kernel(SvdParams 
     __syncthreads();
     long long t1 = clock64();
     if (threadIdx.x == 0 && P.stats) atomicAdd(&g_stats[ST_CYC_BULGE], (unsigned long long)(t1 - t0));
+  }
+}
+
+// The same chase for windows beyond one SM's shared memory (616 < n <= 1160,
+// e.g. c3's 1024 x 1024 slices: 385 KB): a cluster of two CTAs holds the
+// window in distributed shared memory (rows < H on rank 0, the rest on rank
+// 1).  Both CTAs walk the same step loop; the task of sweep i at step t is
+// run by the CTA that owns its pivot column c0 (warp = sweep mod nw, as in
+// the one-CTA kernel), reaching across the boundary through DSMEM where its
+// rows straddle it, and one cluster barrier per step orders the steps.
+// Every task does the arithmetic of hb_task in the same order, so d, e and
+// the reflector log are bitwise those of the other variants.  Clusters take
+// slices lo + c, lo + c + (clusters), ... (equal work per slice).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(768, 1) svd_bulge_cluster_kernel(SvdParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double vsh[32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int n = int(P.n);
+  const int64_t NP = P.NP;
+  unsigned rank, nclusters, cid;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(nclusters));
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+  const int R = n + BW, H = (R + 1) / 2;
+  double* mine = reinterpret_cast<double*>(smem_raw);
+  // generic addresses of both halves (mapa: this CTA's shared address in the
+  // peer's window)
+  WinSplit Ws;
+  {
+    unsigned long long g0, g1;
+    const unsigned long long self = reinterpret_cast<unsigned long long>(mine);
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(g0) : "l"(self), "r"(0u));
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(g1) : "l"(self), "r"(1u));
+    Ws.W0 = reinterpret_cast<double*>(g0);
+    Ws.W1 = reinterpret_cast<double*>(g1);
+    Ws.H = H;
+  }
+  auto cluster_sync = [] {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  };
+  const int r_lo = rank ? H : 0, r_hi = rank ? R : H;  // window rows held here
+  const int64_t kmax = hb_kmax(n), T = hb_steps(n);
+  for (int64_t it = P.lo + cid; it < P.hi; it += nclusters) {
+    const int64_t si = state_index(P, it);
+    if (P.flags[si]) continue;  // (cluster-uniform)
+    long long t0 = clock64();
+    const double* band = P.bandbuf + si * (BW + 1) * NP;
+    for (int e = threadIdx.x; e < (r_hi - r_lo) * HB; e += blockDim.x) {
+      const int r = r_lo + e / HB, d = e % HB - HOFF;
+      mine[e] = (d >= 0 && d <= BW && r + d < n) ? band[d * NP + r] : 0.0;
+    }
+    cluster_sync();
+    double* lg = P.hhlog ? P.hhlog + si * P.hhcap : nullptr;
+    int cur = -1, next = warp;
+    for (int64_t t = 0; t < T; ++t) {
+      if (3 * int64_t(next) == t) {
+        cur = next;
+        next += nw;
+      }
+      const int k = int(t - 3 * int64_t(cur));
+      const bool act = cur >= 0 && k < hb_tasks(n, cur);
+      if (act) {
+        const int c0 = cur + k * BW + 1;
+        if ((c0 < H ? 0u : 1u) == rank)
+          hb_task(Ws, n, cur, k, true, lane, vsh[warp], lg ? lg + (int64_t(cur) * kmax + k) * HLOG : nullptr);
+      }
+      cluster_sync();
+    }
+    double* de = P.debuf + si * 2 * NP;
+    for (int64_t q = r_lo + threadIdx.x; q < r_hi && q < NP; q += blockDim.x) {
+      de[q] = q < n ? *Ws.at(int(q), int(q)) : 0.0;
+      de[NP + q] = q + 1 < n ? *Ws.at(int(q), int(q) + 1) : 0.0;
+    }
+    for (int64_t q = R + threadIdx.x; rank == 1 && q < NP; q += blockDim.x) de[q] = de[NP + q] = 0.0;
+    cluster_sync();  // the next slice's fill must not overtake these reads
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && rank == 0 && P.stats)
+      atomicAdd(&g_stats[ST_CYC_BULGE], (unsigned long long)(t1 - t0));
   }
 }
 
@@ -3516,6 +3613,7 @@ struct Plan {
   int slots_j, slots_r, slots_b, bisect_blocks, slots_v, slots_t, ii_threads, btw, qr_stages, bt_g;
   int64_t hhcap, count;
   bool hb_gmem;
+  bool hb_cluster;  // window split over a 2-CTA cluster (DSMEM); slots_b counts clusters
   int hb_threads;
   size_t vsmem, tsmem;
   size_t off_x, off_w, off_r, off_f, off_band, off_de, off_s, off_rv, off_rcs, off_rcol, off_rcnt,
@@ -3570,6 +3668,10 @@ int g_bisect_side_blocks = [] {
 // with the bulge-chase window in global memory, 3 = diagnostic: the values
 // pass stops after the reduce kernel (outputs undefined; for timing it alone)
 int g_tune_mode = 1;
+const bool g_bulge_cluster = [] {
+  const char* e = getenv("STARM_BULGE_CLUSTER");
+  return !(e && e[0] == '0');
+}();
 int g_stats_on = 0;
 
 int occupancy(const void* fn, int threads, size_t smem, int* per_sm) {
@@ -3633,8 +3735,17 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
   g.internal_s = g.wantv && !have_s && !g.by_slice;
   g.bsmem = size_t(g.n + BW) * HB * sizeof(double);
   g.hb_gmem = g_tune_mode == 2 || g.bsmem > size_t(216 * 1024);
-  g.hb_threads = 32 * hb_warps(g.n, g.hb_gmem ? 32 : 16);
+  // too large for one SM but each half fits: the 2-CTA cluster kernel
+  // (STARM_BULGE_CLUSTER=0 keeps the global-memory window for A/B runs)
+  const size_t half = size_t((g.n + BW + 1) / 2) * HB * sizeof(double);
+  g.hb_cluster = g.hb_gmem && g_tune_mode != 2 && half <= size_t(216 * 1024) && g_bulge_cluster &&
+                 3 * hb_warps(g.n, 24) >= hb_kmax(g.n);  // (one active sweep per warp)
+  g.hb_threads = 32 * hb_warps(g.n, g.hb_cluster ? 24 : (g.hb_gmem ? 32 : 16));
   if (g.hb_gmem) g.bsmem = 0;
+  if (g.hb_cluster) {
+    g.hb_gmem = false;
+    g.bsmem = half;
+  }
   int dev = 0, sms = 0, per = 0;
   STARM_CUDA_TRY(cudaGetDevice(&dev));
   STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -3673,10 +3784,16 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
       const int v = atoi(e);
       if (v >= 1 && v < g.slots_r) g.slots_r = v;
     }
-    rc = occupancy(g.hb_gmem ? (const void*)svd_bulge_kernel<true> : (const void*)svd_bulge_kernel<false>,
-                   g.hb_threads, g.bsmem, &per);
-    if (rc) return rc;
-    g.slots_b = clampc(int64_t(sms) * per);
+    if (g.hb_cluster) {
+      STARM_CUDA_TRY(cudaFuncSetAttribute((const void*)svd_bulge_cluster_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.bsmem)));
+      g.slots_b = clampc(int64_t(sms) / 2);  // clusters (one CTA per SM, two per cluster)
+    } else {
+      rc = occupancy(g.hb_gmem ? (const void*)svd_bulge_kernel<true> : (const void*)svd_bulge_kernel<false>,
+                     g.hb_threads, g.bsmem, &per);
+      if (rc) return rc;
+      g.slots_b = clampc(int64_t(sms) * per);
+    }
     int64_t bb = (count * g.n + 127) / 128;
     g.bisect_blocks = int(bb < int64_t(sms) * 16 ? bb : int64_t(sms) * 16);
     if (g.bisect_blocks < 1) g.bisect_blocks = 1;
@@ -3951,7 +4068,8 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       Pc.hi = per * (c + 1) < count ? per * (c + 1) : count;
       Pc.cctr = nch > 1 ? 8 + c : 2;
       if (Pc.lo >= Pc.hi) continue;
-      if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(Pc);
+      if (pl.hb_cluster) svd_bulge_cluster_kernel<<<2 * pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(Pc);
+      else if (pl.hb_gmem) svd_bulge_kernel<true><<<pl.slots_b, pl.hb_threads, 0, st>>>(Pc);
       else svd_bulge_kernel<false><<<pl.slots_b, pl.hb_threads, pl.bsmem, st>>>(Pc);
       STARM_LAUNCH_CHECK();
       if (ss) {

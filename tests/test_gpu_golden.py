@@ -26,7 +26,7 @@ import pytest
 import oracle
 import paper_2605_16058_b200 as sb
 from paper_2605_16058_b200 import configs as cf
-from helpers import projector_distance, rel_error, sigma_close
+from helpers import projector_distance, random_array, random_orthonormal, rel_error, sigma_close
 
 pytestmark = pytest.mark.gpu
 
@@ -376,3 +376,53 @@ def test_data_driven_transform_at_scale():
     off = d - np.diag(np.diag(d))
     assert np.linalg.norm(off) <= 1e-10 * np.linalg.norm(g)
     assert np.all(np.diff(np.diag(d)) <= 1e-9 * d[0, 0])   # descending
+
+
+# ------------------------------------------------------------------ f3 at scale
+# starm_product (tsvdm.py:219-233) and full_tsvdm (tsvdm.py:236-243) beyond toy
+# sizes: a c1-sized product against the oracle (1e-12, the reference's own
+# A3 bar) including the identity A * I = A, and a lossless full t-SVDM of the
+# c1 tensor (A4: <= 1e-11) with orthonormal factors and descending sigma.
+
+def test_starm_product_at_c1_scale():
+    a = random_array((256, 192, 64), 31)
+    b = random_array((192, 160, 64), 32)
+    ts = sb.TransformSet.build((256, 160, 64), "dct")
+    mats = [tr.matrix for tr in ts]
+    got = sb.starm_product(sb.DenseTensor(a), sb.DenseTensor(b), ts)
+    ref = oracle.starm_product(a, b, mats)
+    assert got.dims == (256, 160, 64)
+    assert rel_error(ref, got.array) <= 1e-12
+    # identity tensor of the product: every transform-domain slice is I
+    eye_hat = np.zeros((192, 192, 64), order="F")
+    eye_hat[np.arange(192), np.arange(192), :] = 1.0
+    ident = oracle.from_transform_domain(eye_hat, [sb.TransformSet.build((192, 192, 64), "dct")[0].matrix])
+    ts_sq = sb.TransformSet.build((256, 192, 64), "dct")
+    back = sb.starm_product(sb.DenseTensor(a), sb.DenseTensor(ident), ts_sq)
+    assert rel_error(a, back.array) <= 1e-12
+    # a custom (Haar) transform takes the dense DMMA route end to end
+    tsh = sb.TransformSet((sb.validate_transform(random_orthonormal(64, 5)),))
+    goth = sb.starm_product(sb.DenseTensor(a), sb.DenseTensor(b), tsh)
+    refh = oracle.starm_product(a, b, [tsh[0].matrix])
+    assert rel_error(refh, goth.array) <= 1e-12
+
+
+def test_full_tsvdm_at_c1_scale():
+    from paper_2605_16058_b200 import configs
+    a = configs.config1(seed=0)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build(a.shape, "dct")
+    res = sb.full_tsvdm(t, ts)
+    assert rel_error(a, res.reconstruct().array) <= 1e-11
+    f = res.factors
+    u, s, v = (np.asarray(z.array if hasattr(z, "array") else z) for z in (f.u, f.s, f.v))
+    m, p, n = a.shape
+    r = min(m, p)
+    assert u.shape == (m, r, n) and s.shape == (r, n) and v.shape == (p, r, n)
+    assert (np.diff(s, axis=0) <= 0).all() and (s >= 0).all()
+    for i in (0, n // 2, n - 1):
+        assert np.abs(u[:, :, i].T @ u[:, :, i] - np.eye(r)).max() <= 1e-10 * np.sqrt(r)
+        assert np.abs(v[:, :, i].T @ v[:, :, i] - np.eye(r)).max() <= 1e-10 * np.sqrt(r)
+    # sigma of the golden c1 run (reference package output, full spectrum)
+    gs = GC["c1/s"]
+    assert gs.shape == s.shape and sigma_close(s, gs)[0]
