@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .tensors import DenseTensor, DeviceTensor, as_device
+from .tensors import DenseTensor, DeviceTensor, as_device, device_to_host
 
 __all__ = ["SLICES_PARALLEL", "SVD_PARALLEL", "STRATEGIES", "SliceSVDSet", "VariableRankFactors",
            "DeviceFactors", "svd_all_slices", "svd_values_only", "svd_truncated_slices",
@@ -146,8 +146,8 @@ class DeviceFactors:
         return self._host_ranks
 
     def to_host(self) -> VariableRankFactors:
-        return VariableRankFactors(self.slice_rows, self.slice_cols, self.ranks,
-                                   self.u_data.cpu().numpy(), self.g_data.cpu().numpy())
+        u, g = device_to_host(self.u_data, self.g_data)
+        return VariableRankFactors(self.slice_rows, self.slice_cols, self.ranks, u, g)
 
 
 # ---------------------------------------------------------------- launches
