@@ -85,6 +85,12 @@ size_t starm_last_error(char* buf, size_t len);
  * FP64 DMMA tiles, cp.async shared-memory staging. */
 int starm_ttm_f64(const double* src, const double* mat, double* dst, int64_t rows,
                   int64_t inner, int64_t batch, int64_t out_cols, void* stream);
+/* starm_ttm_f64 (batch 1) restricted to the fibre block [f0, f0 + nf): src
+ * and dst are the full tensors' buffers (leading dimension `rows`).  The
+ * drop-in tsvdm_fixed_rank / tsvdm_tolerance on a host DenseTensor transform
+ * each block behind the host-to-device copy of the next. */
+int starm_ttm_block_f64(const double* src, const double* mat, double* dst, int64_t rows,
+                        int64_t inner, int64_t out_cols, int64_t f0, int64_t nf, void* stream);
 
 /* float32 twin of starm_ttm_f64 (same view and semantics, f32 in / f32
  * out): the operands are upcast on the device and contracted in FP64 on the

@@ -36,6 +36,8 @@ SIGNATURES = {
     "starm_last_error": (c_size_t, [ctypes.c_char_p, c_size_t]),
     "starm_ttm_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
                               c_void_p]),
+    "starm_ttm_block_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                    c_int64, c_void_p]),
     "starm_dct_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
     "starm_facewise_gemm_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                                         c_int64, c_void_p]),

@@ -30,7 +30,7 @@ import numpy as np
 
 from . import _native as nat
 from .mode_product import (BATCHED, VARIANTS, DeferredResidual, deferrable, forward_device,
-                           pipelined_upload_applies,
+                           pipelined_upload_applies, upload_forward,
                            inverse_device)
 from .slice_svd import (check_status, SLICES_PARALLEL, STRATEGIES, DeviceFactors, SliceSVDSet,
                         VariableRankFactors, pack_offsets_device, svd_full_device,
@@ -288,7 +288,7 @@ def starm_product(a, b, ts: TransformSet, ttm_variant=BATCHED, threads=1):
     ts.check_dims(a.dims)
     host = isinstance(a, DenseTensor)
     dev = nat.require_cuda() if host else a.device
-    ahat = forward_device(as_device(a, dev), ts)
+    ahat = upload_forward(a, ts, dev)
     bhat = forward_device(as_device(b, dev), ts)
     m, p, cols = a.dims[0], a.dims[1], b.dims[1]
     n = prod(a.dims[2:])
@@ -309,7 +309,7 @@ def full_tsvdm(a, ts: TransformSet, threads=1, svd_strategy=SLICES_PARALLEL,
     ts.check_dims(a.dims)
     host = isinstance(a, DenseTensor)
     dev = nat.require_cuda() if host else a.device
-    ahat = forward_device(as_device(a, dev), ts)
+    ahat = upload_forward(a, ts, dev)
     factors = svd_all_slices(ahat.to_host() if host else ahat)
     return TSVDMResult(factors, ts, tuple(a.dims))
 
@@ -392,7 +392,7 @@ def tsvdm_fixed_rank(a, ts: TransformSet, rank, threads=1, svd_strategy=SLICES_P
     dev = (want or nat.require_cuda()) if host else a.device
     n = prod(a.dims[2:])
     r = min(m, p)
-    ahat = forward_device(as_device(a, dev), ts)
+    ahat = upload_forward(a, ts, dev)
     ahat3 = DeviceTensor(ahat.data, (m, p, n))
     ranks = torch.full((n,), rank, dtype=torch.int64, device=dev)
     factors, s = svd_truncated_device(ahat3, ranks, rank * n, keep_values=True)
@@ -441,7 +441,7 @@ def tsvdm_tolerance(a, ts: TransformSet, epsilon, strategy=MEMORY_EFFICIENT, thr
             deferred = DeferredResidual(as_device(a, dev), ts[0])
         ahat = deferred.out
     else:
-        ahat = forward_device(as_device(a, dev), ts)
+        ahat = upload_forward(a, ts, dev)
     ahat3 = DeviceTensor(ahat.data, (m, p, n))
     if strategy == TRUNCATE:
         with clock.stage("stage1-svd"):

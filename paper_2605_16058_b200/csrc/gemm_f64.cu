@@ -474,6 +474,23 @@ extern "C" int starm_ttm_f64(const double* src, const double* mat, double* dst, 
                          rows * out_cols, batch, starm::as_stream(stream));
 }
 
+// The same product restricted to the fibre block [f0, f0 + nf) of a 3-way
+// tensor (batch 1): src and dst are the FULL tensors' buffers (leading
+// dimension `rows`), so the transform can run block by block, e.g. behind the
+// host-to-device copy of each block (the reference's np.matmul in
+// ttm.py:113-135 needs the whole unfolding in memory).
+extern "C" int starm_ttm_block_f64(const double* src, const double* mat, double* dst, int64_t rows,
+                                   int64_t inner, int64_t out_cols, int64_t f0, int64_t nf,
+                                   void* stream) {
+  STARM_CHECK_ARG(rows >= 1 && inner >= 1 && out_cols >= 1 && f0 >= 0 && nf >= 0 && f0 + nf <= rows,
+                  "ttm block: bad extents (rows=%lld inner=%lld out_cols=%lld f0=%lld nf=%lld)",
+                  (long long)rows, (long long)inner, (long long)out_cols, (long long)f0, (long long)nf);
+  if (nf == 0) return STARM_OK;
+  STARM_CHECK_ARG(src && mat && dst, "ttm block: null pointer");
+  return starm::gemm_f64(src + f0, mat, dst + f0, nf, out_cols, inner, rows, inner, rows, 0, 0, 0, 1,
+                         starm::as_stream(stream));
+}
+
 extern "C" int starm_facewise_gemm_f64(const double* a, const double* b, double* c, int64_t m,
                                        int64_t p, int64_t l, int64_t nslices, void* stream) {
   STARM_CHECK_ARG(m >= 1 && p >= 1 && l >= 1 && nslices >= 1,

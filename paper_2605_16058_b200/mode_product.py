@@ -273,6 +273,58 @@ def pipelined_upload_applies(a, ts: TransformSet) -> bool:
             and deferrable(ts, a.dims) and a.data.nbytes >= PIPELINE_MIN_BYTES)
 
 
+def forward_from_host(a: DenseTensor, ts: TransformSet, dev):
+    """Forward transform of a HOST 3-way tensor whose single transform takes
+    the dense DMMA product, block by block: the strided host-to-device copy of
+    fibre run g+1 (starm_copy2d_h2d, copy stream) overlaps the product of run
+    g (starm_ttm_block_f64); the result is bitwise forward_device's (every
+    output element is the same dot product in the same order).  Returns None
+    when it does not apply (other shapes / kinds, small tensors): the caller
+    uploads in one piece."""
+    import torch
+    if (not isinstance(a, DenseTensor) or os.environ.get("STARM_PIPELINE", "1") == "0"
+            or len(a.dims) != 3 or len(ts) != 1 or a.data.nbytes < PIPELINE_MIN_BYTES
+            or _fast_kind(ts[0], a.dims[2]) is not None):
+        return None
+    m, p, n = a.dims
+    rows = m * p
+    op, j, inner = _matrix_operand(ts[0], dev)
+    if j != n or inner != n:
+        return None
+    host = a.data
+    if host.dtype != np.float64 or not host.flags.c_contiguous:
+        return None
+    out = DeviceTensor.empty(a.dims, dev)
+    x = torch.empty(rows * n, dtype=torch.float64, device=dev)
+    step = max(128, -(-rows // PIPELINE_BLOCKS + 127) // 128 * 128)
+    compute = torch.cuda.current_stream(dev)
+    copy = _copy_stream(dev)
+    copy.wait_stream(compute)
+    x.record_stream(copy)
+    hc, hs = nat.register_stream(copy), nat.stream_ptr(dev)
+    src0 = host.ctypes.data
+    for f0 in range(0, rows, step):
+        nf = min(step, rows - f0)
+        nat.call("starm_copy2d_h2d", x.data_ptr() + 8 * f0, 8 * rows, src0 + 8 * f0, 8 * rows,
+                 8 * nf, n, hc)
+        ev = torch.cuda.Event()
+        ev.record(copy)
+        compute.wait_event(ev)
+        nat.call("starm_ttm_block_f64", x.data_ptr(), op.data_ptr(), out.data.data_ptr(), rows, n, n,
+                 f0, nf, hs)
+    return out
+
+
+def upload_forward(a, ts: TransformSet, dev) -> DeviceTensor:
+    """Transform-domain tensor (device) of a host or device tensor: host
+    tensors that qualify go through the block-wise upload."""
+    if isinstance(a, DenseTensor):
+        out = forward_from_host(a, ts, dev)
+        if out is not None:
+            return out
+    return forward_device(as_device(a, dev), ts)
+
+
 class DeferredResidual:
     """The exact FFT DCT of a tensor whose reference-operator residual
     (starm_ttm_residual_bf16) has NOT been added yet: the bf16 operand is

@@ -187,3 +187,37 @@ def test_blockwise_upload_compression_equals_device_resident_call(monkeypatch):
     mats = [tr.matrix for tr in ts]
     o = oracle.tsvdm_tolerance(a, mats, 2e-2)
     assert np.array_equal(got.ranks, o["ranks"])
+
+
+def test_blockwise_dense_upload_equals_device_resident_fixed_rank(monkeypatch):
+    """Dense (Haar) transform: the host call uploads fibre runs and multiplies
+    each behind the next copy (starm_ttm_block_f64); bitwise the one-shot
+    forward product, so the fixed-rank result equals the device-resident one
+    (reference: ttm.py:113-135 then tsvdm.py:246-265)."""
+    import torch
+    from paper_2605_16058_b200 import mode_product as mp_
+    dims = (45, 37, 96)
+    a = random_array(dims, 17)
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet((sb.validate_transform(random_orthonormal(dims[2], 3)),))
+    dev = nat.require_cuda()
+    one = mp_.forward_device(sb.DeviceTensor.from_host(t), ts)
+    monkeypatch.setattr(mp_, "PIPELINE_MIN_BYTES", 0)
+    monkeypatch.setattr(mp_, "PIPELINE_BLOCKS", 5)
+    blk = mp_.forward_from_host(t, ts, dev)
+    assert blk is not None
+    torch.cuda.synchronize()
+    assert torch.equal(one.data, blk.data)
+    ref = sb.tsvdm_fixed_rank(sb.DeviceTensor.from_host(t), ts, 6)
+    got = sb.tsvdm_fixed_rank(t, ts, 6)
+    rf = ref.factors.to_host()
+    assert np.array_equal(got.factors.u_data, rf.u_data) and np.array_equal(got.factors.g_data, rf.g_data)
+    assert got.discarded_energy == ref.discarded_energy and got.total_energy == ref.total_energy
+    o = oracle.tsvdm_fixed_rank(a, [ts[0].matrix], 6)
+    assert abs(got.discarded_energy - o["discarded_energy"]) <= 1e-12 * o["total_energy"]
+    # the DCT kind below the FFT threshold (n = 64: dense product with tr.matrix) qualifies too
+    ts2 = sb.TransformSet.build((45, 37, 64), "dct")
+    t2 = sb.DenseTensor(random_array((45, 37, 64), 18))
+    one2 = mp_.forward_device(sb.DeviceTensor.from_host(t2), ts2)
+    blk2 = mp_.forward_from_host(t2, ts2, dev)
+    assert blk2 is not None and torch.equal(one2.data, blk2.data)
