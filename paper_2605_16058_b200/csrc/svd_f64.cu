@@ -2605,29 +2605,21 @@ __device__ void ii_orth(const double* bd, const double* be, int64_t n, const dou
   }
 }
 
-__global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
+// The items of one thread: g = gtid, gtid + nthreads, ... over (vector j,
+// list position it) pairs, vector index major (the few real items, j < k, of
+// every slice come first and spread over all threads / warps); scratch
+// vectors through the Strided views (global, warp-interleaved, or one
+// compact region per thread in shared memory).
+// Vector j of list position `it` (a no-op unless j heads a cluster chunk).
+__device__ __forceinline__ void bdvec_one(const SvdParams& P, int64_t j, int64_t it, Strided rdd,
+                                          Strided du, Strided du2, Strided dl, Strided z, Strided x) {
   const int64_t n = P.n, NP = P.NP, RP = P.RP, N2 = 2 * P.n;
-  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
-  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  // scratch interleaved within each warp (element i of lane l at i * 32 + l):
-  // coalesced per index, sequential per warp (TLB-friendly)
-  const int64_t vl = 2 * NP;
-  double* wscr = P.iiscr + (gtid >> 5) * (6 * vl * 32) + (gtid & 31);
-  Strided rdd{wscr, 32};
-  Strided du{wscr + 1 * vl * 32, 32};
-  Strided du2{wscr + 2 * vl * 32, 32};
-  Strided dl{wscr + 3 * vl * 32, 32};  // multipliers
-  Strided z{wscr + 4 * vl * 32, 32};   // 1.0 where rows i, i+1 swapped
-  Strided x{wscr + 5 * vl * 32, 32};   // the iterate
-  for (int64_t g = gtid; g < total_work; g += nthreads) {
-    // vector index major: the few real items (j < k) of every slice come first
-    // and spread over all threads / warps
-    const int64_t j = g / P.count, it = g % P.count;
+  {
     const int64_t si = state_index(P, it);
-    if (P.flags[si]) continue;
+    if (P.flags[si]) return;
     const int64_t slice = P.ids ? P.ids[it] : it;
     const int64_t kout = kout_of(P, slice);
-    if (j >= kout) continue;
+    if (j >= kout) return;
     const double* bd = P.debuf + si * 2 * NP;
     const double* be = bd + NP;
     const double* sv = P.s + slice * n;
@@ -2638,7 +2630,7 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
     // cluster run containing j: [r0, ...); j heads a chunk iff (j - r0) % II_CMAX == 0
     int64_t r0 = j;
     while (r0 > 0 && sv[r0 - 1] - sv[r0] <= ctol) --r0;
-    if ((j - r0) % II_CMAX) continue;
+    if ((j - r0) % II_CMAX) return;
     int64_t jend = j + 1;
     while (jend < kout && jend - j < II_CMAX && sv[jend - 1] - sv[jend] <= ctol) ++jend;
     double lprev = 0.0;
@@ -2665,6 +2657,98 @@ __global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work) {
       double* vout = P.vsel + si * RP * NP + jj * RP;
       for (int64_t i = 0; i < RP; ++i) vout[i] = (i < n) ? x[2 * i] * inv : 0.0;
     }
+  }
+}
+
+__device__ __forceinline__ void bdvec_items(const SvdParams& P, int64_t total_work, int64_t gtid,
+                                            int64_t nthreads, Strided rdd, Strided du, Strided du2,
+                                            Strided dl, Strided z, Strided x) {
+  // vector index major: the few real items (j < k) of every slice come first
+  // and spread over all threads / warps
+  for (int64_t g = gtid; g < total_work; g += nthreads)
+    bdvec_one(P, g / P.count, g % P.count, rdd, du, du2, dl, z, x);
+}
+
+// Number of vectors the job computes (sum of k over the listed slices) into
+// counter[5]: the two launches below pick the scratch placement from it.
+__global__ void __launch_bounds__(256) svd_bdvec_count_kernel(SvdParams P) {
+  // also the exclusive prefix sums of k over the list (count + 1 entries at
+  // the start of the global scratch, which only the other launch uses) so
+  // the shared-memory launch can enumerate exactly the real vectors
+  __shared__ long long sc[256];
+  __shared__ long long base;
+  long long* prefix = reinterpret_cast<long long*>(P.iiscr);
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < P.count; c0 += 256) {
+    const int64_t it = c0 + threadIdx.x;
+    long long k = 0;
+    if (it < P.count && !P.flags[state_index(P, it)]) k = kout_of(P, P.ids ? P.ids[it] : it);
+    sc[threadIdx.x] = k;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {  // inclusive scan
+      const long long v = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
+      __syncthreads();
+      sc[threadIdx.x] += v;
+      __syncthreads();
+    }
+    if (it < P.count) prefix[it] = base + sc[threadIdx.x] - k;
+    __syncthreads();
+    if (threadIdx.x == 255) base += sc[255];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    prefix[P.count] = base;
+    P.counter[5] = (unsigned long long)base;
+  }
+}
+
+// Few vectors (at most II_SMEM_OVERSUB per shared-memory slot, e.g. the
+// pruned c2 step's 336 or c1's 640): every thread keeps its six scratch
+// vectors in a compact region of shared memory, so the recurrences run at
+// shared-memory latency instead of walking 2 MB of interleaved scratch per
+// warp through L2.  Same arithmetic, same results.
+constexpr int II_SMEM_OVERSUB = 2;
+
+__global__ void svd_bdvec_kernel(SvdParams P, int64_t total_work, int64_t smem_slots) {
+  if (int64_t(P.counter[5]) <= II_SMEM_OVERSUB * smem_slots) return;  // the shared-memory launch ran
+  const int64_t NP = P.NP;
+  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  // scratch interleaved within each warp (element i of lane l at i * 32 + l):
+  // coalesced per index, sequential per warp (TLB-friendly)
+  const int64_t vl = 2 * NP;
+  double* wscr = P.iiscr + (gtid >> 5) * (6 * vl * 32) + (gtid & 31);
+  bdvec_items(P, total_work, gtid, nthreads, Strided{wscr, 32}, Strided{wscr + 1 * vl * 32, 32},
+              Strided{wscr + 2 * vl * 32, 32}, Strided{wscr + 3 * vl * 32, 32},
+              Strided{wscr + 4 * vl * 32, 32}, Strided{wscr + 5 * vl * 32, 32});
+}
+
+__global__ void svd_bdvec_smem_kernel(SvdParams P, int64_t total_work, int64_t smem_slots) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (int64_t(P.counter[5]) > II_SMEM_OVERSUB * smem_slots) return;
+  // one vector per WARP (lane 0 works): the pivoting branches of different
+  // vectors would serialise inside a warp, and with this few vectors the
+  // chain's instruction latency is all that matters (6 threads of one warp:
+  // 0.84 ms on c2; one lane per warp: see DESIGN)
+  if (threadIdx.x & 31) return;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t vl = 2 * P.NP;
+  const int64_t nthreads = int64_t(gridDim.x) * nwarps;
+  // slot-major over CTAs so consecutive items land on different SMs
+  const int64_t gtid = int64_t(warp) * gridDim.x + blockIdx.x;
+  double* w = reinterpret_cast<double*>(smem_raw) + int64_t(warp) * (6 * vl + 2);
+  const long long* prefix = reinterpret_cast<const long long*>(P.iiscr);
+  const int64_t total = int64_t(P.counter[5]);
+  for (int64_t q = gtid; q < total; q += nthreads) {
+    int64_t lo = 0, hi = P.count;  // prefix[lo] <= q < prefix[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (prefix[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    bdvec_one(P, q - prefix[lo], lo, Strided{w, 1}, Strided{w + vl, 1}, Strided{w + 2 * vl, 1},
+              Strided{w + 3 * vl, 1}, Strided{w + 4 * vl, 1}, Strided{w + 5 * vl, 1});
   }
 }
 
@@ -4091,7 +4175,28 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
     }
   }
   if (pl.run_vec) {
-    svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n);
+    {
+      // scratch placement by the number of vectors (device-side count): the
+      // shared-memory launch for few vectors, the global-scratch one otherwise
+      int dev = 0, sms = 0;
+      STARM_CUDA_TRY(cudaGetDevice(&dev));
+      STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const size_t per = size_t(6 * 2 * pl.NP + 2) * sizeof(double);
+      int tpc = int((216 * 1024) / per);
+      tpc = tpc > 8 ? 8 : tpc;  // (215 registers per thread: at most 9 warps)
+      const int64_t slots = int64_t(tpc) * sms;
+      svd_bdvec_count_kernel<<<1, 256, 0, st>>>(P);
+      STARM_LAUNCH_CHECK();
+      if (tpc >= 1) {
+        STARM_CUDA_TRY(cudaFuncSetAttribute(svd_bdvec_smem_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(per * tpc)));
+        svd_bdvec_smem_kernel<<<sms, 32 * tpc, per * tpc, st>>>(P, count * pl.n, slots);
+        STARM_LAUNCH_CHECK();
+      }
+      svd_bdvec_kernel<<<pl.ii_threads / 128, 128, 0, st>>>(P, count * pl.n, tpc >= 1 ? slots : 0);
+      STARM_LAUNCH_CHECK();
+    }
     STARM_LAUNCH_CHECK();
     if (pl.RP <= 1024 && !g_orth_warp) {
       const size_t osm = orth_smem(pl.RP);
