@@ -1275,15 +1275,37 @@ __device__ __forceinline__ void load_tf(const QrSmemFixed& q, double (&tf)[4][2]
     for (int h = 0; h < 2; ++h) tf[kk][h] = q.t[(4 * kk + tq) * 17 + 8 * h + ph];
 }
 
+// A slice may be factored by a CLUSTER of CTAs (few slices, many SMs): every
+// CTA factors each panel redundantly (same arithmetic, same bits, the panel
+// and T in its own shared memory) and takes every csize-th column group /
+// row tile of the trailing updates; the matrix lives in global memory (L2),
+// so a cluster barrier (release / acquire) after every update orders them.
+struct ClusterPos {
+  int rank, size;
+};
+__device__ __forceinline__ ClusterPos cluster_pos() {
+  unsigned r, n;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return ClusterPos{int(r), int(n)};
+}
+__device__ __forceinline__ void cluster_sync(const ClusterPos& cp) {
+  if (cp.size > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // C <- (I - V T^T V^T) C on rows [r0, r0 + 8 ntiles) x columns [c_start, NP)
 // of X (ld); V = pan (explicit: zero above the pivots), T = q.t.
 // Lane (gq, tq) holds C[2tq + ks][gq] of each block (ks = 0, 1).
-template <int NT, int tw>
+template <int NT, int tw, bool CL>
 __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, const double* pan, int prs,
-                                                double* X, int ld, int ntiles, int NP, int r0, int c_start) {
+                                                double* X, int ld, int ntiles, int NP, int r0, int c_start,
+                                                ClusterPos cpin) {
+  const ClusterPos cp = CL ? cpin : ClusterPos{0, 1};  // (compile-time 1 CTA: the unsplit code)
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
-  const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
+  const int nteams = (NW / tw) * cp.size, team = (warp / tw) * cp.size + cp.rank, wit = warp % tw;
+  const int lteam = warp / tw;  // team inside this CTA (barrier id, Y partials)
   const int my = wit < ntiles ? (ntiles - wit + tw - 1) / tw : 0;
   const int ngroups = (NP - c_start) >> 3;
   double tf[4][2];
@@ -1344,12 +1366,12 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
         yb[warp * YB + (2 * tq + e) * 18 + (r & 3) * 4 + (r >> 2)] =
             (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
       }
-    team_sync(team, tw);
+    team_sync(lteam, tw);
     // Z^T = Y^T T': A[gq][tq] of k-step kk = Y[4kk + tq][gq]; lane ends with
     // zt[h][e] = Z[8h + tq + 4e][gq]
     double zt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double ya[4];
-    team_ysum<tw>(yb + team * tw * YB, gq, tq, ya);
+    team_ysum<tw>(yb + lteam * tw * YB, gq, tq, ya);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
@@ -1373,15 +1395,15 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
   }
 }
 
-template <int NT>
+template <int NT, bool CL>
 __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan, int prs, double* X,
-                                 int ld, int nrows, int NP, int r0, int c_start) {
+                                 int ld, int nrows, int NP, int r0, int c_start, ClusterPos cp) {
   const int ntiles = (nrows - r0) >> 3;
   switch (team_width<NT>(ntiles)) {
-    case 1: team_left_update_t<NT, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
-    case 2: team_left_update_t<NT, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
-    case 4: team_left_update_t<NT, 4>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
-    case 8: team_left_update_t<NT, 8>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start); break;
+    case 1: team_left_update_t<NT, 1, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
+    case 2: team_left_update_t<NT, 2, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
+    case 4: team_left_update_t<NT, 4, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
+    case 8: team_left_update_t<NT, 8, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
     default: return false;
   }
   __syncthreads();
@@ -1391,12 +1413,15 @@ __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan
 // C <- C (I - V T V^T) on rows [rmin, nrows) x columns [j0, NP) of A (ld);
 // V[j][c] = pan2[c * prs + j] (explicit, zero left of the pivots).
 // Lane (gq, tq) holds C[gq][2tq + e] of each block.
-template <int NT, int tw>
+template <int NT, int tw, bool CL>
 __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, const double* pan2, int prs,
-                                                 double* A, int ld, int nrows, int nch, int rmin, int j0) {
+                                                 double* A, int ld, int nrows, int nch, int rmin, int j0,
+                                                 ClusterPos cpin) {
+  const ClusterPos cp = CL ? cpin : ClusterPos{0, 1};
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
-  const int nteams = NW / tw, team = warp / tw, wit = warp % tw;
+  const int nteams = (NW / tw) * cp.size, team = (warp / tw) * cp.size + cp.rank, wit = warp % tw;
+  const int lteam = warp / tw;
   const int my = wit < nch ? (nch - wit + tw - 1) / tw : 0;
   const int ntile = (nrows - rmin) >> 3;
   double tf[4][2];
@@ -1459,12 +1484,12 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
         const int c = 8 * h + 2 * tq + e;
         yb[warp * YB + gq * 18 + (c & 3) * 4 + (c >> 2)] = (y[h][0][e] + y[h][1][e]) + (y[h][2][e] + y[h][3][e]);
       }
-    team_sync(team, tw);
+    team_sync(lteam, tw);
     // Z = Y T': A[gq][tq] of k-step kk = Y[gq][4kk + tq]; lane ends with
     // z[h][e] = Z[gq][8h + tq + 4e]
     double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double ya[4];
-    team_ysum<tw>(yb + team * tw * YB, gq, tq, ya);
+    team_ysum<tw>(yb + lteam * tw * YB, gq, tq, ya);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
@@ -1491,15 +1516,15 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
   }
 }
 
-template <int NT>
+template <int NT, bool CL>
 __device__ bool team_right_update(QrSmemFixed& q, double* ybuf, const double* pan2, int prs, double* A,
-                                  int ld, int nrows, int NP, int rmin, int j0) {
+                                  int ld, int nrows, int NP, int rmin, int j0, ClusterPos cp) {
   const int nch = (NP - j0) >> 3;
   switch (team_width<NT>(nch)) {
-    case 1: team_right_update_t<NT, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
-    case 2: team_right_update_t<NT, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
-    case 4: team_right_update_t<NT, 4>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
-    case 8: team_right_update_t<NT, 8>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0); break;
+    case 1: team_right_update_t<NT, 1, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
+    case 2: team_right_update_t<NT, 2, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
+    case 4: team_right_update_t<NT, 4, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
+    case 8: team_right_update_t<NT, 8, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
     default: return false;
   }
   __syncthreads();
@@ -1522,9 +1547,11 @@ __device__ __forceinline__ void explicit_v(double* pan, int64_t prs, int64_t k0,
 // Householder QR of the tall X (LP rows, NP columns, ld LP) in 16-column
 // panels with compact-WY trailing updates; leaves R in the leading NP x NP
 // block and zeros below it.
-template <int NT>
+template <int NT, bool CL = false>
 __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double* pan, int64_t prs,
-                         double* wbase, double* X, int64_t live, long long& pf, long long& tr) {
+                         double* wbase, double* X, int64_t live, long long& pf, long long& tr,
+                         ClusterPos cpin = ClusterPos{0, 1}) {
+  const ClusterPos cp = CL ? cpin : ClusterPos{0, 1};
   const int64_t LP = P.LP, NP = P.NP;
   const int tid = threadIdx.x;
   for (int64_t k0 = 0; k0 < NP; k0 += BW) {
@@ -1543,13 +1570,16 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
       panel_gram<NT>(q, pan, prs, kc, LP);
       long long _a = clock64();
       if (!(NT == 256 && P.wtwo &&
-            team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
-                                 int(k0 + BW))))
-        P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
-               : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
+            team_left_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
+                                 int(k0 + BW), cp))) {
+        if (cp.rank == 0)  // (the streaming fallback is not split: one CTA of the cluster runs it)
+          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
+                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
+      }
       tr += clock64() - _a;
     }
     __syncthreads();
+    cluster_sync(cp);  // the next panel reads columns every CTA of the cluster updated
   }
   // keep only R (upper triangle of the leading NP x NP block): zero below the
   // diagonal in the rows the band phase reads (< RP; TSQR masks r <= c itself)
@@ -1557,6 +1587,7 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
   for (int c = 0; c < int(NP); ++c)
     for (int r = c + 1 + tid; r < zr; r += NT) X[r + int64_t(c) * lp] = 0.0;
   __syncthreads();
+  cluster_sync(cp);  // (every CTA writes the same zeros; none may run ahead into the band phase)
 }
 
 // Load / factorisation kernel (one CTA per slice, persistent):
@@ -1565,7 +1596,7 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
 //   upper band (bandwidth 16) by alternating 16-column QR and 16-row LQ
 //   panels (compact-WY updates on DMMA, nst-stage cp.async ring) -> the 17
 //   diagonals of B to bandbuf.  Vector jobs also log P1's panels (V, T).
-template <int NT>
+template <int NT, bool CL>
 __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmemFixed& q = *reinterpret_cast<QrSmemFixed*>(smem_raw);
@@ -1576,10 +1607,20 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
   double* wbase = pan + BW * prs;  // per-warp regions (aliases the ring, used exclusively)
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
-  double* X = P.xslots + int64_t(blockIdx.x) * LP * NP;
+  const ClusterPos cp = CL ? cluster_pos() : ClusterPos{0, 1};
+  const int64_t cid = int64_t(blockIdx.x) / cp.size, ncl = int64_t(gridDim.x) / cp.size;
+  double* X = P.xslots + cid * LP * NP;  // one working matrix per cluster
+  int64_t next_static = cid;
 
   for (;;) {
-    if (tid == 0) cur = int64_t(atomicAdd(&P.counter[0], 1ull));
+    // one CTA per slice: dynamic work counter; a cluster per slice: clusters
+    // stride over the list (equal work per slice, no cross-CTA broadcast)
+    if (cp.size == 1) {
+      if (tid == 0) cur = int64_t(atomicAdd(&P.counter[0], 1ull));
+    } else if (tid == 0) {
+      cur = next_static;
+    }
+    next_static += ncl;
     __syncthreads();
     const int64_t it = cur;
     __syncthreads();
@@ -1592,11 +1633,14 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       P.flags[si] = flag;
       if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
     }
+    // (every CTA of a cluster loaded the same X and got the same flag; none
+    // may update X before all have finished writing it)
+    cluster_sync(cp);
     if (flag) continue;
     long long t1 = clock64();
     long long pf = 0, tr = 0, ru = 0;
     // ---------------- QR of the tall X (rows LP)
-    if (P.L > P.n) qr_phase<NT>(P, q, pan, prs, wbase, X, round_up16(P.L), pf, tr);
+    if (P.L > P.n) qr_phase<NT, CL>(P, q, pan, prs, wbase, X, round_up16(P.L), pf, tr, cp);
     long long t2 = clock64();
     // ---------------- band reduction of the leading NP x NP block (rows RP)
     for (int64_t k = 0; k < NP; k += BW) {
@@ -1616,12 +1660,16 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       {
         long long _a = clock64();
         if (!(NT == 256 && P.wtwo &&
-              team_left_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
-                                   int(k + BW))))
-          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
-                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
+              team_left_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
+                                   int(k + BW), cp))) {
+          if (cp.rank == 0)
+            P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
+                   : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
+        }
         tr += clock64() - _a;
       }
+      __syncthreads();
+      cluster_sync(cp);  // the LQ panel reads rows every CTA of the cluster updated
       // LQ half-step on rows [k, k+16), columns [k+16, NP)
       const int64_t j0 = k + BW;
       { long long _a = clock64(); reg = panel_factor_any<NT>(q, pan, prs, j0, NP, X + k, LP, 1, j0); pf += clock64() - _a; }
@@ -1634,7 +1682,7 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
         explicit_v<NT>(pan, prs, j0, NP);
       }
       panel_gram<NT>(q, pan, prs, (j0 / 8) * 8, NP);
-      if (P.rvlog) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
+      if (P.rvlog && cp.rank == 0) {  // vector jobs: keep P1's panel (V, T) for the back-transformation
         double* dst = P.rvlog + (si * (NP / BW) + k / BW) * (BW * NP + BW * BW);
         for (int c = 0; c < BW; ++c)
           for (int64_t jj = tid; jj < NP; jj += NT) dst[c * NP + jj] = pan[c * prs + jj];
@@ -1643,7 +1691,9 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       {
         long long _a = clock64();
         if (NT == 256 && P.wtwo &&
-            team_right_update<NT>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0))) {
+            team_right_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0),
+                                  cp)) {
+        } else if (cp.rank != 0) {
         } else if (P.wtwo) {
           right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         } else {
@@ -1652,12 +1702,15 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
         ru += clock64() - _a;
       }
       __syncthreads();
+      cluster_sync(cp);  // the next QR panel reads columns every CTA of the cluster updated
     }
-    // ---------------- the 17 diagonals of the band
+    // ---------------- the 17 diagonals of the band (every CTA of a cluster
+    // writes the same values; the barrier keeps the next load off X meanwhile)
     double* band = P.bandbuf + si * (BW + 1) * NP;
     for (int d = 0; d <= BW; ++d)
       for (int64_t i = tid; i < NP; i += NT) band[d * NP + i] = (i + d < n) ? X[i + (i + d) * LP] : 0.0;
     __syncthreads();
+    cluster_sync(cp);
     long long t3 = clock64();
     stat_add(P, ST_CYC_LOAD, (unsigned long long)(t1 - t0));
     stat_add(P, ST_CYC_QR, (unsigned long long)(t2 - t1));
@@ -3770,6 +3823,15 @@ int g_bisect_side_blocks = [] {
 // with the bulge-chase window in global memory, 3 = diagnostic: the values
 // pass stops after the reduce kernel (outputs undefined; for timing it alone)
 int g_tune_mode = 1;
+const bool g_reduce_cluster = [] {
+  const char* e = getenv("STARM_REDUCE_CLUSTER");
+  return !(e && e[0] == '0');
+}();
+const int g_reduce_cluster_max = [] {  // largest cluster tried (2, 4 or 8)
+  const char* e = getenv("STARM_REDUCE_CLUSTER_MAX");
+  const int v = e ? atoi(e) : 8;
+  return v >= 2 && v <= 8 ? v : 8;
+}();
 const bool g_bulge_cluster = [] {
   const char* e = getenv("STARM_BULGE_CLUSTER");
   return !(e && e[0] == '0');
@@ -3878,8 +3940,8 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.hhcap = (g.n >= 3 ? (g.n - 2) : 1) * hb_kmax(g.n) * HLOG;
   }
   if (g.bidiag) {
-    rc = g.reduce_nt == 512 ? occupancy((const void*)svd_reduce_kernel<512>, 512, g.rsmem, &per)
-                            : occupancy((const void*)svd_reduce_kernel<256>, 256, g.rsmem, &per);
+    rc = g.reduce_nt == 512 ? occupancy((const void*)svd_reduce_kernel<512, false>, 512, g.rsmem, &per)
+                            : occupancy((const void*)svd_reduce_kernel<256, false>, 256, g.rsmem, &per);
     if (rc) return rc;
     g.slots_r = clampc(int64_t(sms) * per);
     if (const char* e = getenv("STARM_REDUCE_SLOTS")) {  // experiment: fewer slices in flight
@@ -4143,8 +4205,37 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
     P.btw = pl.btw;
   }
   if (pl.run_front) {
-    if (pl.reduce_nt == 512) svd_reduce_kernel<512><<<pl.slots_r, 512, pl.rsmem, st>>>(P);
-    else svd_reduce_kernel<256><<<pl.slots_r, 256, pl.rsmem, st>>>(P);
+    // Few slices (at most half the SMs): a cluster of 2 / 4 / 8 CTAs per slice
+    // splits the trailing updates (team path only: 256 threads, two-stage
+    // rings).  STARM_REDUCE_CLUSTER=0 keeps one CTA per slice (A/B runs).
+    int csz = 1;
+    if (pl.reduce_nt == 256 && pl.wtwo && g_reduce_cluster) {
+      int dev = 0, sms = 0;
+      STARM_CUDA_TRY(cudaGetDevice(&dev));
+      STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      while (csz < g_reduce_cluster_max && count * int64_t(2 * csz) <= int64_t(sms)) csz *= 2;
+    }
+    if (csz > 1) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(count * csz), 1, 1);
+      cfg.blockDim = dim3(256, 1, 1);
+      cfg.dynamicSmemBytes = pl.rsmem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = unsigned(csz);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      STARM_CUDA_TRY(cudaFuncSetAttribute((const void*)svd_reduce_kernel<256, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.rsmem)));
+      STARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, svd_reduce_kernel<256, true>, P));
+    } else if (pl.reduce_nt == 512) {
+      svd_reduce_kernel<512, false><<<pl.slots_r, 512, pl.rsmem, st>>>(P);
+    } else {
+      svd_reduce_kernel<256, false><<<pl.slots_r, 256, pl.rsmem, st>>>(P);
+    }
     STARM_LAUNCH_CHECK();
     if (g_tune_mode == 3) return STARM_OK;
     // Bulge chase and sigma in NCH slice chunks: sigma of chunk c (FP64-pipe
