@@ -97,6 +97,7 @@ struct SvdParams {
   int64_t L, n, LP, NP, RP;
   int transposed, use_qr, bidiag, stats;
   int wtwo;                     // reduce kernel: two-stage warp rings (else one stage)
+  int team_yb;                  // team updates: Y partial buffers (2, or 1 when shared memory is short)
   double tol;
   int max_sweeps, max_inner;
 };
@@ -135,11 +136,13 @@ size_t jacobi_smem_bytes(int ns) {
          (TPB + TPB / 32) * sizeof(double);
 }
 
+constexpr int QR_YZ_DOUBLES = BW * GS + GW * ZS;  // y and z of the streaming updates
 struct __align__(16) QrSmemFixed {
   double t[BW * 17];
   double sg[4][BW * 17];  // per row-quarter partial Gram (NT / 128 used)
-  double y[BW * GS];
-  double z[GW * ZS];
+  // (the streaming updates' y (BW x GS) and z (GW x ZS) live AFTER the panel,
+  // just below their per-warp regions: the team updates, which do not use
+  // them, put their own buffers over the same space)
   double red[16][BW];     // per-warp partials (NT / 32 used)
   double sums[BW];
   double wv[BW];
@@ -912,6 +915,8 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
                                   int64_t kc64, int64_t cs64) {
   constexpr int WR = TWO ? WREG : WREG1;
   constexpr int NW = NT / 32;
+  double* const qy = wbase - QR_YZ_DOUBLES;  // y (BW x GS), z (GW x ZS): just below the warp regions
+  double* const qz = qy + BW * GS;
   const int prs = int(prs64), ld = int(ld64), nrows = int(nrows64), NP = int(NP64);
   const int kc = int(kc64), c_start = int(cs64);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -962,7 +967,7 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
   const double* pa0 = pan + gq * prs + kc + tq;  // A fragments of V^T
   const double* pa1 = pa0 + 8 * prs;
   const double* pv = pan + tq * prs + kc + gq;   // A fragments of V
-  const double* zb = q.z + gq * ZS + tq;
+  const double* zb = qz + gq * ZS + tq;
   if (total > 0) issue(0);
   for (int b = 0; b < nb; ++b) {
     const int c0 = c_start + b * GW;
@@ -1007,7 +1012,7 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
       double sacc = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) sacc += wbase[w * WR + part_off(w, b) + e];
-      q.y[(e / GW) * GS + (e % GW)] = sacc;
+      qy[(e / GW) * GS + (e % GW)] = sacc;
     }
     __syncthreads();
     if (!TWO && my > 0) issue(b * 2 * my + my);  // first chunk of pass 2
@@ -1015,8 +1020,8 @@ __device__ void trailing_update_w(QrSmemFixed& q, double* wbase, const double* p
     for (int e = threadIdx.x; e < BW * GW; e += NT) {
       const int ii = e & 15, c = e >> 4;
       double sacc = 0.0;
-      for (int l = 0; l <= ii; ++l) sacc += q.t[l * 17 + ii] * q.y[l * GS + c];
-      q.z[c * ZS + ii] = sacc;
+      for (int l = 0; l <= ii; ++l) sacc += q.t[l * 17 + ii] * qy[l * GS + c];
+      qz[c * ZS + ii] = sacc;
     }
     __syncthreads();
     double zf[4][4];  // B fragments of Z
@@ -1227,7 +1232,8 @@ __device__ void right_update_w(QrSmemFixed& q, double* wbase, const double* pan2
 // ---------------------------------------------------------------------
 constexpr int TT = 16;  // 8x8 blocks per warp held in registers
 constexpr int YB = 144;  // doubles per warp partial of Y (padded: conflict-free 16-byte reads)
-constexpr int TEAM_SMEM_DOUBLES = 2 * 8 * YB + 8 * TT * 64;  // for 8 warps
+constexpr int TEAM_SMEM_DOUBLES = 2 * 8 * YB + 8 * TT * 64;   // for 8 warps, two Y buffers
+constexpr int TEAM_SMEM_DOUBLES1 = 1 * 8 * YB + 8 * TT * 64;  // one Y buffer (an extra team barrier per group)
 
 // Team sum of the warps' partial Y (fixed warp order): lane gets the four
 // values Y[4kk + tq][gq] (left) / Y[gq][4kk + tq] (right), stored at
@@ -1297,7 +1303,7 @@ __device__ __forceinline__ void cluster_sync(const ClusterPos& cp) {
 // C <- (I - V T^T V^T) C on rows [r0, r0 + 8 ntiles) x columns [c_start, NP)
 // of X (ld); V = pan (explicit: zero above the pivots), T = q.t.
 // Lane (gq, tq) holds C[2tq + ks][gq] of each block (ks = 0, 1).
-template <int NT, int tw, bool CL>
+template <int NT, int tw, bool CL, int nyb>
 __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, const double* pan, int prs,
                                                 double* X, int ld, int ntiles, int NP, int r0, int c_start,
                                                 ClusterPos cpin) {
@@ -1314,7 +1320,7 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
   constexpr int ts = tw * 8;                        // row stride between a warp's blocks
   const double* pA = pan + gq * prs + rw + 2 * tq;  // V[row 2tq (+ks)][col gq (+8h)]
   const double* pB = pan + tq * prs + rw + gq;      // V[row gq][col tq (+8h+4e)]
-  double* st = ybuf + 2 * NW * YB + warp * (TT * 64) + 2 * lane;  // stage slot i: st + 64 i
+  double* st = ybuf + nyb * NW * YB + warp * (TT * 64) + 2 * lane;  // stage slot i: st + 64 i
   auto issue = [&](int g) {
     const double* src = X + (c_start + 8 * g + gq) * ld + rw + 2 * tq;
 #pragma unroll
@@ -1357,7 +1363,7 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
         }
       }
     }
-    double* yb = ybuf + (it & 1) * NW * YB;
+    double* yb = ybuf + (nyb == 2 ? (it & 1) : 0) * NW * YB;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1372,6 +1378,7 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
     double zt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double ya[4];
     team_ysum<tw>(yb + lteam * tw * YB, gq, tq, ya);
+    if (nyb == 1) team_sync(lteam, tw);  // one Y buffer: all reads before the next group's writes
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
@@ -1397,13 +1404,25 @@ __device__ __noinline__ void team_left_update_t(QrSmemFixed& q, double* ybuf, co
 
 template <int NT, bool CL>
 __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan, int prs, double* X,
-                                 int ld, int nrows, int NP, int r0, int c_start, ClusterPos cp) {
+                                 int ld, int nrows, int NP, int r0, int c_start, ClusterPos cp, int nyb) {
   const int ntiles = (nrows - r0) >> 3;
   switch (team_width<NT>(ntiles)) {
-    case 1: team_left_update_t<NT, 1, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
-    case 2: team_left_update_t<NT, 2, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
-    case 4: team_left_update_t<NT, 4, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
-    case 8: team_left_update_t<NT, 8, CL>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp); break;
+    case 1:
+      if (nyb == 2) team_left_update_t<NT, 1, CL, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      else team_left_update_t<NT, 1, CL, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      break;
+    case 2:
+      if (nyb == 2) team_left_update_t<NT, 2, CL, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      else team_left_update_t<NT, 2, CL, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      break;
+    case 4:
+      if (nyb == 2) team_left_update_t<NT, 4, CL, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      else team_left_update_t<NT, 4, CL, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      break;
+    case 8:
+      if (nyb == 2) team_left_update_t<NT, 8, CL, 2>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      else team_left_update_t<NT, 8, CL, 1>(q, ybuf, pan, prs, X, ld, ntiles, NP, r0, c_start, cp);
+      break;
     default: return false;
   }
   __syncthreads();
@@ -1413,7 +1432,7 @@ __device__ bool team_left_update(QrSmemFixed& q, double* ybuf, const double* pan
 // C <- C (I - V T V^T) on rows [rmin, nrows) x columns [j0, NP) of A (ld);
 // V[j][c] = pan2[c * prs + j] (explicit, zero left of the pivots).
 // Lane (gq, tq) holds C[gq][2tq + e] of each block.
-template <int NT, int tw, bool CL>
+template <int NT, int tw, bool CL, int nyb>
 __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, const double* pan2, int prs,
                                                  double* A, int ld, int nrows, int nch, int rmin, int j0,
                                                  ClusterPos cpin) {
@@ -1430,7 +1449,7 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
   constexpr int cs = tw * 8;                          // column stride between a warp's blocks
   const double* pB1 = pan2 + gq * prs + cw + 2 * tq;  // V[col 2tq (+e)][8h + gq]
   const double* pB2 = pan2 + tq * prs + cw + gq;      // V[col gq][8h + tq + 4e]
-  double* st = ybuf + 2 * NW * YB + warp * (TT * 64) + 2 * lane;
+  double* st = ybuf + nyb * NW * YB + warp * (TT * 64) + 2 * lane;
   int ldc = cs * ld;
   auto issue = [&](int t) {
     const double* src = A + (cw + 2 * tq) * ld + rmin + 8 * t + gq;
@@ -1476,7 +1495,7 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
         }
       }
     }
-    double* yb = ybuf + (it & 1) * NW * YB;
+    double* yb = ybuf + (nyb == 2 ? (it & 1) : 0) * NW * YB;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1490,6 +1509,7 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
     double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double ya[4];
     team_ysum<tw>(yb + lteam * tw * YB, gq, tq, ya);
+    if (nyb == 1) team_sync(lteam, tw);  // one Y buffer: all reads before the next group's writes
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
@@ -1518,13 +1538,25 @@ __device__ __noinline__ void team_right_update_t(QrSmemFixed& q, double* ybuf, c
 
 template <int NT, bool CL>
 __device__ bool team_right_update(QrSmemFixed& q, double* ybuf, const double* pan2, int prs, double* A,
-                                  int ld, int nrows, int NP, int rmin, int j0, ClusterPos cp) {
+                                  int ld, int nrows, int NP, int rmin, int j0, ClusterPos cp, int nyb) {
   const int nch = (NP - j0) >> 3;
   switch (team_width<NT>(nch)) {
-    case 1: team_right_update_t<NT, 1, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
-    case 2: team_right_update_t<NT, 2, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
-    case 4: team_right_update_t<NT, 4, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
-    case 8: team_right_update_t<NT, 8, CL>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp); break;
+    case 1:
+      if (nyb == 2) team_right_update_t<NT, 1, CL, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      else team_right_update_t<NT, 1, CL, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      break;
+    case 2:
+      if (nyb == 2) team_right_update_t<NT, 2, CL, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      else team_right_update_t<NT, 2, CL, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      break;
+    case 4:
+      if (nyb == 2) team_right_update_t<NT, 4, CL, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      else team_right_update_t<NT, 4, CL, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      break;
+    case 8:
+      if (nyb == 2) team_right_update_t<NT, 8, CL, 2>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      else team_right_update_t<NT, 8, CL, 1>(q, ybuf, pan2, prs, A, ld, nrows, nch, rmin, j0, cp);
+      break;
     default: return false;
   }
   __syncthreads();
@@ -1569,12 +1601,12 @@ __device__ __noinline__ void qr_phase(const SvdParams& P, QrSmemFixed& q, double
       if (!reg) explicit_v<NT>(pan, prs, k0, LP);
       panel_gram<NT>(q, pan, prs, kc, LP);
       long long _a = clock64();
-      if (!(NT == 256 && P.wtwo &&
+      if (!(NT == 256 && P.team_yb &&
             team_left_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(live), int(NP), int(k0),
-                                 int(k0 + BW), cp))) {
+                                 int(k0 + BW), cp, P.team_yb))) {
         if (cp.rank == 0)  // (the streaming fallback is not split: one CTA of the cluster runs it)
-          P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW)
-                 : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, LP, NP, kc, k0 + BW);
+          P.wtwo ? trailing_update_w<NT, true>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, LP, NP, kc, k0 + BW)
+                 : trailing_update_w<NT, false>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, LP, NP, kc, k0 + BW);
       }
       tr += clock64() - _a;
     }
@@ -1604,7 +1636,7 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
   const int64_t prs = LP + 36;
   double* pan = reinterpret_cast<double*>(smem_raw + sizeof(QrSmemFixed));
   const Ring ring{pan + BW * prs, P.qr_stages};
-  double* wbase = pan + BW * prs;  // per-warp regions (aliases the ring, used exclusively)
+  double* wbase = pan + BW * prs;  // team buffers / y, z + per-warp regions (aliases the ring)
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
   const ClusterPos cp = CL ? cluster_pos() : ClusterPos{0, 1};
@@ -1659,12 +1691,12 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       panel_gram<NT>(q, pan, prs, kc, RP);
       {
         long long _a = clock64();
-        if (!(NT == 256 && P.wtwo &&
+        if (!(NT == 256 && P.team_yb &&
               team_left_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(k),
-                                   int(k + BW), cp))) {
+                                   int(k + BW), cp, P.team_yb))) {
           if (cp.rank == 0)
-            P.wtwo ? trailing_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW)
-                   : trailing_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, kc, k + BW);
+            P.wtwo ? trailing_update_w<NT, true>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, RP, NP, kc, k + BW)
+                   : trailing_update_w<NT, false>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, RP, NP, kc, k + BW);
         }
         tr += clock64() - _a;
       }
@@ -1690,14 +1722,14 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
       }
       {
         long long _a = clock64();
-        if (NT == 256 && P.wtwo &&
+        if (NT == 256 && P.team_yb &&
             team_right_update<NT, CL>(q, wbase, pan, int(prs), X, int(LP), int(NP), int(NP), int(j0), int(j0),
-                                  cp)) {
+                                  cp, P.team_yb)) {
         } else if (cp.rank != 0) {
         } else if (P.wtwo) {
-          right_update_w<NT, true>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+          right_update_w<NT, true>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         } else {
-          right_update_w<NT, false>(q, wbase, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
+          right_update_w<NT, false>(q, wbase + QR_YZ_DOUBLES, pan, prs, X, LP, RP, NP, (j0 / RCH) * RCH, j0, j0);
         }
         ru += clock64() - _a;
       }
@@ -3758,6 +3790,7 @@ struct Plan {
   int64_t L, n, LP, NP, RP;
   int job;                  // effective job after the fallback mapping
   bool transposed, use_qr, wantv, bidiag, run_jacobi, internal_s, wtwo;
+  int team_yb;
   int reduce_nt;
   bool logs;                // right-side transformation logs (vector machinery buffers)
   bool run_front;           // reduce / bulge / bisect
@@ -3823,6 +3856,10 @@ int g_bisect_side_blocks = [] {
 // with the bulge-chase window in global memory, 3 = diagnostic: the values
 // pass stops after the reduce kernel (outputs undefined; for timing it alone)
 int g_tune_mode = 1;
+const bool g_team_off = [] {  // STARM_TEAM_UPDATES=0: streaming trailing updates only (A/B runs)
+  const char* e = getenv("STARM_TEAM_UPDATES");
+  return e && e[0] == '0';
+}();
 const bool g_reduce_cluster = [] {
   const char* e = getenv("STARM_REDUCE_CLUSTER");
   return !(e && e[0] == '0');
@@ -3862,11 +3899,15 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     const size_t fixed = sizeof(QrSmemFixed) + size_t(BW) * size_t(g.LP + 36) * sizeof(double);
     const size_t ring = size_t(GW) * XS * sizeof(double);
     g.qr_stages = 2;
-    auto smem_for = [&](int nt, bool two) {
-      size_t extra = size_t(g.qr_stages) * ring;
-      size_t w = size_t(nt / 32) * (two ? WREG : WREG1) * sizeof(double);
-      if (nt == 256 && two && w < size_t(TEAM_SMEM_DOUBLES) * sizeof(double))
-        w = size_t(TEAM_SMEM_DOUBLES) * sizeof(double);  // team updates' Y partials + stage
+    // after the panel: the streaming updates' y, z and per-warp rings, or
+    // (aliased) the team updates' Y partials + stages, or the load ring
+    auto smem_for = [&](int nt, bool two, int team_yb = 0) {
+      const size_t extra = size_t(g.qr_stages) * ring;
+      size_t w = (size_t(QR_YZ_DOUBLES) + size_t(nt / 32) * (two ? WREG : WREG1)) * sizeof(double);
+      const size_t team = team_yb == 2   ? size_t(TEAM_SMEM_DOUBLES) * sizeof(double)
+                          : team_yb == 1 ? size_t(TEAM_SMEM_DOUBLES1) * sizeof(double)
+                                         : 0;
+      if (team > w) w = team;
       return fixed + (w > extra ? w : extra);
     };
     const size_t cap = size_t(227 * 1024);
@@ -3877,7 +3918,12 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     if (nt == 512 && smem_for(512, false) > cap) nt = 256;
     g.reduce_nt = nt;
     g.wtwo = smem_for(nt, true) <= cap;
-    g.rsmem = smem_for(nt, g.wtwo);
+    // team updates (256 threads): two Y-partial buffers when they fit, one
+    // (an extra team barrier per group) for tall panels (c3: LP = 1024)
+    g.team_yb = 0;
+    if (nt == 256) g.team_yb = smem_for(nt, g.wtwo, 2) <= cap ? 2 : (smem_for(nt, g.wtwo, 1) <= cap ? 1 : 0);
+    if (g_team_off) g.team_yb = 0;
+    g.rsmem = smem_for(nt, g.wtwo, g.team_yb);
     if (g.rsmem > cap) g.bidiag = false;  // panel does not fit: Jacobi path
   }
   // Without the bidiagonal path the state-keeping jobs degrade to the plain
@@ -4186,6 +4232,7 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
   P.use_qr = pl.use_qr;
   P.bidiag = pl.bidiag;
   P.wtwo = pl.wtwo;
+  P.team_yb = pl.team_yb;
   P.lo = 0;
   P.hi = count;
   P.cctr = 2;
@@ -4209,7 +4256,7 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
     // splits the trailing updates (team path only: 256 threads, two-stage
     // rings).  STARM_REDUCE_CLUSTER=0 keeps one CTA per slice (A/B runs).
     int csz = 1;
-    if (pl.reduce_nt == 256 && pl.wtwo && g_reduce_cluster) {
+    if (pl.reduce_nt == 256 && pl.team_yb > 0 && g_reduce_cluster) {
       int dev = 0, sms = 0;
       STARM_CUDA_TRY(cudaGetDevice(&dev));
       STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -4456,6 +4503,7 @@ extern "C" int starm_svd_f64(const double* ahat, int64_t m, int64_t p, int64_t n
     Q.RP = tp.blk.RP;
     Q.transposed = m < p;
     Q.wtwo = tp.blk.wtwo;
+    Q.team_yb = tp.blk.team_yb;
     Q.stats = g_stats_on;
     svd_tsqr_kernel<256><<<tp.slots_q, 256, tp.blk.rsmem, st>>>(Q, S, tp.BR, tp.nbk, tp.SP);
     STARM_LAUNCH_CHECK();

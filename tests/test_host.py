@@ -223,3 +223,22 @@ def test_devices_argument_validation():
     assert _resolve_devices(None) == (None, None)
     with pytest.raises(ValueError, match="devices"):
         _resolve_devices(3.5)
+
+
+def test_blockwise_upload_policy(monkeypatch):
+    """The block-wise host upload applies to host tensors whose forward
+    transform is the deferrable DCT (3-way, power-of-two length >= 256) and
+    that are large enough; STARM_PIPELINE=0 switches it off."""
+    from paper_2605_16058_b200 import mode_product as mp
+    t = sb.DenseTensor(np.zeros((4, 6, 256), order="F"))
+    ts = sb.TransformSet.build(t.dims, "dct")
+    assert not mp.pipelined_upload_applies(t, ts)            # 48 KB: below the size floor
+    monkeypatch.setattr(mp, "PIPELINE_MIN_BYTES", 0)
+    assert mp.pipelined_upload_applies(t, ts)
+    monkeypatch.setenv("STARM_PIPELINE", "0")
+    assert not mp.pipelined_upload_applies(t, ts)
+    monkeypatch.delenv("STARM_PIPELINE")
+    t64 = sb.DenseTensor(np.zeros((4, 6, 64), order="F"))    # n = 64: dense product, not deferrable
+    assert not mp.pipelined_upload_applies(t64, sb.TransformSet.build(t64.dims, "dct"))
+    t4 = sb.DenseTensor(np.zeros((4, 6, 2, 256), order="F"))  # 4-way: not the 3-way fast path
+    assert not mp.pipelined_upload_applies(t4, sb.TransformSet.build(t4.dims, "dct"))
