@@ -77,6 +77,7 @@ struct SvdParams {
   int32_t* status;
   unsigned long long* counter;  // [0] reduce, [1] jacobi / vecout, [2] bulge, [3] orth, [8 + c] bulge chunk c
   int64_t lo, hi;               // bulge / bisect: list positions [lo, hi) of this launch
+  int64_t rlo, rhi;             // reduce kernel: list positions [rlo, rhi) of this launch
   int cctr;                     // bulge: counter index of this launch
   double* xslots;               // per-CTA X (LP x NP)
   double* wslots;               // per-CTA V (RP x NP), vector jobs
@@ -1642,13 +1643,13 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
   const ClusterPos cp = CL ? cluster_pos() : ClusterPos{0, 1};
   const int64_t cid = int64_t(blockIdx.x) / cp.size, ncl = int64_t(gridDim.x) / cp.size;
   double* X = P.xslots + cid * LP * NP;  // one working matrix per cluster
-  int64_t next_static = cid;
+  int64_t next_static = P.rlo + cid;
 
   for (;;) {
     // one CTA per slice: dynamic work counter; a cluster per slice: clusters
     // stride over the list (equal work per slice, no cross-CTA broadcast)
     if (cp.size == 1) {
-      if (tid == 0) cur = int64_t(atomicAdd(&P.counter[0], 1ull));
+      if (tid == 0) cur = P.rlo + int64_t(atomicAdd(&P.counter[0], 1ull));
     } else if (tid == 0) {
       cur = next_static;
     }
@@ -1656,7 +1657,7 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
     __syncthreads();
     const int64_t it = cur;
     __syncthreads();
-    if (it >= P.count) break;
+    if (it >= P.rhi) break;
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
@@ -4253,37 +4254,58 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
   }
   if (pl.run_front) {
     // Few slices (at most half the SMs): a cluster of 2 / 4 / 8 CTAs per slice
-    // splits the trailing updates (team path only: 256 threads, two-stage
-    // rings).  STARM_REDUCE_CLUSTER=0 keeps one CTA per slice (A/B runs).
-    int csz = 1;
-    if (pl.reduce_nt == 256 && pl.team_yb > 0 && g_reduce_cluster) {
-      int dev = 0, sms = 0;
-      STARM_CUDA_TRY(cudaGetDevice(&dev));
-      STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      while (csz < g_reduce_cluster_max && count * int64_t(2 * csz) <= int64_t(sms)) csz *= 2;
+    // splits the trailing updates (team path only).  STARM_REDUCE_CLUSTER=0
+    // keeps one CTA per slice (A/B runs).  A launch of several waves whose
+    // last wave fills at most half the SMs (c3: 512 slices = 3 waves of 148
+    // + 68) runs that remainder as a second launch on clusters.
+    int dev = 0, sms = 0;
+    STARM_CUDA_TRY(cudaGetDevice(&dev));
+    STARM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const bool can_cluster = pl.reduce_nt == 256 && pl.team_yb > 0 && g_reduce_cluster;
+    auto launch_reduce = [&](int64_t lo, int64_t hi) -> int {
+      if (lo >= hi) return STARM_OK;
+      SvdParams Pr = P;
+      Pr.rlo = lo;
+      Pr.rhi = hi;
+      const int64_t cnt = hi - lo;
+      int csz = 1;
+      if (can_cluster)
+        while (csz < g_reduce_cluster_max && cnt * int64_t(2 * csz) <= int64_t(sms)) csz *= 2;
+      if (csz > 1) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(cnt * csz), 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = pl.rsmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = unsigned(csz);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        STARM_CUDA_TRY(cudaFuncSetAttribute((const void*)svd_reduce_kernel<256, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.rsmem)));
+        STARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, svd_reduce_kernel<256, true>, Pr));
+      } else if (pl.reduce_nt == 512) {
+        svd_reduce_kernel<512, false><<<pl.slots_r, 512, pl.rsmem, st>>>(Pr);
+      } else {
+        svd_reduce_kernel<256, false><<<pl.slots_r, 256, pl.rsmem, st>>>(Pr);
+      }
+      STARM_LAUNCH_CHECK();
+      return STARM_OK;
+    };
+    {
+      const int64_t rem = count % pl.slots_r;
+      const bool split = can_cluster && count > pl.slots_r && pl.slots_r == sms && rem > 0 &&
+                         2 * rem <= int64_t(sms);
+      int rcl = launch_reduce(0, split ? count - rem : count);
+      if (rcl) return rcl;
+      if (split) {
+        rcl = launch_reduce(count - rem, count);
+        if (rcl) return rcl;
+      }
     }
-    if (csz > 1) {
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(unsigned(count * csz), 1, 1);
-      cfg.blockDim = dim3(256, 1, 1);
-      cfg.dynamicSmemBytes = pl.rsmem;
-      cfg.stream = st;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = unsigned(csz);
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      STARM_CUDA_TRY(cudaFuncSetAttribute((const void*)svd_reduce_kernel<256, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.rsmem)));
-      STARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, svd_reduce_kernel<256, true>, P));
-    } else if (pl.reduce_nt == 512) {
-      svd_reduce_kernel<512, false><<<pl.slots_r, 512, pl.rsmem, st>>>(P);
-    } else {
-      svd_reduce_kernel<256, false><<<pl.slots_r, 256, pl.rsmem, st>>>(P);
-    }
-    STARM_LAUNCH_CHECK();
     if (g_tune_mode == 3) return STARM_OK;
     // Bulge chase and sigma in NCH slice chunks: sigma of chunk c (FP64-pipe
     // bound, no shared memory) runs on a side stream next to the bulge chase
