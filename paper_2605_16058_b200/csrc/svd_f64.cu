@@ -4271,21 +4271,32 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
       int csz = 1;
       if (can_cluster)
         while (csz < g_reduce_cluster_max && cnt * int64_t(2 * csz) <= int64_t(sms)) csz *= 2;
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute at[1];
       if (csz > 1) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(unsigned(cnt * csz), 1, 1);
-        cfg.blockDim = dim3(256, 1, 1);
-        cfg.dynamicSmemBytes = pl.rsmem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = unsigned(csz);
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
         STARM_CUDA_TRY(cudaFuncSetAttribute((const void*)svd_reduce_kernel<256, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.rsmem)));
+        // halve the cluster until the device can co-schedule at least one
+        // (a partitioned or smaller GPU may not place 8 CTAs of this size)
+        for (; csz > 1; csz /= 2) {
+          cfg.gridDim = dim3(unsigned(cnt * csz), 1, 1);
+          cfg.blockDim = dim3(256, 1, 1);
+          cfg.dynamicSmemBytes = pl.rsmem;
+          cfg.stream = st;
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = unsigned(csz);
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          int nclusters = 0;
+          if (cudaOccupancyMaxActiveClusters(&nclusters, svd_reduce_kernel<256, true>, &cfg) == cudaSuccess &&
+              nclusters >= 1)
+            break;
+          (void)cudaGetLastError();
+        }
+      }
+      if (csz > 1) {
         STARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, svd_reduce_kernel<256, true>, Pr));
       } else if (pl.reduce_nt == 512) {
         svd_reduce_kernel<512, false><<<pl.slots_r, 512, pl.rsmem, st>>>(Pr);
