@@ -3386,6 +3386,8 @@ __host__ __device__ __forceinline__ int64_t bt_nblocks(int64_t n) {
 constexpr int BTV_S = 20;  // V window row stride (doubles, = 4 mod 16: conflict-free B fragments)
 constexpr int BTT_S = 20;  // T row stride
 constexpr int BT_NST = 8;  // blocks in flight (records + T): covers the L2/HBM latency of a block
+constexpr int BTR_S = 18;  // staged record stride (16 would put the 16 records of a block in one bank pair:
+                           // the V-window build read them 16-way conflicted, 47% of the kernel's wavefronts)
 
 // T of every block of every slice: one warp per (list position, block).
 __global__ void __launch_bounds__(128) svd_bt_tlog_kernel(SvdParams P, double* tlog, int64_t nblk) {
@@ -3467,7 +3469,7 @@ __global__ void __launch_bounds__(KB * 4) svd_bt_blocked_kernel(SvdParams P, con
   double* X = reinterpret_cast<double*>(smem_raw);   // [KB][xs]
   double* Vb = X + KB * xs;                          // [2][32 * BTV_S]
   double* Tb = Vb + 2 * 32 * BTV_S;                  // [BT_NST][16 * BTT_S]
-  double* Rb = Tb + BT_NST * BW * BTT_S;             // [BT_NST][16 records * 16] raw log records
+  double* Rb = Tb + BT_NST * BW * BTT_S;             // [BT_NST][16 records * BTR_S] raw log records
   const int ngroups = (n + KB - 1) / KB;
   for (int64_t cta = blockIdx.x; cta < P.count * ngroups; cta += gridDim.x) {
     const int64_t it = cta / ngroups;
@@ -3486,13 +3488,13 @@ __global__ void __launch_bounds__(KB * 4) svd_bt_blocked_kernel(SvdParams P, con
     const double* tl = tlog + si * nblk * (BW * BW);
     // stage block b (records + T) into buffer slot: records of sweeps 16 g + j, task k
     auto stage = [&](int64_t b, int64_t g, int64_t k, int slot) {
-      double* rb = Rb + slot * (BW * BW);
+      double* rb = Rb + slot * (BW * BTR_S);
       double* tb = Tb + slot * (BW * BTT_S);
       for (int e = tid; e < BW * (BW / 2); e += KB * 4) {
         const int j = e / (BW / 2), h = (e % (BW / 2)) * 2;
         const int64_t i = g * BW + j;
         const bool live = i <= n - 3 && k < hb_tasks(n, i);
-        cp_async16(rb + j * BW + h, live ? lg + (i * kmax + k) * HLOG + h : lg, live ? 16 : 0);
+        cp_async16(rb + j * BTR_S + h, live ? lg + (i * kmax + k) * HLOG + h : lg, live ? 16 : 0);
         const int a = e / (BW / 2), c = (e % (BW / 2)) * 2;
         cp_async16(tb + a * BTT_S + c, tl + b * (BW * BW) + a * BW + c, 16);
       }
@@ -3523,12 +3525,12 @@ __global__ void __launch_bounds__(KB * 4) svd_bt_blocked_kernel(SvdParams P, con
       __syncthreads();
       {  // V window of block b from its staged records
         double* Vw = Vb + vslot * (32 * BTV_S);
-        const double* rb = Rb + slot * (BW * BW);
+        const double* rb = Rb + slot * (BW * BTR_S);
         for (int e = tid; e < 32 * BW; e += KB * 4) {
           const int l = e / BW, j = e % BW;
           const int d = l - 1 - j;
           double v = 0.0;
-          if (d >= 0 && d < BW && rb[j * BW] != 0.0) v = d == 0 ? 1.0 : rb[j * BW + d];
+          if (d >= 0 && d < BW && rb[j * BTR_S] != 0.0) v = d == 0 ? 1.0 : rb[j * BTR_S + d];
           Vw[l * BTV_S + j] = v;
         }
       }
@@ -3825,7 +3827,7 @@ const bool g_bt_blocked = [] {
   return !(e && e[0] == '0');
 }();
 size_t bt_blocked_smem(int64_t n, int kb) {
-  return (size_t(kb) * lq_xs(n) + 2 * 32 * BTV_S + size_t(BT_NST) * (BW * BTT_S + BW * BW)) *
+  return (size_t(kb) * lq_xs(n) + 2 * 32 * BTV_S + size_t(BT_NST) * (BW * BTT_S + BW * BTR_S)) *
          sizeof(double);
 }
 // reduce-kernel CTA size: 0 = automatic, else 256 or 512 (env STARM_REDUCE_THREADS)
