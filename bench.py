@@ -358,6 +358,19 @@ def profiled_traffic(kernel, cfg):
         return None
 
 
+def wave_text(slices, sms):
+    """How the reduce launch maps slices to SMs (svd_f64.cu: one CTA per slice,
+    or a cluster of 2 / 4 / 8 CTAs per slice when slices <= SMs / 2; a last
+    partial wave of a multi-wave launch also runs on clusters)."""
+    if slices <= sms // 2:
+        c = 1
+        while c < 8 and slices * 2 * c <= sms:
+            c *= 2
+        return f"{slices} slices on {sms} SMs ({c}-CTA cluster per slice)"
+    waves = -(-slices // sms)
+    return f"{slices} slices on {sms} SMs (one CTA per slice, {waves} wave{'s' if waves > 1 else ''})"
+
+
 def fp64_peak(torch, dev):
     """cuBLAS DGEMM rate on this box (the FP64 denominator; MEASURED_PEAKS.json
     has no FP64 entry)."""
@@ -552,7 +565,7 @@ def run_ours(args):
                    "frac": f_red / t_red / 1e12 / peak,
                    "traffic": profiled_traffic("svd_reduce_kernel", args.config),
                    "algorithmic_flops": f_red, "ms": t_red * 1e3, "slices": n_svd,
-                   "wave": f"{n_svd} slices on {torch.cuda.get_device_properties(dev).multi_processor_count} SMs (one CTA per slice)"}
+                   "wave": wave_text(n_svd, torch.cuda.get_device_properties(dev).multi_processor_count)}
     if unpruned is not None:
         f_full = n * (2 * a_ * b_ ** 2 + 2 * b_ ** 3)
         unpruned["reduce_achieved_tflops"] = f_full / (unpruned["reduce_ms"] / 1e3) / 1e12

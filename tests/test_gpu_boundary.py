@@ -221,3 +221,32 @@ def test_blockwise_dense_upload_equals_device_resident_fixed_rank(monkeypatch):
     one2 = mp_.forward_device(sb.DeviceTensor.from_host(t2), ts2)
     blk2 = mp_.forward_from_host(t2, ts2, dev)
     assert blk2 is not None and torch.equal(one2.data, blk2.data)
+
+
+def test_large_results_return_in_page_locked_buffers(monkeypatch):
+    """device_to_host: results above the size floor are copied into page-locked
+    buffers (numpy views that keep them alive), smaller ones take the
+    pageable copy; values are the same either way."""
+    import torch
+    from paper_2605_16058_b200 import tensors as tn
+    dev = nat.require_cuda()
+    x = torch.arange(1 << 16, dtype=torch.float64, device=dev)
+    y = torch.arange(7, dtype=torch.float64, device=dev)
+    monkeypatch.setattr(tn, "PINNED_RESULT_MIN_BYTES", 1 << 18)
+    a, b = tn.device_to_host(x, y)
+    assert np.array_equal(a, np.arange(1 << 16, dtype=np.float64)) and np.array_equal(b, np.arange(7.0))
+    assert torch.from_numpy(a).is_pinned() and not torch.from_numpy(b).is_pinned()
+    monkeypatch.setenv("STARM_PINNED_RESULTS", "0")
+    c = tn.device_to_host(x)
+    assert np.array_equal(c, a) and not torch.from_numpy(c).is_pinned()
+    # a compression whose factors exceed the floor comes back identical
+    monkeypatch.delenv("STARM_PINNED_RESULTS")
+    monkeypatch.setattr(tn, "PINNED_RESULT_MIN_BYTES", 1 << 10)
+    dims = (40, 36, 32)
+    t = sb.DenseTensor(random_array(dims, 5))
+    ts = sb.TransformSet.build(dims, "dct")
+    got = sb.tsvdm_fixed_rank(t, ts, 7)
+    monkeypatch.setattr(tn, "PINNED_RESULT_MIN_BYTES", 1 << 40)
+    ref = sb.tsvdm_fixed_rank(t, ts, 7)
+    assert np.array_equal(got.factors.u_data, ref.factors.u_data)
+    assert np.array_equal(got.factors.g_data, ref.factors.g_data)
