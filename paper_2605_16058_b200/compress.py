@@ -547,23 +547,17 @@ def tsvdm_tolerance_stream(tensors, ts: TransformSet, epsilon, strategy=MEMORY_E
 
 
 PRUNE = os.environ.get("STARM_PRUNE", "1") != "0"   # STARM_PRUNE=0: diagnostic, unpruned
+PRUNE_REFINE = os.environ.get("STARM_PRUNE_REFINE", "1") != "0"   # 0: the plain energy rule only
 PRUNE_GAMMA = 0.3      # left-out energy target as a fraction of the budget
 PRUNE_MIN = 0.25       # prune only when at least this fraction of the slices drops out
 
 
 def prune_select(ahat3, epsilon):
-    """The slice selection of the pruned tolerance path: per-slice energies f
-    (starm_slice_energy_f64, one 8N-byte D2H), the slices of smallest f whose
-    total stays below PRUNE_GAMMA * eps^2 * sum(f) are left out.  Returns
-    (kept slice ids ascending, e0 = left-out energy, tbound = largest left-out
-    f) or None when too few slices would drop out or f is not finite."""
-    import torch
-    m, p, n = ahat3.dims
-    dev = ahat3.device
-    f_dev = torch.empty(n, dtype=torch.float64, device=dev)
-    nat.call("starm_slice_energy_f64", ahat3.data.data_ptr(), m * p, n, f_dev.data_ptr(),
-             nat.stream_ptr(dev))
-    return prune_choose(f_dev.cpu().numpy(), epsilon)
+    """The slice selection the pruned tolerance path tries first (see
+    prune_plan): (kept slice ids ascending, e0 = left-out energy, tbound =
+    bound on every left-out sigma^2) or None when nothing prunes."""
+    plan = prune_plan(ahat3, epsilon)
+    return plan[0] if plan else None
 
 
 def prune_choose(f, epsilon):
@@ -581,6 +575,67 @@ def prune_choose(f, epsilon):
         return None
     keep_ids = np.sort(order[k:])
     return keep_ids, math.fsum(f[np.sort(order[:k])].tolist()), float(f[order[k - 1]])
+
+
+PRUNE_GAMMA2 = 0.4      # left-out energy cap once the marginal slices carry the sharper bound
+PRUNE_REFINE_MAX = 64   # at most this many marginal slices get the sharper bound
+PRUNE_CLUSTER_SLICES = None   # kept-slice count the refinement aims for (None: half the SMs)
+
+
+def prune_refine(ahat3, f, epsilon, sel):
+    """A second, sharper selection on top of ``sel`` = prune_choose(f): the
+    kept slices of smallest energy are often rank-0 slices whose energy is
+    spread over two or more comparable singular values (c2: sine / cosine
+    pairs, sigma_1^2 ~ f / 2), so f overstates their sigma_max^2.  For the
+    marginal ones (ascending f while the left-out energy stays below
+    PRUNE_GAMMA2 of the budget) compute b_i = ||G_i^2||_F^(1/2) with G_i the
+    slice's Gram matrix: (sum sigma^8)^(1/4) >= sigma_1^2, two small batched
+    DMMA products per slice (starm_facewise_gemm_f64, starm_slice_energy_f64).
+    A marginal slice whose b_i does not exceed the bound ``tbound`` that
+    ``sel`` already certifies against is left out too: tbound is unchanged,
+    only e0 grows.  Worth doing only when it brings the kept count down to
+    half the SMs or fewer, where the reduce kernel puts a cluster of CTAs on
+    each slice.  Returns (keep_ids, e0, tbound) or None."""
+    import torch
+    keep_ids, e0, tbound = sel
+    m, p, n = ahat3.dims
+    dev = ahat3.device
+    half = PRUNE_CLUSTER_SLICES or torch.cuda.get_device_properties(dev).multi_processor_count // 2
+    if keep_ids.size <= half:
+        return None
+    f = np.asarray(f, dtype=np.float64)
+    budget = epsilon * epsilon * float(f.sum())      # (a cap for a heuristic: plain summation will do)
+    fk = f[keep_ids]
+    ordk = keep_ids[np.argsort(fk, kind="stable")[:PRUNE_REFINE_MAX + 1]]
+    cum = e0 + np.cumsum(f[ordk])
+    nc = int(np.searchsorted(cum, PRUNE_GAMMA2 * budget, side="right"))
+    if nc == 0 or nc > PRUNE_REFINE_MAX or keep_ids.size - nc > half:
+        return None
+    cand = np.sort(ordk[:nc])
+    ids = torch.from_numpy(cand.astype(np.int64)).to(dev)
+    a = ahat3.data.view(n, p, m).index_select(0, ids)            # column-major m x p slices
+    at = a.transpose(1, 2).contiguous()                          # column-major p x m: the transposes
+    q = min(m, p)
+    g = torch.empty(nc * q * q, dtype=torch.float64, device=dev)
+    st = nat.stream_ptr(dev)
+    if m <= p:   # G = A A^T (m x m)
+        nat.call("starm_facewise_gemm_f64", a.data_ptr(), at.data_ptr(), g.data_ptr(), m, p, m, nc, st)
+    else:        # G = A^T A (p x p)
+        nat.call("starm_facewise_gemm_f64", at.data_ptr(), a.data_ptr(), g.data_ptr(), p, m, p, nc, st)
+    g2 = torch.empty_like(g)
+    nat.call("starm_facewise_gemm_f64", g.data_ptr(), g.data_ptr(), g2.data_ptr(), q, q, q, nc, st)
+    e8 = torch.empty(nc, dtype=torch.float64, device=dev)
+    nat.call("starm_slice_energy_f64", g2.data_ptr(), q * q, nc, e8.data_ptr(), st)
+    # (sum sigma^8)^(1/4), widened well past the products' rounding
+    b = np.sqrt(np.sqrt(e8.cpu().numpy())) * (1.0 + 1e-9)
+    drop = cand[np.isfinite(b) & (b <= tbound)]
+    if drop.size == 0 or keep_ids.size - drop.size > half:
+        return None
+    keep2 = keep_ids[~np.isin(keep_ids, drop)]
+    # e0 of the larger left-out set, summed exactly like prune_choose's
+    mask = np.ones(n, dtype=bool)
+    mask[keep2] = False
+    return keep2, math.fsum(f[mask].tolist()), tbound
 
 
 def _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred=None):
@@ -605,12 +660,41 @@ def _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred=None):
     if n < 8 or strategy not in (MEMORY_EFFICIENT, COMPUTE_EFFICIENT):
         return None
     with clock.stage("prune-energy"):
-        if deferred is not None and deferred.energies is not None:
-            sel = prune_choose(deferred.energies.cpu().numpy(), epsilon)
-        else:
-            sel = prune_select(ahat3, epsilon)
+        sels = prune_plan(ahat3, epsilon, deferred.energies if deferred is not None else None)
+    # the sharper selection first; if its certificate fails the plain one
+    # (one more values pass over a single wave), then the unpruned path
+    for sel in sels:
+        res = _pruned_attempt(ahat3, epsilon, strategy, clock, deferred, sel)
+        if res is not None:
+            return res
+    return None
+
+
+def prune_plan(ahat3, epsilon, f_dev=None):
+    """The selections the pruned tolerance path tries, in order: the sharper
+    one (prune_refine) when it applies, then the plain energy rule
+    (prune_choose); [] when nothing prunes."""
+    import torch
+    m, p, n = ahat3.dims
+    if f_dev is None:
+        f_dev = torch.empty(n, dtype=torch.float64, device=ahat3.device)
+        nat.call("starm_slice_energy_f64", ahat3.data.data_ptr(), m * p, n, f_dev.data_ptr(),
+                 nat.stream_ptr(ahat3.device))
+    f = f_dev.cpu().numpy()
+    sel = prune_choose(f, epsilon)
     if sel is None:
-        return None
+        return []
+    sharp = prune_refine(ahat3, f, epsilon, sel) if PRUNE_REFINE else None
+    return [sharp, sel] if sharp is not None else [sel]
+
+
+def _pruned_attempt(ahat3, epsilon, strategy, clock, deferred, sel):
+    """One pruned computation with the selection ``sel``; None when its
+    certificate fails."""
+    import torch
+    m, p, n = ahat3.dims
+    r = min(m, p)
+    dev = ahat3.device
     keep_ids, e0, tbound = sel
     if deferred is not None:
         # energies of the exact-DCT slices: the reference operator differs by

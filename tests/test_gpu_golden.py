@@ -426,3 +426,48 @@ def test_full_tsvdm_at_c1_scale():
     # sigma of the golden c1 run (reference package output, full spectrum)
     gs = GC["c1/s"]
     assert gs.shape == s.shape and sigma_close(s, gs)[0]
+
+
+def test_tolerance_pruning_sharper_bound_equals_unpruned(monkeypatch):
+    """prune_refine: marginal kept slices whose energy sits in two equal
+    singular values (sigma_1^2 = f / 2) are left out through the Gram-square
+    bound (sum sigma^8)^(1/4) <= the bound already certified against; ranks
+    and factors are those of the unpruned computation (tsvdm.py:268-321)."""
+    from paper_2605_16058_b200 import compress as cp
+    rng = np.random.default_rng(3)
+    m, p, n = 24, 32, 96
+    a = np.zeros((m, p, n), order="F")
+
+    def ortho(k, r):
+        q, _ = np.linalg.qr(rng.standard_normal((k, r)))
+        return q
+
+    for i in range(n):
+        if i < 8:
+            sig = np.sqrt([1.0e4, 5.0e3])
+        elif i < 40:
+            sig = np.sqrt([60.0, 60.0]) * (1.0 + 0.01 * rng.standard_normal())
+        else:
+            sig = np.array([0.0, 0.0])
+        a[:, :, i] = (ortho(m, 2) * sig) @ ortho(p, 2).T + 0.03 * rng.standard_normal((m, p))
+    t = sb.DenseTensor(a)
+    ts = sb.TransformSet.build((m, p, n), "identity")
+    eps = 0.254
+    monkeypatch.setattr(cp, "PRUNE", False)
+    ref = sb.tsvdm_tolerance(t, ts, eps)
+    monkeypatch.setattr(cp, "PRUNE", True)
+    monkeypatch.setattr(cp, "PRUNE_CLUSTER_SLICES", 16)
+    x = sb.DeviceTensor.from_host(t)
+    plan = cp.prune_plan(x, eps)
+    assert len(plan) == 2 and plan[0][0].size < plan[1][0].size <= n      # the sharper selection comes first
+    assert plan[0][0].size <= 16 and plan[0][2] == plan[1][2]             # same bound, more slices left out
+    clock = sb.StageClock()
+    got = sb.tsvdm_tolerance(t, ts, eps, clock=clock)
+    assert clock.info["prune_certificate"] == "ok" and clock.info["pruned_slices"] == n - plan[0][0].size
+    assert np.array_equal(got.ranks, ref.ranks)
+    assert np.array_equal(got.factors.u_data, ref.factors.u_data)
+    assert np.array_equal(got.factors.g_data, ref.factors.g_data)
+    assert abs(got.total_energy - ref.total_energy) <= 1e-12 * ref.total_energy
+    assert abs(got.discarded_energy - ref.discarded_energy) <= 1e-12 * ref.total_energy
+    o = oracle.tsvdm_tolerance(a, [tr.matrix for tr in ts], eps)
+    assert np.array_equal(got.ranks, o["ranks"])
