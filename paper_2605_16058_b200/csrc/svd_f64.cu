@@ -2208,7 +2208,9 @@ __global__ void svd_bisect_kernel(SvdParams P) {
     // lanes whose brackets coincide split that bracket into k + 1 parts
     // with k distinct probes, and every lane tightens its bracket with all
     // probes of its slice (32 probes per Sturm sweep instead of 1).
+    int nA = 0, nB = 0, nC = 0;  // sweeps of this warp per phase (diagnostic counters)
     while (__any_sync(0xffffffffu, state == 0)) {
+      ++nA;
       bool probe = false;
       if (state == 0) {
         if (converged()) {
@@ -2259,6 +2261,7 @@ __global__ void svd_bisect_kernel(SvdParams P) {
     }
     // ---- phase B: Laguerre inside the bracket
     for (int lt = 0; lt < 16 && __any_sync(0xffffffffu, state == 1); ++lt) {
+      ++nB;
       if (state == 1) {
         double G, H;
         const int64_t c = count_lag(d, e, int(n), x, pivmin, G, H);
@@ -2286,6 +2289,7 @@ __global__ void svd_bisect_kernel(SvdParams P) {
     if (state == 1) state = 2;
     // ---- phase C: bisection to the end for the rest
     while (__any_sync(0xffffffffu, state == 2)) {
+      ++nC;
       if (state == 2) {
         if (converged()) {
           sigma = 0.5 * (lo + hi);
@@ -2298,6 +2302,12 @@ __global__ void svd_bisect_kernel(SvdParams P) {
       }
     }
     if (valid && flag != 2) P.s[j + slice * n] = sigma;
+    if (P.stats && lane == 0) {
+      atomicAdd(&g_stats[ST_SWEEPS], (unsigned long long)nA);
+      atomicAdd(&g_stats[ST_PAIRS], (unsigned long long)nB);
+      atomicAdd(&g_stats[ST_ROTATED], (unsigned long long)nC);
+      atomicMax(&g_stats[ST_CYC_FINAL], (unsigned long long)(nA * 1000000 + nB * 1000 + nC));
+    }
   }
 }
 
