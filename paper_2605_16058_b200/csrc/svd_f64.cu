@@ -3075,10 +3075,9 @@ __global__ void __launch_bounds__(256) svd_orth_block_kernel(SvdParams P) {
 constexpr int BT_REC = 17;   // padded record stride
 constexpr int BT_ROWS = 64;  // LQ panel rows per staged chunk (double-buffered)
 // Sweep-record buffers (records staged BT_NRB - 1 sweeps ahead) and the L2
-// prefetch distance in sweeps used when the reflector log of the launch is
-// too large to still be L2-resident.  Measured (ncu, cold caches): c2 (85 MB
-// of log) 0.617 ms without prefetch, 0.521 with; c1 (33 MB) 0.427 without,
-// 0.648 with; deeper staging (4, 8 buffers) changes neither.
+// prefetch distance in sweeps.  Measured (ncu, cold caches): c2 (85 MB of
+// log) 0.65 ms without prefetch, 0.52 with; c1 (33 MB) 0.42 without, 0.35
+// with; deeper staging (4, 8 buffers) changes neither.
 constexpr int BT_NRB = 2;
 constexpr int BT_PF = 16;
 __host__ __device__ __forceinline__ int64_t bt_stride(int64_t n) { return n + n / 16 + 48; }
@@ -3088,7 +3087,8 @@ __host__ __device__ __forceinline__ size_t bt_smem(int64_t n, int g) {
 }
 __device__ __forceinline__ int sx(int q) { return q + (q >> 4); }
 
-__global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int G, int lq, int pf) {
+template <bool PF>
+__global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int G, int lq) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nthr = blockDim.x;
   const int n = int(P.n);
@@ -3137,17 +3137,18 @@ __global__ void __launch_bounds__(256) svd_backtransform_kernel(SvdParams P, int
       cp_async_commit();
     };
     auto prefetch = [&](int i) {  // one 128-byte line per thread
-      if (pf && i >= 0) {
+      if (PF && i >= 0) {
         const int lines = (int(hb_tasks(n, i)) * HLOG * 8 + 127) / 128;
         if (int(threadIdx.x) < lines)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(lg + int64_t(i) * kmax * HLOG + threadIdx.x * 16));
       }
     };
-    for (int d = 0; d < BT_PF; ++d) prefetch(n - 3 - d);
+    if (PF)
+      for (int d = 0; d < BT_PF; ++d) prefetch(n - 3 - d);
     for (int d = 0; d < BT_NRB - 1; ++d) stage(n - 3 - d);
     for (int i = n - 3; i >= 0; --i) {
       stage(i - (BT_NRB - 1));
-      prefetch(i - BT_PF);
+      if (PF) prefetch(i - BT_PF);
       cp_async_wait<BT_NRB - 1>();
       __syncthreads();
       const int K = int(hb_tasks(n, i));
@@ -3989,7 +3990,8 @@ int make_plan(int64_t m, int64_t p, int64_t count, int64_t nslices, int job, boo
     g.bt_g = 8;  // vectors (warps) per back-transform CTA
     while (g.bt_g > 1 && bt_smem(g.n, g.bt_g) > size_t(200 * 1024)) --g.bt_g;
     g.tsmem = bt_smem(g.n, g.bt_g);
-    rc = occupancy((const void*)svd_backtransform_kernel, 32 * g.bt_g, g.tsmem, &per);
+    rc = occupancy((const void*)svd_backtransform_kernel<true>, 32 * g.bt_g, g.tsmem, &per);
+    if (!rc) rc = occupancy((const void*)svd_backtransform_kernel<false>, 32 * g.bt_g, g.tsmem, &per);
     if (rc) return rc;
     g.btw = per;  // back-transform CTAs per SM
     const int64_t work = count * g.n;
@@ -4447,10 +4449,14 @@ int svd_core(const double* ahat, int64_t m, int64_t p, int64_t nslices, const in
         if (bb > int64_t(sms) * per) bb = int64_t(sms) * per;
         bk<<<unsigned(bb), pl.bt_kb * 4, bsm, st>>>(P, tlog, pl.bt_nblk);
       } else {
-        // L2 prefetch of the sweep records only when the launch's reflector
-        // log is too large to still sit in L2 from the bulge chase
-        const int pf = size_t(count) * size_t(pl.hhcap) * sizeof(double) > (size_t(48) << 20) ? 1 : 0;
-        svd_backtransform_kernel<<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0, pf);
+        // L2 prefetch of the sweep records 16 sweeps ahead (STARM_BT_PREFETCH=0:
+        // the plain instantiation, for A/B runs)
+        int pf = 1;
+        if (const char* e = getenv("STARM_BT_PREFETCH")) pf = e[0] == '1';
+        // (measured, ncu, with both instantiations in the library: c2 0.65 -> 0.52 ms,
+        // c1 0.42 -> 0.35 ms; the timing of this kernel is sensitive to code layout)
+        if (pf) svd_backtransform_kernel<true><<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0);
+        else svd_backtransform_kernel<false><<<unsigned(blocks), 32 * pl.bt_g, pl.tsmem, st>>>(P, pl.bt_g, lkb == 0);
       }
       STARM_LAUNCH_CHECK();
       if (lkb) {
