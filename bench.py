@@ -202,7 +202,7 @@ def run_reference(args):
                                    f"+ threshold; CPU {model}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------ GPU arm helpers
@@ -690,7 +690,7 @@ def run_ours(args):
                           if "orig_error" in wl.extra else {})},
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -823,7 +823,7 @@ def run_sharded(args):
             "result": {"total_rank": int(res.ranks.sum()), "relative_error": res.relative_error,
                        "realised_error": realised},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -843,15 +843,33 @@ def run_dry(args):
     counts = torch.tensor([plan.nf, plan.ns], dtype=torch.int64)
     dist.all_reduce(counts)
     if rank == 0:
-        print(json.dumps({"dry_run": True, "world_size": dist.get_world_size(), "config": args.config,
-                          "fibres": int(counts[0]), "slices": int(counts[1]),
-                          "mode": "replicas" if args.replicas else "sharded"}), flush=True)
+        emit({"dry_run": True, "world_size": dist.get_world_size(), "config": args.config,
+              "fibres": int(counts[0]), "slices": int(counts[1]),
+              "mode": "replicas" if args.replicas else "sharded"})
     dist.barrier()
     dist.destroy_process_group()
 
 
+_JSON_OUT = None   # the process's real stdout (fd 1 is pointed at stderr while the bench runs)
+
+
+def emit(obj):
+    """The one JSON line of this run, on the real stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
     args = parse()
+    # stdout carries exactly one JSON line: libraries that print to fd 1 (the
+    # NCCL version banner does, whatever NCCL_DEBUG_FILE says) land on stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if not (args.gpus > 1 and "WORLD_SIZE" not in os.environ):   # (the relauncher just forwards its children)
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
     _, world, _ = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args))
