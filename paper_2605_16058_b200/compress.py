@@ -568,13 +568,15 @@ def prune_choose(f, epsilon):
     n = f.size
     if n < 8 or not np.isfinite(f).all():
         return None                      # the SVD names the non-finite slice
-    budget = epsilon * epsilon * math.fsum(f.tolist())
+    # (numpy's pairwise sums: deterministic for a given f, so every rank of the
+    # sharded path derives the same numbers; math.fsum cost 0.1 ms per call here)
+    budget = epsilon * epsilon * float(np.sum(f))
     order = np.argsort(f, kind="stable")
     k = int(np.searchsorted(np.cumsum(f[order]), PRUNE_GAMMA * budget, side="right"))
     if k < PRUNE_MIN * n or k >= n:
         return None
     keep_ids = np.sort(order[k:])
-    return keep_ids, math.fsum(f[np.sort(order[:k])].tolist()), float(f[order[k - 1]])
+    return keep_ids, float(np.sum(f[np.sort(order[:k])])), float(f[order[k - 1]])
 
 
 PRUNE_GAMMA2 = 0.4      # left-out energy cap once the marginal slices carry the sharper bound
@@ -635,7 +637,7 @@ def prune_refine(ahat3, f, epsilon, sel):
     # e0 of the larger left-out set, summed exactly like prune_choose's
     mask = np.ones(n, dtype=bool)
     mask[keep2] = False
-    return keep2, math.fsum(f[mask].tolist()), tbound
+    return keep2, float(np.sum(f[mask])), tbound
 
 
 def _tolerance_pruned(ahat3, epsilon, strategy, clock, deferred=None):
