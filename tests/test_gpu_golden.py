@@ -434,6 +434,8 @@ def test_tolerance_pruning_sharper_bound_equals_unpruned(monkeypatch):
     bound (sum sigma^8)^(1/4) <= the bound already certified against; ranks
     and factors are those of the unpruned computation (tsvdm.py:268-321)."""
     from paper_2605_16058_b200 import compress as cp
+    if not cp.PRUNE_REFINE:
+        pytest.skip("STARM_PRUNE_REFINE=0")
     rng = np.random.default_rng(3)
     m, p, n = 24, 32, 96
     a = np.zeros((m, p, n), order="F")
