@@ -475,7 +475,11 @@ __device__ void cgs2_fix(FinalView& fs, double* Q, int64_t ld, int64_t len, cons
 // slot (LP x NP, ld LP); rows < 0 means all P.L rows.
 template <int NT>
 __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, double* __restrict__ X,
-                          double* tile, int64_t row0 = 0, int64_t rows = -1) {
+                          double* tile, int64_t row0 = 0, int64_t rows = -1, int part = 0, int parts = 1) {
+  // part / parts: the CTAs of a cluster each load every parts-th batch / tile
+  // of the slice; the return value is then this CTA's share of the flag as
+  // bits (1: saw a non-finite entry, 2: saw a nonzero entry) for the caller
+  // to combine across the cluster.
   // Batched so that every thread keeps LB loads in flight (the copy is
   // HBM-latency bound otherwise).
   constexpr int LB = 16;
@@ -493,11 +497,12 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
         d[u] = (e < total && r < L && c < n) ? A[(row0 + r) + c * P.m] : 0.0;
       }
     };
-    load_batch(w, 0);
-    for (int64_t e0 = 0; e0 < total; e0 += int64_t(NT) * LB) {
+    const int64_t bstep = int64_t(NT) * LB * parts;
+    load_batch(w, int64_t(NT) * LB * part);
+    for (int64_t e0 = int64_t(NT) * LB * part; e0 < total; e0 += bstep) {
 #pragma unroll
       for (int u = 0; u < LB; ++u) v[u] = w[u];
-      load_batch(w, e0 + int64_t(NT) * LB);
+      load_batch(w, e0 + bstep);
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
         const int64_t e = e0 + tid + int64_t(u) * NT;
@@ -523,8 +528,8 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
         v[u] = (t < ntiles && r < L && c < n) ? A[c + (row0 + r) * P.m] : 0.0;
       }
     };
-    load_tile(0);
-    for (int64_t t = 0; t < ntiles; ++t) {
+    load_tile(part);
+    for (int64_t t = part; t < ntiles; t += parts) {
       const int64_t c0 = (t / nrt) * 32, r0 = (t % nrt) * 128;
 #pragma unroll
       for (int u = 0; u < LT; ++u) {
@@ -534,7 +539,7 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
         tile[(e >> 5) * 33 + (e & 31)] = v[u];
       }
       __syncthreads();
-      load_tile(t + 1);
+      load_tile(t + parts);
 #pragma unroll
       for (int u = 0; u < LT; ++u) {
         const int e = tid + u * NT;
@@ -547,6 +552,7 @@ __device__ int load_slice(const SvdParams& P, const double* __restrict__ A, doub
   }
   bad = __syncthreads_or(bad);
   nonzero = __syncthreads_or(nonzero);
+  if (parts > 1) return (bad ? 1 : 0) | (nonzero ? 2 : 0);
   return bad ? 2 : (nonzero ? 0 : 1);
 }
 
@@ -1661,13 +1667,32 @@ __global__ void __launch_bounds__(NT, 1) svd_reduce_kernel(SvdParams P) {
     const int64_t si = state_index(P, it);
     const int64_t slice = P.ids ? P.ids[it] : it;
     long long t0 = clock64();
-    const int flag = load_slice<NT>(P, P.A + slice * P.m * P.p, X, ring.buf(0));
-    if (tid == 0) {
+    int flag;
+    if (cp.size == 1) {
+      flag = load_slice<NT>(P, P.A + slice * P.m * P.p, X, ring.buf(0));
+    } else {
+      // the cluster's CTAs load interleaved shares of the slice and exchange
+      // their flag bits through distributed shared memory
+      __shared__ int fbits[8];
+      const int mine = load_slice<NT>(P, P.A + slice * P.m * P.p, X, ring.buf(0), 0, -1, cp.rank, cp.size);
+      if (tid < cp.size) {  // thread r writes this CTA's bits into CTA r's fbits[rank]
+        unsigned long long remote;
+        asm volatile("mapa.u64 %0, %1, %2;"
+                     : "=l"(remote)
+                     : "l"(reinterpret_cast<unsigned long long>(&fbits[cp.rank])), "r"(unsigned(tid)));
+        *reinterpret_cast<volatile int*>(remote) = mine;
+      }
+      cluster_sync(cp);
+      int bits = 0;
+      for (int r = 0; r < cp.size; ++r) bits |= fbits[r];
+      flag = (bits & 1) ? 2 : ((bits & 2) ? 0 : 1);
+    }
+    if (tid == 0 && cp.rank == 0) {
       P.flags[si] = flag;
       if (flag == 2) atomicMin(&P.status[0], int32_t(slice));
     }
-    // (every CTA of a cluster loaded the same X and got the same flag; none
-    // may update X before all have finished writing it)
+    // (no CTA of a cluster may update X before all have finished writing it;
+    // the second barrier also keeps the next slice's flag exchange off fbits)
     cluster_sync(cp);
     if (flag) continue;
     long long t1 = clock64();
