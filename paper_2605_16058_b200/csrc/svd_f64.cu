@@ -180,33 +180,6 @@ __device__ __forceinline__ void stage_pair(double* buf, const double* M, int64_t
   cp_async_commit();
 }
 
-// Stage rows [r0, r0+RCH) of 32 contiguous columns col0.. (zero past ncols).
-__device__ __forceinline__ void stage_cols(double* buf, const double* M, int64_t ld, int64_t r0,
-                                           int64_t col0, int64_t ncols) {
-#pragma unroll
-  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
-    const int c = threadIdx.x + q * TPB;
-    const int col = c >> 5;
-    const int r2 = (c & 31) * 2;
-    const bool in = col0 + col < ncols;
-    cp_async16(buf + col * XS + r2, in ? M + r0 + r2 + (col0 + col) * ld : M, in ? 16 : 0);
-  }
-  cp_async_commit();
-}
-
-__device__ __forceinline__ void store_cols(double* M, int64_t ld, int64_t r0, int64_t col0,
-                                           int64_t ncols, const double* buf) {
-#pragma unroll
-  for (int q = 0; q < (GW * RCH / 2) / TPB; ++q) {
-    const int c = threadIdx.x + q * TPB;
-    const int col = c >> 5;
-    const int r2 = (c & 31) * 2;
-    if (col0 + col < ncols)
-      *reinterpret_cast<double2*>(M + r0 + r2 + (col0 + col) * ld) =
-          *reinterpret_cast<const double2*>(buf + col * XS + r2);
-  }
-}
-
 // ======================================================================
 //                               Jacobi core
 // ======================================================================
@@ -3496,7 +3469,6 @@ __global__ void __launch_bounds__(128) svd_bt_tlog_kernel(SvdParams P, double* t
 template <int KB>
 __global__ void __launch_bounds__(KB * 4) svd_bt_blocked_kernel(SvdParams P, const double* tlog,
                                                                int64_t nblk) {
-  constexpr int NW = KB / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
@@ -3666,7 +3638,7 @@ __global__ void __launch_bounds__(TPB, 3) svd_jacobi_kernel(SvdParams P) {
   FinalView fs = final_view(smem_raw, NS);
   __shared__ int64_t cur;
   const int tid = threadIdx.x;
-  const int64_t L = P.L, n = P.n, LP = P.LP, NP = P.NP, RP = P.RP;
+  const int64_t n = P.n, LP = P.LP, NP = P.NP, RP = P.RP;
   double* Xslot = P.xslots + int64_t(blockIdx.x) * LP * NP;
   double* V = WANTV ? P.wslots + int64_t(blockIdx.x) * RP * NP : nullptr;
   const int nb = int(NP / BW);
