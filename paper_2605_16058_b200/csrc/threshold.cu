@@ -376,17 +376,23 @@ __global__ void ranks_kernel(const double* s, int64_t r, int64_t N, const ThStat
                              int64_t* ranks, double* scal, int64_t* j_out) {
   const int mode = st->mode;
   const double tau = st->tau;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    int64_t k = 0;
+  // one warp per slice: lanes stride the r values (coalesced), integer counts
+  // summed by shuffles (one thread per slice walked its column serially:
+  // 0.09 ms for c2's 70 x 361 values)
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < N; i += warps) {
+    int k = 0;
     if (mode >= 0) {
-      for (int64_t row = 0; row < r; ++row) {
+      for (int64_t row = lane; row < r; row += 32) {
         const double x = s[row + i * r];
         const double sq = __dmul_rn(x, x);
         k += (mode == 0) ? (sq > tau) : (sq >= tau);
       }
     }
-    ranks[i] = k;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0) ranks[i] = k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (mode < 0) {
@@ -531,7 +537,7 @@ int threshold_run(const double* s, int64_t r, int64_t nslices, double epsilon, d
   STARM_LAUNCH_CHECK();
   pairwise_kernel<<<1, PW_THREADS, 0, st>>>(fa, fb, pa, pb, count, parts, stt);
   STARM_LAUNCH_CHECK();
-  ranks_kernel<<<grid_for(nslices), 256, 0, st>>>(s, r, nslices, stt, ranks_out, scal_out, j_out);
+  ranks_kernel<<<grid_for(nslices * 32), 256, 0, st>>>(s, r, nslices, stt, ranks_out, scal_out, j_out);
   STARM_LAUNCH_CHECK();
   if (cert_out) {
     cert_kernel<<<1, 1, 0, st>>>(stt, cert_out);
