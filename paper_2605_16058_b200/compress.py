@@ -613,6 +613,8 @@ def prune_refine(ahat3, f, epsilon, sel):
     nc = int(np.searchsorted(cum, PRUNE_GAMMA2 * budget, side="right"))
     if nc == 0 or nc > PRUNE_REFINE_MAX or keep_ids.size - nc > half:
         return None
+    if nc * (2 * m * p + 2 * min(m, p) ** 2) * 8 > (2 << 30):
+        return None                      # (the bound's scratch is capped at 2 GB)
     cand = np.sort(ordk[:nc])
     ids = torch.from_numpy(cand.astype(np.int64)).to(dev)
     a = ahat3.data.view(n, p, m).index_select(0, ids)            # column-major m x p slices
